@@ -1,0 +1,305 @@
+// ORACLE (reference build) — test infrastructure only.
+//
+// _ref/libouro_ref.so: the shared model driver (oracle/driver.hpp) running on
+// the reference's OWN compiled primitives (sources compiled in place from
+// /root/reference/proj/src/ouro, never copied): make_toy_model, quantize_weights,
+// detail::mm, softplus_val/silu_val, maybe_refresh, detect_outliers,
+// fake_quant_step, split_quantize, pack_int4, hybrid_gemm. Plus pin entry points
+// that call the reference's exported end-to-end functions (vmm_forward_raw,
+// quantized_forward, calibrate) so the driver's restatement of the reference's
+// anonymous-namespace code (block, QuantHook, recorder) is checked bit-for-bit.
+#include <cstring>
+
+#include "../oracle_ops.hpp"
+#include "ouro/gemm.hpp"
+#include "ouro/quant.hpp"
+#include "ouro/ssm.hpp"
+#include "ouro/tensor.hpp"
+
+namespace oro {
+
+inline std::vector<double> tvec(const ouro::Tensor& t) { return std::vector<double>(t.ptr(), t.ptr() + t.numel()); }
+inline void tset(ouro::Tensor& t, const std::vector<double>& v) { std::memcpy(t.mut(), v.data(), v.size() * sizeof(double)); }
+
+inline ouro::ModelDims to_ref(const Dims& d) {
+    ouro::ModelDims r;
+    r.image = d.image;
+    r.channels = d.channels;
+    r.patch = d.patch;
+    r.embed = d.embed;
+    r.state = d.state;
+    r.blocks = d.blocks;
+    r.classes = d.classes;
+    r.conv_width = d.conv_width;
+    return r;
+}
+
+inline ouro::ToyVmmModel to_ref(const ModelW& w) {
+    std::vector<ouro::ScanOrder> ord;
+    for (int o : w.orders) ord.push_back(static_cast<ouro::ScanOrder>(o));
+    ouro::ToyVmmModel m = ouro::make_toy_model(to_ref(w.d), ord, 0);
+    tset(m.patch_embed_w, w.patch_w);
+    tset(m.patch_embed_b, w.patch_b);
+    tset(m.head_w, w.head_w);
+    tset(m.head_b, w.head_b);
+    for (std::size_t b = 0; b < w.blocks.size(); ++b) {
+        tset(m.blocks[b].w_in, w.blocks[b].w_in);
+        tset(m.blocks[b].w_gate, w.blocks[b].w_gate);
+        tset(m.blocks[b].conv, w.blocks[b].conv);
+        tset(m.blocks[b].out_proj, w.blocks[b].out_proj);
+        for (std::size_t d = 0; d < w.blocks[b].dirs.size(); ++d) {
+            auto& p = m.blocks[b].dirs[d];
+            const auto& q = w.blocks[b].dirs[d];
+            tset(p.a, q.a);
+            tset(p.w_b, q.w_b);
+            tset(p.w_c, q.w_c);
+            tset(p.w_delta, q.w_delta);
+            tset(p.b_delta, q.b_delta);
+        }
+    }
+    return m;
+}
+
+struct RefOps {
+    using State = ouro::OutlierState;
+    struct Weight {
+        ouro::PackedInt4 packed;
+        std::vector<std::int8_t> codes;
+        std::vector<double> scales;
+        std::size_t rows = 0, cols = 0;
+    };
+    struct Prepared;
+
+    static ModelW make_model(const Dims& d, const std::vector<int>& orders, std::uint64_t seed) {
+        std::vector<ouro::ScanOrder> ord;
+        for (int o : orders) ord.push_back(static_cast<ouro::ScanOrder>(o));
+        ouro::ToyVmmModel m = ouro::make_toy_model(to_ref(d), ord, seed);
+        ModelW w;
+        w.d = d;
+        w.orders = orders;
+        w.patch_w = tvec(m.patch_embed_w);
+        w.patch_b = tvec(m.patch_embed_b);
+        w.head_w = tvec(m.head_w);
+        w.head_b = tvec(m.head_b);
+        for (auto& b : m.blocks) {
+            BlockW bw;
+            bw.w_in = tvec(b.w_in);
+            bw.w_gate = tvec(b.w_gate);
+            bw.conv = tvec(b.conv);
+            bw.out_proj = tvec(b.out_proj);
+            for (auto& p : b.dirs) {
+                DirW dw;
+                dw.a = tvec(p.a);
+                dw.w_b = tvec(p.w_b);
+                dw.w_c = tvec(p.w_c);
+                dw.w_delta = tvec(p.w_delta);
+                dw.b_delta = tvec(p.b_delta);
+                bw.dirs.push_back(std::move(dw));
+            }
+            w.blocks.push_back(std::move(bw));
+        }
+        return w;
+    }
+    static QRows quantize_rows(const std::vector<double>& w, std::size_t rows, unsigned bits) {
+        ouro::Tensor t = ouro::Tensor::zeros({rows, w.size() / rows});
+        tset(t, w);
+        ouro::QuantizedRows q = ouro::quantize_weights(t, bits);
+        QRows r;
+        r.codes = q.codes;
+        r.scales = q.scales;
+        r.deq = tvec(ouro::dequantize_rows(q));
+        return r;
+    }
+    static void mm_nt(const double* a, const double* b, double* c, std::size_t m, std::size_t k, std::size_t n) {
+        ouro::detail::mm(a, b, c, m, k, n, false, true, false);
+    }
+    static double softplus(double x) { return ouro::detail::softplus_val(x); }
+    static double silu(double x) { return ouro::detail::silu_val(x); }
+    static void refresh(State& st, std::size_t t, std::size_t n) { ouro::maybe_refresh(st, t, n); }
+    static bool detect(State& st, const double* x, std::size_t e, std::size_t n, double th, double s, unsigned b) {
+        return ouro::detect_outliers(st, x, e, n, th, s, b).scanned;
+    }
+    static void fake_quant(double* x, std::size_t e, std::size_t n, const State* st, double s, unsigned ab,
+                           unsigned ob) {
+        ouro::OutlierState none;
+        ouro::fake_quant_step(x, e, n, st ? *st : none, s, ab, ob);
+    }
+    static std::vector<std::size_t> list(const State& st, std::size_t) { return st.o_list; }
+    static SplitOperands split(const double* x, std::size_t k, std::size_t c, const std::vector<std::size_t>& o,
+                               double s, unsigned ab, unsigned ob) {
+        ouro::SplitOperands r = ouro::split_quantize(x, k, c, o, s, ab, ob);
+        SplitOperands out;
+        out.inlier_codes = r.inlier_codes;
+        out.outliers.channels = r.outliers.channels;
+        out.outliers.codes = r.outliers.codes;
+        out.outliers.scales = r.outliers.scales;
+        out.outliers.cols = r.outliers.cols;
+        return out;
+    }
+    static GemmResult run_hybrid(const ouro::PackedInt4* wp, const std::int8_t* w, const double* ws, std::size_t m,
+                                 std::size_t k, const std::int8_t* x, std::size_t c, double s,
+                                 const OutlierBuffer& ob) {
+        bool a4 = true;
+        for (std::size_t i = 0; i < k * c; ++i) a4 = a4 && x[i] >= -7 && x[i] <= 7;
+        if (!a4)  // A8 inliers cannot be packed (gemm.cpp:69); the reference's own A8
+                  // oracle is the triple loop (tests/test_gemm.cpp:25-35) -> restated form.
+            return hybrid_gemm(w, ws, m, k, x, c, s, ob);
+        ouro::PackedInt4 local;
+        if (!wp) {
+            local = ouro::pack_int4(w, m, k);
+            wp = &local;
+        }
+        ouro::OutlierBuffer rb;
+        rb.channels = ob.channels;
+        rb.codes = ob.codes;
+        rb.scales = ob.scales;
+        rb.cols = c;
+        ouro::GemmResult g = ouro::hybrid_gemm(*wp, std::vector<double>(ws, ws + m), ouro::pack_int4(x, k, c), s, rb, 1,
+                                               false);
+        GemmResult r;
+        r.acc_inlier = g.acc_inlier;
+        r.acc_outlier = g.acc_outlier;
+        r.output = g.output;
+        return r;
+    }
+    static GemmResult hybrid(const Weight& w, const SplitOperands& sp, double s) {
+        return run_hybrid(&w.packed, w.codes.data(), w.scales.data(), w.rows, w.cols, sp.inlier_codes.data(), 1, s,
+                          sp.outliers);
+    }
+    static GemmResult hybrid_raw(const std::int8_t* w, const double* ws, std::size_t m, std::size_t k,
+                                 const std::int8_t* x, std::size_t c, double s, const OutlierBuffer& ob) {
+        return run_hybrid(nullptr, w, ws, m, k, x, c, s, ob);
+    }
+    static std::vector<std::uint8_t> pack(const std::int8_t* codes, std::size_t r, std::size_t c) {
+        return ouro::pack_int4(codes, r, c).bytes;
+    }
+    template <class Q>
+    static Prepared prepare(const Q& q);
+};
+
+}  // namespace oro
+
+#include "../driver.hpp"
+
+namespace oro {
+struct RefOps::Prepared {
+    struct Blk {
+        Weight in, out;
+        std::vector<Weight> xp;
+    };
+    std::vector<Blk> blocks;
+};
+template <class Q>
+RefOps::Prepared RefOps::prepare(const Q& q) {
+    auto mk = [](const QRows& r) {
+        Weight w;
+        w.codes = r.codes;
+        w.scales = r.scales;
+        w.rows = r.scales.size();
+        w.cols = r.codes.size() / w.rows;
+        w.packed = ouro::pack_int4(w.codes.data(), w.rows, w.cols);
+        return w;
+    };
+    Prepared p;
+    for (const auto& b : q.blocks) {
+        Prepared::Blk pb;
+        pb.in = mk(b.in);
+        pb.out = mk(b.out);
+        for (const auto& x : b.xp) pb.xp.push_back(mk(x));
+        p.blocks.push_back(std::move(pb));
+    }
+    return p;
+}
+}  // namespace oro
+
+using OPS = oro::RefOps;
+#include "../capi_impl.hpp"
+
+// ---- pins: the reference's exported end-to-end functions ----------------------
+extern "C" {
+
+// vmm_forward_raw (ssm.cpp:237-277) with no hook: FP logits, no D1/D2.
+int ref_pin_fp_forward(void* m, const double* images, std::size_t B, double* logits) {
+    return guarded([&] {
+        const oro::ModelW& w = static_cast<ModelH*>(m)->w;
+        ouro::ToyVmmModel rm = oro::to_ref(w);
+        std::size_t pix = w.d.image * w.d.image * w.d.channels;
+        ouro::RawForward r = ouro::vmm_forward_raw(rm, std::vector<double>(images, images + B * pix), B, nullptr, false);
+        std::memcpy(logits, r.logits.data(), r.logits.size() * sizeof(double));
+    });
+}
+
+// calibrate (quant.cpp:129-177) into a calib handle (scan tensors only).
+int ref_pin_calibrate(void* m, const double* images, std::size_t B, const unsigned* bits, std::size_t n_refresh,
+                      double rho, void** out) {
+    return guarded([&] {
+        const oro::ModelW& w = static_cast<ModelH*>(m)->w;
+        ouro::ToyVmmModel rm = oro::to_ref(w);
+        std::size_t pix = w.d.image * w.d.image * w.d.channels;
+        ouro::QuantSpec spec;
+        spec.weight_bits = bits[0];
+        spec.act_bits = bits[1];
+        spec.outlier_bits = bits[2];
+        spec.n_refresh = n_refresh;
+        spec.rho = rho;
+        ouro::CalibrationResult cr = ouro::calibrate(rm, std::vector<double>(images, images + B * pix), B, spec);
+        auto h = std::make_unique<CalibH>();
+        oro::Calib& c = h->c;
+        c.spec = make_spec(bits, n_refresh, rho);
+        c.tokens = cr.tokens;
+        c.embed = cr.embed;
+        c.state = cr.state;
+        c.blocks = cr.blocks;
+        c.ndirs = cr.ndirs;
+        c.d1 = false;
+        c.d2 = false;
+        for (const auto& t : cr.tensors) {
+            oro::TCal tc;
+            tc.theta = t.theta;
+            tc.s_in = t.scale_inlier;
+            tc.s_full = t.scale_full;
+            tc.excluded = t.excluded;
+            c.scan.push_back(std::move(tc));
+        }
+        *out = h.release();
+    });
+}
+
+// quantized_forward (quant.cpp:505-579): logits of the quantized pass
+// (mode 1 dynamic / 2 static / 3 bypass) under a calibration handle.
+int ref_pin_quantized_forward(void* m, void* c, int mode, const double* images, std::size_t B, double* logits_q,
+                              double* logits_fp) {
+    return guarded([&] {
+        const oro::ModelW& w = static_cast<ModelH*>(m)->w;
+        const oro::Calib& k = static_cast<CalibH*>(c)->c;
+        ouro::ToyVmmModel rm = oro::to_ref(w);
+        std::size_t pix = w.d.image * w.d.image * w.d.channels;
+        ouro::CalibrationResult cr;
+        cr.spec.weight_bits = k.spec.wbits;
+        cr.spec.act_bits = k.spec.abits;
+        cr.spec.outlier_bits = k.spec.obits;
+        cr.spec.n_refresh = k.spec.n_refresh;
+        cr.spec.rho = k.spec.rho;
+        cr.tokens = k.tokens;
+        cr.embed = k.embed;
+        cr.state = k.state;
+        cr.blocks = k.blocks;
+        cr.ndirs = k.ndirs;
+        for (const auto& t : k.scan) {
+            ouro::TensorCalib tc;
+            tc.theta = t.theta;
+            tc.scale_inlier = t.s_in;
+            tc.scale_full = t.s_full;
+            tc.excluded = t.excluded;
+            cr.tensors.push_back(std::move(tc));
+        }
+        ouro::QuantMode qm = mode == 1 ? ouro::QuantMode::Dynamic
+                                       : (mode == 2 ? ouro::QuantMode::Static : ouro::QuantMode::Bypass);
+        ouro::QuantEvalResult r = ouro::quantized_forward(rm, std::vector<double>(images, images + B * pix), B, cr, qm,
+                                                          ouro::SpikeSettings{});
+        std::memcpy(logits_q, r.logits_q.data(), r.logits_q.size() * sizeof(double));
+        if (logits_fp) std::memcpy(logits_fp, r.logits_fp.data(), r.logits_fp.size() * sizeof(double));
+    });
+}
+
+}  // extern "C"
