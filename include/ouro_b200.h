@@ -1,0 +1,175 @@
+#ifndef OURO_B200_H
+#define OURO_B200_H
+
+/*
+ * C ABI of the B200-native OuroMamba-Quant inference path (sm_100a).
+ *
+ * Drop-in boundary for the reference's hot path. Conventions follow the
+ * reference C interface (/root/reference/proj/include/ouromamba.h):
+ *   - every call returns an ouro_status; on failure ouro_b200_last_error()
+ *     holds a thread-local message, cleared by the next successful call
+ *     (ouromamba.h:28-29, src/capi.cpp:14-37);
+ *   - NULL handles / pointers are rejected with OURO_ERR_VALIDATION, never a
+ *     crash; _free(NULL) is a no-op (tests/test_capi.cpp:85-114);
+ *   - handles are opaque; no global state besides the per-thread error
+ *     message, so independent contexts may be used from different threads
+ *     (ouromamba.h:4-10).
+ * CUDA launch-configuration errors map to OURO_ERR_VALIDATION, device faults
+ * to OURO_ERR_NUMERIC. Device pointers ("dev") must live on the context's
+ * device; all operator calls are asynchronous on the context's stream.
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ */
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef OURO_STATUS_DEFINED
+#define OURO_STATUS_DEFINED
+typedef enum ouro_status {
+    OURO_OK = 0,
+    OURO_ERR_VALIDATION = 2, /* bad arguments, config or shapes */
+    OURO_ERR_NUMERIC = 3,    /* device fault / non-finite values */
+    OURO_ERR_IO = 4          /* missing, unreadable or unwritable files */
+} ouro_status;
+#endif
+
+typedef struct ouro_b200_ctx ouro_b200_ctx;
+typedef struct ouro_b200_model ouro_b200_model;
+typedef struct ouro_b200_calib ouro_b200_calib;
+typedef struct ouro_b200_trace ouro_b200_trace;
+
+/* Quantization modes (quant.hpp:101): FP = bypass (no activation quantization). */
+enum { OURO_B200_MODE_FP = 0, OURO_B200_MODE_DYNAMIC = 1, OURO_B200_MODE_STATIC = 2 };
+/* Quant-linear epilogue post-ops. */
+enum { OURO_B200_POST_STORE = 0, OURO_B200_POST_INPROJ = 1, OURO_B200_POST_RESID = 2, OURO_B200_POST_BIAS = 3 };
+/* K1 row sources. */
+enum { OURO_B200_SRC_PLAIN = 0, OURO_B200_SRC_RMSNORM = 1, OURO_B200_SRC_MERGE = 2 };
+
+const char* ouro_b200_version(void);
+const char* ouro_b200_last_error(void);
+
+/* ---- context --------------------------------------------------------------- */
+ouro_status ouro_b200_ctx_create(int device, ouro_b200_ctx** out);
+void ouro_b200_ctx_free(ouro_b200_ctx* ctx);
+/* Run on a caller stream (cudaStream_t, e.g. torch.cuda.current_stream()). */
+ouro_status ouro_b200_ctx_set_stream(ouro_b200_ctx* ctx, void* stream);
+ouro_status ouro_b200_ctx_synchronize(ouro_b200_ctx* ctx);
+ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out);
+
+/* ---- operator level (device pointers) ---------------------------------------- */
+
+/* K1: per-step dynamic outlier detector + activation quantizer over S
+ * sequences of T (sample, token) planes of E channels. Replaces, per plane,
+ * maybe_refresh + detect_outliers (quant.hpp:67-80, quant.cpp:303-335) and
+ * split_quantize (gemm.hpp:51-57, gemm.cpp:106-135).
+ *   x      dev f64 [S][T][E] canonical rows (SRC_MERGE: scan output of dir 0)
+ *   x2     dev f64 [S][T][E] scan output of dir 1 (SRC_MERGE, may be NULL)
+ *   gate   dev f64 [S][T][E] (SRC_MERGE)
+ *   order  scan order read at step t (ssm.cpp:30-46), -1 = identity; grid = sqrt(T)
+ *   s_in, s_full  dev f64 [T] calibrated per-step scales (TensorCalib, quant.hpp:36-42)
+ * Outputs (row = s*T + t, dev): codes int8 [S*T][E] (0 at outliers), s_row
+ * f64 [S*T], ocnt int32 [S*T], och uint16 / ocode int8 / oscale f64
+ * [S*T][cap] (outlier list, ascending channel), optional omask uint32
+ * [S*T][ceil(E/32)] and scanned uint8 [S*T] (DetectResult::scanned). */
+ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
+                                      size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
+                                      const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
+                                      unsigned outlier_bits, int mode, int8_t* codes, double* s_row, int32_t* ocnt,
+                                      uint16_t* och, int8_t* ocode, double* oscale, size_t cap, uint32_t* omask,
+                                      uint8_t* scanned);
+
+/* K2: hybrid quant-linear on tcgen05 kind::i8 (hybrid_gemm, gemm.hpp:78-87,
+ * gemm.cpp:181-225): out[m][r] = ws[r]*(s_row[m]*acc_in[m][r]
+ *   + sum_j (oscale[m][j]*w[r][och[m][j]])*ocode[m][j]), then the post-op.
+ *   codes/s_row/ocnt/och/ocode/oscale as produced by K1, M rows of K channels
+ *   w   dev int8 [R][K] weight codes (|code| <= 7), wt its transpose [K][R]
+ *   ws  dev f64 [R] weight row scales
+ * K and R must be multiples of 16. acc_in/acc_out (dev int32 [M][R], may be
+ * NULL) receive the reference's integer planes GemmResult::acc_inlier /
+ * acc_outlier. */
+ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
+                                   const double* s_row, const int32_t* ocnt, const uint16_t* och,
+                                   const int8_t* ocode, const double* oscale, size_t cap, const int8_t* w,
+                                   const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
+                                   double* out2, size_t split, const double* bias, int32_t* acc_in,
+                                   int32_t* acc_out);
+
+/* K3: selective scan of one direction with the QuantHook policy (s6_scan,
+ * ssm.hpp:131-132, ssm.cpp:124-186; QuantHook quant.cpp:456-501), N = 16.
+ *   u     dev f64 [S][T][E] canonical scan input; proj dev f64 [S][T][E+2N]
+ *         rows in scan order = (delta pre-activation | B | C)
+ *   a     dev f64 [E][N]; b_delta dev f64 [E]; o dev f64 [S][T][E] (canonical)
+ *   theta[3], s_in[3], s_full[3]: calibration of a_bar, b_bar, h (s_* dev [T])
+ *   literal dev uint8 [T] (may be NULL): steps where the channel-local detector
+ *   is not exact; force_literal runs the literal detector on every step.
+ *   masks dev uint8 [3][S][T][E] (may be NULL): O(t) per kind after detection. */
+ouro_status ouro_b200_quant_scan(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order, int grid,
+                                 const double* u, const double* proj, const double* a, const double* b_delta,
+                                 double* o, int mode, size_t n_refresh, unsigned act_bits, unsigned outlier_bits,
+                                 const double* theta, const double* const* s_in, const double* const* s_full,
+                                 const uint8_t* literal, int force_literal, uint8_t* masks);
+
+/* f64 projection with the reference's per-output k-ascending order
+ * (detail::mm, tensor.cpp:373-382): out[m][r] = 0.0 + sum_k a[m][k]*w[r][k]. */
+ouro_status ouro_b200_dgemm(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const double* a, size_t lda,
+                            const double* w, int post, double* out, size_t ld_out, double* out2, size_t split,
+                            const double* bias);
+
+/* ---- model level ---------------------------------------------------------------- */
+
+/* dims = {image, channels, patch, embed, state, blocks, classes, conv_width}
+ * (ModelDims, ssm.hpp:42-56); orders = ScanOrder values (ssm.hpp:15).
+ * Weights are seeded exactly as make_toy_model (ssm.cpp:88-120). */
+ouro_status ouro_b200_model_create(ouro_b200_ctx* ctx, const size_t* dims, const int* orders, size_t ndirs,
+                                   uint64_t seed, ouro_b200_model** out);
+void ouro_b200_model_free(ouro_b200_model* m);
+/* Names as the reference checkpoint (ssm.cpp:381-405): "patch_embed.w"-style
+ * names use this repo's spelling: patch_w, patch_b, head_w, head_b,
+ * block<b>.{w_in,w_gate,conv,out_proj}, block<b>.dir<d>.{a,w_b,w_c,w_delta,b_delta}. */
+ouro_status ouro_b200_model_set_tensor(ouro_b200_model* m, const char* name, const double* host, size_t n);
+ouro_status ouro_b200_model_get_tensor(ouro_b200_model* m, const char* name, double* host, size_t cap,
+                                       size_t* n_out);
+
+/* Calibration (CalibrationResult, quant.hpp:44-49) extended with the
+ * linear-input sites of D2. which: 0 = scan tensors [block][dir][kind],
+ * 1 = linear sites [block][site]. Arrays are host memory. */
+ouro_status ouro_b200_calib_create(ouro_b200_model* m, const unsigned* bits /* w,a,o */, size_t n_refresh,
+                                   double rho, int d1, int d2, ouro_b200_calib** out);
+ouro_status ouro_b200_calibrate(ouro_b200_model* m, const double* images_dev, size_t B, const unsigned* bits,
+                                size_t n_refresh, double rho, int d1, int d2, size_t chunk, ouro_b200_calib** out);
+void ouro_b200_calib_free(ouro_b200_calib* c);
+ouro_status ouro_b200_calib_count(ouro_b200_calib* c, int which, size_t* out);
+ouro_status ouro_b200_calib_get(ouro_b200_calib* c, int which, size_t idx, double* theta, double* s_in,
+                                double* s_full, uint8_t* excluded);
+ouro_status ouro_b200_calib_set(ouro_b200_calib* c, int which, size_t idx, double theta, const double* s_in,
+                                const double* s_full, const uint8_t* excluded);
+
+/* Quantized (or FP) Vim forward: images dev f64 [B][image][image][channels],
+ * logits dev f64 [B][classes]. d1 = pre-norm residual, d2 = quantized linear
+ * inputs. Asynchronous on the context stream. */
+ouro_status ouro_b200_forward(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                              const double* images_dev, size_t B, double* logits_dev);
+/* Same through host buffers: H2D of the images and D2H of the logits inside
+ * the call (synchronous). */
+ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                   const double* images_host, size_t B, double* logits_host);
+/* Capture CUDA graphs of ouro_b200_forward for repeated calls with the same
+ * (calib, mode, d1, d2, images, B, logits) (1 = on). */
+ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
+
+/* Parity harness: run a forward over host images and keep every
+ * intermediate of one block (keys documented in DESIGN.md §5). */
+ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                const double* images_host, size_t B, size_t block, ouro_b200_trace** out);
+ouro_status ouro_b200_trace_get(ouro_b200_trace* t, const char* key, void* host, size_t cap, size_t* bytes);
+void ouro_b200_trace_free(ouro_b200_trace* t);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OURO_B200_H */

@@ -1,0 +1,103 @@
+"""ctypes binding of the C ABI in include/ouro_b200.h (libouro_b200.so).
+
+The library is built in-tree (``make -C paper_2503_10959_b200``). There is no
+fallback: if the shared object is missing or the device is not sm_100a, every
+entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "libouro_b200.so")
+
+_P = C.c_void_p
+_SZ = C.c_size_t
+_U = C.c_uint
+_I = C.c_int
+_D = C.c_double
+
+OK, ERR_VALIDATION, ERR_NUMERIC, ERR_IO = 0, 2, 3, 4
+MODE_FP, MODE_DYNAMIC, MODE_STATIC = 0, 1, 2
+POST_STORE, POST_INPROJ, POST_RESID, POST_BIAS = 0, 1, 2, 3
+SRC_PLAIN, SRC_RMSNORM, SRC_MERGE = 0, 1, 2
+
+_SIGS = {
+    "ouro_b200_version": ([], C.c_char_p),
+    "ouro_b200_last_error": ([], C.c_char_p),
+    "ouro_b200_ctx_create": ([_I, C.POINTER(_P)], _I),
+    "ouro_b200_ctx_free": ([_P], None),
+    "ouro_b200_ctx_set_stream": ([_P, _P], _I),
+    "ouro_b200_ctx_synchronize": ([_P], _I),
+    "ouro_b200_ctx_num_sms": ([_P, C.POINTER(_I)], _I),
+    "ouro_b200_detect_quantize": ([_P, _P, _P, _P, _SZ, _SZ, _SZ, _I, _I, _I, _D, _P, _P, _SZ, _U, _U, _I, _P, _P,
+                                   _P, _P, _P, _P, _SZ, _P, _P], _I),
+    "ouro_b200_quant_linear": ([_P, _SZ, _SZ, _SZ, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I, _P, _SZ, _P, _SZ,
+                                _P, _P, _P], _I),
+    "ouro_b200_quant_scan": ([_P, _SZ, _SZ, _SZ, _SZ, _I, _I, _P, _P, _P, _P, _P, _I, _SZ, _U, _U, _P, _P, _P, _P,
+                              _I, _P], _I),
+    "ouro_b200_dgemm": ([_P, _SZ, _SZ, _SZ, _P, _SZ, _P, _I, _P, _SZ, _P, _SZ, _P], _I),
+    "ouro_b200_model_create": ([_P, _P, _P, _SZ, C.c_uint64, C.POINTER(_P)], _I),
+    "ouro_b200_model_free": ([_P], None),
+    "ouro_b200_model_set_tensor": ([_P, C.c_char_p, _P, _SZ], _I),
+    "ouro_b200_model_get_tensor": ([_P, C.c_char_p, _P, _SZ, C.POINTER(_SZ)], _I),
+    "ouro_b200_calib_create": ([_P, _P, _SZ, _D, _I, _I, C.POINTER(_P)], _I),
+    "ouro_b200_calibrate": ([_P, _P, _SZ, _P, _SZ, _D, _I, _I, _SZ, C.POINTER(_P)], _I),
+    "ouro_b200_calib_free": ([_P], None),
+    "ouro_b200_calib_count": ([_P, _I, C.POINTER(_SZ)], _I),
+    "ouro_b200_calib_get": ([_P, _I, _SZ, C.POINTER(_D), _P, _P, _P], _I),
+    "ouro_b200_calib_set": ([_P, _I, _SZ, _D, _P, _P, _P], _I),
+    "ouro_b200_forward": ([_P, _P, _I, _I, _I, _P, _SZ, _P], _I),
+    "ouro_b200_forward_host": ([_P, _P, _I, _I, _I, _P, _SZ, _P], _I),
+    "ouro_b200_model_use_graphs": ([_P, _I], _I),
+    "ouro_b200_trace_run": ([_P, _P, _I, _I, _I, _P, _SZ, _SZ, C.POINTER(_P)], _I),
+    "ouro_b200_trace_get": ([_P, C.c_char_p, _P, _SZ, C.POINTER(_SZ)], _I),
+    "ouro_b200_trace_free": ([_P], None),
+}
+
+EXPORTED = sorted(_SIGS)
+
+
+class OuroError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[status {status}] {msg}")
+        self.status = status
+
+
+class ValidationError(OuroError):
+    pass
+
+
+class NumericError(OuroError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = SO_PATH):
+    """Load libouro_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `make -C {HERE}` (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    msg = _lib.ouro_b200_last_error().decode()
+    if status == ERR_VALIDATION:
+        raise ValidationError(status, msg)
+    if status == ERR_NUMERIC:
+        raise NumericError(status, msg)
+    raise OuroError(status, msg)

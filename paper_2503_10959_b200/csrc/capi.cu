@@ -1,0 +1,487 @@
+// C ABI (include/ouro_b200.h) over the engine and the K1-K4 launchers.
+// Exception -> status mapping mirrors the reference's guarded()
+// (/root/reference/proj/src/capi.cpp:18-37).
+#include <cstring>
+#include <exception>
+#include <string>
+#include <tuple>
+
+#include "../../include/ouro_b200.h"
+#include "engine.h"
+
+using ob::require;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename Fn>
+ouro_status guarded(Fn&& fn) {
+    try {
+        fn();
+        g_last_error.clear();
+        return OURO_OK;
+    } catch (const ob::ValidationError& e) {
+        g_last_error = e.what();
+        return OURO_ERR_VALIDATION;
+    } catch (const ob::NumericError& e) {
+        g_last_error = e.what();
+        return OURO_ERR_NUMERIC;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("internal error: ") + e.what();
+        return OURO_ERR_VALIDATION;
+    }
+}
+}  // namespace
+
+struct ouro_b200_ctx {
+    std::unique_ptr<ob::Context> c;
+};
+struct ouro_b200_model {
+    ouro_b200_ctx* ctx = nullptr;
+    std::unique_ptr<ob::Model> m;
+    bool graphs = false;
+    struct GraphKey {
+        const void* cal;
+        int mode, d1, d2;
+        const double* img;
+        size_t B;
+        double* logits;
+        bool operator==(const GraphKey& o) const {
+            return std::tie(cal, mode, d1, d2, img, B, logits) == std::tie(o.cal, o.mode, o.d1, o.d2, o.img, o.B, o.logits);
+        }
+    };
+    GraphKey key{};
+    int key_hits = 0;
+    cudaGraphExec_t exec = nullptr;
+    ~ouro_b200_model() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+struct ouro_b200_calib {
+    std::unique_ptr<ob::Calibration> c;
+};
+struct ouro_b200_trace {
+    ob::Model::TraceSink sink;
+};
+
+extern "C" {
+
+const char* ouro_b200_version(void) { return "0.1.0-sm100a"; }
+const char* ouro_b200_last_error(void) { return g_last_error.c_str(); }
+
+ouro_status ouro_b200_ctx_create(int device, ouro_b200_ctx** out) {
+    return guarded([&] {
+        require(out != nullptr, "ctx_create: out is NULL");
+        auto h = std::make_unique<ouro_b200_ctx>();
+        h->c = std::make_unique<ob::Context>(device);
+        *out = h.release();
+    });
+}
+void ouro_b200_ctx_free(ouro_b200_ctx* ctx) { delete ctx; }
+
+ouro_status ouro_b200_ctx_set_stream(ouro_b200_ctx* ctx, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx_set_stream: ctx is NULL");
+        ctx->c->set_stream(static_cast<cudaStream_t>(stream));
+    });
+}
+ouro_status ouro_b200_ctx_synchronize(ouro_b200_ctx* ctx) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx_synchronize: ctx is NULL");
+        ob::cuda_check(cudaStreamSynchronize(ctx->c->stream), "synchronize");
+    });
+}
+ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out) {
+    return guarded([&] {
+        require(ctx != nullptr && out != nullptr, "ctx_num_sms: NULL argument");
+        *out = ctx->c->num_sms;
+    });
+}
+
+ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
+                                      size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
+                                      const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
+                                      unsigned outlier_bits, int mode, int8_t* codes, double* s_row, int32_t* ocnt,
+                                      uint16_t* och, int8_t* ocode, double* oscale, size_t cap, uint32_t* omask,
+                                      uint8_t* scanned) {
+    return guarded([&] {
+        require(ctx && x && codes && s_row && ocnt && och && ocode && oscale, "detect_quantize: NULL argument");
+        require(mode == ob::MODE_DYNAMIC || mode == ob::MODE_STATIC, "detect_quantize: mode must be dynamic or static");
+        require(mode == ob::MODE_STATIC ? s_full != nullptr : s_in != nullptr, "detect_quantize: missing scales");
+        require(act_bits >= 2 && act_bits <= 8 && outlier_bits >= act_bits && outlier_bits <= 8,
+                "detect_quantize: bit widths must satisfy 2 <= act <= outlier <= 8");
+        require(cap >= E, "detect_quantize: outlier capacity must be >= E");
+        require(src != ob::K1_SRC_MERGE || gate != nullptr, "detect_quantize: merge source needs the gate");
+        ob::K1Params k;
+        k.S = static_cast<int>(S);
+        k.T = static_cast<int>(T);
+        k.E = static_cast<int>(E);
+        k.src = src;
+        k.x = x;
+        k.x2 = x2;
+        k.gate = gate;
+        k.order = order;
+        k.grid = grid;
+        k.mode = mode;
+        k.n_refresh = static_cast<int>(n_refresh);
+        k.abits = act_bits;
+        k.obits = outlier_bits;
+        k.window = mode == ob::MODE_DYNAMIC ? (n_refresh > 0 ? static_cast<int>(n_refresh) : static_cast<int>(T)) : 8;
+        k.cal.theta = theta;
+        k.cal.s_in = s_in;
+        k.cal.s_full = s_full;
+        k.codes = codes;
+        k.s_row = s_row;
+        k.ocnt = ocnt;
+        k.och = och;
+        k.ocode = ocode;
+        k.oscale = oscale;
+        k.cap = static_cast<int>(cap);
+        k.omask = omask;
+        k.scanned = scanned;
+        ob::cuda_check(ob::launch_k1(k, ctx->c->stream), "detect_quantize");
+    });
+}
+
+ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
+                                   const double* s_row, const int32_t* ocnt, const uint16_t* och,
+                                   const int8_t* ocode, const double* oscale, size_t cap, const int8_t* w,
+                                   const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
+                                   double* out2, size_t split, const double* bias, int32_t* acc_in,
+                                   int32_t* acc_out) {
+    return guarded([&] {
+        require(ctx && codes && s_row && ocnt && och && ocode && oscale && w && wt && ws && out,
+                "quant_linear: NULL argument");
+        require(K % 16 == 0 && R % 16 == 0, "quant_linear: K and R must be multiples of 16");
+        require(post != ob::POST_INPROJ || (out2 != nullptr && split % 32 == 0 && split < R),
+                "quant_linear: in_proj post-op needs out2 and a split that is a multiple of 32");
+        require(post != ob::POST_BIAS, "quant_linear: bias post-op is not part of the hybrid epilogue");
+        ob::QLinParams q;
+        q.M = static_cast<int>(M);
+        q.R = static_cast<int>(R);
+        q.K = static_cast<int>(K);
+        q.a.codes = const_cast<int8_t*>(codes);
+        q.a.s_row = const_cast<double*>(s_row);
+        q.a.ocnt = const_cast<int*>(ocnt);
+        q.a.och = const_cast<uint16_t*>(och);
+        q.a.ocode = const_cast<int8_t*>(ocode);
+        q.a.oscale = const_cast<double*>(oscale);
+        q.a.cap = static_cast<int>(cap);
+        q.w = w;
+        q.wt = wt;
+        q.ws = ws;
+        q.epi.post = post;
+        q.epi.out = out;
+        q.epi.ld_out = static_cast<int>(ld_out);
+        q.epi.out2 = out2;
+        q.epi.split = static_cast<int>(split);
+        q.epi.bias = bias;
+        q.epi.acc_in = acc_in;
+        q.epi.acc_out = acc_out;
+        ob::cuda_check(ob::launch_qlinear(q, ctx->c->stream, ctx->c->num_sms), "quant_linear");
+    });
+}
+
+ouro_status ouro_b200_quant_scan(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order, int grid,
+                                 const double* u, const double* proj, const double* a, const double* b_delta,
+                                 double* o, int mode, size_t n_refresh, unsigned act_bits, unsigned outlier_bits,
+                                 const double* theta, const double* const* s_in, const double* const* s_full,
+                                 const uint8_t* literal, int force_literal, uint8_t* masks) {
+    return guarded([&] {
+        require(ctx && u && proj && a && b_delta && o, "quant_scan: NULL argument");
+        require(N == 16, "quant_scan: this build keeps N = 16 states per channel");
+        require(mode == ob::MODE_FP || (theta && s_in && s_full), "quant_scan: quantized modes need calibration");
+        ob::ScanParams p;
+        p.S = static_cast<int>(S);
+        p.T = static_cast<int>(T);
+        p.E = static_cast<int>(E);
+        p.N = static_cast<int>(N);
+        p.order = order;
+        p.grid = grid;
+        p.u = u;
+        p.proj = proj;
+        p.a = a;
+        p.b_delta = b_delta;
+        p.o = o;
+        p.mode = mode;
+        p.n_refresh = static_cast<int>(n_refresh);
+        p.abits = act_bits;
+        p.obits = outlier_bits;
+        if (mode != ob::MODE_FP)
+            for (int k = 0; k < 3; ++k) {
+                p.cal[k].theta = theta[k];
+                p.cal[k].s_in = s_in[k];
+                p.cal[k].s_full = s_full[k];
+            }
+        p.literal = literal;
+        p.literal_any = literal != nullptr ? 1 : 0;
+        p.force_literal = force_literal;
+        p.masks = masks;
+        ob::cuda_check(ob::launch_scan(p, ctx->c->stream, nullptr), "quant_scan");
+    });
+}
+
+ouro_status ouro_b200_dgemm(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const double* a, size_t lda,
+                            const double* w, int post, double* out, size_t ld_out, double* out2, size_t split,
+                            const double* bias) {
+    return guarded([&] {
+        require(ctx && a && w && out, "dgemm: NULL argument");
+        ob::DGemmParams g;
+        g.M = static_cast<int>(M);
+        g.R = static_cast<int>(R);
+        g.K = static_cast<int>(K);
+        g.a = a;
+        g.lda = static_cast<int>(lda);
+        g.w = w;
+        g.epi.post = post;
+        g.epi.out = out;
+        g.epi.ld_out = static_cast<int>(ld_out);
+        g.epi.out2 = out2;
+        g.epi.split = static_cast<int>(split);
+        g.epi.bias = bias;
+        ob::cuda_check(ob::launch_dgemm(g, ctx->c->stream), "dgemm");
+    });
+}
+
+ouro_status ouro_b200_model_create(ouro_b200_ctx* ctx, const size_t* dims, const int* orders, size_t ndirs,
+                                   uint64_t seed, ouro_b200_model** out) {
+    return guarded([&] {
+        require(ctx && dims && orders && out, "model_create: NULL argument");
+        ob::Dims d;
+        d.image = static_cast<int>(dims[0]);
+        d.channels = static_cast<int>(dims[1]);
+        d.patch = static_cast<int>(dims[2]);
+        d.embed = static_cast<int>(dims[3]);
+        d.state = static_cast<int>(dims[4]);
+        d.blocks = static_cast<int>(dims[5]);
+        d.classes = static_cast<int>(dims[6]);
+        d.conv_width = static_cast<int>(dims[7]);
+        auto h = std::make_unique<ouro_b200_model>();
+        h->ctx = ctx;
+        h->m = std::make_unique<ob::Model>(ctx->c.get(),
+                                           ob::make_toy_model(d, std::vector<int>(orders, orders + ndirs), seed));
+        *out = h.release();
+    });
+}
+void ouro_b200_model_free(ouro_b200_model* m) { delete m; }
+
+ouro_status ouro_b200_model_set_tensor(ouro_b200_model* m, const char* name, const double* host, size_t n) {
+    return guarded([&] {
+        require(m && name && host, "model_set_tensor: NULL argument");
+        m->m->set_tensor(name, host, n);
+        if (m->exec) {
+            cudaGraphExecDestroy(m->exec);
+            m->exec = nullptr;
+        }
+    });
+}
+ouro_status ouro_b200_model_get_tensor(ouro_b200_model* m, const char* name, double* host, size_t cap,
+                                       size_t* n_out) {
+    return guarded([&] {
+        require(m && name, "model_get_tensor: NULL argument");
+        auto it = m->m->host.t.find(name);
+        require(it != m->m->host.t.end(), std::string("model_get_tensor: unknown tensor '") + name + "'");
+        if (n_out) *n_out = it->second.size();
+        if (host) std::memcpy(host, it->second.data(), std::min(cap, it->second.size()) * sizeof(double));
+    });
+}
+
+static ob::QuantSpec spec_from(const unsigned* bits, size_t n_refresh, double rho) {
+    ob::QuantSpec s;
+    s.wbits = bits[0];
+    s.abits = bits[1];
+    s.obits = bits[2];
+    s.n_refresh = static_cast<int>(n_refresh);
+    s.rho = rho;
+    s.validate();
+    require(s.abits <= 8, "activation bits above 8 do not fit the int8 operand");
+    require(s.wbits <= 4, "weight codes must fit the int4 range (bits <= 4)");
+    return s;
+}
+
+ouro_status ouro_b200_calib_create(ouro_b200_model* m, const unsigned* bits, size_t n_refresh, double rho, int d1,
+                                   int d2, ouro_b200_calib** out) {
+    return guarded([&] {
+        require(m && bits && out, "calib_create: NULL argument");
+        auto h = std::make_unique<ouro_b200_calib>();
+        h->c = std::make_unique<ob::Calibration>();
+        ob::Calibration& c = *h->c;
+        const ob::Dims& d = m->m->d;
+        c.spec = spec_from(bits, n_refresh, rho);
+        c.d1 = d1 != 0;
+        c.d2 = d2 != 0;
+        c.tokens = d.tokens();
+        c.embed = d.embed;
+        c.blocks = d.blocks;
+        c.ndirs = static_cast<int>(m->m->host.orders.size());
+        ob::TensorCal z;
+        z.s_in.assign(c.tokens, 1.0);
+        z.s_full.assign(c.tokens, 1.0);
+        z.excluded.assign(c.embed, 0);
+        c.scan.assign(static_cast<size_t>(c.blocks) * c.ndirs * 3, z);
+        if (c.d2) c.lin.assign(static_cast<size_t>(c.blocks) * c.nsites(), z);
+        *out = h.release();
+    });
+}
+
+ouro_status ouro_b200_calibrate(ouro_b200_model* m, const double* images_dev, size_t B, const unsigned* bits,
+                                size_t n_refresh, double rho, int d1, int d2, size_t chunk, ouro_b200_calib** out) {
+    return guarded([&] {
+        require(m && images_dev && bits && out, "calibrate: NULL argument");
+        require(B >= 1, "calibrate: need at least one image");
+        auto h = std::make_unique<ouro_b200_calib>();
+        h->c = m->m->calibrate(images_dev, static_cast<int>(B), spec_from(bits, n_refresh, rho), d1 != 0, d2 != 0,
+                               static_cast<int>(chunk));
+        *out = h.release();
+    });
+}
+void ouro_b200_calib_free(ouro_b200_calib* c) { delete c; }
+
+ouro_status ouro_b200_calib_count(ouro_b200_calib* c, int which, size_t* out) {
+    return guarded([&] {
+        require(c && out, "calib_count: NULL argument");
+        *out = which == 0 ? c->c->scan.size() : c->c->lin.size();
+    });
+}
+ouro_status ouro_b200_calib_get(ouro_b200_calib* c, int which, size_t idx, double* theta, double* s_in,
+                                double* s_full, uint8_t* excluded) {
+    return guarded([&] {
+        require(c != nullptr, "calib_get: calib is NULL");
+        auto& v = which == 0 ? c->c->scan : c->c->lin;
+        require(idx < v.size(), "calib_get: index out of range");
+        const ob::TensorCal& t = v[idx];
+        if (theta) *theta = t.theta;
+        if (s_in) std::memcpy(s_in, t.s_in.data(), t.s_in.size() * sizeof(double));
+        if (s_full) std::memcpy(s_full, t.s_full.data(), t.s_full.size() * sizeof(double));
+        if (excluded) std::memcpy(excluded, t.excluded.data(), t.excluded.size());
+    });
+}
+ouro_status ouro_b200_calib_set(ouro_b200_calib* c, int which, size_t idx, double theta, const double* s_in,
+                                const double* s_full, const uint8_t* excluded) {
+    return guarded([&] {
+        require(c != nullptr, "calib_set: calib is NULL");
+        auto& v = which == 0 ? c->c->scan : c->c->lin;
+        require(idx < v.size(), "calib_set: index out of range");
+        ob::TensorCal& t = v[idx];
+        t.theta = theta;
+        if (s_in) std::memcpy(t.s_in.data(), s_in, t.s_in.size() * sizeof(double));
+        if (s_full) std::memcpy(t.s_full.data(), s_full, t.s_full.size() * sizeof(double));
+        if (excluded) std::memcpy(t.excluded.data(), excluded, t.excluded.size());
+        c->c->dirty = true;
+    });
+}
+
+ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on) {
+    return guarded([&] {
+        require(m != nullptr, "model_use_graphs: model is NULL");
+        m->graphs = on != 0;
+        if (!m->graphs && m->exec) {
+            cudaGraphExecDestroy(m->exec);
+            m->exec = nullptr;
+        }
+    });
+}
+
+ouro_status ouro_b200_forward(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                              const double* images_dev, size_t B, double* logits_dev) {
+    return guarded([&] {
+        require(m && images_dev && logits_dev, "forward: NULL argument");
+        require(mode == ob::MODE_FP || c != nullptr, "forward: quantized modes need a calibration");
+        ob::Calibration* cal = c ? c->c.get() : nullptr;
+        cudaStream_t st = m->ctx->c->stream;
+        ouro_b200_model::GraphKey key{cal, mode, d1, d2, images_dev, B, logits_dev};
+        // graphs need a capturable stream (not the legacy default stream)
+        const bool stale = (cal && cal->dirty) || st == nullptr;
+        if (m->graphs && !stale && m->exec && m->key == key) {
+            ob::cuda_check(cudaGraphLaunch(m->exec, st), "graph launch");
+            return;
+        }
+        if (m->graphs && !stale && m->key == key && m->key_hits >= 1) {
+            // second identical call: capture the launch sequence once, replay from now on
+            cudaGraph_t g = nullptr;
+            ob::cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            try {
+                m->m->forward(cal, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev, nullptr,
+                              nullptr);
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ob::cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+            if (m->exec) cudaGraphExecDestroy(m->exec);
+            m->exec = nullptr;
+            ob::cuda_check(cudaGraphInstantiate(&m->exec, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            ob::cuda_check(cudaGraphLaunch(m->exec, st), "graph launch");
+            return;
+        }
+        m->m->forward(cal, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev, nullptr, nullptr);
+        if (m->key == key) {
+            ++m->key_hits;
+        } else {
+            m->key = key;
+            m->key_hits = 1;
+            if (m->exec) {
+                cudaGraphExecDestroy(m->exec);
+                m->exec = nullptr;
+            }
+        }
+    });
+}
+
+ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                   const double* images_host, size_t B, double* logits_host) {
+    return guarded([&] {
+        require(m && images_host && logits_host, "forward_host: NULL argument");
+        ob::Model& mm = *m->m;
+        const size_t pix = static_cast<size_t>(mm.d.image) * mm.d.image * mm.d.channels;
+        cudaStream_t st = m->ctx->c->stream;
+        mm.w.img.ensure(B * pix);
+        mm.w.logits.ensure(B * mm.d.classes);
+        ob::cuda_check(cudaMemcpyAsync(mm.w.img.p, images_host, B * pix * sizeof(double), cudaMemcpyHostToDevice, st),
+                       "H2D images");
+        ouro_status s = ouro_b200_forward(m, c, mode, d1, d2, mm.w.img.p, B, mm.w.logits.p);
+        if (s != OURO_OK) throw ob::ValidationError(g_last_error);
+        ob::cuda_check(cudaMemcpyAsync(logits_host, mm.w.logits.p, B * mm.d.classes * sizeof(double),
+                                       cudaMemcpyDeviceToHost, st),
+                       "D2H logits");
+        ob::cuda_check(cudaStreamSynchronize(st), "forward_host sync");
+    });
+}
+
+ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                const double* images_host, size_t B, size_t block, ouro_b200_trace** out) {
+    return guarded([&] {
+        require(m && images_host && out, "trace_run: NULL argument");
+        require(mode == ob::MODE_FP || c != nullptr, "trace_run: quantized modes need a calibration");
+        ob::Model& mm = *m->m;
+        require(block < static_cast<size_t>(mm.d.blocks), "trace_run: block out of range");
+        const size_t pix = static_cast<size_t>(mm.d.image) * mm.d.image * mm.d.channels;
+        cudaStream_t st = m->ctx->c->stream;
+        ob::DevBuf<double> img, logits;
+        img.upload(images_host, B * pix, st);
+        logits.ensure(B * mm.d.classes);
+        auto h = std::make_unique<ouro_b200_trace>();
+        h->sink.block = static_cast<int>(block);
+        mm.forward(c ? c->c.get() : nullptr, mode, d1 != 0, d2 != 0, img.p, static_cast<int>(B), logits.p, &h->sink,
+                   nullptr);
+        std::vector<char> lb(B * mm.d.classes * sizeof(double));
+        ob::cuda_check(cudaStreamSynchronize(st), "trace sync");
+        ob::cuda_check(cudaMemcpy(lb.data(), logits.p, lb.size(), cudaMemcpyDeviceToHost), "trace logits");
+        h->sink.blobs["logits"] = std::move(lb);
+        *out = h.release();
+    });
+}
+ouro_status ouro_b200_trace_get(ouro_b200_trace* t, const char* key, void* host, size_t cap, size_t* bytes) {
+    return guarded([&] {
+        require(t && key, "trace_get: NULL argument");
+        auto it = t->sink.blobs.find(key);
+        require(it != t->sink.blobs.end(), std::string("trace_get: no entry '") + key + "'");
+        if (bytes) *bytes = it->second.size();
+        if (host) std::memcpy(host, it->second.data(), std::min(cap, it->second.size()));
+    });
+}
+void ouro_b200_trace_free(ouro_b200_trace* t) { delete t; }
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// Host engine of the B200 quantized VMM inference path: model weights and
+// calibration tables resident in HBM, workspace sized per batch, and the
+// forward as a fixed sequence of K1/K2/K3/K4 launches on one stream (captured
+// into a CUDA graph per (batch, mode)).
+#pragma once
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace ob {
+
+// Error taxonomy of the reference (common.hpp:11-21 -> ouromamba.h:16-21).
+struct ValidationError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+inline void require(bool c, const std::string& m) {
+    if (!c) throw ValidationError(m);
+}
+void cuda_check(cudaError_t e, const char* what);
+
+struct Dims {  // ModelDims, ssm.hpp:42-56
+    int image = 32, channels = 3, patch = 4, embed = 16, state = 4, blocks = 2, classes = 10, conv_width = 3;
+    int grid() const { return image / patch; }
+    int tokens() const { return grid() * grid(); }
+    int patch_vals() const { return patch * patch * channels; }
+};
+
+struct QuantSpec {  // QuantSpec, quant.hpp:21-28
+    unsigned wbits = 4, abits = 8, obits = 8;
+    int n_refresh = 10;
+    double rho = 0.01;
+    void validate() const;
+};
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release();
+    void ensure(size_t count);  // grow-only
+    void upload(const T* host, size_t count, cudaStream_t st);
+};
+
+struct QWeight {  // one W4 quant-linear operand
+    int rows = 0, cols = 0;
+    DevBuf<int8_t> codes, codes_t;  // [rows][cols], [cols][rows]
+    DevBuf<double> scales;          // [rows]
+};
+
+class Context;
+
+struct HostModel {  // ToyVmmModel tensors in f64 (ssm.hpp:58-66)
+    Dims d;
+    std::vector<int> orders;
+    std::map<std::string, std::vector<double>> t;
+};
+HostModel make_toy_model(const Dims& d, const std::vector<int>& orders, uint64_t seed);
+
+struct TensorCal {
+    double theta = 0.0;
+    std::vector<double> s_in, s_full;
+    std::vector<uint8_t> excluded;
+};
+
+class Calibration {
+  public:
+    QuantSpec spec;
+    bool d1 = true, d2 = true;
+    int tokens = 0, embed = 0, blocks = 0, ndirs = 0;
+    std::vector<TensorCal> scan;  // [block][dir][kind]
+    std::vector<TensorCal> lin;   // [block][site]
+    int nsites() const { return ndirs + 2; }
+    // device mirror
+    DevBuf<double> dev;               // packed s_in/s_full tables
+    DevBuf<uint8_t> literal;          // [block][dir][T]
+    std::vector<int> literal_any;     // [block][dir]
+    bool dirty = true;
+    void upload(cudaStream_t st);
+    const double* s_in_dev(bool is_lin, size_t idx) const;
+    const double* s_full_dev(bool is_lin, size_t idx) const;
+};
+
+class Model {
+  public:
+    Model(Context* ctx, HostModel hm);
+    Context* ctx;
+    HostModel host;
+    Dims d;
+    // FP device weights
+    DevBuf<double> patch_w, patch_b, head_w, head_b;
+    struct DirDev {
+        DevBuf<double> a, b_delta, xp;  // xp: (E+2N) x E = w_delta | w_b | w_c
+    };
+    struct BlockDev {
+        DevBuf<double> w_inproj, conv, out_proj;  // w_inproj: 2E x E = w_in | w_gate
+        std::vector<DirDev> dirs;
+    };
+    std::vector<BlockDev> blocks;
+    // quantized weights (weight_bits); built on demand
+    unsigned qbits = 0;
+    DevBuf<double> patch_deq, head_deq;
+    struct BlockQ {
+        QWeight in, out;
+        std::vector<QWeight> xp;
+        DevBuf<double> conv_deq, in_deq, out_deq;
+        std::vector<DevBuf<double>> xp_deq;
+    };
+    std::vector<BlockQ> qblocks;
+
+    void set_tensor(const std::string& name, const double* data, size_t n);
+    void upload_fp();
+    void quantize(unsigned bits);
+    bool fp_dirty = true;
+
+    // workspace
+    struct Work {
+        int S = 0;
+        DevBuf<double> x, patches, u0, gate, u, xin, pooled, logits, img;
+        DevBuf<double> proj, o;  // per dir stacked
+        DevBuf<int8_t> codes, ocode;
+        DevBuf<double> s_row, oscale;
+        DevBuf<int> ocnt;
+        DevBuf<uint16_t> och;
+        DevBuf<uint32_t> omask;
+        DevBuf<uint8_t> scanned, masks;
+        DevBuf<unsigned long long> peaks;
+        DevBuf<int32_t> acc_in, acc_out;
+    } w;
+    void ensure_work(int S, bool trace);
+
+    struct TraceSink {
+        int block = -1;
+        std::map<std::string, std::vector<char>> blobs;
+    };
+    // Runs the whole forward on `ctx` stream; images/logits are device pointers.
+    void forward(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S, double* logits,
+                 TraceSink* trace, unsigned long long* calib_peaks);
+    std::unique_ptr<Calibration> calibrate(const double* images_dev, int S, const QuantSpec& spec, bool d1, bool d2,
+                                           int chunk);
+};
+
+class Context {
+  public:
+    explicit Context(int device);
+    ~Context();
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    void set_stream(cudaStream_t s);
+};
+
+}  // namespace ob

@@ -1,0 +1,257 @@
+// K2 — mixed-precision quant-linear: int8/int4-code inlier GEMM on the 5th-gen
+// tensor cores (tcgen05.mma kind::i8, int32 accumulators in TMEM) with the
+// hybrid epilogue of the reference fused in (gemm.cpp:181-225):
+//
+//   acc[m][r]  = sum_k x_code[m][k] * w_code[r][k]            (exact int32)
+//   y          = S_m * acc                                    gemm.cpp:207
+//   y         += (s_j * w[r][ch_j]) * xo_j   for j ascending   gemm.cpp:208-216
+//   y          = ws[r] * y                                    gemm.cpp:218-219
+//
+// then the layer's post-op (in_proj split + SiLU gate, D1 residual add, ...).
+// Orientation: the reference computes y[out][token] with activations K x C;
+// here rows are tokens (A = activation codes, M x K, K-major) and columns are
+// output features (B = weight codes, R x K, K-major), so both operands are the
+// canonical K-major UMMA layout and the output rows are the next layer's
+// token-major activations.
+//
+// Structure (persistent, one CTA per SM, 8 warps):
+//   warp 0      TMA producer: 128x128 A tile + BNx128 B tile per K-block, 128B swizzle
+//   warp 1      MMA issuer: 4 x tcgen05.mma.kind::i8 (M=128, N=BN, K=32) per K-block
+//   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulators)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b, f64 dequant + outlier terms, post-op
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100_ptx.cuh"
+
+namespace ob {
+
+constexpr int kBM = 128, kBK = 128, kStages = 4, kThreads = 256;
+
+template <int BN>
+struct K2Smem {
+    static constexpr int kABytes = kBM * kBK;
+    static constexpr int kBBytes = BN * kBK;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kBarOff = kStages * kStageBytes;
+    static constexpr int kTotal = kBarOff + 256 + 1024;  // barriers + tmem slot + alignment slack
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const QLinParams p) {
+    using L = K2Smem<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* empty = full + kStages;
+    uint64_t* acc_full = empty + kStages;
+    uint64_t* acc_empty = acc_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.R + BN - 1) / BN;
+    const int tiles = m_tiles * n_tiles;
+    const int kblocks = (p.K + kBK - 1) / kBK;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tmA);
+        ptx::tma_prefetch(&tmB);
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(full + s, 1);
+            ptx::mbar_init(empty + s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(acc_full + s, 1);
+            ptx::mbar_init(acc_empty + s, 4);  // one arrive per epilogue warp
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<2 * BN>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int m0 = (tile / n_tiles) * kBM, n0 = (tile % n_tiles) * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    ptx::mbar_wait(empty + stage, phase ^ 1);
+                    uint8_t* sa = smem + stage * L::kStageBytes;
+                    ptx::mbar_arrive_expect_tx(full + stage, L::kStageBytes);
+                    ptx::tma_load_2d(sa, &tmA, full + stage, kb * kBK, m0);
+                    ptx::tma_load_2d(sa + L::kABytes, &tmB, full + stage, kb * kBK, n0);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            constexpr uint32_t idesc = ptx::idesc_i8(kBM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+                const int buf = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ptx::mbar_wait(acc_empty + buf, aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + buf * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    ptx::mbar_wait(full + stage, phase);
+                    ptx::tc_fence_after();
+                    uint8_t* sa = smem + stage * L::kStageBytes;
+                    const uint64_t da = ptx::smem_desc_sw128(sa);
+                    const uint64_t db = ptx::smem_desc_sw128(sa + L::kABytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 32; ++k)  // K=32 bytes per MMA: +2 in 16-byte units
+                        ptx::mma_i8(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    ptx::mma_commit(empty + stage);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(acc_full + buf);
+            }
+        }
+    } else if (warp >= 4) {  // ---- epilogue
+        const int q = warp - 4;  // TMEM lane quarter this warp may access
+        int it = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+            const int buf = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            const int m0 = (tile / n_tiles) * kBM, n0 = (tile % n_tiles) * BN;
+            ptx::mbar_wait(acc_full + buf, aphase);
+            ptx::tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            const bool rv = row < p.M;
+            const double S = rv ? p.a.s_row[row] : 0.0;
+            const int cnt = rv ? p.a.ocnt[row] : 0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int r0 = n0 + c * 32;
+                if (r0 >= p.R) break;  // uniform across the warp
+                uint32_t acc[32];
+                ptx::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * BN + c * 32, acc);
+                if (!rv) continue;
+                double y[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[j] = dmul(S, static_cast<double>(static_cast<int32_t>(acc[j])));
+                int32_t aout[32];
+                const bool want_out = p.epi.acc_out != nullptr;
+                if (want_out)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) aout[j] = 0;
+                for (int o = 0; o < cnt; ++o) {
+                    const size_t oi = static_cast<size_t>(row) * p.a.cap + o;
+                    const int ch = p.a.och[oi];
+                    const int xo_i = p.a.ocode[oi];
+                    const double xo = static_cast<double>(xo_i);
+                    const double osc = p.a.oscale[oi];
+                    const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(ch) * p.R + r0);
+                    int4 w01 = __ldg(wp), w23 = __ldg(wp + 1);
+                    const int8_t* wv = reinterpret_cast<const int8_t*>(&w01);
+                    const int8_t* wv2 = reinterpret_cast<const int8_t*>(&w23);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int wq = j < 16 ? wv[j] : wv2[j - 16];
+                        const double coeff = dmul(osc, static_cast<double>(wq));
+                        y[j] = dadd(y[j], dmul(coeff, xo));
+                        if (want_out) aout[j] += wq * xo_i;
+                    }
+                }
+                const int nvalid = min(32, p.R - r0);
+                double* orow;
+                int col0;
+                if (p.epi.post == POST_INPROJ && r0 >= p.epi.split) {
+                    orow = p.epi.out2 + static_cast<size_t>(row) * p.epi.split;
+                    col0 = r0 - p.epi.split;
+                } else {
+                    orow = p.epi.out + static_cast<size_t>(row) * p.epi.ld_out;
+                    col0 = r0;
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < nvalid) {
+                        double v = dmul(__ldg(p.ws + r0 + j), y[j]);
+                        if (p.epi.post == POST_INPROJ && r0 >= p.epi.split) v = silu_d(v);
+                        if (p.epi.post == POST_RESID) v = dadd(orow[col0 + j], v);
+                        orow[col0 + j] = v;
+                    }
+                }
+                if (p.epi.acc_in)
+                    for (int j = 0; j < nvalid; ++j)
+                        p.epi.acc_in[static_cast<size_t>(row) * p.R + r0 + j] = static_cast<int32_t>(acc[j]);
+                if (want_out)
+                    for (int j = 0; j < nvalid; ++j) p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(acc_empty + buf);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc<2 * BN>(tmem_base);
+}
+
+// ---- host side -------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+// 2-D int8 tensor [rows][cols] (cols contiguous), box = box_rows x 128 bytes, 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN>
+static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) {
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, p.a.codes, p.M, p.K, kBM) || !make_map(&tb, p.w, p.R, p.K, BN)) return cudaErrorInvalidValue;
+    const int smem = K2Smem<BN>::kTotal;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k2_qlinear<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
+    const int grid = tiles < num_sms ? tiles : num_sms;
+    k2_qlinear<BN><<<grid, kThreads, smem, st>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
+    if (p.M < 1 || p.R < 1 || p.K < 1 || (p.K % 16) != 0 || (p.R % 16) != 0) return cudaErrorInvalidValue;
+    if (p.epi.post == POST_INPROJ && (p.epi.split % 32) != 0) return cudaErrorInvalidValue;
+    return launch_bn<128>(p, st, num_sms);
+}
+
+}  // namespace ob

@@ -1,0 +1,148 @@
+// K4 — auxiliary kernels of the Vim forward (< 1 % of the work): the f64
+// projection GEMM used for patch embedding, the head and the FP (calibration /
+// bypass) linear layers; patch gather; causal depthwise conv; mean pool.
+// Each keeps the reference's per-output operation order so FP results match
+// the CPU reference bit-for-bit (modulo libm ulps in exp/log1p).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ob {
+
+// Y[m][r] = 0.0 + sum_{k ascending} A[m][k] * W[r][k]  (detail::mm !ta,tb;
+// tensor.cpp:373-382), 64x64 output tile per CTA, 4x4 per thread, k staged
+// through shared memory 16 at a time. Every output keeps its own sequential
+// k order, so tiling does not change a bit of the result.
+constexpr int DG_BM = 64, DG_BN = 64, DG_BK = 16;
+
+__global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
+    __shared__ double sa[DG_BK][DG_BM + 1];
+    __shared__ double sw[DG_BK][DG_BN + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int m0 = blockIdx.y * DG_BM, r0 = blockIdx.x * DG_BN;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < p.K; k0 += DG_BK) {
+        for (int idx = threadIdx.x; idx < DG_BM * DG_BK; idx += 256) {
+            const int r = idx / DG_BK, k = idx % DG_BK;
+            const int gm = m0 + r, gk = k0 + k;
+            sa[k][r] = (gm < p.M && gk < p.K) ? p.a[static_cast<size_t>(gm) * p.lda + gk] : 0.0;
+            const int gr = r0 + r;
+            sw[k][r] = (gr < p.R && gk < p.K) ? p.w[static_cast<size_t>(gr) * p.K + gk] : 0.0;
+        }
+        __syncthreads();
+        const int kk = min(DG_BK, p.K - k0);
+        for (int k = 0; k < kk; ++k) {
+            double av[4], wv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = sa[k][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wv[j] = sw[k][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = dadd(acc[i][j], dmul(av[i], wv[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty + 16 * i;
+        if (m >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = r0 + tx + 16 * j;
+            if (r >= p.R) continue;
+            double y = dadd(0.0, acc[i][j]);
+            const GemmEpi& e = p.epi;
+            switch (e.post) {
+                case POST_INPROJ:
+                    if (r >= e.split) {
+                        e.out2[static_cast<size_t>(m) * e.split + (r - e.split)] = silu_d(y);
+                        continue;
+                    }
+                    break;
+                case POST_RESID: y = dadd(e.out[static_cast<size_t>(m) * e.ld_out + r], y); break;
+                case POST_BIAS: y = dadd(y, e.bias[r]); break;
+                default: break;
+            }
+            e.out[static_cast<size_t>(m) * e.ld_out + r] = y;
+        }
+    }
+}
+
+cudaError_t launch_dgemm(const DGemmParams& p, cudaStream_t st) {
+    if (p.M < 1 || p.R < 1 || p.K < 1) return cudaErrorInvalidValue;
+    dim3 grid((p.R + DG_BN - 1) / DG_BN, (p.M + DG_BM - 1) / DG_BM);
+    k4_dgemm<<<grid, 256, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// patches[s][t][p] = img[s][gather(t,p)] with gather of ssm.cpp:72-84:
+// (grid row, grid col, patch row, patch col, channel).
+__global__ void k4_patch_gather(const double* __restrict__ img, double* __restrict__ patches, int S, int image,
+                                int channels, int patch) {
+    const int g = image / patch, L = g * g, pv = patch * patch * channels;
+    const size_t total = static_cast<size_t>(S) * L * pv;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int pidx = static_cast<int>(i % pv);
+        const size_t st = i / pv;
+        const int t = static_cast<int>(st % L);
+        const size_t s = st / L;
+        const int gr = t / g, gc = t % g;
+        const int ch = pidx % channels, pc = (pidx / channels) % patch, pr = pidx / (channels * patch);
+        const size_t src = (static_cast<size_t>(gr * patch + pr) * image + gc * patch + pc) * channels + ch;
+        patches[i] = img[s * static_cast<size_t>(image) * image * channels + src];
+    }
+}
+
+cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,
+                                cudaStream_t st) {
+    k4_patch_gather<<<1184, 256, 0, st>>>(img, patches, S, image, channels, patch);
+    return cudaGetLastError();
+}
+
+// Depthwise causal conv over tokens, ssm.cpp:200-212:
+// u[t][c] = 0.0 + sum_{k ascending, t-(W-1-k) >= 0} taps[c][k] * u0[t-(W-1-k)][c].
+__global__ void k4_conv(const double* __restrict__ u0, const double* __restrict__ taps, double* __restrict__ u,
+                        int S, int T, int E, int W) {
+    const size_t total = static_cast<size_t>(S) * T * E;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % E);
+        const int t = static_cast<int>((i / E) % T);
+        const size_t base = i - static_cast<size_t>(t) * E;  // (s, 0, c)
+        double s = 0.0;
+        for (int k = 0; k < W; ++k) {
+            const int src = t - (W - 1 - k);
+            if (src < 0) continue;
+            s = dadd(s, dmul(taps[c * W + k], u0[base + static_cast<size_t>(src) * E]));
+        }
+        u[i] = s;
+    }
+}
+
+cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, int T, int E, int W, cudaStream_t st) {
+    k4_conv<<<2368, 256, 0, st>>>(u0, taps, u, S, T, E, W);
+    return cudaGetLastError();
+}
+
+// pooled[s][i] = (sum_{t ascending} x[s][t][i]) * (1/T), ssm.cpp:266-270.
+__global__ void k4_meanpool(const double* __restrict__ x, double* __restrict__ pooled, int S, int T, int E) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (i >= E) return;
+    double acc = 0.0;
+    for (int t = 0; t < T; ++t) acc = dadd(acc, x[(static_cast<size_t>(s) * T + t) * E + i]);
+    pooled[static_cast<size_t>(s) * E + i] = dmul(acc, __ddiv_rn(1.0, static_cast<double>(T)));
+}
+
+cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st) {
+    k4_meanpool<<<dim3((E + 127) / 128, S), 128, 0, st>>>(x, pooled, S, T, E);
+    return cudaGetLastError();
+}
+
+}  // namespace ob

@@ -1,0 +1,129 @@
+// Kernel parameter blocks and launchers (host/device shared, internal to the
+// library; the public boundary is include/ouro_b200.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ob {
+
+enum Mode { MODE_FP = 0, MODE_DYNAMIC = 1, MODE_STATIC = 2 };  // quant.hpp:101 (FP == bypass)
+enum K1Src { K1_SRC_PLAIN = 0, K1_SRC_RMSNORM = 1, K1_SRC_MERGE = 2 };
+
+// Calibration of one activation tensor (TensorCalib, quant.hpp:36-42), device side.
+struct SiteCal {
+    double theta = 0.0;
+    const double* s_in = nullptr;    // [T]
+    const double* s_full = nullptr;  // [T]
+};
+
+// Quantized activation operand of one quant-linear call: row m = (sample, step).
+struct QAct {
+    int8_t* codes = nullptr;      // [M][E] inlier codes, 0 at outlier positions
+    double* s_row = nullptr;      // [M] inlier scale of the row's plane (S^I(t) or S_full(t))
+    int* ocnt = nullptr;          // [M] |O(t)|
+    uint16_t* och = nullptr;      // [M][cap] outlier channels, ascending
+    int8_t* ocode = nullptr;      // [M][cap] outlier codes (o_bits)
+    double* oscale = nullptr;     // [M][cap] per-channel outlier scales
+    int cap = 0;
+};
+
+struct K1Params {
+    int S = 0, T = 0, E = 0;      // sequences (samples), steps, channels
+    int src = K1_SRC_PLAIN;
+    const double* x = nullptr;    // [S][T][E] canonical rows (PLAIN/RMSNORM) or o_dir0 (MERGE)
+    const double* x2 = nullptr;   // o_dir1 (MERGE), may be null
+    const double* gate = nullptr; // (MERGE)
+    int order = -1, grid = 0;     // step t reads canonical row scan_perm(order, t); -1 = identity
+    int mode = MODE_DYNAMIC, n_refresh = 10, abits = 8, obits = 8, window = 10;
+    SiteCal cal;
+    // quantized outputs (rows in step order, row = s*T + t)
+    int8_t* codes = nullptr;
+    double* s_row = nullptr;
+    int* ocnt = nullptr;
+    uint16_t* och = nullptr;
+    int8_t* ocode = nullptr;
+    double* oscale = nullptr;
+    int cap = 0;
+    uint32_t* omask = nullptr;    // optional [S*T][ceil(E/32)]
+    uint8_t* scanned = nullptr;   // optional [S*T]
+    // FP mode outputs
+    double* xout = nullptr;                 // [S*T][E] materialized input rows
+    unsigned long long* peaks = nullptr;    // [T][E] running max |x| (f64 bits), calibration
+};
+cudaError_t launch_k1(const K1Params& p, cudaStream_t st);
+
+// Post-ops fused into the quant-linear / f64 GEMM epilogues.
+enum PostOp {
+    POST_STORE = 0,    // out[m][r] = y
+    POST_INPROJ = 1,   // r <  E: u0[m][r] = y ; r >= E: gate[m][r-E] = silu(y)   (ssm.cpp:196-198)
+    POST_RESID = 2,    // out[m][r] += y   (D1 residual)
+    POST_BIAS = 3,     // out[m][r] = y + bias[r]  (patch embed / head, ssm.cpp:254-256, 271-274)
+};
+
+struct GemmEpi {
+    int post = POST_STORE;
+    double* out = nullptr;        // [M][ld_out]
+    int ld_out = 0;
+    double* out2 = nullptr;       // gate for POST_INPROJ, [M][E]
+    int split = 0;                // E for POST_INPROJ
+    const double* bias = nullptr; // POST_BIAS
+    int32_t* acc_in = nullptr;    // optional [M][R] (parity)
+    int32_t* acc_out = nullptr;   // optional [M][R] (parity)
+};
+
+// K2: hybrid quant-linear, Y[m][r] = ws[r]*(S_m*acc[m][r] + sum_j (s_j*w[r][ch_j])*xo_j)
+// (gemm.cpp:181-225) with the int8 inlier GEMM on tcgen05 kind::i8.
+struct QLinParams {
+    int M = 0, R = 0, K = 0;
+    QAct a;                        // activation codes, row-major [M][K]
+    const int8_t* w = nullptr;     // [R][K] weight codes (K-major), |code| <= 7
+    const int8_t* wt = nullptr;    // [K][R] transposed codes for the outlier gather
+    const double* ws = nullptr;    // [R] weight row scales
+    GemmEpi epi;
+};
+cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms);
+
+// f64 GEMM with the reference's per-output k-ascending sum (detail::mm,
+// tensor.cpp:373-382): Y[m][r] = 0.0 + sum_k A[m][k] * W[r][k].
+struct DGemmParams {
+    int M = 0, R = 0, K = 0;
+    const double* a = nullptr;   // [M][lda]
+    int lda = 0;
+    const double* w = nullptr;   // [R][K]
+    GemmEpi epi;
+};
+cudaError_t launch_dgemm(const DGemmParams& p, cudaStream_t st);
+
+// K3: selective scan with the QuantHook policy.
+struct ScanKindCal {
+    double theta = 0.0;
+    const double* s_in = nullptr;
+    const double* s_full = nullptr;
+    unsigned long long* peaks = nullptr;  // calibration recording [T][E] (FP mode)
+};
+struct ScanParams {
+    int S = 0, T = 0, E = 0, N = 0;
+    int order = 0, grid = 0;          // scan order of this direction
+    const double* u = nullptr;        // [S][T][E] canonical scan input (conv output)
+    const double* proj = nullptr;     // [S][T][E+2N] x_proj output rows in scan order (dpre | B | C)
+    const double* a = nullptr;        // [E][N] continuous state matrix
+    const double* b_delta = nullptr;  // [E]
+    double* o = nullptr;              // [S][T][E] scan output at canonical positions
+    int mode = MODE_DYNAMIC, n_refresh = 10, abits = 8, obits = 8;
+    ScanKindCal cal[3];               // a_bar, b_bar, h
+    const uint8_t* literal = nullptr; // [T] (device) 1 where the channel-local detector shortcut is not exact
+    int literal_any = 0;              // host summary of `literal`
+    int force_literal = 0;
+    uint8_t* masks = nullptr;         // optional [3][S][T][E] O(t) after detection (parity)
+};
+cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
+
+// K4 auxiliaries.
+cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,
+                                cudaStream_t st);
+cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, int T, int E, int W,
+                        cudaStream_t st);
+cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st);
+
+}  // namespace ob

@@ -1,0 +1,324 @@
+"""Host-side objects over the C ABI: Context (device + stream), Model (weights
+resident in HBM), Calibration (CalibrationResult + D2 sites) and the operator
+entry points (K1 detect/quantize, K2 quant-linear, K3 quantized scan, f64
+projection). Device buffers are torch CUDA tensors; only their pointers cross
+the boundary.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _ptr(t):
+    """Raw pointer of a torch tensor / numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        assert t.flags.c_contiguous
+        return t.ctypes.data_as(C.c_void_p)
+    assert t.is_contiguous(), "tensors crossing the C ABI must be contiguous"
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Dims:
+    """ModelDims (ssm.hpp:42-56)."""
+    image: int = 224
+    channels: int = 3
+    patch: int = 16
+    embed: int = 768
+    state: int = 16
+    blocks: int = 24
+    classes: int = 1000
+    conv_width: int = 4
+
+    @property
+    def grid(self) -> int:
+        return self.image // self.patch
+
+    @property
+    def tokens(self) -> int:
+        return self.grid * self.grid
+
+    @property
+    def pix(self) -> int:
+        return self.image * self.image * self.channels
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.image, self.channels, self.patch, self.embed, self.state, self.blocks, self.classes,
+                         self.conv_width], dtype=np.uint64)
+
+
+VIM_T = Dims(embed=192)
+VIM_S = Dims(embed=384)
+VIM_B = Dims(embed=768)
+
+
+@dataclass
+class QuantSpec:
+    """QuantSpec (quant.hpp:21-28) + the two declared extensions."""
+    wbits: int = 4
+    abits: int = 8
+    obits: int = 8
+    n_refresh: int = 10
+    rho: float = 0.01
+    d1: bool = True
+    d2: bool = True
+
+    def bits(self) -> np.ndarray:
+        return np.array([self.wbits, self.abits, self.obits], dtype=np.uint32)
+
+
+@dataclass
+class TensorCal:
+    theta: float
+    s_in: np.ndarray
+    s_full: np.ndarray
+    excluded: np.ndarray
+
+
+class Context:
+    """One device + one stream (ouro_b200_ctx)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        """Bind to `stream` (torch.cuda.Stream / raw handle); default: torch's
+        current stream, so operator calls are ordered with the torch ops that
+        allocate and fill their buffers."""
+        self.lib = L.load()
+        h = C.c_void_p()
+        L.check(self.lib.ouro_b200_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(device)
+        self.set_stream(stream)
+
+    def __del__(self):
+        try:
+            self.lib.ouro_b200_ctx_free(self.h)
+        except Exception:
+            pass
+
+    def set_stream(self, stream) -> None:
+        """Run on a caller stream (torch.cuda.Stream or raw handle)."""
+        raw = getattr(stream, "cuda_stream", stream)
+        L.check(self.lib.ouro_b200_ctx_set_stream(self.h, C.c_void_p(raw)))
+
+    def synchronize(self) -> None:
+        L.check(self.lib.ouro_b200_ctx_synchronize(self.h))
+
+    @property
+    def num_sms(self) -> int:
+        v = C.c_int()
+        L.check(self.lib.ouro_b200_ctx_num_sms(self.h, C.byref(v)))
+        return v.value
+
+    # ---- operators (device tensors) --------------------------------------------
+    def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
+                        mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, out=None,
+                        omask=None, scanned=None):
+        """K1 over S x T planes. Returns dict of device tensors (codes, s_row, ocnt, och, ocode, oscale)."""
+        import torch
+        dev = x.device
+        rows = S * T
+        o = out or {}
+        codes = o.get("codes") if o.get("codes") is not None else torch.empty(rows, E, dtype=torch.int8, device=dev)
+        s_row = o.get("s_row") if o.get("s_row") is not None else torch.empty(rows, dtype=torch.float64, device=dev)
+        ocnt = o.get("ocnt") if o.get("ocnt") is not None else torch.empty(rows, dtype=torch.int32, device=dev)
+        och = o.get("och") if o.get("och") is not None else torch.empty(rows, E, dtype=torch.int16, device=dev)
+        ocode = o.get("ocode") if o.get("ocode") is not None else torch.empty(rows, E, dtype=torch.int8, device=dev)
+        oscale = o.get("oscale") if o.get("oscale") is not None else torch.empty(rows, E, dtype=torch.float64,
+                                                                                  device=dev)
+        L.check(self.lib.ouro_b200_detect_quantize(
+            self.h, _ptr(x), _ptr(x2), _ptr(gate), S, T, E, src, order, grid, float(theta), _ptr(s_in), _ptr(s_full),
+            n_refresh, act_bits, outlier_bits, mode, _ptr(codes), _ptr(s_row), _ptr(ocnt), _ptr(och), _ptr(ocode),
+            _ptr(oscale), E, _ptr(omask), _ptr(scanned)))
+        return dict(codes=codes, s_row=s_row, ocnt=ocnt, och=och, ocode=ocode, oscale=oscale)
+
+    def quant_linear(self, act: dict, w, wt, ws, *, post=L.POST_STORE, out=None, out2=None, split=0, acc_in=None,
+                     acc_out=None):
+        """K2: hybrid quant-linear over K1's operand dict; returns `out`."""
+        import torch
+        M, K = act["codes"].shape
+        R = w.shape[0]
+        if out is None:
+            out = torch.empty(M, R, dtype=torch.float64, device=w.device)
+        ld = out.shape[1]
+        L.check(self.lib.ouro_b200_quant_linear(
+            self.h, M, R, K, _ptr(act["codes"]), _ptr(act["s_row"]), _ptr(act["ocnt"]), _ptr(act["och"]),
+            _ptr(act["ocode"]), _ptr(act["oscale"]), act["codes"].shape[1], _ptr(w), _ptr(wt), _ptr(ws), post,
+            _ptr(out), ld, _ptr(out2), split, None, _ptr(acc_in), _ptr(acc_out)))
+        return out
+
+    def quant_scan(self, *, S, T, E, order, grid, u, proj, a, b_delta, o, mode, n_refresh=10, act_bits=8,
+                   outlier_bits=8, theta=None, s_in=None, s_full=None, literal=None, force_literal=False,
+                   masks=None):
+        """K3 for one direction. theta: 3 floats; s_in/s_full: 3 device tensors each."""
+        th = (C.c_double * 3)(*(theta or (0.0, 0.0, 0.0)))
+        si = (C.c_void_p * 3)(*[t.data_ptr() for t in s_in]) if s_in is not None else None
+        sf = (C.c_void_p * 3)(*[t.data_ptr() for t in s_full]) if s_full is not None else None
+        L.check(self.lib.ouro_b200_quant_scan(
+            self.h, S, T, E, 16, order, grid, _ptr(u), _ptr(proj), _ptr(a), _ptr(b_delta), _ptr(o), mode, n_refresh,
+            act_bits, outlier_bits, th if theta is not None else None, si, sf, _ptr(literal), int(force_literal),
+            _ptr(masks)))
+        return o
+
+    def dgemm(self, a, w, *, post=L.POST_STORE, out=None, out2=None, split=0, bias=None):
+        import torch
+        M, K = a.shape
+        R = w.shape[0]
+        if out is None:
+            out = torch.empty(M, R, dtype=torch.float64, device=a.device)
+        L.check(self.lib.ouro_b200_dgemm(self.h, M, R, K, _ptr(a), a.stride(0), _ptr(w), post, _ptr(out),
+                                         out.shape[1], _ptr(out2), split, _ptr(bias)))
+        return out
+
+
+class Calibration:
+    """CalibrationResult (quant.hpp:44-49): scan tensors [block][dir][kind]
+    plus (D2) linear-input sites [block][site]."""
+
+    def __init__(self, model: "Model", h, spec: QuantSpec):
+        self.model, self.h, self.spec = model, h, spec
+        self.lib = model.lib
+
+    def __del__(self):
+        try:
+            self.lib.ouro_b200_calib_free(self.h)
+        except Exception:
+            pass
+
+    def count(self, which: int) -> int:
+        n = C.c_size_t()
+        L.check(self.lib.ouro_b200_calib_count(self.h, which, C.byref(n)))
+        return n.value
+
+    def get(self, which: int, idx: int) -> TensorCal:
+        d = self.model.dims
+        th = C.c_double()
+        si = np.empty(d.tokens, np.float64)
+        sf = np.empty(d.tokens, np.float64)
+        ex = np.empty(d.embed, np.uint8)
+        L.check(self.lib.ouro_b200_calib_get(self.h, which, idx, C.byref(th), _ptr(si), _ptr(sf), _ptr(ex)))
+        return TensorCal(th.value, si, sf, ex)
+
+    def set(self, which: int, idx: int, tc: TensorCal) -> None:
+        L.check(self.lib.ouro_b200_calib_set(self.h, which, idx, float(tc.theta),
+                                             _ptr(np.ascontiguousarray(tc.s_in, np.float64)),
+                                             _ptr(np.ascontiguousarray(tc.s_full, np.float64)),
+                                             _ptr(np.ascontiguousarray(tc.excluded, np.uint8))))
+
+    def export(self):
+        return ([self.get(0, i) for i in range(self.count(0))], [self.get(1, i) for i in range(self.count(1))])
+
+
+class Trace:
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        try:
+            self.lib.ouro_b200_trace_free(self.h)
+        except Exception:
+            pass
+
+    def get(self, key: str, dtype) -> np.ndarray:
+        n = C.c_size_t()
+        L.check(self.lib.ouro_b200_trace_get(self.h, key.encode(), None, 0, C.byref(n)))
+        out = np.empty(n.value // np.dtype(dtype).itemsize, dtype)
+        L.check(self.lib.ouro_b200_trace_get(self.h, key.encode(), _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def has(self, key: str) -> bool:
+        n = C.c_size_t()
+        return self.lib.ouro_b200_trace_get(self.h, key.encode(), None, 0, C.byref(n)) == 0
+
+
+class Model:
+    """Toy Vim model (ToyVmmModel, ssm.hpp:58-66) resident on one B200."""
+
+    def __init__(self, ctx: Context, dims: Dims, seed: int, orders=(0, 1)):
+        self.ctx, self.lib, self.dims, self.orders = ctx, ctx.lib, dims, tuple(orders)
+        h = C.c_void_p()
+        o = np.array(orders, dtype=np.int32)
+        L.check(self.lib.ouro_b200_model_create(ctx.h, _ptr(dims.as_array()), _ptr(o), len(orders), seed,
+                                                C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.lib.ouro_b200_model_free(self.h)
+        except Exception:
+            pass
+
+    def set_tensor(self, name: str, v: np.ndarray) -> None:
+        v = np.ascontiguousarray(v, np.float64).ravel()
+        L.check(self.lib.ouro_b200_model_set_tensor(self.h, name.encode(), _ptr(v), v.size))
+
+    def get_tensor(self, name: str) -> np.ndarray:
+        n = C.c_size_t()
+        L.check(self.lib.ouro_b200_model_get_tensor(self.h, name.encode(), None, 0, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        L.check(self.lib.ouro_b200_model_get_tensor(self.h, name.encode(), _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def new_calibration(self, spec: QuantSpec) -> Calibration:
+        h = C.c_void_p()
+        L.check(self.lib.ouro_b200_calib_create(self.h, _ptr(spec.bits()), spec.n_refresh, spec.rho, int(spec.d1),
+                                                int(spec.d2), C.byref(h)))
+        return Calibration(self, h, spec)
+
+    def calibration_from(self, scan, lin, spec: QuantSpec) -> Calibration:
+        cal = self.new_calibration(spec)
+        for i, t in enumerate(scan):
+            cal.set(0, i, t)
+        for i, t in enumerate(lin):
+            cal.set(1, i, t)
+        return cal
+
+    def calibrate(self, images, spec: QuantSpec, chunk: int = 0) -> Calibration:
+        """calibrate (quant.cpp:129-177) on the GPU; images: device f64 tensor [B, H, W, C]."""
+        h = C.c_void_p()
+        B = images.numel() // self.dims.pix
+        L.check(self.lib.ouro_b200_calibrate(self.h, _ptr(images), B, _ptr(spec.bits()), spec.n_refresh, spec.rho,
+                                             int(spec.d1), int(spec.d2), chunk, C.byref(h)))
+        return Calibration(self, h, spec)
+
+    def use_graphs(self, on: bool = True) -> None:
+        L.check(self.lib.ouro_b200_model_use_graphs(self.h, int(on)))
+
+    def forward(self, images, calib: Calibration | None, mode: int, *, d1=True, d2=True, logits=None):
+        """Device forward: images f64 CUDA tensor [B, H, W, C] -> logits f64 [B, classes] (async)."""
+        import torch
+        B = images.numel() // self.dims.pix
+        if logits is None:
+            logits = torch.empty(B, self.dims.classes, dtype=torch.float64, device=images.device)
+        L.check(self.lib.ouro_b200_forward(self.h, calib.h if calib else None, mode, int(d1), int(d2),
+                                           _ptr(images), B, _ptr(logits)))
+        return logits
+
+    def forward_host(self, images: np.ndarray, calib: Calibration | None, mode: int, *, d1=True, d2=True,
+                     logits: np.ndarray | None = None) -> np.ndarray:
+        """End-to-end call with host buffers (H2D + forward + D2H inside)."""
+        images = np.ascontiguousarray(images, np.float64)
+        B = images.size // self.dims.pix
+        if logits is None:
+            logits = np.empty((B, self.dims.classes), np.float64)
+        L.check(self.lib.ouro_b200_forward_host(self.h, calib.h if calib else None, mode, int(d1), int(d2),
+                                                _ptr(images), B, _ptr(logits)))
+        return logits
+
+    def trace(self, images: np.ndarray, calib: Calibration | None, mode: int, block: int, *, d1=True,
+              d2=True) -> Trace:
+        images = np.ascontiguousarray(images, np.float64)
+        B = images.size // self.dims.pix
+        h = C.c_void_p()
+        L.check(self.lib.ouro_b200_trace_run(self.h, calib.h if calib else None, mode, int(d1), int(d2),
+                                             _ptr(images), B, block, C.byref(h)))
+        return Trace(self.lib, h)

@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a path against the CPU oracle (oracle/, pinned to the
+reference build) on identical seeded inputs.
+
+Bar (north star): bit-exact outlier masks, quantized codes and int32
+accumulators; f64 floating outputs within 1e-9 relative (libm exp/log1p on
+the GPU differ from glibc by <= 1 ulp, nothing else differs).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DIMS = dict(image=32, channels=3, patch=8, embed=64, state=16, blocks=2, classes=10, conv_width=4)
+SEED = 1234
+B = 3
+RTOL_F64 = 1e-9
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def pair(oracle_checker, gpu_ctx):
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    od = O.Dims(**DIMS)
+    om = oracle_checker.model(od, SEED)
+    gm = ob.Model(gpu_ctx, ob.Dims(**DIMS), SEED)
+    imgs = oracle_checker.normal(99, B * od.pix).reshape(B, od.image, od.image, od.channels)
+    cimgs = oracle_checker.normal(7, 4 * od.pix).reshape(4, od.image, od.image, od.channels)
+    return om, gm, imgs, cimgs
+
+
+def test_seeded_weights_identical(pair):
+    om, gm, _, _ = pair
+    for name in om.tensor_names():
+        assert np.array_equal(om.get(name), gm.get_tensor(name)), name
+
+
+@pytest.mark.parametrize("d1", [True, False])
+def test_fp_forward_matches_oracle(pair, d1):
+    om, gm, imgs, _ = pair
+    want = om.forward(imgs, None, 0, d1=d1, d2=True)
+    got = gm.forward_host(imgs, None, 0, d1=d1, d2=True)
+    assert rel_err(got, want) <= RTOL_F64
+
+
+def _spec(abits, n_refresh=3, rho=0.05, d1=True, d2=True):
+    from oracle import oracle as O
+    return O.Spec(wbits=4, abits=abits, obits=8, n_refresh=n_refresh, rho=rho, d1=d1, d2=d2)
+
+
+def _gspec(s):
+    import paper_2503_10959_b200 as ob
+    return ob.QuantSpec(s.wbits, s.abits, s.obits, s.n_refresh, s.rho, s.d1, s.d2)
+
+
+@pytest.mark.parametrize("abits", [4, 8])
+def test_gpu_calibration_matches_oracle(pair, abits):
+    import torch
+    om, gm, _, cimgs = pair
+    spec = _spec(abits)
+    want = om.calibrate(cimgs, spec).export()
+    got_scan, got_lin = gm.calibrate(torch.from_numpy(cimgs).cuda(), _gspec(spec)).export()
+    assert len(got_scan) == len(want.scan) and len(got_lin) == len(want.lin)
+    for g, w in zip(got_scan + got_lin, want.scan + want.lin):
+        assert abs(g.theta - w.theta) <= RTOL_F64 * abs(w.theta)
+        assert rel_err(g.s_in, w.s_in) <= RTOL_F64
+        assert rel_err(g.s_full, w.s_full) <= RTOL_F64
+        assert np.array_equal(g.excluded, w.excluded)
+
+
+def _import_calib(gm, cal, spec):
+    import paper_2503_10959_b200 as ob
+    conv = lambda t: ob.TensorCal(t.theta, t.s_in, t.s_full, t.excluded)
+    return gm.calibration_from([conv(t) for t in cal.scan], [conv(t) for t in cal.lin], _gspec(spec))
+
+
+@pytest.mark.parametrize("abits,mode,d2", [(4, 1, True), (8, 1, True), (4, 2, True), (4, 1, False), (8, 2, False)])
+def test_quantized_forward_logits(pair, abits, mode, d2):
+    om, gm, imgs, cimgs = pair
+    spec = _spec(abits, d2=d2)
+    ocal = om.calibrate(cimgs, spec)
+    gcal = _import_calib(gm, ocal.export(), spec)
+    want = om.forward(imgs, ocal, mode, d1=True, d2=d2)
+    got = gm.forward_host(imgs, gcal, mode, d1=True, d2=d2)
+    assert rel_err(got, want) <= RTOL_F64, (got, want)
+
+
+@pytest.mark.parametrize("abits", [4, 8])
+def test_block_trace_bit_exact(pair, abits):
+    """Per-block intermediates of sample-level traces: codes, outlier lists,
+    masks and accumulators bit-exact; f64 tensors within tolerance."""
+    from oracle import oracle as O
+    om, gm, imgs, cimgs = pair
+    spec = _spec(abits, rho=0.1)
+    ocal = om.calibrate(cimgs, spec)
+    gcal = _import_calib(gm, ocal.export(), spec)
+    d = om.dims
+    L, E, N = d.tokens, d.embed, d.state
+    nd = 2
+    blk = 1
+    gt = gm.trace(imgs, gcal, 1, blk)
+    n_out_total = 0
+    for s in range(B):
+        ot = om.trace(imgs[s], ocal, 1, blk)
+        rows = slice(s * L, (s + 1) * L)
+        for key in ("x_in", "u0", "gate", "u", "x_out"):
+            g = gt.get(key, np.float64).reshape(B * L, E)[rows]
+            assert rel_err(g, ot.get(key).reshape(L, E)) <= RTOL_F64, key
+        for site, R in ((0, 2 * E), (1, E + 2 * N), (2, E + 2 * N), (3, E)):
+            p = f"lin{site}."
+            g_codes = gt.get(p + "codes", np.int8).reshape(B * L, E)[rows]
+            assert np.array_equal(g_codes, ot.get(p + "codes").reshape(L, E)), p + "codes"
+            g_cnt = gt.get(p + "ocnt", np.int32)[rows]
+            g_och = gt.get(p + "och", np.uint16).reshape(B * L, E)[rows]
+            g_ocode = gt.get(p + "ocode", np.int8).reshape(B * L, E)[rows]
+            g_osc = gt.get(p + "oscale", np.float64).reshape(B * L, E)[rows]
+            o_mask = ot.get(p + "omask").reshape(L, E)
+            o_ocode = ot.get(p + "ocode").reshape(L, E)
+            o_osc = ot.get(p + "oscale").reshape(L, E)
+            for t in range(L):
+                chans = np.nonzero(o_mask[t])[0]
+                assert g_cnt[t] == len(chans), (p, t)
+                assert np.array_equal(g_och[t, :len(chans)], chans), (p, t)
+                assert np.array_equal(g_ocode[t, :len(chans)], o_ocode[t, chans]), (p, t)
+                assert np.array_equal(g_osc[t, :len(chans)], o_osc[t, chans]), (p, t)
+                n_out_total += len(chans)
+            g_mask_bits = gt.get(p + "omask", np.uint32).reshape(B * L, -1)[rows]
+            unpacked = ((g_mask_bits[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(L, -1)[:, :E]
+            assert np.array_equal(unpacked.astype(np.uint8), o_mask), p + "omask"
+            assert np.array_equal(gt.get(p + "scanned", np.uint8)[rows], ot.get(p + "scanned")), p + "scanned"
+            assert np.array_equal(gt.get(p + "acc_in", np.int32).reshape(B * L, R)[rows],
+                                  ot.get(p + "acc_in").reshape(L, R)), p + "acc_in"
+            assert np.array_equal(gt.get(p + "acc_out", np.int32).reshape(B * L, R)[rows],
+                                  ot.get(p + "acc_out").reshape(L, R)), p + "acc_out"
+        for dd in range(nd):
+            perm = np.array([_perm(dd, t, d.grid) for t in range(L)])
+            g_proj = gt.get(f"dir{dd}.proj", np.float64).reshape(B * L, E + 2 * N)[rows]
+            assert rel_err(g_proj, ot.get(f"lin{1 + dd}.out").reshape(L, E + 2 * N)) <= RTOL_F64
+            g_o = gt.get(f"dir{dd}.o", np.float64).reshape(B * L, E)[rows]
+            o_o = ot.get(f"dir{dd}.o").reshape(L, E)
+            assert rel_err(g_o[perm], o_o) <= RTOL_F64, f"dir{dd}.o"
+            g_m = gt.get(f"dir{dd}.masks", np.uint8).reshape(3, B, L, E)
+            for k in range(3):
+                assert np.array_equal(g_m[k, s], ot.get(f"dir{dd}.mask{k}").reshape(L, E)), (dd, k)
+    assert n_out_total > 0, "the fixture must exercise the outlier path"
+
+
+def _perm(order, t, g):
+    m = g * g
+    fast, slow = t % g, t // g
+    return [slow * g + fast, m - 1 - (slow * g + fast), fast * g + slow, m - 1 - (fast * g + slow)][order]
+
+
+def test_literal_scan_equals_channel_local(pair, gpu_ctx):
+    """The literal detector (cross-channel max, quant.cpp:313-335) and the
+    channel-local form agree wherever C(t) holds."""
+    import torch
+    import paper_2503_10959_b200 as ob
+    om, gm, imgs, cimgs = pair
+    spec = _spec(4, rho=0.1)
+    ocal = om.calibrate(cimgs, spec).export()
+    d = om.dims
+    L, E, N = d.tokens, d.embed, d.state
+    S = 2
+    g = torch.Generator().manual_seed(5)
+    u = torch.randn(S, L, E, dtype=torch.float64, generator=g).cuda()
+    proj = (0.5 * torch.randn(S, L, E + 2 * N, dtype=torch.float64, generator=g)).cuda()
+    a = torch.from_numpy(om.get("block0.dir0.a")).cuda()
+    bd = torch.zeros(E, dtype=torch.float64).cuda()
+    tc = [ocal.scan[k] for k in range(3)]
+    s_in = [torch.from_numpy(t.s_in).cuda() for t in tc]
+    s_full = [torch.from_numpy(t.s_full).cuda() for t in tc]
+    outs = []
+    for force in (False, True):
+        o = torch.zeros(S, L, E, dtype=torch.float64, device="cuda")
+        masks = torch.zeros(3, S, L, E, dtype=torch.uint8, device="cuda")
+        gpu_ctx.quant_scan(S=S, T=L, E=E, order=1, grid=d.grid, u=u, proj=proj, a=a, b_delta=bd, o=o,
+                           mode=ob.MODE_DYNAMIC, n_refresh=3, act_bits=4, outlier_bits=8,
+                           theta=[t.theta for t in tc], s_in=s_in, s_full=s_full, force_literal=force, masks=masks)
+        outs.append((o.cpu().numpy(), masks.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
