@@ -161,6 +161,17 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
  * (calib, mode, d1, d2, images, B, logits) (1 = on). */
 ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
 
+/* One forward with CUDA events around every launch: per kernel family
+ * {K1 detect/quantize, K2 quant-linear, K3 scan, f64 projection, aux} the
+ * summed device milliseconds (ms[5]) and launch counts (launches[5]). */
+ouro_status ouro_b200_forward_profile(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                      const double* images_dev, size_t B, double* logits_dev, double* ms,
+                                      int* launches);
+
+/* Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA),
+ * the roofline denominator of the f64 scan (no vendor figure is used). */
+ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops);
+
 /* Parity harness: run a forward over host images and keep every
  * intermediate of one block (keys documented in DESIGN.md §5). */
 ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,

@@ -450,6 +450,38 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
     });
 }
 
+ouro_status ouro_b200_forward_profile(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                      const double* images_dev, size_t B, double* logits_dev, double* ms,
+                                      int* launches) {
+    return guarded([&] {
+        require(m && images_dev && logits_dev && ms && launches, "forward_profile: NULL argument");
+        require(mode == ob::MODE_FP || c != nullptr, "forward_profile: quantized modes need a calibration");
+        ob::Model& mm = *m->m;
+        mm.timing = ob::Model::Timing{};
+        mm.timing.on = true;
+        try {
+            mm.forward(c ? c->c.get() : nullptr, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev,
+                       nullptr, nullptr);
+        } catch (...) {
+            mm.timing.on = false;
+            throw;
+        }
+        mm.timing_collect();
+        mm.timing.on = false;
+        for (int i = 0; i < ob::Model::FAM_COUNT; ++i) {
+            ms[i] = mm.timing.ms[i];
+            launches[i] = mm.timing.launches[i];
+        }
+    });
+}
+
+ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops) {
+    return guarded([&] {
+        require(ctx && tflops, "measure_fp64_peak: NULL argument");
+        *tflops = ob::measure_fp64_peak(ctx->c->stream, ctx->c->num_sms);
+    });
+}
+
 ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
                                 const double* images_host, size_t B, size_t block, ouro_b200_trace** out) {
     return guarded([&] {

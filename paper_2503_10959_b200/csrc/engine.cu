@@ -373,7 +373,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
     auto tb = [&](int b) { return tr_on && trace->block == b; };
 
     // patch embed: x = patches . W^T + b (ssm.cpp:253-256), FP or W4-dequantized weights
+    tick_begin(FAM_AUX);
     cuda_check(launch_patch_gather(images, w.patches.p, S, d.image, d.channels, d.patch, st), "patch gather");
+    tick_end(FAM_AUX);
     {
         DGemmParams g;
         g.M = static_cast<int>(rows);
@@ -386,7 +388,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         g.epi.out = w.x.p;
         g.epi.ld_out = E;
         g.epi.bias = patch_b.p;
+        tick_begin(FAM_DGEMM);
         cuda_check(launch_dgemm(g, st), "patch embed");
+        tick_end(FAM_DGEMM);
     }
     if (tr_on) grab(trace, "x_embed", w.x.p, rows * E, st);
 
@@ -467,7 +471,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             q.wt = qw->codes_t.p;
             q.ws = qw->scales.p;
             q.epi = epi;
+            tick_begin(FAM_K2);
             cuda_check(launch_qlinear(q, st, ctx->num_sms), "quant linear");
+            tick_end(FAM_K2);
         } else {
             DGemmParams g;
             g.M = static_cast<int>(rows);
@@ -477,7 +483,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             g.lda = E;
             g.w = wdeq_or_fp;
             g.epi = epi;
+            tick_begin(FAM_DGEMM);
             cuda_check(launch_dgemm(g, st), "f64 linear");
+            tick_end(FAM_DGEMM);
         }
     };
 
@@ -487,7 +495,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         if (tb(b)) grab(trace, "x_in", w.x.p, rows * E, st);
         // in_proj input: RMSNorm(x) (D1) or x
         K1Params k = k1_base(d1 ? K1_SRC_RMSNORM : K1_SRC_PLAIN, w.x.p, -1, b, 0, true);
+        tick_begin(FAM_K1);
         cuda_check(launch_k1(k, st), "K1 in_proj");
+        tick_end(FAM_K1);
         if (tb(b) && !qlin) grab(trace, "xn", w.xin.p, rows * E, st);
         {
             GemmEpi e;
@@ -499,7 +509,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             linear(bq ? &bq->in : nullptr, quant ? bq->in_deq.p : bd.w_inproj.p, 2 * E, e, b);
             trace_lin(b, 0, 2 * E);
         }
+        tick_begin(FAM_AUX);
         cuda_check(launch_conv(w.u0.p, quant ? bq->conv_deq.p : bd.conv.p, w.u.p, S, L, E, d.conv_width, st), "conv");
+        tick_end(FAM_AUX);
         if (tb(b)) {
             grab(trace, "u0", w.u0.p, rows * E, st);
             grab(trace, "gate", w.gate.p, rows * E, st);
@@ -510,7 +522,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             double* proj = w.proj.p + static_cast<size_t>(dd) * rows * P;
             double* o = w.o.p + static_cast<size_t>(dd) * rows * E;
             K1Params kx = k1_base(K1_SRC_PLAIN, w.u.p, order, b, 1 + dd, true);
+            tick_begin(FAM_K1);
             cuda_check(launch_k1(kx, st), "K1 x_proj");
+            tick_end(FAM_K1);
             GemmEpi e;
             e.post = POST_STORE;
             e.out = proj;
@@ -549,7 +563,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
                     sp.cal[kk].peaks = calib_peaks + base + ((static_cast<size_t>(b) * nd + dd) * 3 + kk) * L * E;
             }
             bool lit = false;
+            tick_begin(FAM_K3);
             cuda_check(launch_scan(sp, st, &lit), "scan");
+            tick_end(FAM_K3);
             if (tb(b)) {
                 std::string p = "dir" + std::to_string(dd) + ".";
                 grab(trace, p + "proj", proj, rows * P, st);
@@ -561,7 +577,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         K1Params km = k1_base(K1_SRC_MERGE, w.o.p, -1, b, nsites - 1, true);
         km.x2 = nd > 1 ? w.o.p + rows * E : nullptr;
         km.gate = w.gate.p;
+        tick_begin(FAM_K1);
         cuda_check(launch_k1(km, st), "K1 out_proj");
+        tick_end(FAM_K1);
         if (tb(b) && !qlin) grab(trace, "y", w.xin.p, rows * E, st);
         {
             GemmEpi e;
@@ -573,7 +591,9 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         }
         if (tb(b)) grab(trace, "x_out", w.x.p, rows * E, st);
     }
+    tick_begin(FAM_AUX);
     cuda_check(launch_meanpool(w.x.p, w.pooled.p, S, L, E, st), "meanpool");
+    tick_end(FAM_AUX);
     {
         DGemmParams g;
         g.M = S;
@@ -586,8 +606,35 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         g.epi.out = logits;
         g.epi.ld_out = d.classes;
         g.epi.bias = head_b.p;
+        tick_begin(FAM_DGEMM);
         cuda_check(launch_dgemm(g, st), "head");
+        tick_end(FAM_DGEMM);
     }
+}
+
+void Model::tick_begin(int fam) {
+    if (!timing.on) return;
+    cudaEvent_t a, b;
+    cuda_check(cudaEventCreate(&a), "event");
+    cuda_check(cudaEventCreate(&b), "event");
+    cuda_check(cudaEventRecord(a, ctx->stream), "event record");
+    timing.ev.push_back({fam, {a, b}});
+}
+void Model::tick_end(int fam) {
+    if (!timing.on) return;
+    cuda_check(cudaEventRecord(timing.ev.back().second.second, ctx->stream), "event record");
+    timing.launches[fam] += 1;
+}
+void Model::timing_collect() {
+    cuda_check(cudaStreamSynchronize(ctx->stream), "timing sync");
+    for (auto& e : timing.ev) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, e.second.first, e.second.second), "elapsed");
+        timing.ms[e.first] += ms;
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    timing.ev.clear();
 }
 
 // calibrate (quant.cpp:129-177) on the device: FP forward with per-(tensor, t,

@@ -154,6 +154,18 @@ class Model {
     } w;
     void ensure_work(int S, bool trace);
 
+    // Per-kernel-family device time of one forward (CUDA events on the stream).
+    enum Family { FAM_K1 = 0, FAM_K2 = 1, FAM_K3 = 2, FAM_DGEMM = 3, FAM_AUX = 4, FAM_COUNT = 5 };
+    struct Timing {
+        bool on = false;
+        std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+        double ms[FAM_COUNT] = {0, 0, 0, 0, 0};
+        int launches[FAM_COUNT] = {0, 0, 0, 0, 0};
+    } timing;
+    void tick_begin(int fam);
+    void tick_end(int fam);
+    void timing_collect();
+
     struct TraceSink {
         int block = -1;
         std::map<std::string, std::vector<char>> blobs;

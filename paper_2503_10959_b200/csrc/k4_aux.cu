@@ -145,4 +145,44 @@ cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E
     return cudaGetLastError();
 }
 
+// FP64 pipe probe: 8 independent DFMA chains per thread, 4 CTAs x 256 threads
+// per SM; the result is folded into a store so nothing is dead code.
+__global__ void __launch_bounds__(256) k4_dfma_probe(double* out, int iters, double a, double b) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = threadIdx.x * 1e-3 + j;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = fma(v[j], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+    if (s == 12345.678) out[0] = s;
+}
+
+double measure_fp64_peak(cudaStream_t st, int num_sms) {
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return 0.0;
+    const int iters = 4096, blocks = num_sms * 4, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k4_dfma_probe<<<blocks, threads, 0, st>>>(out, iters, 0.999999, 1e-7);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0, st);
+        k4_dfma_probe<<<blocks, threads, 0, st>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    return flops / (best * 1e-3) / 1e12;
+}
+
 }  // namespace ob

@@ -124,6 +124,7 @@ cudaError_t launch_patch_gather(const double* img, double* patches, int S, int i
                                 cudaStream_t st);
 cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, int T, int E, int W,
                         cudaStream_t st);
+double measure_fp64_peak(cudaStream_t st, int num_sms);  // TFLOP/s (DFMA = 2 flops)
 cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st);
 
 }  // namespace ob

@@ -119,6 +119,12 @@ class Context:
         L.check(self.lib.ouro_b200_ctx_num_sms(self.h, C.byref(v)))
         return v.value
 
+    def measure_fp64_peak(self) -> float:
+        """Measured DFMA throughput of this device in TFLOP/s."""
+        v = C.c_double()
+        L.check(self.lib.ouro_b200_measure_fp64_peak(self.h, C.byref(v)))
+        return v.value
+
     # ---- operators (device tensors) --------------------------------------------
     def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
                         mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, out=None,
@@ -302,6 +308,20 @@ class Model:
         L.check(self.lib.ouro_b200_forward(self.h, calib.h if calib else None, mode, int(d1), int(d2),
                                            _ptr(images), B, _ptr(logits)))
         return logits
+
+    FAMILIES = ("k1_detect_quant", "k2_quant_linear", "k3_scan", "f64_projection", "aux")
+
+    def forward_profile(self, images, calib, mode: int, *, d1=True, d2=True, logits=None):
+        """One forward with per-kernel-family CUDA-event timing -> (logits, {family: (ms, launches)})."""
+        import torch
+        B = images.numel() // self.dims.pix
+        if logits is None:
+            logits = torch.empty(B, self.dims.classes, dtype=torch.float64, device=images.device)
+        ms = (C.c_double * 5)()
+        n = (C.c_int * 5)()
+        L.check(self.lib.ouro_b200_forward_profile(self.h, calib.h if calib else None, mode, int(d1), int(d2),
+                                                   _ptr(images), B, _ptr(logits), ms, n))
+        return logits, {f: (ms[i], n[i]) for i, f in enumerate(self.FAMILIES)}
 
     def forward_host(self, images: np.ndarray, calib: Calibration | None, mode: int, *, d1=True, d2=True,
                      logits: np.ndarray | None = None) -> np.ndarray:
