@@ -161,6 +161,11 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
  * (calib, mode, d1, d2, images, B, logits) (1 = on). */
 ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
 
+/* Engine options: "scan_variant" = 0 auto (fast K3 path wherever the
+ * channel-local detector is exact), 1 per-direction reference scan kernel,
+ * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid). */
+ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long value);
+
 /* One forward with CUDA events around every launch: per kernel family
  * {K1 detect/quantize, K2 quant-linear, K3 scan, f64 projection, aux} the
  * summed device milliseconds (ms[5]) and launch counts (launches[5]). */

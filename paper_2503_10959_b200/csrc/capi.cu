@@ -450,6 +450,23 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
     });
 }
 
+ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long value) {
+    return guarded([&] {
+        require(m && key, "model_set_option: NULL argument");
+        const std::string k(key);
+        if (k == "scan_variant") {
+            require(value >= 0 && value <= 2, "model_set_option: scan_variant must be 0, 1 or 2");
+            m->m->scan_variant = static_cast<int>(value);
+        } else {
+            throw ob::ValidationError("model_set_option: unknown option '" + k + "'");
+        }
+        if (m->exec) {
+            cudaGraphExecDestroy(m->exec);
+            m->exec = nullptr;
+        }
+    });
+}
+
 ouro_status ouro_b200_forward_profile(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
                                       const double* images_dev, size_t B, double* logits_dev, double* ms,
                                       int* launches) {

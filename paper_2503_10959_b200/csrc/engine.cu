@@ -289,7 +289,7 @@ void Model::ensure_work(int S, bool trace) {
     w.scanned.ensure(rows);
     if (trace) {
         w.omask.ensure(rows * ((E + 31) / 32));
-        w.masks.ensure(3 * rows * E);
+        w.masks.ensure(2 * 3 * rows * E);
         w.acc_in.ensure(rows * std::max(2 * E, E + 2 * N));
         w.acc_out.ensure(rows * std::max(2 * E, E + 2 * N));
     }
@@ -517,6 +517,8 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             grab(trace, "gate", w.gate.p, rows * E, st);
             grab(trace, "u", w.u.p, rows * E, st);
         }
+        ScanParams sps[2];
+        bool any_literal = false;
         for (int dd = 0; dd < nd; ++dd) {
             const int order = host.orders[dd];
             double* proj = w.proj.p + static_cast<size_t>(dd) * rows * P;
@@ -531,7 +533,8 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             e.ld_out = P;
             linear(bq ? &bq->xp[dd] : nullptr, quant ? bq->xp_deq[dd].p : bd.dirs[dd].xp.p, P, e, b);
             trace_lin(b, 1 + dd, P);
-            ScanParams sp;
+            ScanParams& sp = sps[dd];
+            sp = ScanParams{};
             sp.S = S;
             sp.T = L;
             sp.E = E;
@@ -555,25 +558,37 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
                     sp.cal[kk].s_full = cal->s_full_dev(false, si);
                 }
                 sp.literal = cal->literal.p + (static_cast<size_t>(b) * nd + dd) * L;
-                sp.literal_any = cal->literal_any[static_cast<size_t>(b) * nd + dd];
-                if (tb(b)) sp.masks = w.masks.p;
+                sp.literal_any = mode == MODE_DYNAMIC ? cal->literal_any[static_cast<size_t>(b) * nd + dd] : 0;
+                any_literal = any_literal || sp.literal_any;
+                if (tb(b)) sp.masks = w.masks.p + static_cast<size_t>(dd) * 3 * rows * E;
             } else if (calib_peaks) {
                 const size_t base = static_cast<size_t>(d.blocks) * nsites * L * E;
                 for (int kk = 0; kk < 3; ++kk)
                     sp.cal[kk].peaks = calib_peaks + base + ((static_cast<size_t>(b) * nd + dd) * 3 + kk) * L * E;
             }
-            bool lit = false;
-            tick_begin(FAM_K3);
-            cuda_check(launch_scan(sp, st, &lit), "scan");
-            tick_end(FAM_K3);
-            if (tb(b)) {
-                std::string p = "dir" + std::to_string(dd) + ".";
-                grab(trace, p + "proj", proj, rows * P, st);
-                grab(trace, p + "o", o, rows * E, st);
-                if (quant && mode == MODE_DYNAMIC) grab(trace, p + "masks", w.masks.p, 3 * rows * E, st);
-                trace->blobs[p + "literal"] = std::vector<char>(1, static_cast<char>(lit ? 1 : 0));
+        }
+        // K3: both directions in one launch on the fast path; the literal
+        // detector (or FP recording) runs the per-direction kernel.
+        bool lit = false;
+        tick_begin(FAM_K3);
+        if (quant && !any_literal && scan_variant != 1) {
+            cuda_check(launch_scan_fast(sps, nd, st, scan_variant == 2 ? 1 : 0), "scan");
+        } else {
+            for (int dd = 0; dd < nd; ++dd) {
+                bool l = false;
+                cuda_check(launch_scan(sps[dd], st, &l), "scan");
+                lit = lit || l;
             }
         }
+        tick_end(FAM_K3);
+        if (tb(b))
+            for (int dd = 0; dd < nd; ++dd) {
+                std::string p = "dir" + std::to_string(dd) + ".";
+                grab(trace, p + "proj", sps[dd].proj, rows * P, st);
+                grab(trace, p + "o", sps[dd].o, rows * E, st);
+                if (quant && mode == MODE_DYNAMIC) grab(trace, p + "masks", sps[dd].masks, 3 * rows * E, st);
+                trace->blobs[p + "literal"] = std::vector<char>(1, static_cast<char>(lit ? 1 : 0));
+            }
         K1Params km = k1_base(K1_SRC_MERGE, w.o.p, -1, b, nsites - 1, true);
         km.x2 = nd > 1 ? w.o.p + rows * E : nullptr;
         km.gate = w.gate.p;

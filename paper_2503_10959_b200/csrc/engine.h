@@ -137,6 +137,7 @@ class Model {
     void upload_fp();
     void quantize(unsigned bits);
     bool fp_dirty = true;
+    int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only
 
     // workspace
     struct Work {

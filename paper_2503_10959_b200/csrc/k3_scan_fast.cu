@@ -1,0 +1,292 @@
+// K3 fast path: quantized S6 selective scan for the dynamic / static modes
+// where the channel-local detector is exact, both scan
+// directions in one launch.
+//
+// Work split. A CTA owns 128 channels of one (sample, direction); two
+// adjacent lanes own one channel, 8 of its N = 16 states each, so a warp
+// covers 16 channels and the per-thread state (h: 8 doubles, A: 8 floats)
+// leaves room for 24 resident warps per SM. The two halves of a channel
+// exchange exactly two values per step through shuffles: the h peak (max is
+// order-free) and the running output sum — the first half computes
+// 0 + C_0 h_0 + ... + C_7 h_7 in order and the second half continues the
+// same chain with C_8 h_8 ... C_15 h_15, which is the reference's sequential
+// sum (ssm.cpp:170-174) bit-for-bit.
+//
+// Steps are processed in chunks of 8. Everything that does not depend on the
+// carried state is computed for the whole chunk first, with the chunk's steps
+// as independent instruction streams, and staged in shared memory: per step
+// B, C and the calibrated scales; per channel delta = softplus(dpre + b_delta)
+// (ssm.cpp:150-151), the exact a_bar peak exp(delta * max_m A) and u.
+//
+// Exactness of the codes (quant.cpp:29-35 in f64):
+//  * peaks: a_bar > 0, delta >= 0, so max_m a_bar = exp(fl(delta * Amax)) and
+//    max_m |b_bar| = fl(delta * max_m |B_m|) exactly (monotone rounding), which
+//    gives the detector decisions and the per-channel outlier scales;
+//  * a_bar and b_bar codes: q = x / s evaluated in f32 (ex2.approx for the
+//    exp) with a proven relative error bound; round(q) is used when q lies
+//    farther than that bound from a half-integer, otherwise the element is
+//    recomputed in f64 with the IEEE quotient (rate ~1e-4). Dequantized values
+//    are code * s in f64, exactly fake_quant_step's;
+//  * the h update, h quantization (quant_code_inv) and the output are f64 in
+//    the reference's operation order.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ob {
+
+constexpr int kCh = 128;       // channels per CTA
+constexpr int kThr = 2 * kCh;  // two threads per channel
+constexpr int kChunk = 8;      // steps staged per chunk
+
+struct ScanDirs {
+    ScanParams d[2];
+};
+
+struct StepShared {
+    double B[16], C[16];
+    double Sa, Sb, Sh, invSh, Bmax;
+    float BSf[16];  // f32(B_m) * f32(1/S_b): the inlier b_bar quotient per unit delta
+    float invSaf, invSbf;
+    int refresh, pad;
+};
+
+struct ScanSmem {
+    StepShared st[kChunk];
+    double delta[kChunk][kCh];
+    double peak_a[kChunk][kCh];
+    double u[kChunk][kCh];
+    float deltaf[kChunk][kCh];
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Small integer held in a float (|v| < 2^22) -> exact double without the
+// conversion pipe (1.5 * 2^23 places the integer in the low mantissa bits).
+__device__ __forceinline__ double small_int_to_double(float v) {
+    const int iv = __float_as_int(v + 12582912.0f) - 0x4B400000;
+    return __hiloint2double(0x43300000, static_cast<unsigned>(iv + 65536)) - (4503599627370496.0 + 65536.0);
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
+    extern __shared__ __align__(16) uint8_t scan_smem_raw[];
+    ScanSmem& sh = *reinterpret_cast<ScanSmem*>(scan_smem_raw);
+    const ScanParams& p = P.d[blockIdx.z];
+    const int s = blockIdx.y, tid = threadIdx.x, c = tid >> 1, half = tid & 1;
+    const int i = blockIdx.x * kCh + c;
+    const bool active = i < p.E;
+    const int E = p.E, T = p.T, P2 = E + 32, m0 = half * 8;
+    const unsigned lane = threadIdx.x & 31;
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
+    const float qaf = static_cast<float>(qa), qof = static_cast<float>(qo);
+
+    float A2f[8];
+    double Amax = -1e300;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const double a = active ? p.a[static_cast<size_t>(i) * 16 + m0 + m] : -1.0;
+        A2f[m] = __double2float_rn(a * 1.4426950408889634);  // log2(e)
+        Amax = fmax(Amax, a);
+    }
+    Amax = fmax(Amax, __shfl_xor_sync(0xffffffffu, Amax, 1));
+    const double bd = active ? p.b_delta[i] : 0.0;
+    double h[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) h[m] = 0.0;
+    bool inA = false, inB = false, inH = false;
+    const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
+
+    for (int t0 = 0; t0 < T; t0 += kChunk) {
+        const int nt = min(kChunk, T - t0);
+        __syncthreads();  // previous chunk consumed
+        for (int idx = tid; idx < nt * 32; idx += kThr) {  // B | C of the x_proj rows (scan order)
+            const int tt = idx >> 5, j = idx & 31;
+            const double v = p.proj[(static_cast<size_t>(s) * T + t0 + tt) * P2 + E + j];
+            if (j < 16) sh.st[tt].B[j] = v;
+            else sh.st[tt].C[j - 16] = v;
+        }
+        if (tid < nt) {
+            const int t = t0 + tid;
+            StepShared& ss = sh.st[tid];
+            const double Sa = dyn ? p.cal[0].s_in[t] : p.cal[0].s_full[t];
+            const double Sb = dyn ? p.cal[1].s_in[t] : p.cal[1].s_full[t];
+            const double Sh = dyn ? p.cal[2].s_in[t] : p.cal[2].s_full[t];
+            ss.Sa = Sa;
+            ss.Sb = Sb;
+            ss.Sh = Sh;
+            ss.invSh = __ddiv_rn(1.0, Sh);
+            ss.invSaf = __double2float_rn(__ddiv_rn(1.0, Sa));
+            ss.invSbf = __double2float_rn(__ddiv_rn(1.0, Sb));
+            ss.refresh = refresh_at(t, p.n_refresh) ? 1 : 0;
+        }
+        {  // state-independent per-channel values: this thread takes 4 of the 8 steps
+            double dp[kChunk / 2], uu[kChunk / 2];
+#pragma unroll
+            for (int j = 0; j < kChunk / 2; ++j) {
+                const int tt = half * (kChunk / 2) + j, t = t0 + tt;
+                dp[j] = 0.0;
+                uu[j] = 0.0;
+                if (tt < nt && active) {
+                    dp[j] = p.proj[(static_cast<size_t>(s) * T + t) * P2 + i];
+                    uu[j] = p.u[(static_cast<size_t>(s) * T + scan_perm(p.order, t, p.grid)) * E + i];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kChunk / 2; ++j) {
+                const int tt = half * (kChunk / 2) + j;
+                const double delta = softplus_d(dadd(dp[j], bd));
+                sh.delta[tt][c] = delta;
+                sh.deltaf[tt][c] = __double2float_rn(delta);
+                sh.peak_a[tt][c] = exp(dmul(delta, Amax));
+                sh.u[tt][c] = uu[j];
+            }
+        }
+        __syncthreads();
+        if (tid < nt * 16) {
+            const int tt = tid >> 4, m = tid & 15;
+            StepShared& ss = sh.st[tt];
+            ss.BSf[m] = __double2float_rn(ss.B[m]) * ss.invSbf;
+        } else if (tid >= 128 && tid < 128 + nt) {
+            const int tt = tid - 128;
+            double bm = 0.0;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) bm = fmax(bm, fabs(sh.st[tt].B[m]));
+            sh.st[tt].Bmax = bm;
+        }
+        __syncthreads();
+
+        for (int tt = 0; tt < nt; ++tt) {
+            const int t = t0 + tt;
+            const StepShared& ss = sh.st[tt];
+            const double delta = sh.delta[tt][c];
+            const float df = sh.deltaf[tt][c];
+            const double pa = sh.peak_a[tt][c];
+            const double uv = sh.u[tt][c];
+            const double pb = dmul(delta, ss.Bmax);
+            if (dyn) {
+                if (ss.refresh) inA = inB = inH = false;  // maybe_refresh, quant.cpp:303-311
+                if (pa > thA) inA = true;                  // detect_outliers, channel-local form
+                if (pb > thB) inB = true;
+            }
+            double sA, sB;
+            float invA, kB, qAf, qBf;
+            if (inA) {
+                sA = scale_from_peak(pa, qo);
+                invA = __double2float_rn(__ddiv_rn(1.0, sA));
+                qAf = qof;
+            } else {
+                sA = ss.Sa;
+                invA = ss.invSaf;
+                qAf = qaf;
+            }
+            if (inB) {
+                sB = scale_from_peak(pb, qo);
+                kB = __double2float_rn(__ddiv_rn(1.0, sB)) / ss.invSbf;
+                qBf = qof;
+            } else {
+                sB = ss.Sb;
+                kB = 1.0f;
+                qBf = qaf;
+            }
+            const float dfb = df * kB;
+            const bool tinyA = sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                // a_bar: q = 2^(delta*A*log2e) / sA, |rel err| <= (3|x2| + 16) 2^-24
+                const float x2 = df * A2f[m];
+                const float qa_f = ex2_approx(x2) * invA;
+                const float ra = rintf(qa_f);
+                const float marg_a = fmaf(qa_f, fmaf(fabsf(x2), 3.0f, 16.0f) * 5.9604645e-8f, 1e-6f);
+                // b_bar: q = delta * B / sB, |rel err| <= 12 * 2^-24
+                const float qb_f = dfb * ss.BSf[m0 + m];
+                const float rb = rintf(qb_f);
+                const float marg_b = fmaf(fabsf(qb_f), 7.1525574e-7f, 1e-6f);
+                double a_q, b_q;
+                if (EXACT || fabsf(qa_f - ra) > 0.5f - marg_a || tinyA) {
+                    const double ax = exp(dmul(delta, p.a[static_cast<size_t>(active ? i : 0) * 16 + m0 + m]));
+                    a_q = dmul(quant_code_div(ax, sA, static_cast<double>(qAf)), sA);
+                } else {
+                    a_q = dmul(small_int_to_double(fminf(ra, qAf)), sA);
+                }
+                if (EXACT || fabsf(qb_f - rb) > 0.5f - marg_b) {
+                    const double bx = dmul(delta, ss.B[m0 + m]);
+                    b_q = dmul(quant_code_div(bx, sB, static_cast<double>(qBf)), sB);
+                } else {
+                    b_q = dmul(small_int_to_double(fminf(fmaxf(rb, -qBf), qBf)), sB);
+                }
+                h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
+            }
+            double ph = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+            ph = fmax(ph, __shfl_xor_sync(0xffffffffu, ph, 1));
+            if (dyn && ph > thH) inH = true;
+            double sH, invH, qH;
+            if (inH) {
+                sH = scale_from_peak(ph, qo);
+                invH = __ddiv_rn(1.0, sH);
+                qH = qo;
+            } else {
+                sH = ss.Sh;
+                invH = ss.invSh;
+                qH = qa;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) h[m] = dmul(quant_code_inv(h[m], sH, invH, qH), sH);  // carried state
+            // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: first half, then the second half continues
+            double o = 0.0;
+            if (half == 0) {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) o = dadd(o, dmul(ss.C[m], h[m]));
+            }
+            o = __shfl_sync(0xffffffffu, o, lane & ~1u);
+            if (half == 1) {
+#pragma unroll
+                for (int m = 0; m < 8; ++m) o = dadd(o, dmul(ss.C[8 + m], h[m]));
+                if (active) {
+                    p.o[(static_cast<size_t>(s) * T + scan_perm(p.order, t, p.grid)) * E + i] = o;
+                    if (p.masks) {
+                        const size_t b = (static_cast<size_t>(s) * T + t) * E + i;
+                        const size_t kst = static_cast<size_t>(p.S) * T * E;
+                        p.masks[b] = inA;
+                        p.masks[kst + b] = inB;
+                        p.masks[2 * kst + b] = inH;
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <bool EXACT>
+static cudaError_t launch_fast(const ScanDirs& P, int ndirs, cudaStream_t st) {
+    static bool attr = false;
+    const int smem = static_cast<int>(sizeof(ScanSmem));
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k3_scan_fast<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
+    k3_scan_fast<EXACT><<<grid, kThr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, cudaStream_t st, int force_exact) {
+    if (ndirs < 1 || ndirs > 2) return cudaErrorInvalidValue;
+    ScanDirs P;
+    for (int k = 0; k < ndirs; ++k) {
+        P.d[k] = dirs[k];
+        if (dirs[k].N != 16 || dirs[k].E != dirs[0].E || dirs[k].S != dirs[0].S || dirs[k].T != dirs[0].T)
+            return cudaErrorInvalidValue;
+        if (dirs[k].mode != MODE_DYNAMIC && dirs[k].mode != MODE_STATIC) return cudaErrorInvalidValue;
+    }
+    return force_exact ? launch_fast<true>(P, ndirs, st) : launch_fast<false>(P, ndirs, st);
+}
+
+}  // namespace ob

@@ -118,6 +118,9 @@ struct ScanParams {
     uint8_t* masks = nullptr;         // optional [3][S][T][E] O(t) after detection (parity)
 };
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
+// Fast path (dynamic/static, channel-local detector): all directions in one launch.
+// force_exact = 1 disables the certified f32 codes (every element exact f64).
+cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, cudaStream_t st, int force_exact);
 
 // K4 auxiliaries.
 cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,

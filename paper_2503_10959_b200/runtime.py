@@ -296,6 +296,10 @@ class Model:
                                              int(spec.d1), int(spec.d2), chunk, C.byref(h)))
         return Calibration(self, h, spec)
 
+    def set_option(self, key: str, value: int) -> None:
+        """Engine option, e.g. scan_variant (0 auto, 1 reference kernel, 2 exact codes)."""
+        L.check(self.lib.ouro_b200_model_set_option(self.h, key.encode(), int(value)))
+
     def use_graphs(self, on: bool = True) -> None:
         L.check(self.lib.ouro_b200_model_use_graphs(self.h, int(on)))
 

@@ -185,3 +185,18 @@ def test_literal_scan_equals_channel_local(pair, gpu_ctx):
         outs.append((o.cpu().numpy(), masks.cpu().numpy()))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("abits", [4, 8])
+def test_scan_variants_identical(pair, abits):
+    """K3 fast path (certified f32 codes + exact fallbacks), its all-exact
+    variant and the per-direction reference kernel agree bit-for-bit."""
+    om, gm, imgs, cimgs = pair
+    spec = _spec(abits, rho=0.05)
+    gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
+    outs = []
+    for v in (0, 1, 2):
+        gm.set_option("scan_variant", v)
+        outs.append(gm.forward_host(imgs, gcal, 1))
+    gm.set_option("scan_variant", 0)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
