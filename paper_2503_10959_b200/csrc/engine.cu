@@ -571,7 +571,8 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         // detector (or FP recording) runs the per-direction kernel.
         bool lit = false;
         tick_begin(FAM_K3);
-        if (quant && !any_literal && scan_variant != 1) {
+        const bool fast_ok = quant && cal->spec.obits == 8 && (cal->spec.abits == 4 || cal->spec.abits == 8);
+        if (fast_ok && !any_literal && scan_variant != 1) {
             cuda_check(launch_scan_fast(sps, nd, st, scan_variant == 2 ? 1 : 0), "scan");
         } else {
             for (int dd = 0; dd < nd; ++dd) {

@@ -47,7 +47,9 @@ struct StepShared {
     double Sa, Sb, Sh, invSh, Bmax;
     float BSf[16];  // f32(B_m) * f32(1/S_b): the inlier b_bar quotient per unit delta
     float invSaf, invSbf;
-    int refresh, pad;
+    float halfA;  // 0.5 - certification margin of the inlier a_bar quotient at this step
+    int refresh;
+    int crow;  // canonical token of this scan step (ssm.cpp:30-46)
 };
 
 struct ScanSmem {
@@ -64,15 +66,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Small integer held in a float (|v| < 2^22) -> exact double without the
-// conversion pipe (1.5 * 2^23 places the integer in the low mantissa bits).
-__device__ __forceinline__ double small_int_to_double(float v) {
-    const int iv = __float_as_int(v + 12582912.0f) - 0x4B400000;
-    return __hiloint2double(0x43300000, static_cast<unsigned>(iv + 65536)) - (4503599627370496.0 + 65536.0);
+// Small integer (|v| < 2^16) -> exact double without the conversion pipe.
+__device__ __forceinline__ double int_to_double_small(int v) {
+    return __hiloint2double(0x43300000, static_cast<unsigned>(v + 65536)) - (4503599627370496.0 + 65536.0);
 }
 
-template <bool EXACT>
-__global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
+template <bool EXACT, int ABITS>
+__global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
     extern __shared__ __align__(16) uint8_t scan_smem_raw[];
     ScanSmem& sh = *reinterpret_cast<ScanSmem*>(scan_smem_raw);
     const ScanParams& p = P.d[blockIdx.z];
@@ -82,8 +82,11 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
     const int E = p.E, T = p.T, P2 = E + 32, m0 = half * 8;
     const unsigned lane = threadIdx.x & 31;
     const bool dyn = p.mode == MODE_DYNAMIC;
-    const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
-    const float qaf = static_cast<float>(qa), qof = static_cast<float>(qo);
+    constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;  // outlier_bits = 8
+    constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
+    const double* __restrict__ proj = p.proj;
+    const double* __restrict__ uin = p.u;
+    double* __restrict__ oout = p.o;
 
     float A2f[8];
     double Amax = -1e300;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
         __syncthreads();  // previous chunk consumed
         for (int idx = tid; idx < nt * 32; idx += kThr) {  // B | C of the x_proj rows (scan order)
             const int tt = idx >> 5, j = idx & 31;
-            const double v = p.proj[(static_cast<size_t>(s) * T + t0 + tt) * P2 + E + j];
+            const double v = proj[(static_cast<size_t>(s) * T + t0 + tt) * P2 + E + j];
             if (j < 16) sh.st[tt].B[j] = v;
             else sh.st[tt].C[j - 16] = v;
         }
@@ -122,7 +125,11 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
             ss.invSh = __ddiv_rn(1.0, Sh);
             ss.invSaf = __double2float_rn(__ddiv_rn(1.0, Sa));
             ss.invSbf = __double2float_rn(__ddiv_rn(1.0, Sb));
+            ss.halfA = 0.5f - fmaf(static_cast<float>(qa) + 1.0f,
+                                   fmaf(fmaxf(0.0f, -__log2f(__double2float_rn(Sa))), 3.0f, 19.0f) * 5.9604645e-8f,
+                                   1e-6f);
             ss.refresh = refresh_at(t, p.n_refresh) ? 1 : 0;
+            ss.crow = scan_perm(p.order, t, p.grid);
         }
         {  // state-independent per-channel values: this thread takes 4 of the 8 steps
             double dp[kChunk / 2], uu[kChunk / 2];
@@ -132,8 +139,9 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
                 dp[j] = 0.0;
                 uu[j] = 0.0;
                 if (tt < nt && active) {
-                    dp[j] = p.proj[(static_cast<size_t>(s) * T + t) * P2 + i];
-                    uu[j] = p.u[(static_cast<size_t>(s) * T + scan_perm(p.order, t, p.grid)) * E + i];
+                    dp[j] = proj[(static_cast<size_t>(s) * T + t) * P2 + i];
+                    const int cr = p.order == 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid));
+                    uu[j] = uin[(static_cast<size_t>(s) * T + cr) * E + i];
                 }
             }
 #pragma unroll
@@ -194,31 +202,47 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
                 qBf = qaf;
             }
             const float dfb = df * kB;
-            const bool tinyA = sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
+            // Certification margins (in units of q) on the range where rounding
+            // matters, |q| <= qmax + 1: a_bar has |dq| <= q (3|x2| + 16) 2^-24
+            // with |x2| <= 1 + log2(1/s) there; b_bar has |dq| <= |q| 12 2^-24.
+            const float halfA = inA ? 0.5f - fmaf(qof + 1.0f,
+                                                  fmaf(fmaxf(0.0f, -__log2f(__double2float_rn(sA))), 3.0f, 19.0f) *
+                                                      5.9604645e-8f,
+                                                  1e-6f)
+                                    : ss.halfA;
+            const float halfB = 0.5f - fmaf(qBf + 1.0f, 7.1525574e-7f, 1e-6f);
+            const float capA = qAf + 0.25f, capB = qBf + 0.25f;
+            // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23),
+            // clamped before rounding so the integer is the reference's clipped code
+            int ca[8], cb[8];
+            unsigned fail = (EXACT || sA < 1e-30) ? 0xFFFFu : 0u;  // ex2.approx.ftz flushes below 2^-126
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                // a_bar: q = 2^(delta*A*log2e) / sA, |rel err| <= (3|x2| + 16) 2^-24
-                const float x2 = df * A2f[m];
-                const float qa_f = ex2_approx(x2) * invA;
-                const float ra = rintf(qa_f);
-                const float marg_a = fmaf(qa_f, fmaf(fabsf(x2), 3.0f, 16.0f) * 5.9604645e-8f, 1e-6f);
-                // b_bar: q = delta * B / sB, |rel err| <= 12 * 2^-24
-                const float qb_f = dfb * ss.BSf[m0 + m];
-                const float rb = rintf(qb_f);
-                const float marg_b = fmaf(fabsf(qb_f), 7.1525574e-7f, 1e-6f);
-                double a_q, b_q;
-                if (EXACT || fabsf(qa_f - ra) > 0.5f - marg_a || tinyA) {
-                    const double ax = exp(dmul(delta, p.a[static_cast<size_t>(active ? i : 0) * 16 + m0 + m]));
-                    a_q = dmul(quant_code_div(ax, sA, static_cast<double>(qAf)), sA);
-                } else {
-                    a_q = dmul(small_int_to_double(fminf(ra, qAf)), sA);
+                const float qa_f = fminf(ex2_approx(df * A2f[m]) * invA, capA);
+                const float ta = qa_f + 12582912.0f;
+                ca[m] = __float_as_int(ta) - 0x4B400000;
+                fail |= (fabsf(qa_f - (ta - 12582912.0f)) > halfA) ? (1u << m) : 0u;
+                const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
+                const float tb = qb_f + 12582912.0f;
+                cb[m] = __float_as_int(tb) - 0x4B400000;
+                fail |= (fabsf(qb_f - (tb - 12582912.0f)) > halfB) ? (1u << (m + 8)) : 0u;
+            }
+            if (fail) {  // rare: q within its error bound of a half-integer -> exact f64 code
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    if ((fail >> m) & 1u) {
+                        const double ax = exp(dmul(delta, p.a[static_cast<size_t>(active ? i : 0) * 16 + m0 + m]));
+                        ca[m] = static_cast<int>(quant_code_div(ax, sA, static_cast<double>(qAf)));
+                    }
+                    if ((fail >> (m + 8)) & 1u)
+                        cb[m] = static_cast<int>(quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
                 }
-                if (EXACT || fabsf(qb_f - rb) > 0.5f - marg_b) {
-                    const double bx = dmul(delta, ss.B[m0 + m]);
-                    b_q = dmul(quant_code_div(bx, sB, static_cast<double>(qBf)), sB);
-                } else {
-                    b_q = dmul(small_int_to_double(fminf(fmaxf(rb, -qBf), qBf)), sB);
-                }
+            }
+            // pass 2: dequantized values (code * s, fake_quant_step) and the update
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const double a_q = dmul(int_to_double_small(ca[m]), sA);
+                const double b_q = dmul(int_to_double_small(cb[m]), sB);
                 h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
             }
             double ph = 0.0;
@@ -236,8 +260,26 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
                 invH = ss.invSh;
                 qH = qa;
             }
+            {  // h codes: q = h * (1/sH) clamped to +-(qH + 1/4), rounded with 1.5*2^52 (the low word
+               // is the integer); within 1e-12 of a half-integer the IEEE quotient decides
+                int ch[8];
+                unsigned hf = 0;
+                const double capH = qH + 0.25;
 #pragma unroll
-            for (int m = 0; m < 8; ++m) h[m] = dmul(quant_code_inv(h[m], sH, invH, qH), sH);  // carried state
+                for (int m = 0; m < 8; ++m) {
+                    const double q2 = fmin(fmax(dmul(h[m], invH), -capH), capH);
+                    const double th = dadd(q2, 6755399441055744.0);
+                    ch[m] = __double2loint(th);
+                    hf |= (fabs(dadd(q2, -dadd(th, -6755399441055744.0))) > 0.4999999999990) ? (1u << m) : 0u;
+                }
+                if (hf) {
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        if ((hf >> m) & 1u) ch[m] = static_cast<int>(quant_code_div(h[m], sH, qH));
+                }
+#pragma unroll
+                for (int m = 0; m < 8; ++m) h[m] = dmul(int_to_double_small(ch[m]), sH);  // carried state
+            }
             // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: first half, then the second half continues
             double o = 0.0;
             if (half == 0) {
@@ -249,7 +291,7 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
 #pragma unroll
                 for (int m = 0; m < 8; ++m) o = dadd(o, dmul(ss.C[8 + m], h[m]));
                 if (active) {
-                    p.o[(static_cast<size_t>(s) * T + scan_perm(p.order, t, p.grid)) * E + i] = o;
+                    oout[(static_cast<size_t>(s) * T + ss.crow) * E + i] = o;
                     if (p.masks) {
                         const size_t b = (static_cast<size_t>(s) * T + t) * E + i;
                         const size_t kst = static_cast<size_t>(p.S) * T * E;
@@ -263,17 +305,18 @@ __global__ void __launch_bounds__(kThr, 3) k3_scan_fast(const ScanDirs P) {
     }
 }
 
-template <bool EXACT>
+template <bool EXACT, int ABITS>
 static cudaError_t launch_fast(const ScanDirs& P, int ndirs, cudaStream_t st) {
     static bool attr = false;
     const int smem = static_cast<int>(sizeof(ScanSmem));
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k3_scan_fast<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e =
+            cudaFuncSetAttribute(k3_scan_fast<EXACT, ABITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
-    k3_scan_fast<EXACT><<<grid, kThr, smem, st>>>(P);
+    k3_scan_fast<EXACT, ABITS><<<grid, kThr, smem, st>>>(P);
     return cudaGetLastError();
 }
 
@@ -286,7 +329,12 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, cudaStream_t st,
             return cudaErrorInvalidValue;
         if (dirs[k].mode != MODE_DYNAMIC && dirs[k].mode != MODE_STATIC) return cudaErrorInvalidValue;
     }
-    return force_exact ? launch_fast<true>(P, ndirs, st) : launch_fast<false>(P, ndirs, st);
+    if (dirs[0].obits != 8) return cudaErrorNotSupported;  // fast path is built for 8-bit outliers
+    switch (dirs[0].abits) {
+        case 4: return force_exact ? launch_fast<true, 4>(P, ndirs, st) : launch_fast<false, 4>(P, ndirs, st);
+        case 8: return force_exact ? launch_fast<true, 8>(P, ndirs, st) : launch_fast<false, 8>(P, ndirs, st);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 }  // namespace ob
