@@ -18,7 +18,9 @@
 //   warp 0      TMA producer: 128x128 A tile + BNx128 B tile per K-block, 128B swizzle
 //   warp 1      MMA issuer: 4 x tcgen05.mma.kind::i8 (M=128, N=BN, K=32) per K-block
 //   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulators)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b, f64 dequant + outlier terms, post-op
+//   warps 4-11  epilogue: tcgen05.ld 32x32b, f64 dequant + outlier terms per row, then a
+//               shared-memory transpose so ws[r] * y, the post-op and the stores run
+//               one lane per column (coalesced 256 B rows)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -28,14 +30,15 @@
 
 namespace ob {
 
-constexpr int kBM = 128, kBK = 128, kStages = 4, kThreads = 256;
+constexpr int kBM = 128, kBK = 128, kStages = 4, kEpiWarps = 8, kThreads = 128 + 32 * kEpiWarps;
 
 template <int BN>
 struct K2Smem {
     static constexpr int kABytes = kBM * kBK;
     static constexpr int kBBytes = BN * kBK;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kBarOff = kStages * kStageBytes;
+    static constexpr int kEpiOff = kStages * kStageBytes;              // per-warp 32 x 33 f64 transpose tiles
+    static constexpr int kBarOff = kEpiOff + kEpiWarps * 32 * 33 * 8;
     static constexpr int kTotal = kBarOff + 256 + 1024;  // barriers + tmem slot + alignment slack
 };
 
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(acc_full + s, 1);
-            ptx::mbar_init(acc_empty + s, 4);  // one arrive per epilogue warp
+            ptx::mbar_init(acc_empty + s, kEpiWarps);  // one arrive per epilogue warp
         }
         ptx::fence_barrier_init();
     }
@@ -124,8 +127,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mma_commit(acc_full + buf);
             }
         }
-    } else if (warp >= 4) {  // ---- epilogue
-        const int q = warp - 4;  // TMEM lane quarter this warp may access
+    } else if (warp >= 4) {  // ---- epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
+        const int ew = warp - 4;
+        const int q = warp & 3;       // TMEM lanes 32q..32q+31 (a warp may only touch its quarter)
+        const int chalf = ew >> 2;    // which half of the BN columns
+        double* stage = reinterpret_cast<double*>(smem + L::kEpiOff) + ew * (32 * 33);
+        const bool want_out = p.epi.acc_out != nullptr;
         int it = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
@@ -133,22 +140,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int m0 = (tile / n_tiles) * kBM, n0 = (tile % n_tiles) * BN;
             ptx::mbar_wait(acc_full + buf, aphase);
             ptx::tc_fence_after();
-            const int row = m0 + q * 32 + lane;
+            const int rbase = m0 + q * 32;
+            const int row = rbase + lane;
             const bool rv = row < p.M;
             const double S = rv ? p.a.s_row[row] : 0.0;
             const int cnt = rv ? p.a.ocnt[row] : 0;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int cc = 0; cc < BN / 64; ++cc) {
+                const int c = chalf * (BN / 64) + cc;
                 const int r0 = n0 + c * 32;
                 if (r0 >= p.R) break;  // uniform across the warp
                 uint32_t acc[32];
                 ptx::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * BN + c * 32, acc);
-                if (!rv) continue;
+                // phase 1, thread = row: S_m * acc (gemm.cpp:207) + outlier terms in ascending
+                // channel order (gemm.cpp:208-216), staged transposed through shared memory
                 double y[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) y[j] = dmul(S, static_cast<double>(static_cast<int32_t>(acc[j])));
                 int32_t aout[32];
-                const bool want_out = p.epi.acc_out != nullptr;
                 if (want_out)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) aout[j] = 0;
@@ -170,30 +179,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (want_out) aout[j] += wq * xo_i;
                     }
                 }
-                const int nvalid = min(32, p.R - r0);
-                double* orow;
-                int col0;
-                if (p.epi.post == POST_INPROJ && r0 >= p.epi.split) {
-                    orow = p.epi.out2 + static_cast<size_t>(row) * p.epi.split;
-                    col0 = r0 - p.epi.split;
-                } else {
-                    orow = p.epi.out + static_cast<size_t>(row) * p.epi.ld_out;
-                    col0 = r0;
-                }
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (j < nvalid) {
-                        double v = dmul(__ldg(p.ws + r0 + j), y[j]);
-                        if (p.epi.post == POST_INPROJ && r0 >= p.epi.split) v = silu_d(v);
-                        if (p.epi.post == POST_RESID) v = dadd(orow[col0 + j], v);
-                        orow[col0 + j] = v;
+                for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = y[j];
+                if (rv && (p.epi.acc_in || want_out)) {  // parity planes (test path)
+                    const int nv = min(32, p.R - r0);
+                    for (int j = 0; j < nv; ++j) {
+                        if (p.epi.acc_in) p.epi.acc_in[static_cast<size_t>(row) * p.R + r0 + j] = static_cast<int32_t>(acc[j]);
+                        if (want_out) p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
                     }
                 }
-                if (p.epi.acc_in)
-                    for (int j = 0; j < nvalid; ++j)
-                        p.epi.acc_in[static_cast<size_t>(row) * p.R + r0 + j] = static_cast<int32_t>(acc[j]);
-                if (want_out)
-                    for (int j = 0; j < nvalid; ++j) p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
+                __syncwarp();
+                // phase 2, lane = column: ws[r] * y (gemm.cpp:218-219) + post-op, coalesced rows
+                const int col = r0 + lane;
+                const bool cv = col < p.R;
+                const double wsr = cv ? __ldg(p.ws + col) : 0.0;
+                const bool gate = p.epi.post == POST_INPROJ && r0 >= p.epi.split;
+                double* obase;
+                size_t ld;
+                int ocol;
+                if (gate) {
+                    obase = p.epi.out2;
+                    ld = static_cast<size_t>(p.epi.split);
+                    ocol = col - p.epi.split;
+                } else {
+                    obase = p.epi.out;
+                    ld = static_cast<size_t>(p.epi.ld_out);
+                    ocol = col;
+                }
+                const int nrows = min(32, p.M - rbase);
+#pragma unroll 4
+                for (int rr = 0; rr < nrows; ++rr) {
+                    double v = dmul(wsr, stage[rr * 33 + lane]);
+                    double* dst = obase + static_cast<size_t>(rbase + rr) * ld + ocol;
+                    if (gate) v = silu_d(v);
+                    if (p.epi.post == POST_RESID && cv) v = dadd(*dst, v);
+                    if (cv) *dst = v;
+                }
+                __syncwarp();
             }
             ptx::tc_fence_before();
             __syncwarp();
