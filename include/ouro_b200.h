@@ -71,32 +71,36 @@ ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out);
  *   gate   dev f64 [S][T][E] (SRC_MERGE)
  *   order  scan order read at step t (ssm.cpp:30-46), -1 = identity; grid = sqrt(T)
  *   s_in, s_full  dev f64 [T] calibrated per-step scales (TensorCalib, quant.hpp:36-42)
+ *   literal  1 = run the verbatim detector (cross-channel max per plane); 0 =
+ *          channel-parallel kernel, exact when fl(nextafter(theta)/q_a) > s_in[t]
+ *          for every t (the caller checks), unless `scanned`
+ *          is requested
  * Outputs (row = s*T + t, dev): codes int8 [S*T][E] (0 at outliers), s_row
- * f64 [S*T], ocnt int32 [S*T], och uint16 / ocode int8 / oscale f64
- * [S*T][cap] (outlier list, ascending channel), optional omask uint32
- * [S*T][ceil(E/32)] and scanned uint8 [S*T] (DetectResult::scanned). */
+ * f64 [S*T], ocnt int32 [S*T] = |O(t)|, omask uint32 [S*T][ceil(E/32)]
+ * (bit ch%32 of word ch/32 = channel in O(t)), ocode int8 / oscale f64
+ * [S*T][E] written at outlier positions only, optional scanned uint8 [S*T]
+ * (DetectResult::scanned; literal kernel). rs_work: dev f64 [S*T] scratch
+ * for SRC_RMSNORM on the channel-parallel kernel. */
 ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
                                       size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
                                       const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
-                                      unsigned outlier_bits, int mode, int8_t* codes, double* s_row, int32_t* ocnt,
-                                      uint16_t* och, int8_t* ocode, double* oscale, size_t cap, uint32_t* omask,
-                                      uint8_t* scanned);
+                                      unsigned outlier_bits, int mode, int literal, int8_t* codes, double* s_row,
+                                      int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
+                                      uint8_t* scanned, double* rs_work);
 
 /* K2: hybrid quant-linear on tcgen05 kind::i8 (hybrid_gemm, gemm.hpp:78-87,
  * gemm.cpp:181-225): out[m][r] = ws[r]*(s_row[m]*acc_in[m][r]
- *   + sum_j (oscale[m][j]*w[r][och[m][j]])*ocode[m][j]), then the post-op.
- *   codes/s_row/ocnt/och/ocode/oscale as produced by K1, M rows of K channels
- *   w   dev int8 [R][K] weight codes (|code| <= 7), wt its transpose [K][R]
- *   ws  dev f64 [R] weight row scales
- * K and R must be multiples of 16. acc_in/acc_out (dev int32 [M][R], may be
- * NULL) receive the reference's integer planes GemmResult::acc_inlier /
- * acc_outlier. */
+ *   + sum_{ch in O(m), ascending} (oscale[m][ch]*w[r][ch])*ocode[m][ch]),
+ * then the post-op. The activation operand is K1's output (M rows of K
+ * channels); w dev int8 [R][K] weight codes (|code| <= 7), wt its transpose
+ * [K][R]; ws dev f64 [R] weight row scales. K and R must be multiples of 16.
+ * acc_in/acc_out (dev int32 [M][R], may be NULL) receive the reference's
+ * integer planes GemmResult::acc_inlier / acc_outlier. */
 ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
-                                   const double* s_row, const int32_t* ocnt, const uint16_t* och,
-                                   const int8_t* ocode, const double* oscale, size_t cap, const int8_t* w,
-                                   const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
-                                   double* out2, size_t split, const double* bias, int32_t* acc_in,
-                                   int32_t* acc_out);
+                                   const double* s_row, const int32_t* ocnt, const uint32_t* omask,
+                                   const int8_t* ocode, const double* oscale, const int8_t* w, const int8_t* wt,
+                                   const double* ws, int post, double* out, size_t ld_out, double* out2, size_t split,
+                                   const double* bias, int32_t* acc_in, int32_t* acc_out);
 
 /* K3: selective scan of one direction with the QuantHook policy (s6_scan,
  * ssm.hpp:131-132, ssm.cpp:124-186; QuantHook quant.cpp:456-501), N = 16.
@@ -163,7 +167,9 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
 
 /* Engine options: "scan_variant" = 0 auto (fast K3 path wherever the
  * channel-local detector is exact), 1 per-direction reference scan kernel,
- * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid). */
+ * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid);
+ * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
+ * detector kernel everywhere. */
 ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long value);
 
 /* One forward with CUDA events around every launch: per kernel family

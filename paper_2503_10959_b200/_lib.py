@@ -31,10 +31,10 @@ _SIGS = {
     "ouro_b200_ctx_set_stream": ([_P, _P], _I),
     "ouro_b200_ctx_synchronize": ([_P], _I),
     "ouro_b200_ctx_num_sms": ([_P, C.POINTER(_I)], _I),
-    "ouro_b200_detect_quantize": ([_P, _P, _P, _P, _SZ, _SZ, _SZ, _I, _I, _I, _D, _P, _P, _SZ, _U, _U, _I, _P, _P,
-                                   _P, _P, _P, _P, _SZ, _P, _P], _I),
-    "ouro_b200_quant_linear": ([_P, _SZ, _SZ, _SZ, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I, _P, _SZ, _P, _SZ,
-                                _P, _P, _P], _I),
+    "ouro_b200_detect_quantize": ([_P, _P, _P, _P, _SZ, _SZ, _SZ, _I, _I, _I, _D, _P, _P, _SZ, _U, _U, _I, _I, _P,
+                                   _P, _P, _P, _P, _P, _P, _P], _I),
+    "ouro_b200_quant_linear": ([_P, _SZ, _SZ, _SZ, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P, _SZ, _P,
+                                _P, _P], _I),
     "ouro_b200_quant_scan": ([_P, _SZ, _SZ, _SZ, _SZ, _I, _I, _P, _P, _P, _P, _P, _I, _SZ, _U, _U, _P, _P, _P, _P,
                               _I, _P], _I),
     "ouro_b200_dgemm": ([_P, _SZ, _SZ, _SZ, _P, _SZ, _P, _I, _P, _SZ, _P, _SZ, _P], _I),

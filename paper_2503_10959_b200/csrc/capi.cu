@@ -101,17 +101,17 @@ ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out) {
 ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
                                       size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
                                       const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
-                                      unsigned outlier_bits, int mode, int8_t* codes, double* s_row, int32_t* ocnt,
-                                      uint16_t* och, int8_t* ocode, double* oscale, size_t cap, uint32_t* omask,
-                                      uint8_t* scanned) {
+                                      unsigned outlier_bits, int mode, int literal, int8_t* codes, double* s_row,
+                                      int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
+                                      uint8_t* scanned, double* rs_work) {
     return guarded([&] {
-        require(ctx && x && codes && s_row && ocnt && och && ocode && oscale, "detect_quantize: NULL argument");
+        require(ctx && x && codes && s_row && ocnt && omask && ocode && oscale, "detect_quantize: NULL argument");
         require(mode == ob::MODE_DYNAMIC || mode == ob::MODE_STATIC, "detect_quantize: mode must be dynamic or static");
         require(mode == ob::MODE_STATIC ? s_full != nullptr : s_in != nullptr, "detect_quantize: missing scales");
         require(act_bits >= 2 && act_bits <= 8 && outlier_bits >= act_bits && outlier_bits <= 8,
                 "detect_quantize: bit widths must satisfy 2 <= act <= outlier <= 8");
-        require(cap >= E, "detect_quantize: outlier capacity must be >= E");
         require(src != ob::K1_SRC_MERGE || gate != nullptr, "detect_quantize: merge source needs the gate");
+        require(src >= 0 && src <= 2, "detect_quantize: unknown source");
         ob::K1Params k;
         k.S = static_cast<int>(S);
         k.T = static_cast<int>(T);
@@ -130,27 +130,26 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
         k.cal.theta = theta;
         k.cal.s_in = s_in;
         k.cal.s_full = s_full;
+        k.rs = rs_work;
+        k.force_literal = literal;
         k.codes = codes;
         k.s_row = s_row;
         k.ocnt = ocnt;
-        k.och = och;
+        k.omask = omask;
         k.ocode = ocode;
         k.oscale = oscale;
-        k.cap = static_cast<int>(cap);
-        k.omask = omask;
         k.scanned = scanned;
         ob::cuda_check(ob::launch_k1(k, ctx->c->stream), "detect_quantize");
     });
 }
 
 ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
-                                   const double* s_row, const int32_t* ocnt, const uint16_t* och,
-                                   const int8_t* ocode, const double* oscale, size_t cap, const int8_t* w,
-                                   const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
-                                   double* out2, size_t split, const double* bias, int32_t* acc_in,
-                                   int32_t* acc_out) {
+                                   const double* s_row, const int32_t* ocnt, const uint32_t* omask,
+                                   const int8_t* ocode, const double* oscale, const int8_t* w, const int8_t* wt,
+                                   const double* ws, int post, double* out, size_t ld_out, double* out2, size_t split,
+                                   const double* bias, int32_t* acc_in, int32_t* acc_out) {
     return guarded([&] {
-        require(ctx && codes && s_row && ocnt && och && ocode && oscale && w && wt && ws && out,
+        require(ctx && codes && s_row && ocnt && omask && ocode && oscale && w && wt && ws && out,
                 "quant_linear: NULL argument");
         require(K % 16 == 0 && R % 16 == 0, "quant_linear: K and R must be multiples of 16");
         require(post != ob::POST_INPROJ || (out2 != nullptr && split % 32 == 0 && split < R),
@@ -163,10 +162,10 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
         q.a.codes = const_cast<int8_t*>(codes);
         q.a.s_row = const_cast<double*>(s_row);
         q.a.ocnt = const_cast<int*>(ocnt);
-        q.a.och = const_cast<uint16_t*>(och);
+        q.a.omask = const_cast<uint32_t*>(omask);
         q.a.ocode = const_cast<int8_t*>(ocode);
         q.a.oscale = const_cast<double*>(oscale);
-        q.a.cap = static_cast<int>(cap);
+        q.a.J = static_cast<int>((K + 31) / 32);
         q.w = w;
         q.wt = wt;
         q.ws = ws;
@@ -457,6 +456,9 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         if (k == "scan_variant") {
             require(value >= 0 && value <= 2, "model_set_option: scan_variant must be 0, 1 or 2");
             m->m->scan_variant = static_cast<int>(value);
+        } else if (k == "k1_variant") {
+            require(value >= 0 && value <= 1, "model_set_option: k1_variant must be 0 or 1");
+            m->m->k1_variant = static_cast<int>(value);
         } else {
             throw ob::ValidationError("model_set_option: unknown option '" + k + "'");
         }

@@ -283,12 +283,12 @@ void Model::ensure_work(int S, bool trace) {
     w.codes.ensure(rows * E);
     w.ocode.ensure(rows * E);
     w.oscale.ensure(rows * E);
-    w.och.ensure(rows * E);
+    w.omask.ensure(rows * ((E + 31) / 32));
+    w.rs.ensure(rows);
     w.s_row.ensure(rows);
     w.ocnt.ensure(rows);
     w.scanned.ensure(rows);
     if (trace) {
-        w.omask.ensure(rows * ((E + 31) / 32));
         w.masks.ensure(2 * 3 * rows * E);
         w.acc_in.ensure(rows * std::max(2 * E, E + 2 * N));
         w.acc_out.ensure(rows * std::max(2 * E, E + 2 * N));
@@ -299,13 +299,16 @@ void Model::ensure_work(int S, bool trace) {
 void Calibration::upload(cudaStream_t st) {
     if (!dirty) return;
     const size_t T = tokens;
+    // per tensor: s_in[T] | s_full[T] | 1/s_in[T] | 1/s_full[T]
     std::vector<double> h;
-    h.reserve((scan.size() + lin.size()) * 2 * T);
+    h.reserve((scan.size() + lin.size()) * 4 * T);
     for (auto* v : {&scan, &lin})
         for (auto& tc : *v) {
             require(tc.s_in.size() == T && tc.s_full.size() == T, "calibration tables have the wrong length");
             h.insert(h.end(), tc.s_in.begin(), tc.s_in.end());
             h.insert(h.end(), tc.s_full.begin(), tc.s_full.end());
+            for (double x : tc.s_in) h.push_back(1.0 / x);
+            for (double x : tc.s_full) h.push_back(1.0 / x);
         }
     dev.upload(h.data(), h.size(), st);
     // Channel-local detector check C(t) = fl(nextafter(theta,+inf)/q_a) > S^I(t)
@@ -326,14 +329,23 @@ void Calibration::upload(cudaStream_t st) {
                     }
             }
     literal.upload(lit.data(), lit.size(), st);
+    // the same check for the linear-input sites (K1 channel-parallel kernel)
+    lin_literal.assign(lin.size(), 0);
+    for (size_t i = 0; i < lin.size(); ++i) {
+        const double up = std::nextafter(lin[i].theta, INFINITY) / qa;
+        for (size_t t = 0; t < T; ++t)
+            if (!(up > lin[i].s_in[t])) lin_literal[i] = 1;
+    }
     cuda_check(cudaStreamSynchronize(st), "calib upload");
     dirty = false;
 }
 const double* Calibration::s_in_dev(bool is_lin, size_t idx) const {
-    size_t base = (is_lin ? scan.size() + idx : idx) * 2 * tokens;
+    size_t base = (is_lin ? scan.size() + idx : idx) * 4 * tokens;
     return dev.p + base;
 }
 const double* Calibration::s_full_dev(bool is_lin, size_t idx) const { return s_in_dev(is_lin, idx) + tokens; }
+const double* Calibration::inv_in_dev(bool is_lin, size_t idx) const { return s_in_dev(is_lin, idx) + 2 * tokens; }
+const double* Calibration::inv_full_dev(bool is_lin, size_t idx) const { return s_in_dev(is_lin, idx) + 3 * tokens; }
 
 // ---- forward ------------------------------------------------------------------
 namespace {
@@ -413,15 +425,19 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             k.cal.theta = cal->lin[li].theta;
             k.cal.s_in = cal->s_in_dev(true, li);
             k.cal.s_full = cal->s_full_dev(true, li);
+            k.inv_in = cal->inv_in_dev(true, li);
+            k.inv_full = cal->inv_full_dev(true, li);
+            k.rs = w.rs.p;
             k.codes = w.codes.p;
             k.s_row = w.s_row.p;
             k.ocnt = w.ocnt.p;
-            k.och = w.och.p;
+            k.omask = w.omask.p;
             k.ocode = w.ocode.p;
             k.oscale = w.oscale.p;
-            k.cap = E;
-            k.scanned = w.scanned.p;
-            if (tb(b)) k.omask = w.omask.p;
+            // literal detector where the channel-local form is not exact, on request,
+            // and in trace mode (it also reports DetectResult::scanned)
+            k.force_literal = (mode == MODE_DYNAMIC && cal->lin_literal[li]) || k1_variant == 1 || tb(b);
+            if (tb(b)) k.scanned = w.scanned.p;
         } else {
             k.mode = MODE_FP;
             k.window = 8;
@@ -435,10 +451,10 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         a.codes = w.codes.p;
         a.s_row = w.s_row.p;
         a.ocnt = w.ocnt.p;
-        a.och = w.och.p;
+        a.omask = w.omask.p;
         a.ocode = w.ocode.p;
         a.oscale = w.oscale.p;
-        a.cap = E;
+        a.J = (E + 31) / 32;
         return a;
     };
     auto trace_lin = [&](int b, int site, int R) {
@@ -447,7 +463,6 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         grab(trace, p + "codes", w.codes.p, rows * E, st);
         grab(trace, p + "s_row", w.s_row.p, rows, st);
         grab(trace, p + "ocnt", w.ocnt.p, rows, st);
-        grab(trace, p + "och", w.och.p, rows * E, st);
         grab(trace, p + "ocode", w.ocode.p, rows * E, st);
         grab(trace, p + "oscale", w.oscale.p, rows * E, st);
         grab(trace, p + "omask", w.omask.p, rows * ((E + 31) / 32), st);

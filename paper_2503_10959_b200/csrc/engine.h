@@ -100,10 +100,13 @@ class Calibration {
     DevBuf<double> dev;               // packed s_in/s_full tables
     DevBuf<uint8_t> literal;          // [block][dir][T]
     std::vector<int> literal_any;     // [block][dir]
+    std::vector<int> lin_literal;     // [block][site]: some step fails the channel-local check
     bool dirty = true;
     void upload(cudaStream_t st);
     const double* s_in_dev(bool is_lin, size_t idx) const;
     const double* s_full_dev(bool is_lin, size_t idx) const;
+    const double* inv_in_dev(bool is_lin, size_t idx) const;
+    const double* inv_full_dev(bool is_lin, size_t idx) const;
 };
 
 class Model {
@@ -137,6 +140,7 @@ class Model {
     void upload_fp();
     void quantize(unsigned bits);
     bool fp_dirty = true;
+    int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
     int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only
 
     // workspace
@@ -145,9 +149,8 @@ class Model {
         DevBuf<double> x, patches, u0, gate, u, xin, pooled, logits, img;
         DevBuf<double> proj, o;  // per dir stacked
         DevBuf<int8_t> codes, ocode;
-        DevBuf<double> s_row, oscale;
+        DevBuf<double> s_row, oscale, rs;
         DevBuf<int> ocnt;
-        DevBuf<uint16_t> och;
         DevBuf<uint32_t> omask;
         DevBuf<uint8_t> scanned, masks;
         DevBuf<unsigned long long> peaks;

@@ -9,20 +9,134 @@
 //                                          if s_dyn > S^I(t): O |= {ch: |x| > theta}
 //   split_quantize     gemm.cpp:106-135    inliers -> code(x, S^I(t), a_bits),
 //                                          outliers -> own scale |x|/q_o, code at o_bits
-// Layout/work split: one warp owns one (sample, refresh window); lane l owns
-// channels l, l+32, ... (so every cross-channel quantity of the reference —
-// the detector's max, D1's RMSNorm sum — is a warp shuffle reduction), and the
-// warp walks the window's tokens in step order carrying O as a per-lane bit
-// mask. Rows are read with 256 B coalesced loads; the outlier list of every
-// row is compacted in ascending channel order with ballots, which is the order
-// the hybrid epilogue adds outlier terms in (gemm.cpp:208-216).
+// Output operand (QAct): codes [M][E] (0 at outliers), per-row mask words
+// [M][J] (bit ch%32 of word ch/32 = channel in O(t)), dense outlier codes and
+// scales [M][E] written at outlier positions only, |O(t)| per row and the
+// row's inlier scale. The hybrid epilogue walks the mask words in ascending
+// channel order, the order the reference adds outlier terms in
+// (gemm.cpp:208-216).
+//
+// Two kernels:
+//  * k1_channel (fast path): one thread owns two channels of one (sample,
+//    refresh window) and walks the window's tokens. Exact whenever
+//    C(t) = fl(nextafter(theta,+inf)/q_a) > S^I(t) holds (host-checked per
+//    site and step): then O(t) = O_r(t) U {ch: |x| > theta}
+//    and channels never interact. Rows are read as 16-byte vectors, codes
+//    stored as char2; D1's RMSNorm factor comes from k1_rownorm.
+//  * k1_literal: one warp owns one (sample, window) with lane l holding
+//    channels l, l+32, ...; the cross-channel maximum of detect_outliers is a
+//    warp reduction, so the reference is followed verbatim (also provides
+//    DetectResult::scanned).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ob {
 
+// D1 RMSNorm factor per token row: 1/sqrt(mean(x^2) + 1e-6) with the sum taken
+// as 32 lane-strided partials (channel k -> partial k%32, k ascending) combined
+// by an xor butterfly (oracle/driver.hpp rmsnorm_row).
+__global__ void __launch_bounds__(256) k1_rownorm(const double* __restrict__ x, double* __restrict__ rs, long rows,
+                                                  int E) {
+    const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const double* xr = x + r * E;
+    double ps = 0.0;
+    for (int k = lane; k < E; k += 32) {
+        const double v = xr[k];
+        ps = dadd(ps, dmul(v, v));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ps = dadd(ps, __shfl_xor_sync(0xffffffffu, ps, o));
+    if (lane == 0) {
+        const double ms = __ddiv_rn(ps, static_cast<double>(E));
+        rs[r] = __ddiv_rn(1.0, __dsqrt_rn(dadd(ms, 1e-6)));
+    }
+}
+
+template <int SRC>
+__device__ __forceinline__ double2 k1_load2(const K1Params& p, size_t src, size_t crow_global) {
+    if (SRC == K1_SRC_MERGE) {
+        // merged = (0 + o_0) + o_1 (ssm.cpp:214-229), y = merged * gate (ssm.cpp:231)
+        const double2 a = *reinterpret_cast<const double2*>(p.x + src);
+        const double2 g = *reinterpret_cast<const double2*>(p.gate + src);
+        double m0 = dadd(0.0, a.x), m1 = dadd(0.0, a.y);
+        if (p.x2) {
+            const double2 b = *reinterpret_cast<const double2*>(p.x2 + src);
+            m0 = dadd(m0, b.x);
+            m1 = dadd(m1, b.y);
+        }
+        return make_double2(dmul(m0, g.x), dmul(m1, g.y));
+    }
+    double2 v = *reinterpret_cast<const double2*>(p.x + src);
+    if (SRC == K1_SRC_RMSNORM) {
+        const double r = p.rs[crow_global];
+        v.x = dmul(v.x, r);
+        v.y = dmul(v.y, r);
+    }
+    return v;
+}
+
+template <int SRC>
+__global__ void __launch_bounds__(128) k1_channel(const K1Params p) {
+    const int E = p.E, T = p.T, J = (E + 31) >> 5;
+    const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * 2;  // channels ch, ch+1
+    const int lane = threadIdx.x & 31;
+    const int win = p.window, nwin = (T + win - 1) / win;
+    const int s = blockIdx.y / nwin;
+    const int t0 = (blockIdx.y % nwin) * win, t1 = min(T, t0 + win);
+    const bool active = ch < E;  // E is a multiple of 32
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
+    const double theta = p.cal.theta;
+    bool in0 = false, in1 = false;
+    for (int t = t0; t < t1; ++t) {
+        const int crow = p.order < 0 ? t : (p.order == 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid)));
+        const size_t cg = static_cast<size_t>(s) * T + crow;
+        const size_t row = static_cast<size_t>(s) * T + t;
+        double2 v = make_double2(0.0, 0.0);
+        if (active) v = k1_load2<SRC>(p, cg * E + ch, cg);
+        if (dyn) {
+            if (refresh_at(t, p.n_refresh)) in0 = in1 = false;  // maybe_refresh
+            if (fabs(v.x) > theta) in0 = true;                   // detect_outliers, channel-local form
+            if (fabs(v.y) > theta) in1 = true;
+        }
+        const double S = dyn ? p.cal.s_in[t] : p.cal.s_full[t];
+        const double inv = dyn ? (p.inv_in ? p.inv_in[t] : __ddiv_rn(1.0, S))
+                               : (p.inv_full ? p.inv_full[t] : __ddiv_rn(1.0, S));
+        int c0 = 0, c1 = 0;
+        if (active) {
+            if (in0) {
+                const double os = scale_from_peak(fabs(v.x), qo);  // scale_for over the 1-value row
+                p.ocode[row * E + ch] = static_cast<int8_t>(static_cast<int>(quant_code_div(v.x, os, qo)));
+                p.oscale[row * E + ch] = os;
+            } else {
+                c0 = static_cast<int>(quant_code_inv(v.x, S, inv, qa));
+            }
+            if (in1) {
+                const double os = scale_from_peak(fabs(v.y), qo);
+                p.ocode[row * E + ch + 1] = static_cast<int8_t>(static_cast<int>(quant_code_div(v.y, os, qo)));
+                p.oscale[row * E + ch + 1] = os;
+            } else {
+                c1 = static_cast<int>(quant_code_inv(v.y, S, inv, qa));
+            }
+            *reinterpret_cast<char2*>(p.codes + row * E + ch) =
+                make_char2(static_cast<signed char>(c0), static_cast<signed char>(c1));
+        }
+        // mask word of channels 32w..32w+31: 16 lanes x 2 bits
+        unsigned bits = active ? ((in0 ? 1u : 0u) | (in1 ? 2u : 0u)) << ((lane & 15) * 2) : 0u;
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+        if (active && (lane & 15) == 0) {
+            p.omask[row * J + (ch >> 5)] = bits;
+            if (bits) atomicAdd(p.ocnt + row, __popc(bits));
+        }
+        if (ch == 0) p.s_row[row] = S;
+    }
+}
+
 template <int JMAX, int SRC>
-__global__ void __launch_bounds__(256) k1_detect_quant(const K1Params p) {
+__global__ void __launch_bounds__(256) k1_literal(const K1Params p) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int win = p.window;
@@ -47,7 +161,6 @@ __global__ void __launch_bounds__(256) k1_detect_quant(const K1Params p) {
             double x = 0.0;
             if (j < J && ch < E) {
                 if (SRC == K1_SRC_MERGE) {
-                    // merged = (0 + o_0) + o_1 (ssm.cpp:214-229), y = merged * gate (ssm.cpp:231)
                     double m = dadd(0.0, p.x[src + ch]);
                     if (p.x2) m = dadd(m, p.x2[src + ch]);
                     x = dmul(m, p.gate[src + ch]);
@@ -104,8 +217,7 @@ __global__ void __launch_bounds__(256) k1_detect_quant(const K1Params p) {
             S = p.cal.s_full[t];
         }
         const double inv = __ddiv_rn(1.0, S);
-        int base = 0;
-        int8_t* crow_codes = p.codes + row * E;
+        int cnt = 0;
 #pragma unroll
         for (int j = 0; j < JMAX; ++j) {
             const int ch = j * 32 + lane;
@@ -113,30 +225,23 @@ __global__ void __launch_bounds__(256) k1_detect_quant(const K1Params p) {
             const bool isout = valid && ((inmask >> j) & 1u);
             if (valid) {
                 double c = 0.0;
-                if (!isout) c = quant_code_inv(v[j], S, inv, qa);
-                crow_codes[ch] = static_cast<int8_t>(static_cast<int>(c));
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, isout);
-            if (bal) {
                 if (isout) {
-                    const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                    const double ap = fabs(v[j]);
-                    const double os = scale_from_peak(ap, qo);  // scale_for over the 1-value row
-                    const double oc = quant_code_div(v[j], os, qo);
-                    const size_t o = row * p.cap + pos;
-                    p.och[o] = static_cast<uint16_t>(ch);
-                    p.ocode[o] = static_cast<int8_t>(static_cast<int>(oc));
-                    p.oscale[o] = os;
+                    const double os = scale_from_peak(fabs(v[j]), qo);
+                    p.ocode[row * E + ch] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[j], os, qo)));
+                    p.oscale[row * E + ch] = os;
+                } else {
+                    c = quant_code_inv(v[j], S, inv, qa);
                 }
-                base += __popc(bal);
+                p.codes[row * E + ch] = static_cast<int8_t>(static_cast<int>(c));
             }
-            if (p.omask && j < J) {
+            if (j < J) {
                 const unsigned mb = __ballot_sync(0xffffffffu, isout);
+                cnt += __popc(mb);
                 if (lane == 0) p.omask[row * J + j] = mb;
             }
         }
         if (lane == 0) {
-            p.ocnt[row] = base;
+            p.ocnt[row] = cnt;
             p.s_row[row] = S;
             if (p.scanned) p.scanned[row] = trig ? 1 : 0;
         }
@@ -144,26 +249,46 @@ __global__ void __launch_bounds__(256) k1_detect_quant(const K1Params p) {
 }
 
 template <int SRC>
-static cudaError_t launch_src(const K1Params& p, cudaStream_t st) {
+static cudaError_t launch_literal(const K1Params& p, cudaStream_t st) {
     const int J = (p.E + 31) / 32;
     const int nwin = (p.T + p.window - 1) / p.window;
     const long warps = static_cast<long>(p.S) * nwin;
     const int threads = 256;
     const unsigned blocks = static_cast<unsigned>((warps * 32 + threads - 1) / threads);
-    if (J <= 8) k1_detect_quant<8, SRC><<<blocks, threads, 0, st>>>(p);
-    else if (J <= 16) k1_detect_quant<16, SRC><<<blocks, threads, 0, st>>>(p);
-    else if (J <= 24) k1_detect_quant<24, SRC><<<blocks, threads, 0, st>>>(p);
-    else if (J <= 32) k1_detect_quant<32, SRC><<<blocks, threads, 0, st>>>(p);
+    if (J <= 8) k1_literal<8, SRC><<<blocks, threads, 0, st>>>(p);
+    else if (J <= 16) k1_literal<16, SRC><<<blocks, threads, 0, st>>>(p);
+    else if (J <= 24) k1_literal<24, SRC><<<blocks, threads, 0, st>>>(p);
+    else if (J <= 32) k1_literal<32, SRC><<<blocks, threads, 0, st>>>(p);
     else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+template <int SRC>
+static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(p.ocnt, 0, static_cast<size_t>(p.S) * p.T * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    if (SRC == K1_SRC_RMSNORM) {
+        const long rows = static_cast<long>(p.S) * p.T;
+        k1_rownorm<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(p.x, p.rs, rows, p.E);
+    }
+    const int nwin = (p.T + p.window - 1) / p.window;
+    dim3 grid((p.E / 2 + 127) / 128, p.S * nwin);
+    k1_channel<SRC><<<grid, 128, 0, st>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k1(const K1Params& p, cudaStream_t st) {
     if (p.E < 1 || p.E > 1024 || p.T < 1 || p.S < 1 || p.window < 1) return cudaErrorInvalidValue;
+    // the channel-parallel kernel needs: a quantizing mode, no DetectResult
+    // output, the channel-local detector exact (no literal steps), E % 32 == 0
+    // and (RMSNORM) a row-factor buffer
+    const bool fast = p.mode != MODE_FP && !p.scanned && !p.force_literal && (p.E % 32) == 0 &&
+                      (p.src != K1_SRC_RMSNORM || p.rs != nullptr);
     switch (p.src) {
-        case K1_SRC_PLAIN: return launch_src<K1_SRC_PLAIN>(p, st);
-        case K1_SRC_RMSNORM: return launch_src<K1_SRC_RMSNORM>(p, st);
-        case K1_SRC_MERGE: return launch_src<K1_SRC_MERGE>(p, st);
+        case K1_SRC_PLAIN: return fast ? launch_channel<K1_SRC_PLAIN>(p, st) : launch_literal<K1_SRC_PLAIN>(p, st);
+        case K1_SRC_RMSNORM:
+            return fast ? launch_channel<K1_SRC_RMSNORM>(p, st) : launch_literal<K1_SRC_RMSNORM>(p, st);
+        case K1_SRC_MERGE: return fast ? launch_channel<K1_SRC_MERGE>(p, st) : launch_literal<K1_SRC_MERGE>(p, st);
         default: return cudaErrorInvalidValue;
     }
 }

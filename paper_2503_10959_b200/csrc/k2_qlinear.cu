@@ -161,9 +161,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (want_out)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) aout[j] = 0;
+                // walk O(t) in ascending channel order: mask word by word, bit by bit
+                int word = -1;
+                unsigned bits = 0;
                 for (int o = 0; o < cnt; ++o) {
-                    const size_t oi = static_cast<size_t>(row) * p.a.cap + o;
-                    const int ch = p.a.och[oi];
+                    while (bits == 0) bits = p.a.omask[static_cast<size_t>(row) * p.a.J + (++word)];
+                    const int ch = word * 32 + (__ffs(bits) - 1);
+                    bits &= bits - 1;
+                    const size_t oi = static_cast<size_t>(row) * p.K + ch;
                     const int xo_i = p.a.ocode[oi];
                     const double xo = static_cast<double>(xo_i);
                     const double osc = p.a.oscale[oi];

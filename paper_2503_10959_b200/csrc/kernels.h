@@ -22,10 +22,10 @@ struct QAct {
     int8_t* codes = nullptr;      // [M][E] inlier codes, 0 at outlier positions
     double* s_row = nullptr;      // [M] inlier scale of the row's plane (S^I(t) or S_full(t))
     int* ocnt = nullptr;          // [M] |O(t)|
-    uint16_t* och = nullptr;      // [M][cap] outlier channels, ascending
-    int8_t* ocode = nullptr;      // [M][cap] outlier codes (o_bits)
-    double* oscale = nullptr;     // [M][cap] per-channel outlier scales
-    int cap = 0;
+    uint32_t* omask = nullptr;    // [M][J] bit ch%32 of word ch/32: channel in O(t)
+    int8_t* ocode = nullptr;      // [M][E] outlier codes (o_bits), valid at outlier positions only
+    double* oscale = nullptr;     // [M][E] per-channel outlier scales, valid at outlier positions only
+    int J = 0;                    // mask words per row, ceil(E/32)
 };
 
 struct K1Params {
@@ -37,16 +37,18 @@ struct K1Params {
     int order = -1, grid = 0;     // step t reads canonical row scan_perm(order, t); -1 = identity
     int mode = MODE_DYNAMIC, n_refresh = 10, abits = 8, obits = 8, window = 10;
     SiteCal cal;
-    // quantized outputs (rows in step order, row = s*T + t)
+    const double* inv_in = nullptr;    // optional [T] 1/s_in (host-computed); else divided in-kernel
+    const double* inv_full = nullptr;  // optional [T] 1/s_full
+    double* rs = nullptr;              // [S*T] D1 row factors (workspace of the fast RMSNorm path)
+    int force_literal = 0;             // run the literal detector kernel
+    // quantized outputs (rows in step order, row = s*T + t): the QAct operand
     int8_t* codes = nullptr;
     double* s_row = nullptr;
     int* ocnt = nullptr;
-    uint16_t* och = nullptr;
-    int8_t* ocode = nullptr;
-    double* oscale = nullptr;
-    int cap = 0;
-    uint32_t* omask = nullptr;    // optional [S*T][ceil(E/32)]
-    uint8_t* scanned = nullptr;   // optional [S*T]
+    uint32_t* omask = nullptr;    // [S*T][ceil(E/32)]
+    int8_t* ocode = nullptr;      // [S*T][E] dense
+    double* oscale = nullptr;     // [S*T][E] dense
+    uint8_t* scanned = nullptr;   // optional [S*T] (DetectResult::scanned; literal kernel only)
     // FP mode outputs
     double* xout = nullptr;                 // [S*T][E] materialized input rows
     unsigned long long* peaks = nullptr;    // [T][E] running max |x| (f64 bits), calibration

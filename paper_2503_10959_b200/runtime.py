@@ -127,25 +127,27 @@ class Context:
 
     # ---- operators (device tensors) --------------------------------------------
     def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
-                        mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, out=None,
-                        omask=None, scanned=None):
-        """K1 over S x T planes. Returns dict of device tensors (codes, s_row, ocnt, och, ocode, oscale)."""
+                        mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, literal=False,
+                        scanned=None):
+        """K1 over S x T planes. Returns the QAct operand as a dict of device
+        tensors: codes, s_row, ocnt, omask (uint32 words), ocode/oscale (dense,
+        valid at outlier positions)."""
         import torch
         dev = x.device
         rows = S * T
-        o = out or {}
-        codes = o.get("codes") if o.get("codes") is not None else torch.empty(rows, E, dtype=torch.int8, device=dev)
-        s_row = o.get("s_row") if o.get("s_row") is not None else torch.empty(rows, dtype=torch.float64, device=dev)
-        ocnt = o.get("ocnt") if o.get("ocnt") is not None else torch.empty(rows, dtype=torch.int32, device=dev)
-        och = o.get("och") if o.get("och") is not None else torch.empty(rows, E, dtype=torch.int16, device=dev)
-        ocode = o.get("ocode") if o.get("ocode") is not None else torch.empty(rows, E, dtype=torch.int8, device=dev)
-        oscale = o.get("oscale") if o.get("oscale") is not None else torch.empty(rows, E, dtype=torch.float64,
-                                                                                  device=dev)
+        J = (E + 31) // 32
+        codes = torch.empty(rows, E, dtype=torch.int8, device=dev)
+        s_row = torch.empty(rows, dtype=torch.float64, device=dev)
+        ocnt = torch.empty(rows, dtype=torch.int32, device=dev)
+        omask = torch.zeros(rows, J, dtype=torch.int32, device=dev)
+        ocode = torch.zeros(rows, E, dtype=torch.int8, device=dev)
+        oscale = torch.zeros(rows, E, dtype=torch.float64, device=dev)
+        rs = torch.empty(rows, dtype=torch.float64, device=dev) if src == L.SRC_RMSNORM else None
         L.check(self.lib.ouro_b200_detect_quantize(
             self.h, _ptr(x), _ptr(x2), _ptr(gate), S, T, E, src, order, grid, float(theta), _ptr(s_in), _ptr(s_full),
-            n_refresh, act_bits, outlier_bits, mode, _ptr(codes), _ptr(s_row), _ptr(ocnt), _ptr(och), _ptr(ocode),
-            _ptr(oscale), E, _ptr(omask), _ptr(scanned)))
-        return dict(codes=codes, s_row=s_row, ocnt=ocnt, och=och, ocode=ocode, oscale=oscale)
+            n_refresh, act_bits, outlier_bits, mode, int(literal), _ptr(codes), _ptr(s_row), _ptr(ocnt), _ptr(omask),
+            _ptr(ocode), _ptr(oscale), _ptr(scanned), _ptr(rs)))
+        return dict(codes=codes, s_row=s_row, ocnt=ocnt, omask=omask, ocode=ocode, oscale=oscale)
 
     def quant_linear(self, act: dict, w, wt, ws, *, post=L.POST_STORE, out=None, out2=None, split=0, acc_in=None,
                      acc_out=None):
@@ -157,8 +159,8 @@ class Context:
             out = torch.empty(M, R, dtype=torch.float64, device=w.device)
         ld = out.shape[1]
         L.check(self.lib.ouro_b200_quant_linear(
-            self.h, M, R, K, _ptr(act["codes"]), _ptr(act["s_row"]), _ptr(act["ocnt"]), _ptr(act["och"]),
-            _ptr(act["ocode"]), _ptr(act["oscale"]), act["codes"].shape[1], _ptr(w), _ptr(wt), _ptr(ws), post,
+            self.h, M, R, K, _ptr(act["codes"]), _ptr(act["s_row"]), _ptr(act["ocnt"]), _ptr(act["omask"]),
+            _ptr(act["ocode"]), _ptr(act["oscale"]), _ptr(w), _ptr(wt), _ptr(ws), post,
             _ptr(out), ld, _ptr(out2), split, None, _ptr(acc_in), _ptr(acc_out)))
         return out
 

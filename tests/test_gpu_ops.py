@@ -1,8 +1,8 @@
 """Operator-level GPU parity (K1 detector/quantizer, K2 quant-linear) against
 the oracle's restatement of detect_outliers / split_quantize / hybrid_gemm.
 Mirrors the reference's own operator tests (tests/test_gemm.cpp,
-tests/test_quant.cpp): integer planes bit-exact, output == scale
-decomposition."""
+tests/test_quant.cpp): integer planes bit-exact, output == the reference's
+fused epilogue bit-for-bit."""
 import numpy as np
 import pytest
 
@@ -12,6 +12,21 @@ pytestmark = pytest.mark.gpu
 def _dev(a):
     import torch
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _mask_words(mask_rows: np.ndarray) -> np.ndarray:
+    """[M][K] 0/1 -> [M][ceil(K/32)] uint32 words (bit ch%32 of word ch/32)."""
+    M, K = mask_rows.shape
+    J = (K + 31) // 32
+    padded = np.zeros((M, J * 32), np.uint64)
+    padded[:, :K] = mask_rows
+    w = (padded.reshape(M, J, 32) << np.arange(32, dtype=np.uint64)).sum(axis=2)
+    return w.astype(np.uint32).view(np.int32)
+
+
+def _unpack(words: np.ndarray, K: int) -> np.ndarray:
+    w = words.view(np.uint32)
+    return ((w[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(w.shape[0], -1)[:, :K].astype(np.uint8)
 
 
 @pytest.mark.parametrize("M,R,K,n_o", [(128, 128, 128, 0), (300, 160, 256, 5), (1000, 800, 768, 12),
@@ -24,16 +39,21 @@ def test_quant_linear_shared_outliers_bit_exact(oracle_checker, gpu_ctx, M, R, K
     w = rng.integers(-7, 8, size=(R, K), dtype=np.int8)
     ws = rng.uniform(0.005, 0.02, size=R)
     x = rng.integers(-7, 8, size=(M, K), dtype=np.int8)   # rows = tokens (columns of the reference plane)
-    chans = np.sort(rng.choice(K, size=n_o, replace=False)).astype(np.uint64)
-    x[:, chans.astype(np.int64)] = 0
+    chans = np.sort(rng.choice(K, size=n_o, replace=False)).astype(np.int64)
+    x[:, chans] = 0
     ocodes = rng.integers(-127, 128, size=(n_o, M), dtype=np.int8)
     oscales = rng.uniform(0.005, 0.02, size=n_o)
     s_in = float(rng.uniform(0.005, 0.02))
-    acc_in, acc_out, out = oracle_checker.hybrid_gemm(w, ws, x.T.copy(), s_in, chans, ocodes, oscales)
+    acc_in, acc_out, out = oracle_checker.hybrid_gemm(w, ws, x.T.copy(), s_in, chans.astype(np.uint64), ocodes,
+                                                      oscales)
+    mask = np.zeros((M, K), np.uint8)
+    mask[:, chans] = 1
+    dense_code = np.zeros((M, K), np.int8)
+    dense_code[:, chans] = ocodes.T
+    dense_scale = np.zeros((M, K), np.float64)
+    dense_scale[:, chans] = oscales
     act = dict(codes=_dev(x), s_row=_dev(np.full(M, s_in)), ocnt=_dev(np.full(M, n_o, np.int32)),
-               och=_dev(np.tile(np.pad(chans.astype(np.int16), (0, K - n_o)), (M, 1))),
-               ocode=_dev(np.pad(ocodes.T, ((0, 0), (0, K - n_o)))),
-               oscale=_dev(np.tile(np.pad(oscales, (0, K - n_o)), (M, 1))))
+               omask=_dev(_mask_words(mask)), ocode=_dev(dense_code), oscale=_dev(dense_scale))
     g_in = torch.zeros(M, R, dtype=torch.int32, device="cuda")
     g_out = torch.zeros(M, R, dtype=torch.int32, device="cuda")
     y = gpu_ctx.quant_linear(act, _dev(w), _dev(w.T.copy()), _dev(ws), acc_in=g_in, acc_out=g_out)
@@ -49,7 +69,7 @@ def test_quant_linear_validation(gpu_ctx):
     act = dict(codes=torch.zeros(4, 20, dtype=torch.int8, device="cuda"),
                s_row=torch.ones(4, dtype=torch.float64, device="cuda"),
                ocnt=torch.zeros(4, dtype=torch.int32, device="cuda"),
-               och=torch.zeros(4, 20, dtype=torch.int16, device="cuda"),
+               omask=torch.zeros(4, 1, dtype=torch.int32, device="cuda"),
                ocode=torch.zeros(4, 20, dtype=torch.int8, device="cuda"),
                oscale=torch.zeros(4, 20, dtype=torch.float64, device="cuda"))
     w = torch.zeros(32, 20, dtype=torch.int8, device="cuda")
@@ -57,10 +77,12 @@ def test_quant_linear_validation(gpu_ctx):
         gpu_ctx.quant_linear(act, w, w.t().contiguous(), torch.ones(32, dtype=torch.float64, device="cuda"))
 
 
+@pytest.mark.parametrize("literal", [False, True])
 @pytest.mark.parametrize("abits,n_refresh,mode", [(4, 3, 1), (8, 1, 1), (4, 0, 1), (4, 3, 2)])
-def test_detect_quantize_matches_oracle(oracle_checker, gpu_ctx, abits, n_refresh, mode):
+def test_detect_quantize_matches_oracle(oracle_checker, gpu_ctx, abits, n_refresh, mode, literal):
     """K1 == maybe_refresh + detect_outliers + split_quantize per (sample,
-    token) plane, state carried along the token order (D2)."""
+    token) plane, state carried along the token order (D2); both the
+    channel-parallel kernel and the literal one."""
     import torch
     S, T, E = 3, 40, 96
     rng = np.random.default_rng(abits * 10 + n_refresh)
@@ -72,20 +94,22 @@ def test_detect_quantize_matches_oracle(oracle_checker, gpu_ctx, abits, n_refres
     theta = float(np.quantile(clean.max(axis=0), 0.99)) * 1.5
     s_in = np.maximum(clean.max(axis=1), 1e-3) / qa
     s_full = s_in * 1.3
-    # oracle: detector state per sequence, then split_quantize per token
+    assert np.all(np.nextafter(theta, np.inf) / qa > s_in)  # the channel-local form is exact here
     _, masks, scanned = oracle_checker.quant_stream(x.reshape(S, T, E, 1), theta, s_in, s_full, n_refresh, abits, 8,
                                                     mode)
+    sc = torch.zeros(S * T, dtype=torch.uint8, device="cuda") if literal else None
     res = gpu_ctx.detect_quantize(_dev(x), S=S, T=T, E=E, theta=theta, s_in=_dev(s_in), s_full=_dev(s_full),
-                                  n_refresh=n_refresh, act_bits=abits, outlier_bits=8, mode=mode,
-                                  scanned=(sc := torch.zeros(S * T, dtype=torch.uint8, device="cuda")))
+                                  n_refresh=n_refresh, act_bits=abits, outlier_bits=8, mode=mode, literal=literal,
+                                  scanned=sc)
     torch.cuda.synchronize()
     codes = res["codes"].cpu().numpy().reshape(S, T, E)
     ocnt = res["ocnt"].cpu().numpy().reshape(S, T)
-    och = res["och"].cpu().numpy().view(np.uint16).reshape(S, T, E)
+    omask = _unpack(res["omask"].cpu().numpy(), E).reshape(S, T, E)
     ocode = res["ocode"].cpu().numpy().reshape(S, T, E)
     osc = res["oscale"].cpu().numpy().reshape(S, T, E)
     s_row = res["s_row"].cpu().numpy().reshape(S, T)
     n_outliers = 0
+    assert np.array_equal(omask, masks)
     for s in range(S):
         for t in range(T):
             chans = np.nonzero(masks[s, t])[0]
@@ -93,11 +117,35 @@ def test_detect_quantize_matches_oracle(oracle_checker, gpu_ctx, abits, n_refres
             inl, oc, os_ = oracle_checker.split_quantize(x[s, t].reshape(E, 1), chans, S_t, abits, 8)
             assert np.array_equal(codes[s, t], inl[:, 0]), (s, t)
             assert ocnt[s, t] == len(chans)
-            assert np.array_equal(och[s, t, :len(chans)], chans)
-            assert np.array_equal(ocode[s, t, :len(chans)], oc[:, 0])
-            assert np.array_equal(osc[s, t, :len(chans)], os_)
+            assert np.array_equal(ocode[s, t, chans], oc[:, 0])
+            assert np.array_equal(osc[s, t, chans], os_)
             assert s_row[s, t] == S_t
             n_outliers += len(chans)
     if mode == 1:
-        assert np.array_equal(sc.cpu().numpy().reshape(S, T), scanned)
+        if literal:
+            assert np.array_equal(sc.cpu().numpy().reshape(S, T), scanned)
         assert n_outliers > 0
+
+
+@pytest.mark.parametrize("src", [1, 2])
+def test_detect_quantize_sources(oracle_checker, gpu_ctx, src):
+    """RMSNorm (D1) and merge-gate sources: channel-parallel == literal kernel."""
+    import torch
+    S, T, E = 2, 25, 64
+    rng = np.random.default_rng(src)
+    x = _dev(rng.normal(size=(S, T, E)) * 3)
+    x2 = _dev(rng.normal(size=(S, T, E)))
+    gate = _dev(rng.normal(size=(S, T, E)))
+    s_in = _dev(np.full(T, 0.4))
+    outs = []
+    for lit in (False, True):
+        r = gpu_ctx.detect_quantize(x, S=S, T=T, E=E, theta=2.9, s_in=s_in, s_full=s_in, n_refresh=4, act_bits=4,
+                                    outlier_bits=8, mode=1, src=src, x2=x2, gate=gate, literal=lit)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in r.items()})
+    a, b = outs
+    for k in ("codes", "s_row", "ocnt", "omask"):
+        assert np.array_equal(a[k], b[k]), k
+    m = _unpack(a["omask"], E).astype(bool)
+    assert m.any()
+    assert np.array_equal(a["ocode"][m], b["ocode"][m]) and np.array_equal(a["oscale"][m], b["oscale"][m])
