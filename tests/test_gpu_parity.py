@@ -79,14 +79,18 @@ def _import_calib(gm, cal, spec):
     return gm.calibration_from([conv(t) for t in cal.scan], [conv(t) for t in cal.lin], _gspec(spec))
 
 
-@pytest.mark.parametrize("abits,mode,d2", [(4, 1, True), (8, 1, True), (4, 2, True), (4, 1, False), (8, 2, False)])
-def test_quantized_forward_logits(pair, abits, mode, d2):
+@pytest.mark.parametrize("abits,mode,d1,d2", [(4, 1, True, True), (8, 1, True, True), (4, 2, True, True),
+                                              (4, 1, True, False), (8, 2, True, False), (8, 1, False, False),
+                                              (8, 2, False, False)])
+def test_quantized_forward_logits(pair, abits, mode, d1, d2):
+    """d1 = d2 = False is the reference's own quantized pass (quantized_forward,
+    quant.cpp:519-526), which the oracle equals bit-for-bit (test_oracle_pin)."""
     om, gm, imgs, cimgs = pair
-    spec = _spec(abits, d2=d2)
+    spec = _spec(abits, d1=d1, d2=d2)
     ocal = om.calibrate(cimgs, spec)
     gcal = _import_calib(gm, ocal.export(), spec)
-    want = om.forward(imgs, ocal, mode, d1=True, d2=d2)
-    got = gm.forward_host(imgs, gcal, mode, d1=True, d2=d2)
+    want = om.forward(imgs, ocal, mode, d1=d1, d2=d2)
+    got = gm.forward_host(imgs, gcal, mode, d1=d1, d2=d2)
     assert rel_err(got, want) <= RTOL_F64, (got, want)
 
 
