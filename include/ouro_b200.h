@@ -45,7 +45,8 @@ typedef struct ouro_b200_trace ouro_b200_trace;
 /* Quantization modes (quant.hpp:101): FP = bypass (no activation quantization). */
 enum { OURO_B200_MODE_FP = 0, OURO_B200_MODE_DYNAMIC = 1, OURO_B200_MODE_STATIC = 2 };
 /* Quant-linear epilogue post-ops. */
-enum { OURO_B200_POST_STORE = 0, OURO_B200_POST_INPROJ = 1, OURO_B200_POST_RESID = 2, OURO_B200_POST_BIAS = 3 };
+enum { OURO_B200_POST_STORE = 0, OURO_B200_POST_INPROJ = 1, OURO_B200_POST_RESID = 2, OURO_B200_POST_BIAS = 3,
+       OURO_B200_POST_XPROJ = 4 /* first `split` columns: softplus(y + bias[r]) */ };
 /* K1 row sources. */
 enum { OURO_B200_SRC_PLAIN = 0, OURO_B200_SRC_RMSNORM = 1, OURO_B200_SRC_MERGE = 2 };
 
@@ -105,7 +106,8 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
 /* K3: selective scan of one direction with the QuantHook policy (s6_scan,
  * ssm.hpp:131-132, ssm.cpp:124-186; QuantHook quant.cpp:456-501), N = 16.
  *   u     dev f64 [S][T][E] canonical scan input; proj dev f64 [S][T][E+2N]
- *         rows in scan order = (delta pre-activation | B | C)
+ *         rows in scan order = (delta pre-activation | B | C), the x_proj
+ *         quant-linear output; delta = softplus(dpre + b_delta) in-kernel
  *   a     dev f64 [E][N]; b_delta dev f64 [E]; o dev f64 [S][T][E] (canonical)
  *   theta[3], s_in[3], s_full[3]: calibration of a_bar, b_bar, h (s_* dev [T])
  *   literal dev uint8 [T] (may be NULL): steps where the channel-local detector
@@ -178,6 +180,12 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
 ouro_status ouro_b200_forward_profile(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
                                       const double* images_dev, size_t B, double* logits_dev, double* ms,
                                       int* launches);
+
+/* Same, one entry per launch in issue order: family[k] (0-4 as above) and
+ * ms[k]; *n = number of launches (entries beyond cap are dropped). */
+ouro_status ouro_b200_forward_profile_launches(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                               const double* images_dev, size_t B, double* logits_dev, double* ms,
+                                               int* family, size_t cap, size_t* n);
 
 /* Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA),
  * the roofline denominator of the f64 scan (no vendor figure is used). */

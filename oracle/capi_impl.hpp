@@ -272,6 +272,7 @@ int oro_trace(void* m, void* c, int mode, int d1, int d2, const double* image, s
         put(*th, "xn", bt.xn);
         put(*th, "u0", bt.u0);
         put(*th, "gate", bt.gate);
+        put(*th, "gate_pre", bt.gpre);
         put(*th, "u", bt.u);
         put(*th, "merged", bt.merged);
         put(*th, "y", bt.y);

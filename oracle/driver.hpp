@@ -146,7 +146,7 @@ struct DirTrace {
     std::vector<std::uint8_t> scanned[3];            // L
 };
 struct BlockTrace {
-    std::vector<double> x_in, xn, u0, gate, u, merged, y, x_out;  // L x E
+    std::vector<double> x_in, xn, u0, gate, gpre, u, merged, y, x_out;  // L x E
     LinTrace lin[6];                                              // sites (ndirs <= 4)
     std::vector<DirTrace> dirs;
 };
@@ -404,6 +404,7 @@ struct Driver {
                 quant_linear(ss, b, 0, t, xn.data() + t * e, prep.blocks[b].in, out.data(), lt, 2 * e);
                 for (std::size_t i = 0; i < e; ++i) {
                     u0[t * e + i] = out[i];
+                    if (bt) bt->gpre.push_back(out[e + i]);
                     gate[t * e + i] = Ops::silu(out[e + i]);
                 }
             }
@@ -411,6 +412,7 @@ struct Driver {
             const double* wg = mode == MODE_FP ? blk.w_gate.data() : q->blocks[b].in.deq.data() + e * e;
             const double* wi = mode == MODE_FP ? blk.w_in.data() : q->blocks[b].in.deq.data();
             Ops::mm_nt(xn.data(), wg, gate.data(), L, e, e);
+            if (bt) bt->gpre = gate;
             for (double& v : gate) v = Ops::silu(v);
             Ops::mm_nt(xn.data(), wi, u0.data(), L, e, e);
         }

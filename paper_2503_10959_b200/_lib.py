@@ -20,7 +20,7 @@ _D = C.c_double
 
 OK, ERR_VALIDATION, ERR_NUMERIC, ERR_IO = 0, 2, 3, 4
 MODE_FP, MODE_DYNAMIC, MODE_STATIC = 0, 1, 2
-POST_STORE, POST_INPROJ, POST_RESID, POST_BIAS = 0, 1, 2, 3
+POST_STORE, POST_INPROJ, POST_RESID, POST_BIAS, POST_XPROJ = 0, 1, 2, 3, 4
 SRC_PLAIN, SRC_RMSNORM, SRC_MERGE = 0, 1, 2
 
 _SIGS = {
@@ -53,6 +53,7 @@ _SIGS = {
     "ouro_b200_model_use_graphs": ([_P, _I], _I),
     "ouro_b200_model_set_option": ([_P, C.c_char_p, C.c_long], _I),
     "ouro_b200_forward_profile":([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P], _I),
+    "ouro_b200_forward_profile_launches": ([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_trace_run": ([_P, _P, _I, _I, _I, _P, _SZ, _SZ, C.POINTER(_P)], _I),
     "ouro_b200_trace_get": ([_P, C.c_char_p, _P, _SZ, C.POINTER(_SZ)], _I),

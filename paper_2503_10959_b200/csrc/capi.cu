@@ -155,6 +155,7 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
         require(post != ob::POST_INPROJ || (out2 != nullptr && split % 32 == 0 && split < R),
                 "quant_linear: in_proj post-op needs out2 and a split that is a multiple of 32");
         require(post != ob::POST_BIAS, "quant_linear: bias post-op is not part of the hybrid epilogue");
+        require(post != ob::POST_XPROJ || (bias != nullptr && split <= R), "quant_linear: x_proj post-op needs bias");
         ob::QLinParams q;
         q.M = static_cast<int>(M);
         q.R = static_cast<int>(R);
@@ -490,6 +491,32 @@ ouro_status ouro_b200_forward_profile(ouro_b200_model* m, ouro_b200_calib* c, in
         for (int i = 0; i < ob::Model::FAM_COUNT; ++i) {
             ms[i] = mm.timing.ms[i];
             launches[i] = mm.timing.launches[i];
+        }
+    });
+}
+
+ouro_status ouro_b200_forward_profile_launches(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
+                                               const double* images_dev, size_t B, double* logits_dev, double* ms,
+                                               int* family, size_t cap, size_t* n) {
+    return guarded([&] {
+        require(m && images_dev && logits_dev && ms && family && n, "forward_profile_launches: NULL argument");
+        ob::Model& mm = *m->m;
+        mm.timing = ob::Model::Timing{};
+        mm.timing.on = true;
+        mm.timing.keep_list = true;
+        try {
+            mm.forward(c ? c->c.get() : nullptr, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev,
+                       nullptr, nullptr);
+        } catch (...) {
+            mm.timing.on = false;
+            throw;
+        }
+        mm.timing_collect();
+        mm.timing.on = false;
+        *n = mm.timing.list.size();
+        for (size_t k = 0; k < std::min(cap, mm.timing.list.size()); ++k) {
+            family[k] = mm.timing.list[k].first;
+            ms[k] = mm.timing.list[k].second;
         }
     });
 }

@@ -529,7 +529,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         tick_end(FAM_AUX);
         if (tb(b)) {
             grab(trace, "u0", w.u0.p, rows * E, st);
-            grab(trace, "gate", w.gate.p, rows * E, st);
+            grab(trace, "gate_pre", w.gate.p, rows * E, st);
             grab(trace, "u", w.u.p, rows * E, st);
         }
         ScanParams sps[2];
@@ -542,7 +542,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             tick_begin(FAM_K1);
             cuda_check(launch_k1(kx, st), "K1 x_proj");
             tick_end(FAM_K1);
-            GemmEpi e;
+            GemmEpi e;  // dpre | B | C (softplus(dpre + b_delta) runs in the scan's chunk pre-pass)
             e.post = POST_STORE;
             e.out = proj;
             e.ld_out = P;
@@ -662,6 +662,7 @@ void Model::timing_collect() {
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, e.second.first, e.second.second), "elapsed");
         timing.ms[e.first] += ms;
+        if (timing.keep_list) timing.list.push_back({e.first, static_cast<double>(ms)});
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
     }

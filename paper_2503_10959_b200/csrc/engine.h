@@ -165,6 +165,8 @@ class Model {
         std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
         double ms[FAM_COUNT] = {0, 0, 0, 0, 0};
         int launches[FAM_COUNT] = {0, 0, 0, 0, 0};
+        bool keep_list = false;
+        std::vector<std::pair<int, double>> list;  // (family, ms) per launch, in order
     } timing;
     void tick_begin(int fam);
     void tick_end(int fam);

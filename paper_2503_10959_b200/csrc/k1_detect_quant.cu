@@ -66,7 +66,7 @@ __device__ __forceinline__ double2 k1_load2(const K1Params& p, size_t src, size_
             m0 = dadd(m0, b.x);
             m1 = dadd(m1, b.y);
         }
-        return make_double2(dmul(m0, g.x), dmul(m1, g.y));
+        return make_double2(dmul(m0, silu_d(g.x)), dmul(m1, silu_d(g.y)));  // gate = silu(x W_g^T)
     }
     double2 v = *reinterpret_cast<const double2*>(p.x + src);
     if (SRC == K1_SRC_RMSNORM) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256) k1_literal(const K1Params p) {
                 if (SRC == K1_SRC_MERGE) {
                     double m = dadd(0.0, p.x[src + ch]);
                     if (p.x2) m = dadd(m, p.x2[src + ch]);
-                    x = dmul(m, p.gate[src + ch]);
+                    x = dmul(m, silu_d(p.gate[src + ch]));
                 } else {
                     x = p.x[src + ch];
                 }

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int rr = 0; rr < nrows; ++rr) {
                     double v = dmul(wsr, stage[rr * 33 + lane]);
                     double* dst = obase + static_cast<size_t>(rbase + rr) * ld + ocol;
-                    if (gate) v = silu_d(v);
+                    if (p.epi.post == POST_XPROJ && col < p.epi.split) v = softplus_d(dadd(v, p.epi.bias[col]));
                     if (p.epi.post == POST_RESID && cv) v = dadd(*dst, v);
                     if (cv) *dst = v;
                 }

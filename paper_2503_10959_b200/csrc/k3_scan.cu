@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(LITERAL ? 1024 : 128) k3_scan(const ScanParams
         const double dpre = active ? pr[i] : 0.0;
         const double uv = active ? p.u[(static_cast<size_t>(s) * T + c) * E + i] : 0.0;
         const bool lit = LITERAL && (p.force_literal || (p.literal && p.literal[t]));
-        const double delta = softplus_d(dadd(dpre, bd));
+        const double delta = softplus_d(dadd(dpre, bd));  // ssm.cpp:150-151
         double a[N], b[N];
 #pragma unroll
         for (int m = 0; m < N; ++m) {

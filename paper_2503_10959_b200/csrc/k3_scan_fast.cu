@@ -46,7 +46,7 @@ struct StepShared {
     double B[16], C[16];
     double Sa, Sb, Sh, invSh, Bmax;
     float BSf[16];  // f32(B_m) * f32(1/S_b): the inlier b_bar quotient per unit delta
-    float invSaf, invSbf;
+    float invSaf, invSbf, invShf;
     float halfA;  // 0.5 - certification margin of the inlier a_bar quotient at this step
     int refresh;
     int crow;  // canonical token of this scan step (ssm.cpp:30-46)
@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
     for (int m = 0; m < 8; ++m) h[m] = 0.0;
     bool inA = false, inB = false, inH = false;
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
+    const float thHf = __double2float_rn(thH);
 
     for (int t0 = 0; t0 < T; t0 += kChunk) {
         const int nt = min(kChunk, T - t0);
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             ss.Sb = Sb;
             ss.Sh = Sh;
             ss.invSh = __ddiv_rn(1.0, Sh);
+            ss.invShf = __double2float_rn(ss.invSh);
             ss.invSaf = __double2float_rn(__ddiv_rn(1.0, Sa));
             ss.invSbf = __double2float_rn(__ddiv_rn(1.0, Sb));
             ss.halfA = 0.5f - fmaf(static_cast<float>(qa) + 1.0f,
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
 #pragma unroll
             for (int j = 0; j < kChunk / 2; ++j) {
                 const int tt = half * (kChunk / 2) + j;
-                const double delta = softplus_d(dadd(dp[j], bd));
+                const double delta = softplus_d(dadd(dp[j], bd));  // ssm.cpp:150-151
                 sh.delta[tt][c] = delta;
                 sh.deltaf[tt][c] = __double2float_rn(delta);
                 sh.peak_a[tt][c] = exp(dmul(delta, Amax));
@@ -213,69 +215,100 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             const float halfB = 0.5f - fmaf(qBf + 1.0f, 7.1525574e-7f, 1e-6f);
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
             // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23),
-            // clamped before rounding so the integer is the reference's clipped code
+            // clamped before rounding so the integer is the reference's clipped code.
+            // An element within its error bound of a half-integer sends the step
+            // through the exact pass (rate ~1e-4).
             int ca[8], cb[8];
-            unsigned fail = (EXACT || sA < 1e-30) ? 0xFFFFu : 0u;  // ex2.approx.ftz flushes below 2^-126
+            bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
                 const float qa_f = fminf(ex2_approx(df * A2f[m]) * invA, capA);
                 const float ta = qa_f + 12582912.0f;
                 ca[m] = __float_as_int(ta) - 0x4B400000;
-                fail |= (fabsf(qa_f - (ta - 12582912.0f)) > halfA) ? (1u << m) : 0u;
+                redo |= fabsf(qa_f - (ta - 12582912.0f)) > halfA;
                 const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                 const float tb = qb_f + 12582912.0f;
                 cb[m] = __float_as_int(tb) - 0x4B400000;
-                fail |= (fabsf(qb_f - (tb - 12582912.0f)) > halfB) ? (1u << (m + 8)) : 0u;
+                redo |= fabsf(qb_f - (tb - 12582912.0f)) > halfB;
             }
-            if (fail) {  // rare: q within its error bound of a half-integer -> exact f64 code
+            if (redo) {  // exact f64 codes where the f32 quotient is not certified
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
-                    if ((fail >> m) & 1u) {
+                    const float qa_f = fminf(ex2_approx(df * A2f[m]) * invA, capA);
+                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA) {
                         const double ax = exp(dmul(delta, p.a[static_cast<size_t>(active ? i : 0) * 16 + m0 + m]));
                         ca[m] = static_cast<int>(quant_code_div(ax, sA, static_cast<double>(qAf)));
                     }
-                    if ((fail >> (m + 8)) & 1u)
+                    const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
+                    if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
                         cb[m] = static_cast<int>(quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
                 }
             }
-            // pass 2: dequantized values (code * s, fake_quant_step) and the update
+            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
                 const double a_q = dmul(int_to_double_small(ca[m]), sA);
                 const double b_q = dmul(int_to_double_small(cb[m]), sB);
                 h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
             }
-            double ph = 0.0;
+            // h detection + codes. Rounding to f32 is monotone, so the f32 peak
+            // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
+            // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
+            // needs the exact f64 peak. Outlier channels (rare) take the exact peak
+            // for their scale.
+            float hfv[8];
+            float phf = 0.0f;
 #pragma unroll
-            for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
-            ph = fmax(ph, __shfl_xor_sync(0xffffffffu, ph, 1));
-            if (dyn && ph > thH) inH = true;
-            double sH, invH, qH;
+            for (int m = 0; m < 8; ++m) {
+                hfv[m] = __double2float_rn(h[m]);
+                phf = fmaxf(phf, fabsf(hfv[m]));
+            }
+            phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
+            const unsigned pair = 3u << (lane & ~1u);
+            if (dyn && !inH) {
+                if (phf > thHf) {
+                    inH = true;
+                } else if (phf == thHf) {
+                    double ph = 0.0;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                    ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                    if (ph > thH) inH = true;
+                }
+            }
+            double sH, qH;
+            float invHf;
             if (inH) {
+                double ph = 0.0;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
                 sH = scale_from_peak(ph, qo);
-                invH = __ddiv_rn(1.0, sH);
+                invHf = __double2float_rn(__ddiv_rn(1.0, sH));
                 qH = qo;
             } else {
                 sH = ss.Sh;
-                invH = ss.invSh;
+                invHf = ss.invShf;
                 qH = qa;
             }
-            {  // h codes: q = h * (1/sH) clamped to +-(qH + 1/4), rounded with 1.5*2^52 (the low word
-               // is the integer); within 1e-12 of a half-integer the IEEE quotient decides
+            {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
+                const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
+                const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
                 int ch[8];
-                unsigned hf = 0;
-                const double capH = qH + 0.25;
+                bool hredo = EXACT;
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
-                    const double q2 = fmin(fmax(dmul(h[m], invH), -capH), capH);
-                    const double th = dadd(q2, 6755399441055744.0);
-                    ch[m] = __double2loint(th);
-                    hf |= (fabs(dadd(q2, -dadd(th, -6755399441055744.0))) > 0.4999999999990) ? (1u << m) : 0u;
+                    const float q = fminf(fmaxf(hfv[m] * invHf, -capH), capH);
+                    const float th = q + 12582912.0f;
+                    ch[m] = __float_as_int(th) - 0x4B400000;
+                    hredo |= fabsf(q - (th - 12582912.0f)) > halfH;
                 }
-                if (hf) {
+                if (hredo) {
 #pragma unroll
-                    for (int m = 0; m < 8; ++m)
-                        if ((hf >> m) & 1u) ch[m] = static_cast<int>(quant_code_div(h[m], sH, qH));
+                    for (int m = 0; m < 8; ++m) {
+                        const float q = fminf(fmaxf(hfv[m] * invHf, -capH), capH);
+                        if (EXACT || fabsf(q - rintf(q)) > halfH) ch[m] = static_cast<int>(quant_code_div(h[m], sH, qH));
+                    }
                 }
 #pragma unroll
                 for (int m = 0; m < 8; ++m) h[m] = dmul(int_to_double_small(ch[m]), sH);  // carried state

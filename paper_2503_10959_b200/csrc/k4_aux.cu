@@ -60,12 +60,15 @@ __global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
             switch (e.post) {
                 case POST_INPROJ:
                     if (r >= e.split) {
-                        e.out2[static_cast<size_t>(m) * e.split + (r - e.split)] = silu_d(y);
+                        e.out2[static_cast<size_t>(m) * e.split + (r - e.split)] = y;  // SiLU applied by K1 (merge)
                         continue;
                     }
                     break;
                 case POST_RESID: y = dadd(e.out[static_cast<size_t>(m) * e.ld_out + r], y); break;
                 case POST_BIAS: y = dadd(y, e.bias[r]); break;
+                case POST_XPROJ:
+                    if (r < e.split) y = softplus_d(dadd(y, e.bias[r]));
+                    break;
                 default: break;
             }
             e.out[static_cast<size_t>(m) * e.ld_out + r] = y;

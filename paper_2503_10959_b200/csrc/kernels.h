@@ -58,9 +58,10 @@ cudaError_t launch_k1(const K1Params& p, cudaStream_t st);
 // Post-ops fused into the quant-linear / f64 GEMM epilogues.
 enum PostOp {
     POST_STORE = 0,    // out[m][r] = y
-    POST_INPROJ = 1,   // r <  E: u0[m][r] = y ; r >= E: gate[m][r-E] = silu(y)   (ssm.cpp:196-198)
+    POST_INPROJ = 1,   // r <  E: u0[m][r] = y ; r >= E: gate_pre[m][r-E] = y (SiLU in the merge K1) (ssm.cpp:196-198)
     POST_RESID = 2,    // out[m][r] += y   (D1 residual)
     POST_BIAS = 3,     // out[m][r] = y + bias[r]  (patch embed / head, ssm.cpp:254-256, 271-274)
+    POST_XPROJ = 4,    // r < split: out = softplus(y + bias[r]) (delta, ssm.cpp:150-151); else out = y (B | C)
 };
 
 struct GemmEpi {

@@ -329,6 +329,21 @@ class Model:
                                                    _ptr(images), B, _ptr(logits), ms, n))
         return logits, {f: (ms[i], n[i]) for i, f in enumerate(self.FAMILIES)}
 
+    def forward_profile_launches(self, images, calib, mode: int, *, d1=True, d2=True, logits=None):
+        """One forward with CUDA events around every launch -> [(family, ms)] in issue order."""
+        import torch
+        B = images.numel() // self.dims.pix
+        if logits is None:
+            logits = torch.empty(B, self.dims.classes, dtype=torch.float64, device=images.device)
+        cap = 4096
+        ms = (C.c_double * cap)()
+        fam = (C.c_int * cap)()
+        n = C.c_size_t()
+        L.check(self.lib.ouro_b200_forward_profile_launches(self.h, calib.h if calib else None, mode, int(d1),
+                                                            int(d2), _ptr(images), B, _ptr(logits), ms, fam, cap,
+                                                            C.byref(n)))
+        return [(self.FAMILIES[fam[k]], ms[k]) for k in range(min(n.value, cap))]
+
     def forward_host(self, images: np.ndarray, calib: Calibration | None, mode: int, *, d1=True, d2=True,
                      logits: np.ndarray | None = None) -> np.ndarray:
         """End-to-end call with host buffers (H2D + forward + D2H inside)."""

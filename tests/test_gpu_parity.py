@@ -112,7 +112,7 @@ def test_block_trace_bit_exact(pair, abits):
     for s in range(B):
         ot = om.trace(imgs[s], ocal, 1, blk)
         rows = slice(s * L, (s + 1) * L)
-        for key in ("x_in", "u0", "gate", "u", "x_out"):
+        for key in ("x_in", "u0", "gate_pre", "u", "x_out"):
             g = gt.get(key, np.float64).reshape(B * L, E)[rows]
             assert rel_err(g, ot.get(key).reshape(L, E)) <= RTOL_F64, key
         for site, R in ((0, 2 * E), (1, E + 2 * N), (2, E + 2 * N), (3, E)):
