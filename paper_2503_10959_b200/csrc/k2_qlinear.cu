@@ -37,14 +37,15 @@ struct K2Smem {
     static constexpr int kABytes = kBM * kBK;
     static constexpr int kBBytes = BN * kBK;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kEpiOff = kStages * kStageBytes;              // per-warp 32 x 33 f64 transpose tiles
-    static constexpr int kBarOff = kEpiOff + kEpiWarps * 32 * 33 * 8;
+    static constexpr int kEpiOff = kStages * kStageBytes;  // per-warp 32 x 32 f64 output tiles (2 TMA boxes)
+    static constexpr int kBarOff = kEpiOff + kEpiWarps * 8192;
     static constexpr int kTotal = kBarOff + 256 + 1024;  // barriers + tmem slot + alignment slack
 };
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const QLinParams p) {
+    k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, const QLinParams p) {
     using L = K2Smem<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -52,7 +53,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + kStages;
     uint64_t* acc_full = empty + kStages;
     uint64_t* acc_empty = acc_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* res_bar = acc_empty + 2;  // per epilogue warp: residual tile loads
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + kEpiWarps);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.R + BN - 1) / BN;
@@ -70,6 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(acc_full + s, 1);
             ptx::mbar_init(acc_empty + s, kEpiWarps);  // one arrive per epilogue warp
         }
+        for (int w = 0; w < kEpiWarps; ++w) ptx::mbar_init(res_bar + w, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<2 * BN>(tmem_slot);
@@ -131,8 +134,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ew = warp - 4;
         const int q = warp & 3;       // TMEM lanes 32q..32q+31 (a warp may only touch its quarter)
         const int chalf = ew >> 2;    // which half of the BN columns
-        double* stage = reinterpret_cast<double*>(smem + L::kEpiOff) + ew * (32 * 33);
+        // per-warp output tile: two 32-row x 16-double boxes, 128B-swizzled (TMA layout)
+        uint8_t* stg = smem + L::kEpiOff + ew * 8192;
+        uint64_t* rbar = res_bar + ew;
+        uint32_t rphase = 0;
         const bool want_out = p.epi.acc_out != nullptr;
+        const bool resid = p.epi.post == POST_RESID;
         int it = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
@@ -150,10 +157,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int c = chalf * (BN / 64) + cc;
                 const int r0 = n0 + c * 32;
                 if (r0 >= p.R) break;  // uniform across the warp
+                const bool to2 = p.epi.post == POST_INPROJ && r0 >= p.epi.split;
+                const CUtensorMap* om = to2 ? &tmO2 : &tmO;
+                const int oc0 = to2 ? r0 - p.epi.split : r0;
+                if (lane == 0) {
+                    ptx::bulk_wait_read0();  // the previous tile's store has left the staging buffer
+                    if (resid) {             // D1 residual: bring x[rows][r0..r0+31] into the staging tile
+                        ptx::mbar_arrive_expect_tx(rbar, 8192);
+                        ptx::tma_load_2d(stg, om, rbar, oc0, rbase);
+                        ptx::tma_load_2d(stg + 4096, om, rbar, oc0 + 16, rbase);
+                    }
+                }
+                __syncwarp();
                 uint32_t acc[32];
                 ptx::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * BN + c * 32, acc);
-                // phase 1, thread = row: S_m * acc (gemm.cpp:207) + outlier terms in ascending
-                // channel order (gemm.cpp:208-216), staged transposed through shared memory
+                // thread = row: S_m * acc (gemm.cpp:207), outlier terms in ascending channel
+                // order (gemm.cpp:208-216), ws[r] * y (gemm.cpp:218-219), post-op
                 double y[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) y[j] = dmul(S, static_cast<double>(static_cast<int32_t>(acc[j])));
@@ -184,8 +203,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (want_out) aout[j] += wq * xo_i;
                     }
                 }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = y[j];
                 if (rv && (p.epi.acc_in || want_out)) {  // parity planes (test path)
                     const int nv = min(32, p.R - r0);
                     for (int j = 0; j < nv; ++j) {
@@ -193,39 +210,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (want_out) p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
                     }
                 }
-                __syncwarp();
-                // phase 2, lane = column: ws[r] * y (gemm.cpp:218-219) + post-op, coalesced rows
-                const int col = r0 + lane;
-                const bool cv = col < p.R;
-                const double wsr = cv ? __ldg(p.ws + col) : 0.0;
-                const bool gate = p.epi.post == POST_INPROJ && r0 >= p.epi.split;
-                double* obase;
-                size_t ld;
-                int ocol;
-                if (gate) {
-                    obase = p.epi.out2;
-                    ld = static_cast<size_t>(p.epi.split);
-                    ocol = col - p.epi.split;
-                } else {
-                    obase = p.epi.out;
-                    ld = static_cast<size_t>(p.epi.ld_out);
-                    ocol = col;
+                if (resid) {
+                    ptx::mbar_wait(rbar, rphase);
+                    rphase ^= 1;
                 }
-                const int nrows = min(32, p.M - rbase);
-#pragma unroll 4
-                for (int rr = 0; rr < nrows; ++rr) {
-                    double v = dmul(wsr, stage[rr * 33 + lane]);
-                    double* dst = obase + static_cast<size_t>(rbase + rr) * ld + ocol;
-                    if (p.epi.post == POST_XPROJ && col < p.epi.split) v = softplus_d(dadd(v, p.epi.bias[col]));
-                    if (p.epi.post == POST_RESID && cv) v = dadd(*dst, v);
-                    if (cv) *dst = v;
+#pragma unroll
+                for (int j2 = 0; j2 < 16; ++j2) {  // 16-byte chunk j2 = columns 2*j2, 2*j2+1
+                    double2* cell = reinterpret_cast<double2*>(stg + (j2 >> 3) * 4096 + lane * 128 +
+                                                               (((j2 & 7) ^ (lane & 7)) << 4));
+                    double v0 = y[2 * j2], v1 = y[2 * j2 + 1];
+                    const int ca = r0 + 2 * j2;
+                    v0 = dmul(ca < p.R ? __ldg(p.ws + ca) : 0.0, v0);
+                    v1 = dmul(ca + 1 < p.R ? __ldg(p.ws + ca + 1) : 0.0, v1);
+                    if (p.epi.post == POST_XPROJ) {
+                        if (ca < p.epi.split) v0 = softplus_d(dadd(v0, p.epi.bias[ca]));
+                        if (ca + 1 < p.epi.split) v1 = softplus_d(dadd(v1, p.epi.bias[ca + 1]));
+                    }
+                    if (resid) {
+                        const double2 x = *cell;
+                        v0 = dadd(x.x, v0);
+                        v1 = dadd(x.y, v1);
+                    }
+                    *cell = make_double2(v0, v1);
                 }
+                ptx::fence_async_smem();
                 __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(om, stg, oc0, rbase);
+                    ptx::tma_store_2d(om, stg + 4096, oc0 + 16, rbase);
+                    ptx::bulk_commit();
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(acc_empty + buf);
         }
+        if (lane == 0) ptx::bulk_wait0();
     }
     __syncthreads();
     if (warp == 2) ptx::tmem_dealloc<2 * BN>(tmem_base);
@@ -258,10 +278,30 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int b
     return r == CUDA_SUCCESS;
 }
 
+// 2-D f64 tensor [rows][cols] (row pitch ld doubles): 32-row x 16-double boxes, 128B swizzle.
+static bool make_map_f64(CUtensorMap* m, const double* base, int rows, int cols, int ld) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+    cuuint32_t box[2] = {16, 32};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <int BN>
 static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) {
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, to, to2;
     if (!make_map(&ta, p.a.codes, p.M, p.K, kBM) || !make_map(&tb, p.w, p.R, p.K, BN)) return cudaErrorInvalidValue;
+    const bool inproj = p.epi.post == POST_INPROJ;
+    const int ocols = inproj ? p.epi.split : p.R;
+    if (!make_map_f64(&to, p.epi.out, p.M, ocols, p.epi.ld_out)) return cudaErrorInvalidValue;
+    if (!make_map_f64(&to2, inproj ? p.epi.out2 : p.epi.out, p.M, inproj ? p.R - p.epi.split : ocols,
+                      inproj ? p.epi.split : p.epi.ld_out))
+        return cudaErrorInvalidValue;
     const int smem = K2Smem<BN>::kTotal;
     static bool attr_set = false;
     if (!attr_set) {
@@ -271,13 +311,14 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
     }
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
-    k2_qlinear<BN><<<grid, kThreads, smem, st>>>(ta, tb, p);
+    k2_qlinear<BN><<<grid, kThreads, smem, st>>>(ta, tb, to, to2, p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.M < 1 || p.R < 1 || p.K < 1 || (p.K % 16) != 0 || (p.R % 16) != 0) return cudaErrorInvalidValue;
     if (p.epi.post == POST_INPROJ && (p.epi.split % 32) != 0) return cudaErrorInvalidValue;
+    if ((p.epi.ld_out % 2) != 0) return cudaErrorInvalidValue;  // TMA: 16-byte row pitch
     return launch_bn<128>(p, st, num_sms);
 }
 

@@ -10,12 +10,13 @@ codes = torch.randint(-7, 8, (M, K), dtype=torch.int8, device="cuda", generator=
 w = torch.randint(-7, 8, (R, K), dtype=torch.int8, device="cuda", generator=g)
 wt = w.t().contiguous()
 ws = torch.rand(R, dtype=torch.float64, device="cuda", generator=g) * 0.01 + 0.005
-chans = torch.stack([torch.randperm(K, device="cuda", generator=g)[:max(n_o, 1)].sort().values for _ in range(1)])
-och = torch.zeros(M, K, dtype=torch.int16, device="cuda")
-if n_o:
-    och[:, :n_o] = chans[0, :n_o].to(torch.int16)
+chans = torch.randperm(K, device="cuda", generator=g)[:n_o].sort().values.cpu().numpy()
+words = np.zeros((K + 31) // 32, np.uint32)
+for ch in chans:
+    words[ch // 32] |= np.uint32(1) << np.uint32(ch % 32)
+omask = torch.from_numpy(np.tile(words.view(np.int32), (M, 1))).cuda()
 act = dict(codes=codes, s_row=torch.full((M,), 0.01, dtype=torch.float64, device="cuda"),
-           ocnt=torch.full((M,), n_o, dtype=torch.int32, device="cuda"), och=och,
+           ocnt=torch.full((M,), n_o, dtype=torch.int32, device="cuda"), omask=omask,
            ocode=torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda", generator=g),
            oscale=torch.rand(M, K, dtype=torch.float64, device="cuda", generator=g) * 0.01)
 out = torch.empty(M, R, dtype=torch.float64, device="cuda")
