@@ -94,7 +94,8 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
  *   + sum_{ch in O(m), ascending} (oscale[m][ch]*w[r][ch])*ocode[m][ch]),
  * then the post-op. The activation operand is K1's output (M rows of K
  * channels); w dev int8 [R][K] weight codes (|code| <= 7), wt its transpose
- * [K][R]; ws dev f64 [R] weight row scales. K and R must be multiples of 16.
+ * [K][R]; ws dev f64 [R] weight row scales. K must be a multiple of 16 and R
+ * of 32; acc_in and acc_out are requested together.
  * acc_in/acc_out (dev int32 [M][R], may be NULL) receive the reference's
  * integer planes GemmResult::acc_inlier / acc_outlier. */
 ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,

@@ -151,7 +151,8 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
     return guarded([&] {
         require(ctx && codes && s_row && ocnt && omask && ocode && oscale && w && wt && ws && out,
                 "quant_linear: NULL argument");
-        require(K % 16 == 0 && R % 16 == 0, "quant_linear: K and R must be multiples of 16");
+        require(K % 16 == 0 && R % 32 == 0, "quant_linear: K must be a multiple of 16 and R of 32");
+        require((acc_in == nullptr) == (acc_out == nullptr), "quant_linear: acc_in and acc_out go together");
         require(post != ob::POST_INPROJ || (out2 != nullptr && split % 32 == 0 && split < R),
                 "quant_linear: in_proj post-op needs out2 and a split that is a multiple of 32");
         require(post != ob::POST_BIAS, "quant_linear: bias post-op is not part of the hybrid epilogue");

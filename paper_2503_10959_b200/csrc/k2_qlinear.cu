@@ -42,7 +42,7 @@ struct K2Smem {
     static constexpr int kTotal = kBarOff + 256 + 1024;  // barriers + tmem slot + alignment slack
 };
 
-template <int BN>
+template <int BN, int POST, bool PLANES>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, const QLinParams p) {
@@ -138,8 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* stg = smem + L::kEpiOff + ew * 8192;
         uint64_t* rbar = res_bar + ew;
         uint32_t rphase = 0;
-        const bool want_out = p.epi.acc_out != nullptr;
-        const bool resid = p.epi.post == POST_RESID;
+        constexpr bool resid = POST == POST_RESID;
         int it = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
@@ -157,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int c = chalf * (BN / 64) + cc;
                 const int r0 = n0 + c * 32;
                 if (r0 >= p.R) break;  // uniform across the warp
-                const bool to2 = p.epi.post == POST_INPROJ && r0 >= p.epi.split;
+                const bool to2 = POST == POST_INPROJ && r0 >= p.epi.split;
                 const CUtensorMap* om = to2 ? &tmO2 : &tmO;
                 const int oc0 = to2 ? r0 - p.epi.split : r0;
                 if (lane == 0) {
@@ -176,8 +175,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 double y[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) y[j] = dmul(S, static_cast<double>(static_cast<int32_t>(acc[j])));
-                int32_t aout[32];
-                if (want_out)
+                int32_t aout[PLANES ? 32 : 1];
+                if (PLANES)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) aout[j] = 0;
                 // walk O(t) in ascending channel order: mask word by word, bit by bit
@@ -200,14 +199,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int wq = j < 16 ? wv[j] : wv2[j - 16];
                         const double coeff = dmul(osc, static_cast<double>(wq));
                         y[j] = dadd(y[j], dmul(coeff, xo));
-                        if (want_out) aout[j] += wq * xo_i;
+                        if (PLANES) aout[j] += wq * xo_i;
                     }
                 }
-                if (rv && (p.epi.acc_in || want_out)) {  // parity planes (test path)
-                    const int nv = min(32, p.R - r0);
-                    for (int j = 0; j < nv; ++j) {
-                        if (p.epi.acc_in) p.epi.acc_in[static_cast<size_t>(row) * p.R + r0 + j] = static_cast<int32_t>(acc[j]);
-                        if (want_out) p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
+                if (PLANES && rv) {  // the reference's integer planes (parity path)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        p.epi.acc_in[static_cast<size_t>(row) * p.R + r0 + j] = static_cast<int32_t>(acc[j]);
+                        p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
                     }
                 }
                 if (resid) {
@@ -219,10 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     double2* cell = reinterpret_cast<double2*>(stg + (j2 >> 3) * 4096 + lane * 128 +
                                                                (((j2 & 7) ^ (lane & 7)) << 4));
                     double v0 = y[2 * j2], v1 = y[2 * j2 + 1];
-                    const int ca = r0 + 2 * j2;
-                    v0 = dmul(ca < p.R ? __ldg(p.ws + ca) : 0.0, v0);
-                    v1 = dmul(ca + 1 < p.R ? __ldg(p.ws + ca + 1) : 0.0, v1);
-                    if (p.epi.post == POST_XPROJ) {
+                    const int ca = r0 + 2 * j2;  // R % 32 == 0: the chunk is in range
+                    const double2 w2 = __ldg(reinterpret_cast<const double2*>(p.ws + ca));
+                    v0 = dmul(w2.x, v0);
+                    v1 = dmul(w2.y, v1);
+                    if (POST == POST_XPROJ) {
                         if (ca < p.epi.split) v0 = softplus_d(dadd(v0, p.epi.bias[ca]));
                         if (ca + 1 < p.epi.split) v1 = softplus_d(dadd(v1, p.epi.bias[ca + 1]));
                     }
@@ -292,7 +292,7 @@ static bool make_map_f64(CUtensorMap* m, const double* base, int rows, int cols,
     return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int POST, bool PLANES>
 static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) {
     CUtensorMap ta, tb, to, to2;
     if (!make_map(&ta, p.a.codes, p.M, p.K, kBM) || !make_map(&tb, p.w, p.R, p.K, BN)) return cudaErrorInvalidValue;
@@ -305,21 +305,34 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
     const int smem = K2Smem<BN>::kTotal;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k2_qlinear<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e =
+            cudaFuncSetAttribute(k2_qlinear<BN, POST, PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
-    k2_qlinear<BN><<<grid, kThreads, smem, st>>>(ta, tb, to, to2, p);
+    k2_qlinear<BN, POST, PLANES><<<grid, kThreads, smem, st>>>(ta, tb, to, to2, p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.M < 1 || p.R < 1 || p.K < 1 || (p.K % 16) != 0 || (p.R % 16) != 0) return cudaErrorInvalidValue;
     if (p.epi.post == POST_INPROJ && (p.epi.split % 32) != 0) return cudaErrorInvalidValue;
-    if ((p.epi.ld_out % 2) != 0) return cudaErrorInvalidValue;  // TMA: 16-byte row pitch
-    return launch_bn<128>(p, st, num_sms);
+    if ((p.epi.ld_out % 2) != 0 || (p.R % 32) != 0) return cudaErrorInvalidValue;  // TMA pitch, whole chunks
+    const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
+    if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
+#define K2_CASE(P)                                                                                       \
+    case P:                                                                                              \
+        return planes ? launch_bn<128, P, true>(p, st, num_sms) : launch_bn<128, P, false>(p, st, num_sms);
+    switch (p.epi.post) {
+        K2_CASE(POST_STORE)
+        K2_CASE(POST_INPROJ)
+        K2_CASE(POST_RESID)
+        K2_CASE(POST_XPROJ)
+        default: return cudaErrorInvalidValue;
+    }
+#undef K2_CASE
 }
 
 }  // namespace ob
