@@ -4,31 +4,32 @@
 //
 // Work split. A CTA owns 128 channels of one (sample, direction); two
 // adjacent lanes own one channel, 8 of its N = 16 states each, so a warp
-// covers 16 channels and the per-thread state (h: 8 doubles, A: 8 floats)
-// leaves room for 24 resident warps per SM. The two halves of a channel
-// exchange exactly two values per step through shuffles: the h peak (max is
-// order-free) and the running output sum — the first half computes
-// 0 + C_0 h_0 + ... + C_7 h_7 in order and the second half continues the
-// same chain with C_8 h_8 ... C_15 h_15, which is the reference's sequential
-// sum (ssm.cpp:170-174) bit-for-bit.
+// covers 16 channels. The two halves of a channel exchange two values per step
+// through shuffles: the h peak (max is order-free) and the running output sum —
+// the first half computes 0 + C_0 h_0 + ... + C_7 h_7 in order and the second
+// half continues the same chain with C_8 h_8 ... C_15 h_15, which is the
+// reference's sequential sum (ssm.cpp:170-174) bit-for-bit.
 //
 // Steps are processed in chunks of 8. Everything that does not depend on the
 // carried state is computed for the whole chunk first, with the chunk's steps
 // as independent instruction streams, and staged in shared memory: per step
-// B, C and the calibrated scales; per channel delta = softplus(dpre + b_delta)
-// (ssm.cpp:150-151), the exact a_bar peak exp(delta * max_m A) and u.
+// B, C and the calibrated scales; per channel x = dpre + b_delta (exact), an
+// f32 delta = softplus(x) with its proven relative error bound, and u.
 //
-// Exactness of the codes (quant.cpp:29-35 in f64):
-//  * peaks: a_bar > 0, delta >= 0, so max_m a_bar = exp(fl(delta * Amax)) and
-//    max_m |b_bar| = fl(delta * max_m |B_m|) exactly (monotone rounding), which
-//    gives the detector decisions and the per-channel outlier scales;
-//  * a_bar and b_bar codes: q = x / s evaluated in f32 (ex2.approx for the
-//    exp) with a proven relative error bound; round(q) is used when q lies
-//    farther than that bound from a half-integer, otherwise the element is
-//    recomputed in f64 with the IEEE quotient (rate ~1e-4). Dequantized values
-//    are code * s in f64, exactly fake_quant_step's;
-//  * the h update, h quantization (quant_code_inv) and the output are f64 in
-//    the reference's operation order.
+// Exactness (the reference values are f64, quant.cpp:29-35). Every code,
+// detector decision and dequantized value equals the reference's:
+//  * detector peaks: a_bar > 0 and delta >= 0, so max_m a_bar = exp(fl(delta*
+//    Amax)) and max_m |b_bar| = fl(delta*max_m|B_m|) (monotone rounding). Both
+//    are evaluated in f32 with error bounds; a decision within the bound of
+//    theta, an outlier channel's scale and every fallback below use the exact
+//    f64 delta = softplus(x), exp and IEEE quotients;
+//  * a_bar and b_bar codes: q = x / s in f32 (ex2.approx for the exp) with a
+//    proven relative error bound; round(q) is used when q is farther than that
+//    bound from a half-integer, else the element is recomputed in f64 (rare).
+//    Dequantized values are code * s in f64, as fake_quant_step's;
+//  * h update (f64, reference order), h codes certified the same way from the
+//    f32 rounding of the exact h (the f32 peak equals fl32 of the exact peak),
+//    the output sum in the reference's order.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -44,20 +45,20 @@ struct ScanDirs {
 
 struct StepShared {
     double B[16], C[16];
-    double Sa, Sb, Sh, invSh, Bmax;
+    double Sa, Sb, Sh, Bmax;
     float BSf[16];  // f32(B_m) * f32(1/S_b): the inlier b_bar quotient per unit delta
-    float invSaf, invSbf, invShf;
-    float halfA;  // 0.5 - certification margin of the inlier a_bar quotient at this step
+    float invSaf, invSbf, invShf, Bmaxf;
+    float LA;  // ln2 * (1 + max(0, log2(1/S_a))): bound of ln2*|log2 a_bar| where inlier rounding matters
     int refresh;
     int crow;  // canonical token of this scan step (ssm.cpp:30-46)
 };
 
 struct ScanSmem {
     StepShared st[kChunk];
-    double delta[kChunk][kCh];
-    double peak_a[kChunk][kCh];
+    double x[kChunk][kCh];      // dpre + b_delta, exact (softplus on demand)
     double u[kChunk][kCh];
-    float deltaf[kChunk][kCh];
+    float deltaf[kChunk][kCh];  // f32 softplus(x)
+    float epsd[kChunk][kCh];    // relative error bound of deltaf
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -66,9 +67,20 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Small integer (|v| < 2^16) -> exact double without the conversion pipe.
+// Small integer code -> exact double by hi/lo word assembly + one DADD. (The
+// conversion pipe, I2F.F64, is quarter rate: 1.7x slower scan when measured.)
 __device__ __forceinline__ double int_to_double_small(int v) {
     return __hiloint2double(0x43300000, static_cast<unsigned>(v + 65536)) - (4503599627370496.0 + 65536.0);
+}
+
+// f32 softplus(x) = max(x,0) + log1p(exp(-|x|)) and its relative error bound:
+// x rounded to f32 (2^-24), ex2.approx (2^-22 + the argument's rounding,
+// <= 1.4|x| 2^-24 relative), log1pf (1 ulp), one add: <= (12 + 3 max(0,-x)) 2^-24.
+// Below x = -80 ex2.approx.ftz flushes; the bound is then 1 (always exact).
+__device__ __forceinline__ float softplus_f32(float x, float& eps) {
+    const float e = ex2_approx(-fabsf(x) * 1.44269504f);
+    eps = x < -80.0f ? 1.0f : fmaf(fmaxf(0.0f, -x), 3.0f, 12.0f) * 5.9604645e-8f;
+    return fmaxf(x, 0.0f) + log1pf(e);
 }
 
 template <bool EXACT, int ABITS>
@@ -81,29 +93,32 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
     const bool active = i < p.E;
     const int E = p.E, T = p.T, P2 = E + 32, m0 = half * 8;
     const unsigned lane = threadIdx.x & 31;
+    const unsigned pair = 3u << (lane & ~1u);
     const bool dyn = p.mode == MODE_DYNAMIC;
     constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;  // outlier_bits = 8
     constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
     const double* __restrict__ proj = p.proj;
     const double* __restrict__ uin = p.u;
     double* __restrict__ oout = p.o;
+    const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
 
     float A2f[8];
     double Amax = -1e300;
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-        const double a = active ? p.a[static_cast<size_t>(i) * 16 + m0 + m] : -1.0;
+        const double a = active ? arow[m0 + m] : -1.0;
         A2f[m] = __double2float_rn(a * 1.4426950408889634);  // log2(e)
         Amax = fmax(Amax, a);
     }
     Amax = fmax(Amax, __shfl_xor_sync(0xffffffffu, Amax, 1));
+    const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
     const double bd = active ? p.b_delta[i] : 0.0;
     double h[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) h[m] = 0.0;
     bool inA = false, inB = false, inH = false;
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
-    const float thHf = __double2float_rn(thH);
+    const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
 
     for (int t0 = 0; t0 < T; t0 += kChunk) {
         const int nt = min(kChunk, T - t0);
@@ -123,13 +138,10 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             ss.Sa = Sa;
             ss.Sb = Sb;
             ss.Sh = Sh;
-            ss.invSh = __ddiv_rn(1.0, Sh);
-            ss.invShf = __double2float_rn(ss.invSh);
+            ss.invShf = __double2float_rn(__ddiv_rn(1.0, Sh));
             ss.invSaf = __double2float_rn(__ddiv_rn(1.0, Sa));
             ss.invSbf = __double2float_rn(__ddiv_rn(1.0, Sb));
-            ss.halfA = 0.5f - fmaf(static_cast<float>(qa) + 1.0f,
-                                   fmaf(fmaxf(0.0f, -__log2f(__double2float_rn(Sa))), 3.0f, 19.0f) * 5.9604645e-8f,
-                                   1e-6f);
+            ss.LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(Sa))));
             ss.refresh = refresh_at(t, p.n_refresh) ? 1 : 0;
             ss.crow = scan_perm(p.order, t, p.grid);
         }
@@ -149,10 +161,11 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
 #pragma unroll
             for (int j = 0; j < kChunk / 2; ++j) {
                 const int tt = half * (kChunk / 2) + j;
-                const double delta = softplus_d(dadd(dp[j], bd));  // ssm.cpp:150-151
-                sh.delta[tt][c] = delta;
-                sh.deltaf[tt][c] = __double2float_rn(delta);
-                sh.peak_a[tt][c] = exp(dmul(delta, Amax));
+                const double x = dadd(dp[j], bd);  // softplus argument, ssm.cpp:150-151
+                float eps;
+                sh.x[tt][c] = x;
+                sh.deltaf[tt][c] = softplus_f32(__double2float_rn(x), eps);
+                sh.epsd[tt][c] = eps;
                 sh.u[tt][c] = uu[j];
             }
         }
@@ -167,32 +180,66 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
 #pragma unroll
             for (int m = 0; m < 16; ++m) bm = fmax(bm, fabs(sh.st[tt].B[m]));
             sh.st[tt].Bmax = bm;
+            sh.st[tt].Bmaxf = __double2float_rn(bm);
         }
         __syncthreads();
 
         for (int tt = 0; tt < nt; ++tt) {
             const int t = t0 + tt;
             const StepShared& ss = sh.st[tt];
-            const double delta = sh.delta[tt][c];
             const float df = sh.deltaf[tt][c];
-            const double pa = sh.peak_a[tt][c];
+            const float ed = sh.epsd[tt][c];
             const double uv = sh.u[tt][c];
-            const double pb = dmul(delta, ss.Bmax);
+            // exact delta and peaks, computed on demand (decisions near theta, outlier
+            // scales, fallbacks)
+            bool have = false;
+            double delta = 0.0, pa = 0.0, pb = 0.0;
+            auto exact = [&]() {
+                if (!have) {
+                    delta = softplus_d(sh.x[tt][c]);
+                    pa = exp(dmul(delta, Amax));
+                    pb = dmul(delta, ss.Bmax);
+                    have = true;
+                }
+            };
             if (dyn) {
                 if (ss.refresh) inA = inB = inH = false;  // maybe_refresh, quant.cpp:303-311
-                if (pa > thA) inA = true;                  // detect_outliers, channel-local form
-                if (pb > thB) inB = true;
+                // detect_outliers, channel-local form, on certified f32 peaks
+                const float x2m = df * Amax2f;
+                const float paf = ex2_approx(x2m);
+                const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
+                const float pbf = df * ss.Bmaxf;
+                const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
+                if (!inA) {
+                    if (paf > thAf * (1.0f + ea)) {
+                        inA = true;
+                    } else if (paf >= thAf * (1.0f - ea)) {
+                        exact();
+                        if (pa > thA) inA = true;
+                    }
+                }
+                if (!inB) {
+                    if (pbf > thBf * (1.0f + eb)) {
+                        inB = true;
+                    } else if (pbf >= thBf * (1.0f - eb)) {
+                        exact();
+                        if (pb > thB) inB = true;
+                    }
+                }
+                if (inA || inB) exact();
             }
             double sA, sB;
-            float invA, kB, qAf, qBf;
+            float invA, kB, qAf, qBf, LA;
             if (inA) {
                 sA = scale_from_peak(pa, qo);
                 invA = __double2float_rn(__ddiv_rn(1.0, sA));
                 qAf = qof;
+                LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
             } else {
                 sA = ss.Sa;
                 invA = ss.invSaf;
                 qAf = qaf;
+                LA = ss.LA;
             }
             if (inB) {
                 sB = scale_from_peak(pb, qo);
@@ -204,20 +251,14 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
                 qBf = qaf;
             }
             const float dfb = df * kB;
-            // Certification margins (in units of q) on the range where rounding
-            // matters, |q| <= qmax + 1: a_bar has |dq| <= q (3|x2| + 16) 2^-24
-            // with |x2| <= 1 + log2(1/s) there; b_bar has |dq| <= |q| 12 2^-24.
-            const float halfA = inA ? 0.5f - fmaf(qof + 1.0f,
-                                                  fmaf(fmaxf(0.0f, -__log2f(__double2float_rn(sA))), 3.0f, 19.0f) *
-                                                      5.9604645e-8f,
-                                                  1e-6f)
-                                    : ss.halfA;
-            const float halfB = 0.5f - fmaf(qBf + 1.0f, 7.1525574e-7f, 1e-6f);
+            // Certification margins (in units of q) where rounding matters (|q| <= qmax+1):
+            // a_bar: |dq| <= q (ln2 |x2| (ed + 2^-23) + 2^-21), ln2 |x2| <= LA there;
+            // b_bar: |dq| <= |q| (ed + 8 2^-24).
+            const float halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+            const float halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
-            // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23),
-            // clamped before rounding so the integer is the reference's clipped code.
-            // An element within its error bound of a half-integer sends the step
-            // through the exact pass (rate ~1e-4).
+            // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23), clamped
+            // before rounding so the integer is the reference's clipped code
             int ca[8], cb[8];
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
 #pragma unroll
@@ -232,13 +273,13 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
                 redo |= fabsf(qb_f - (tb - 12582912.0f)) > halfB;
             }
             if (redo) {  // exact f64 codes where the f32 quotient is not certified
+                exact();
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
                     const float qa_f = fminf(ex2_approx(df * A2f[m]) * invA, capA);
-                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA) {
-                        const double ax = exp(dmul(delta, p.a[static_cast<size_t>(active ? i : 0) * 16 + m0 + m]));
-                        ca[m] = static_cast<int>(quant_code_div(ax, sA, static_cast<double>(qAf)));
-                    }
+                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
+                        ca[m] = static_cast<int>(
+                            quant_code_div(exp(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf)));
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
                         cb[m] = static_cast<int>(quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
@@ -254,8 +295,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             // h detection + codes. Rounding to f32 is monotone, so the f32 peak
             // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
             // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
-            // needs the exact f64 peak. Outlier channels (rare) take the exact peak
-            // for their scale.
+            // needs the exact f64 peak. Outlier channels take the exact peak for their scale.
             float hfv[8];
             float phf = 0.0f;
 #pragma unroll
@@ -264,7 +304,6 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
                 phf = fmaxf(phf, fabsf(hfv[m]));
             }
             phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
-            const unsigned pair = 3u << (lane & ~1u);
             if (dyn && !inH) {
                 if (phf > thHf) {
                     inH = true;
@@ -294,24 +333,24 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
                 const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
                 const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
-                int ch[8];
+                int chd[8];
                 bool hredo = EXACT;
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
                     const float q = fminf(fmaxf(hfv[m] * invHf, -capH), capH);
                     const float th = q + 12582912.0f;
-                    ch[m] = __float_as_int(th) - 0x4B400000;
+                    chd[m] = __float_as_int(th) - 0x4B400000;
                     hredo |= fabsf(q - (th - 12582912.0f)) > halfH;
                 }
                 if (hredo) {
 #pragma unroll
                     for (int m = 0; m < 8; ++m) {
                         const float q = fminf(fmaxf(hfv[m] * invHf, -capH), capH);
-                        if (EXACT || fabsf(q - rintf(q)) > halfH) ch[m] = static_cast<int>(quant_code_div(h[m], sH, qH));
+                        if (EXACT || fabsf(q - rintf(q)) > halfH) chd[m] = static_cast<int>(quant_code_div(h[m], sH, qH));
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 8; ++m) h[m] = dmul(int_to_double_small(ch[m]), sH);  // carried state
+                for (int m = 0; m < 8; ++m) h[m] = dmul(int_to_double_small(chd[m]), sH);  // carried state
             }
             // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: first half, then the second half continues
             double o = 0.0;
