@@ -67,11 +67,16 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Small integer code -> exact double by hi/lo word assembly + one DADD. (The
-// conversion pipe, I2F.F64, is quarter rate: 1.7x slower scan when measured.)
-__device__ __forceinline__ double int_to_double_small(int v) {
-    return __hiloint2double(0x43300000, static_cast<unsigned>(v + 65536)) - (4503599627370496.0 + 65536.0);
+// Codes travel as the f32 bit pattern of q + 1.5*2^23 = 0x4B400000 + code (the
+// round-to-nearest magic); that word under the exponent of 2^52 is
+// 2^52 + 0x4B400000 + code exactly, and one DADD recovers the code as a double.
+// (The conversion pipe, I2F.F64, is quarter rate: 1.7x slower scan when measured.)
+constexpr unsigned kMagicBits = 0x4B400000u;
+__device__ __forceinline__ double code_bits_to_double(unsigned bits) {
+    return __hiloint2double(0x43300000, bits) - (4503599627370496.0 + 1262485504.0);
 }
+__device__ __forceinline__ unsigned code_to_bits(int code) { return kMagicBits + static_cast<unsigned>(code); }
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
 // f32 softplus(x) = max(x,0) + log1p(exp(-|x|)) and its relative error bound:
 // x rounded to f32 (2^-24), ex2.approx (2^-22 + the argument's rounding,
@@ -102,13 +107,13 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
     double* __restrict__ oout = p.o;
     const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
 
-    float A2f[8];
+    float2 A2f[4];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
     double Amax = -1e300;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-        const double a = active ? arow[m0 + m] : -1.0;
-        A2f[m] = __double2float_rn(a * 1.4426950408889634);  // log2(e)
-        Amax = fmax(Amax, a);
+    for (int k = 0; k < 4; ++k) {
+        const double a0 = active ? arow[m0 + 2 * k] : -1.0, a1 = active ? arow[m0 + 2 * k + 1] : -1.0;
+        A2f[k] = make_float2(__double2float_rn(a0 * 1.4426950408889634), __double2float_rn(a1 * 1.4426950408889634));
+        Amax = fmax(Amax, fmax(a0, a1));
     }
     Amax = fmax(Amax, __shfl_xor_sync(0xffffffffu, Amax, 1));
     const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
@@ -258,50 +263,64 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             const float halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
             // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23), clamped
-            // before rounding so the integer is the reference's clipped code
-            int ca[8], cb[8];
+            // before rounding so the integer is the reference's clipped code. Two elements
+            // per packed f32x2 instruction; codes are kept as magic bit patterns.
+            unsigned ca[8], cb[8];
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
+            const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const float qa_f = fminf(ex2_approx(df * A2f[m]) * invA, capA);
-                const float ta = qa_f + 12582912.0f;
-                ca[m] = __float_as_int(ta) - 0x4B400000;
-                redo |= fabsf(qa_f - (ta - 12582912.0f)) > halfA;
-                const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
-                const float tb = qb_f + 12582912.0f;
-                cb[m] = __float_as_int(tb) - 0x4B400000;
-                redo |= fabsf(qb_f - (tb - 12582912.0f)) > halfB;
+            for (int k = 0; k < 4; ++k) {
+                const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
+                float2 qa2 = __fmul2_rn(make_float2(ex2_approx(x2.x), ex2_approx(x2.y)), f2(invA));
+                qa2.x = fminf(qa2.x, capA);
+                qa2.y = fminf(qa2.y, capA);
+                const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
+                const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
+                const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
+                ca[2 * k] = __float_as_uint(ta.x);
+                ca[2 * k + 1] = __float_as_uint(ta.y);
+                float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
+                qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
+                qb2.y = fminf(fmaxf(qb2.y, -capB), capB);
+                const float2 tb = __fadd2_rn(qb2, f2(12582912.0f));
+                const float2 rb = __fadd2_rn(tb, f2(-12582912.0f));
+                const float2 db = __fadd2_rn(qb2, make_float2(-rb.x, -rb.y));
+                cb[2 * k] = __float_as_uint(tb.x);
+                cb[2 * k + 1] = __float_as_uint(tb.y);
+                redo |= (fabsf(da.x) > halfA) | (fabsf(da.y) > halfA) | (fabsf(db.x) > halfB) | (fabsf(db.y) > halfB);
             }
             if (redo) {  // exact f64 codes where the f32 quotient is not certified
                 exact();
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
-                    const float qa_f = fminf(ex2_approx(df * A2f[m]) * invA, capA);
+                    const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
+                    const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
                     if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
-                        ca[m] = static_cast<int>(
-                            quant_code_div(exp(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf)));
+                        ca[m] = code_to_bits(static_cast<int>(
+                            quant_code_div(exp(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
-                        cb[m] = static_cast<int>(quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
+                        cb[m] = code_to_bits(static_cast<int>(
+                            quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf))));
                 }
             }
             // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                const double a_q = dmul(int_to_double_small(ca[m]), sA);
-                const double b_q = dmul(int_to_double_small(cb[m]), sB);
+                const double a_q = dmul(code_bits_to_double(ca[m]), sA);
+                const double b_q = dmul(code_bits_to_double(cb[m]), sB);
                 h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
             }
             // h detection + codes. Rounding to f32 is monotone, so the f32 peak
             // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
             // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
             // needs the exact f64 peak. Outlier channels take the exact peak for their scale.
-            float hfv[8];
+            float2 hfv[4];
             float phf = 0.0f;
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                hfv[m] = __double2float_rn(h[m]);
-                phf = fmaxf(phf, fabsf(hfv[m]));
+            for (int k = 0; k < 4; ++k) {
+                hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
+                phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
             }
             phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
             if (dyn && !inH) {
@@ -333,35 +352,46 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
             {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
                 const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
                 const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
-                int chd[8];
+                unsigned chd[8];
                 bool hredo = EXACT;
 #pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const float q = fminf(fmaxf(hfv[m] * invHf, -capH), capH);
-                    const float th = q + 12582912.0f;
-                    chd[m] = __float_as_int(th) - 0x4B400000;
-                    hredo |= fabsf(q - (th - 12582912.0f)) > halfH;
+                for (int k = 0; k < 4; ++k) {
+                    float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                    q.x = fminf(fmaxf(q.x, -capH), capH);
+                    q.y = fminf(fmaxf(q.y, -capH), capH);
+                    const float2 th = __fadd2_rn(q, f2(12582912.0f));
+                    const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
+                    const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
+                    chd[2 * k] = __float_as_uint(th.x);
+                    chd[2 * k + 1] = __float_as_uint(th.y);
+                    hredo |= (fabsf(dh.x) > halfH) | (fabsf(dh.y) > halfH);
                 }
                 if (hredo) {
 #pragma unroll
                     for (int m = 0; m < 8; ++m) {
-                        const float q = fminf(fmaxf(hfv[m] * invHf, -capH), capH);
-                        if (EXACT || fabsf(q - rintf(q)) > halfH) chd[m] = static_cast<int>(quant_code_div(h[m], sH, qH));
+                        const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
+                        const float q = fminf(fmaxf(hv * invHf, -capH), capH);
+                        if (EXACT || fabsf(q - rintf(q)) > halfH)
+                            chd[m] = code_to_bits(static_cast<int>(quant_code_div(h[m], sH, qH)));
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 8; ++m) h[m] = dmul(int_to_double_small(chd[m]), sH);  // carried state
+                for (int m = 0; m < 8; ++m) h[m] = dmul(code_bits_to_double(chd[m]), sH);  // carried state
             }
-            // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: first half, then the second half continues
+            // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: both halves form their products,
+            // the first half sums from 0, the second continues the same chain
+            double pr[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) pr[m] = dmul(ss.C[m0 + m], h[m]);
             double o = 0.0;
             if (half == 0) {
 #pragma unroll
-                for (int m = 0; m < 8; ++m) o = dadd(o, dmul(ss.C[m], h[m]));
+                for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
             }
             o = __shfl_sync(0xffffffffu, o, lane & ~1u);
             if (half == 1) {
 #pragma unroll
-                for (int m = 0; m < 8; ++m) o = dadd(o, dmul(ss.C[8 + m], h[m]));
+                for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
                 if (active) {
                     oout[(static_cast<size_t>(s) * T + ss.crow) * E + i] = o;
                     if (p.masks) {
