@@ -288,6 +288,7 @@ void Model::ensure_work(int S, bool trace) {
     w.s_row.ensure(rows);
     w.ocnt.ensure(rows);
     w.scanned.ensure(rows);
+    w.scan_steps.ensure(scan_fast_workspace_bytes(S, static_cast<int>(L), static_cast<int>(nd)));
     if (trace) {
         w.masks.ensure(2 * 3 * rows * E);
         w.acc_in.ensure(rows * std::max(2 * E, E + 2 * N));
@@ -571,6 +572,8 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
                     sp.cal[kk].theta = cal->scan[si].theta;
                     sp.cal[kk].s_in = cal->s_in_dev(false, si);
                     sp.cal[kk].s_full = cal->s_full_dev(false, si);
+                    sp.cal[kk].inv_in = cal->inv_in_dev(false, si);
+                    sp.cal[kk].inv_full = cal->inv_full_dev(false, si);
                 }
                 sp.literal = cal->literal.p + (static_cast<size_t>(b) * nd + dd) * L;
                 sp.literal_any = mode == MODE_DYNAMIC ? cal->literal_any[static_cast<size_t>(b) * nd + dd] : 0;
@@ -588,7 +591,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         tick_begin(FAM_K3);
         const bool fast_ok = quant && cal->spec.obits == 8 && (cal->spec.abits == 4 || cal->spec.abits == 8);
         if (fast_ok && !any_literal && scan_variant != 1) {
-            cuda_check(launch_scan_fast(sps, nd, st, scan_variant == 2 ? 1 : 0), "scan");
+            cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant == 2 ? 1 : 0), "scan");
         } else {
             for (int dd = 0; dd < nd; ++dd) {
                 bool l = false;

@@ -152,7 +152,7 @@ class Model {
         DevBuf<double> s_row, oscale, rs;
         DevBuf<int> ocnt;
         DevBuf<uint32_t> omask;
-        DevBuf<uint8_t> scanned, masks;
+        DevBuf<uint8_t> scanned, masks, scan_steps;
         DevBuf<unsigned long long> peaks;
         DevBuf<int32_t> acc_in, acc_out;
     } w;

@@ -4,7 +4,9 @@
 //
 // Work split. A CTA owns 128 channels of one (sample, direction); two
 // adjacent lanes own one channel, 8 of its N = 16 states each, so a warp
-// covers 16 channels. The two halves of a channel exchange two values per step
+// covers 16 channels. Warps are independent: each stages its own copy of the
+// per-step values in its own shared-memory slice and synchronises only with
+// __syncwarp, so a warp delayed by a rare exact fallback never stalls the others. The two halves of a channel exchange two values per step
 // through shuffles: the h peak (max is order-free) and the running output sum —
 // the first half computes 0 + C_0 h_0 + ... + C_7 h_7 in order and the second
 // half continues the same chain with C_8 h_8 ... C_15 h_15, which is the
@@ -12,7 +14,7 @@
 //
 // Steps are processed in chunks of 8. Everything that does not depend on the
 // carried state is computed for the whole chunk first, with the chunk's steps
-// as independent instruction streams, and staged in shared memory: per step
+// as independent instruction streams, and staged in the warp's shared memory: per step
 // B, C and the calibrated scales; per channel x = dpre + b_delta (exact), an
 // f32 delta = softplus(x) with its proven relative error bound, and u.
 //
@@ -32,6 +34,7 @@
 //    the output sum in the reference's order.
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100_ptx.cuh"
 
 namespace ob {
 
@@ -43,7 +46,7 @@ struct ScanDirs {
     ScanParams d[2];
 };
 
-struct StepShared {
+struct __align__(16) StepShared {
     double B[16], C[16];
     double Sa, Sb, Sh, Bmax;
     float BSf[16];  // f32(B_m) * f32(1/S_b): the inlier b_bar quotient per unit delta
@@ -53,12 +56,19 @@ struct StepShared {
     int crow;  // canonical token of this scan step (ssm.cpp:30-46)
 };
 
-struct ScanSmem {
-    StepShared st[kChunk];
-    double x[kChunk][kCh];      // dpre + b_delta, exact (softplus on demand)
-    double u[kChunk][kCh];
-    float deltaf[kChunk][kCh];  // f32 softplus(x)
-    float epsd[kChunk][kCh];    // relative error bound of deltaf
+static_assert(sizeof(StepShared) % 16 == 0, "bulk-copied step tables");
+constexpr int kWarpCh = 16;  // channels per warp
+// Per-warp slice: step tables and raw per-channel inputs are double-buffered
+// (chunk k+1 is in flight while chunk k is scanned); x / deltaf / epsd hold
+// the current chunk.
+struct WarpSmem {
+    StepShared st[2][kChunk];
+    double dp[2][kChunk][kWarpCh];  // x_proj delta pre-activations (raw)
+    double u[2][kChunk][kWarpCh];
+    double x[kChunk][kWarpCh];      // dpre + b_delta, exact (softplus on demand)
+    float deltaf[kChunk][kWarpCh];  // f32 softplus(x)
+    float epsd[kChunk][kWarpCh];    // relative error bound of deltaf
+    uint64_t bar[2];
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -88,16 +98,75 @@ __device__ __forceinline__ float softplus_f32(float x, float& eps) {
     return fmaxf(x, 0.0f) + log1pf(e);
 }
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(ptx::smem_u32(dst)), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     ptx::smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+                 : "memory");
+}
+
+// Per (direction, sample, scan step) tables the scan consumes: B, C, the
+// calibrated scales and their f32 inverses, the b_bar quotients per unit delta
+// and max_m |B_m|. One warp per step; lane j holds column E + j of the x_proj row.
+__global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndirs, StepShared* __restrict__ out) {
+    const int gw = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const ScanParams& p0 = P.d[0];
+    const int S = p0.S, T = p0.T;
+    if (gw >= ndirs * S * T) return;
+    const int dd = gw / (S * T), st_idx = gw - dd * S * T, t = st_idx % T;
+    const ScanParams& p = P.d[dd];
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    const double v = p.proj[static_cast<size_t>(st_idx) * (p.E + 32) + p.E + lane];
+    StepShared& ss = out[gw];
+    const double Sb = dyn ? p.cal[1].s_in[t] : p.cal[1].s_full[t];
+    const double* ib = dyn ? p.cal[1].inv_in : p.cal[1].inv_full;
+    const float invSbf = __double2float_rn(ib ? ib[t] : __ddiv_rn(1.0, Sb));
+    double bm = fabs(v);
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    if (lane < 16) {
+        ss.B[lane] = v;
+        ss.BSf[lane] = __double2float_rn(v) * invSbf;
+    } else {
+        ss.C[lane - 16] = v;
+    }
+    if (lane == 0) {
+        const double Sa = dyn ? p.cal[0].s_in[t] : p.cal[0].s_full[t];
+        const double Sh = dyn ? p.cal[2].s_in[t] : p.cal[2].s_full[t];
+        const double* ia = dyn ? p.cal[0].inv_in : p.cal[0].inv_full;
+        const double* ih = dyn ? p.cal[2].inv_in : p.cal[2].inv_full;
+        ss.Sa = Sa;
+        ss.Sb = Sb;
+        ss.Sh = Sh;
+        ss.Bmax = bm;
+        ss.Bmaxf = __double2float_rn(bm);
+        ss.invSaf = __double2float_rn(ia ? ia[t] : __ddiv_rn(1.0, Sa));
+        ss.invSbf = invSbf;
+        ss.invShf = __double2float_rn(ih ? ih[t] : __ddiv_rn(1.0, Sh));
+        ss.LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(Sa))));
+        ss.refresh = refresh_at(t, p.n_refresh) ? 1 : 0;
+        ss.crow = scan_perm(p.order, t, p.grid);
+    }
+}
+
 template <bool EXACT, int ABITS>
-__global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
+__global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t scan_smem_raw[];
-    ScanSmem& sh = *reinterpret_cast<ScanSmem*>(scan_smem_raw);
+    const int warp = threadIdx.x >> 5;
+    WarpSmem& sh = reinterpret_cast<WarpSmem*>(scan_smem_raw)[warp];
     const ScanParams& p = P.d[blockIdx.z];
-    const int s = blockIdx.y, tid = threadIdx.x, c = tid >> 1, half = tid & 1;
-    const int i = blockIdx.x * kCh + c;
+    const unsigned lane = threadIdx.x & 31;
+    const int s = blockIdx.y, c = lane >> 1, half = lane & 1;
+    const int cw = blockIdx.x * kCh + warp * kWarpCh;  // first channel of this warp
+    if (cw >= p.E) return;  // no CTA-wide barriers below
+    const int i = cw + c;
     const bool active = i < p.E;
     const int E = p.E, T = p.T, P2 = E + 32, m0 = half * 8;
-    const unsigned lane = threadIdx.x & 31;
     const unsigned pair = 3u << (lane & ~1u);
     const bool dyn = p.mode == MODE_DYNAMIC;
     constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;  // outlier_bits = 8
@@ -106,7 +175,6 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
     const double* __restrict__ uin = p.u;
     double* __restrict__ oout = p.o;
     const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
-
     float2 A2f[4];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
     double Amax = -1e300;
 #pragma unroll
@@ -117,84 +185,64 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
     }
     Amax = fmax(Amax, __shfl_xor_sync(0xffffffffu, Amax, 1));
     const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
-    const double bd = active ? p.b_delta[i] : 0.0;
     double h[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) h[m] = 0.0;
     bool inA = false, inB = false, inH = false;
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
-
-    for (int t0 = 0; t0 < T; t0 += kChunk) {
+    // chunk staging: lane -> (step, channel) = (lane >> 4 + 2k, lane & 15)
+    const int sc = lane & 15, sic = cw + sc;
+    const double bd = sic < E ? p.b_delta[sic] : 0.0;
+    const StepShared* wsteps = steps + (static_cast<size_t>(blockIdx.z) * p.S + s) * T;
+    if (lane == 0) {
+        ptx::mbar_init(&sh.bar[0], 1);
+        ptx::mbar_init(&sh.bar[1], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncwarp();
+    auto issue = [&](int t0, int buf) {  // async copies of chunk t0 into buffer buf
         const int nt = min(kChunk, T - t0);
-        __syncthreads();  // previous chunk consumed
-        for (int idx = tid; idx < nt * 32; idx += kThr) {  // B | C of the x_proj rows (scan order)
-            const int tt = idx >> 5, j = idx & 31;
-            const double v = proj[(static_cast<size_t>(s) * T + t0 + tt) * P2 + E + j];
-            if (j < 16) sh.st[tt].B[j] = v;
-            else sh.st[tt].C[j - 16] = v;
-        }
-        if (tid < nt) {
-            const int t = t0 + tid;
-            StepShared& ss = sh.st[tid];
-            const double Sa = dyn ? p.cal[0].s_in[t] : p.cal[0].s_full[t];
-            const double Sb = dyn ? p.cal[1].s_in[t] : p.cal[1].s_full[t];
-            const double Sh = dyn ? p.cal[2].s_in[t] : p.cal[2].s_full[t];
-            ss.Sa = Sa;
-            ss.Sb = Sb;
-            ss.Sh = Sh;
-            ss.invShf = __double2float_rn(__ddiv_rn(1.0, Sh));
-            ss.invSaf = __double2float_rn(__ddiv_rn(1.0, Sa));
-            ss.invSbf = __double2float_rn(__ddiv_rn(1.0, Sb));
-            ss.LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(Sa))));
-            ss.refresh = refresh_at(t, p.n_refresh) ? 1 : 0;
-            ss.crow = scan_perm(p.order, t, p.grid);
-        }
-        {  // state-independent per-channel values: this thread takes 4 of the 8 steps
-            double dp[kChunk / 2], uu[kChunk / 2];
 #pragma unroll
-            for (int j = 0; j < kChunk / 2; ++j) {
-                const int tt = half * (kChunk / 2) + j, t = t0 + tt;
-                dp[j] = 0.0;
-                uu[j] = 0.0;
-                if (tt < nt && active) {
-                    dp[j] = proj[(static_cast<size_t>(s) * T + t) * P2 + i];
-                    const int cr = p.order == 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid));
-                    uu[j] = uin[(static_cast<size_t>(s) * T + cr) * E + i];
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < kChunk / 2; ++j) {
-                const int tt = half * (kChunk / 2) + j;
-                const double x = dadd(dp[j], bd);  // softplus argument, ssm.cpp:150-151
-                float eps;
-                sh.x[tt][c] = x;
-                sh.deltaf[tt][c] = softplus_f32(__double2float_rn(x), eps);
-                sh.epsd[tt][c] = eps;
-                sh.u[tt][c] = uu[j];
-            }
+        for (int k = 0; k < kChunk / 2; ++k) {
+            const int tt = (lane >> 4) + 2 * k, t = min(t0 + tt, T - 1);
+            const bool ok = tt < nt && sic < E;
+            const int cr = p.order == 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid));
+            cp_async8(&sh.dp[buf][tt][sc], proj + (static_cast<size_t>(s) * T + t) * P2 + (ok ? sic : 0), ok);
+            cp_async8(&sh.u[buf][tt][sc], uin + (static_cast<size_t>(s) * T + cr) * E + (ok ? sic : 0), ok);
         }
-        __syncthreads();
-        if (tid < nt * 16) {
-            const int tt = tid >> 4, m = tid & 15;
-            StepShared& ss = sh.st[tt];
-            ss.BSf[m] = __double2float_rn(ss.B[m]) * ss.invSbf;
-        } else if (tid >= 128 && tid < 128 + nt) {
-            const int tt = tid - 128;
-            double bm = 0.0;
-#pragma unroll
-            for (int m = 0; m < 16; ++m) bm = fmax(bm, fabs(sh.st[tt].B[m]));
-            sh.st[tt].Bmax = bm;
-            sh.st[tt].Bmaxf = __double2float_rn(bm);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (lane == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
+            ptx::mbar_arrive_expect_tx(&sh.bar[buf], bytes);
+            bulk_g2s(&sh.st[buf][0], wsteps + t0, bytes, &sh.bar[buf]);
         }
-        __syncthreads();
+    };
+    issue(0, 0);
+
+    for (int t0 = 0, ci = 0; t0 < T; t0 += kChunk, ++ci) {
+        const int nt = min(kChunk, T - t0), cur = ci & 1;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();  // chunk ci's per-channel inputs landed; chunk ci-1 consumed
+#pragma unroll
+        for (int k = 0; k < kChunk / 2; ++k) {
+            const int tt = (lane >> 4) + 2 * k;
+            const double x = dadd(sh.dp[cur][tt][sc], bd);  // softplus argument, ssm.cpp:150-151
+            float eps;
+            sh.x[tt][sc] = x;
+            sh.deltaf[tt][sc] = softplus_f32(__double2float_rn(x), eps);
+            sh.epsd[tt][sc] = eps;
+        }
+        if (t0 + kChunk < T) issue(t0 + kChunk, cur ^ 1);
+        __syncwarp();
+        ptx::mbar_wait(&sh.bar[cur], (ci >> 1) & 1);
 
         for (int tt = 0; tt < nt; ++tt) {
             const int t = t0 + tt;
-            const StepShared& ss = sh.st[tt];
+            const StepShared& ss = sh.st[cur][tt];
             const float df = sh.deltaf[tt][c];
             const float ed = sh.epsd[tt][c];
-            const double uv = sh.u[tt][c];
+            const double uv = sh.u[cur][tt][c];
             // exact delta and peaks, computed on demand (decisions near theta, outlier
             // scales, fallbacks)
             bool have = false;
@@ -408,9 +456,9 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P) {
 }
 
 template <bool EXACT, int ABITS>
-static cudaError_t launch_fast(const ScanDirs& P, int ndirs, cudaStream_t st) {
+static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
     static bool attr = false;
-    const int smem = static_cast<int>(sizeof(ScanSmem));
+    const int smem = static_cast<int>(sizeof(WarpSmem)) * (kThr / 32);
     if (!attr) {
         cudaError_t e =
             cudaFuncSetAttribute(k3_scan_fast<EXACT, ABITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -418,11 +466,16 @@ static cudaError_t launch_fast(const ScanDirs& P, int ndirs, cudaStream_t st) {
         attr = true;
     }
     dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
-    k3_scan_fast<EXACT, ABITS><<<grid, kThr, smem, st>>>(P);
+    k3_scan_fast<EXACT, ABITS><<<grid, kThr, smem, st>>>(P, steps);
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, cudaStream_t st, int force_exact) {
+size_t scan_fast_workspace_bytes(int S, int T, int ndirs) {
+    return static_cast<size_t>(ndirs) * S * T * sizeof(StepShared);
+}
+
+cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
+                             int force_exact) {
     if (ndirs < 1 || ndirs > 2) return cudaErrorInvalidValue;
     ScanDirs P;
     for (int k = 0; k < ndirs; ++k) {
@@ -432,10 +485,18 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, cudaStream_t st,
         if (dirs[k].mode != MODE_DYNAMIC && dirs[k].mode != MODE_STATIC) return cudaErrorInvalidValue;
     }
     if (dirs[0].obits != 8) return cudaErrorNotSupported;  // fast path is built for 8-bit outliers
+    if (dirs[0].abits != 4 && dirs[0].abits != 8) return cudaErrorNotSupported;
+    const int S = dirs[0].S, T = dirs[0].T;
+    if (!work || work_bytes < scan_fast_workspace_bytes(S, T, ndirs) || (reinterpret_cast<uintptr_t>(work) & 15))
+        return cudaErrorInvalidValue;
+    StepShared* steps = static_cast<StepShared*>(work);
+    const int warps = ndirs * S * T;
+    k3_step_tables<<<(warps + 7) / 8, 256, 0, st>>>(P, ndirs, steps);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     switch (dirs[0].abits) {
-        case 4: return force_exact ? launch_fast<true, 4>(P, ndirs, st) : launch_fast<false, 4>(P, ndirs, st);
-        case 8: return force_exact ? launch_fast<true, 8>(P, ndirs, st) : launch_fast<false, 8>(P, ndirs, st);
-        default: return cudaErrorNotSupported;
+        case 4: return force_exact ? launch_fast<true, 4>(P, ndirs, steps, st) : launch_fast<false, 4>(P, ndirs, steps, st);
+        default: return force_exact ? launch_fast<true, 8>(P, ndirs, steps, st) : launch_fast<false, 8>(P, ndirs, steps, st);
     }
 }
 

@@ -103,6 +103,8 @@ struct ScanKindCal {
     double theta = 0.0;
     const double* s_in = nullptr;
     const double* s_full = nullptr;
+    const double* inv_in = nullptr;       // optional [T] 1/s_in, 1/s_full (IEEE quotients); else divided in-kernel
+    const double* inv_full = nullptr;
     unsigned long long* peaks = nullptr;  // calibration recording [T][E] (FP mode)
 };
 struct ScanParams {
@@ -123,7 +125,11 @@ struct ScanParams {
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
 // Fast path (dynamic/static, channel-local detector): all directions in one launch.
 // force_exact = 1 disables the certified f32 codes (every element exact f64).
-cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, cudaStream_t st, int force_exact);
+// Fast exact scan, both directions in one launch (plus a step-table prep
+// launch); work = scan_fast_workspace_bytes(S, T, ndirs) bytes, 16-aligned.
+size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
+cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
+                             int force_exact);
 
 // K4 auxiliaries.
 cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,
