@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             // exact delta and peaks, computed on demand (decisions near theta, outlier
             // scales, fallbacks)
             bool have = false;
-            double delta = 0.0, pa = 0.0, pb = 0.0;
+            double delta, pa, pb;
             auto exact = [&]() {
                 if (!have) {
                     delta = softplus_d(sh.x[tt][c]);
@@ -255,53 +255,51 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                     have = true;
                 }
             };
+            // inlier scales (static mode; dynamic steps where neither tensor is an outlier)
+            double sA = ss.Sa, sB = ss.Sb;
+            float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf, LA = ss.LA;
             if (dyn) {
-                if (ss.refresh) inA = inB = inH = false;  // maybe_refresh, quant.cpp:303-311
+                const bool rf = ss.refresh != 0;  // maybe_refresh, quant.cpp:303-311
+                inA = inA && !rf;
+                inB = inB && !rf;
+                inH = inH && !rf;
                 // detect_outliers, channel-local form, on certified f32 peaks
                 const float x2m = df * Amax2f;
                 const float paf = ex2_approx(x2m);
                 const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
                 const float pbf = df * ss.Bmaxf;
                 const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
-                if (!inA) {
-                    if (paf > thAf * (1.0f + ea)) {
-                        inA = true;
-                    } else if (paf >= thAf * (1.0f - ea)) {
-                        exact();
-                        if (pa > thA) inA = true;
+                // one branch off the inlier path: outlier channels and decisions within the bound
+                if (inA | inB | (paf >= thAf * (1.0f - ea)) | (pbf >= thBf * (1.0f - eb))) {
+                    if (!inA) {
+                        if (paf > thAf * (1.0f + ea)) {
+                            inA = true;
+                        } else if (paf >= thAf * (1.0f - ea)) {
+                            exact();
+                            if (pa > thA) inA = true;
+                        }
+                    }
+                    if (!inB) {
+                        if (pbf > thBf * (1.0f + eb)) {
+                            inB = true;
+                        } else if (pbf >= thBf * (1.0f - eb)) {
+                            exact();
+                            if (pb > thB) inB = true;
+                        }
+                    }
+                    if (inA || inB) exact();
+                    if (inA) {
+                        sA = scale_from_peak(pa, qo);
+                        invA = __double2float_rn(__ddiv_rn(1.0, sA));
+                        qAf = qof;
+                        LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                    }
+                    if (inB) {
+                        sB = scale_from_peak(pb, qo);
+                        kB = __double2float_rn(__ddiv_rn(1.0, sB)) / ss.invSbf;
+                        qBf = qof;
                     }
                 }
-                if (!inB) {
-                    if (pbf > thBf * (1.0f + eb)) {
-                        inB = true;
-                    } else if (pbf >= thBf * (1.0f - eb)) {
-                        exact();
-                        if (pb > thB) inB = true;
-                    }
-                }
-                if (inA || inB) exact();
-            }
-            double sA, sB;
-            float invA, kB, qAf, qBf, LA;
-            if (inA) {
-                sA = scale_from_peak(pa, qo);
-                invA = __double2float_rn(__ddiv_rn(1.0, sA));
-                qAf = qof;
-                LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
-            } else {
-                sA = ss.Sa;
-                invA = ss.invSaf;
-                qAf = qaf;
-                LA = ss.LA;
-            }
-            if (inB) {
-                sB = scale_from_peak(pb, qo);
-                kB = __double2float_rn(__ddiv_rn(1.0, sB)) / ss.invSbf;
-                qBf = qof;
-            } else {
-                sB = ss.Sb;
-                kB = 1.0f;
-                qBf = qaf;
             }
             const float dfb = df * kB;
             // Certification margins (in units of q) where rounding matters (|q| <= qmax+1):
@@ -371,31 +369,29 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                 phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
             }
             phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
-            if (dyn && !inH) {
-                if (phf > thHf) {
-                    inH = true;
-                } else if (phf == thHf) {
+            double sH = ss.Sh, qH = qa;
+            float invHf = ss.invShf;
+            if (dyn && (inH | (phf >= thHf))) {
+                if (!inH) {
+                    if (phf > thHf) {
+                        inH = true;
+                    } else {  // phf == fl32(theta): the exact peak decides
+                        double ph = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                        ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                        if (ph > thH) inH = true;
+                    }
+                }
+                if (inH) {
                     double ph = 0.0;
 #pragma unroll
                     for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
                     ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
-                    if (ph > thH) inH = true;
+                    sH = scale_from_peak(ph, qo);
+                    invHf = __double2float_rn(__ddiv_rn(1.0, sH));
+                    qH = qo;
                 }
-            }
-            double sH, qH;
-            float invHf;
-            if (inH) {
-                double ph = 0.0;
-#pragma unroll
-                for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
-                ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
-                sH = scale_from_peak(ph, qo);
-                invHf = __double2float_rn(__ddiv_rn(1.0, sH));
-                qH = qo;
-            } else {
-                sH = ss.Sh;
-                invHf = ss.invShf;
-                qH = qa;
             }
             {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
                 const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;

@@ -5,19 +5,19 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 cur, hdr, line = None, None, None
-agg, samp, src, nfun = collections.Counter(), collections.Counter(), {}, 0
+agg, samp, src, nfun, fname = collections.Counter(), collections.Counter(), {}, 0, None
 for r in rows:
     if not r: continue
     if r[0] == "Function Name":
-        nfun += 1
-        if nfun > 1: break
+        if nfun and r[1] != fname: break
+        fname, nfun = r[1], 1
     if r[0] == "File Path": cur = r[1].split('/')[-1]; continue
     if r[0] == "Line No": hdr = r; continue
     if hdr is None or len(r) < 8: continue
     if r[0]: line = (cur, int(r[0])); src[line] = r[1][:95]
     ie, sm = hdr.index("Instructions Executed"), hdr.index("# Samples")
     if line and r[ie].isdigit():
-        agg[line] += int(r[ie]); samp[line] += int(r[sm] or 0)
+        agg[line] += int(r[ie]); samp[line] += int(r[sm]) if r[sm].isdigit() else 0
 ts = sum(samp.values()) or 1
 ti = sum(agg.values()) or 1
 for k in sorted(samp, key=lambda k: -samp[k])[:top]:
