@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23), clamped
             // before rounding so the integer is the reference's clipped code. Two elements
             // per packed f32x2 instruction; codes are kept as magic bit patterns.
-            unsigned ca[8], cb[8];
+            unsigned ca[8];  // a_bar codes as magic bits, b_bar codes as exact f32 integers
+            float cb[8];
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
             const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
 #pragma unroll
@@ -331,8 +332,8 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                 const float2 tb = __fadd2_rn(qb2, f2(12582912.0f));
                 const float2 rb = __fadd2_rn(tb, f2(-12582912.0f));
                 const float2 db = __fadd2_rn(qb2, make_float2(-rb.x, -rb.y));
-                cb[2 * k] = __float_as_uint(tb.x);
-                cb[2 * k + 1] = __float_as_uint(tb.y);
+                cb[2 * k] = rb.x;
+                cb[2 * k + 1] = rb.y;
                 redo |= (fabsf(da.x) > halfA) | (fabsf(da.y) > halfA) | (fabsf(db.x) > halfB) | (fabsf(db.y) > halfB);
             }
             if (redo) {  // exact f64 codes where the f32 quotient is not certified
@@ -346,15 +347,15 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                             quant_code_div(exp(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
-                        cb[m] = code_to_bits(static_cast<int>(
-                            quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf))));
+                        cb[m] = static_cast<float>(
+                            quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
                 }
             }
             // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
                 const double a_q = dmul(code_bits_to_double(ca[m]), sA);
-                const double b_q = dmul(code_bits_to_double(cb[m]), sB);
+                const double b_q = dmul(static_cast<double>(cb[m]), sB);
                 h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
             }
             // h detection + codes. Rounding to f32 is monotone, so the f32 peak
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
                 const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
                 const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
-                unsigned chd[8];
+                float chd[8];  // h codes as exact f32 integers (F2F.F64 balances the XU and FP64 pipes)
                 bool hredo = EXACT;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -406,8 +407,8 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                     const float2 th = __fadd2_rn(q, f2(12582912.0f));
                     const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
                     const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
-                    chd[2 * k] = __float_as_uint(th.x);
-                    chd[2 * k + 1] = __float_as_uint(th.y);
+                    chd[2 * k] = rh.x;
+                    chd[2 * k + 1] = rh.y;
                     hredo |= (fabsf(dh.x) > halfH) | (fabsf(dh.y) > halfH);
                 }
                 if (hredo) {
@@ -416,11 +417,11 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                         const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
                         const float q = fminf(fmaxf(hv * invHf, -capH), capH);
                         if (EXACT || fabsf(q - rintf(q)) > halfH)
-                            chd[m] = code_to_bits(static_cast<int>(quant_code_div(h[m], sH, qH)));
+                            chd[m] = static_cast<float>(quant_code_div(h[m], sH, qH));
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 8; ++m) h[m] = dmul(code_bits_to_double(chd[m]), sH);  // carried state
+                for (int m = 0; m < 8; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
             }
             // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: both halves form their products,
             // the first half sums from 0, the second continues the same chain
