@@ -36,6 +36,8 @@
 #include "kernels.h"
 #include "sm100_ptx.cuh"
 
+#include <type_traits>
+
 namespace ob {
 
 constexpr int kCh = 128;       // channels per CTA
@@ -52,6 +54,7 @@ struct __align__(16) StepShared {
     float BSf[16];  // f32(B_m) * f32(1/S_b): the inlier b_bar quotient per unit delta
     float invSaf, invSbf, invShf, Bmaxf;
     float LA;  // ln2 * (1 + max(0, log2(1/S_a))): bound of ln2*|log2 a_bar| where inlier rounding matters
+    float BSmaxf;  // max_m |BSf[m]|: no b_bar quotient of a channel exceeds delta * BSmaxf
     int refresh;
     int crow;  // canonical token of this scan step (ssm.cpp:30-46)
 };
@@ -129,12 +132,17 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
     double bm = fabs(v);
 #pragma unroll
     for (int o = 8; o >= 1; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    float bs = 0.0f;
     if (lane < 16) {
+        bs = __double2float_rn(v) * invSbf;
         ss.B[lane] = v;
-        ss.BSf[lane] = __double2float_rn(v) * invSbf;
+        ss.BSf[lane] = bs;
     } else {
         ss.C[lane - 16] = v;
     }
+    bs = fabsf(bs);
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) bs = fmaxf(bs, __shfl_xor_sync(0xffffffffu, bs, o));
     if (lane == 0) {
         const double Sa = dyn ? p.cal[0].s_in[t] : p.cal[0].s_full[t];
         const double Sh = dyn ? p.cal[2].s_in[t] : p.cal[2].s_full[t];
@@ -145,6 +153,7 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         ss.Sh = Sh;
         ss.Bmax = bm;
         ss.Bmaxf = __double2float_rn(bm);
+        ss.BSmaxf = bs;
         ss.invSaf = __double2float_rn(ia ? ia[t] : __ddiv_rn(1.0, Sa));
         ss.invSbf = invSbf;
         ss.invShf = __double2float_rn(ih ? ih[t] : __ddiv_rn(1.0, Sh));
@@ -258,14 +267,15 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             // inlier scales (static mode; dynamic steps where neither tensor is an outlier)
             double sA = ss.Sa, sB = ss.Sb;
             float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf, LA = ss.LA;
+            // f32 a_bar peak: the detector's certified estimate and the clipping bound below
+            const float x2m = df * Amax2f;
+            const float paf = ex2_approx(x2m);
             if (dyn) {
                 const bool rf = ss.refresh != 0;  // maybe_refresh, quant.cpp:303-311
                 inA = inA && !rf;
                 inB = inB && !rf;
                 inH = inH && !rf;
                 // detect_outliers, channel-local form, on certified f32 peaks
-                const float x2m = df * Amax2f;
-                const float paf = ex2_approx(x2m);
                 const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
                 const float pbf = df * ss.Bmaxf;
                 const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
@@ -315,27 +325,41 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             float cb[8];
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
             const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
+            auto pass1 = [&](auto clamp) {
+                constexpr bool CL = decltype(clamp)::value;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
-                float2 qa2 = __fmul2_rn(make_float2(ex2_approx(x2.x), ex2_approx(x2.y)), f2(invA));
-                qa2.x = fminf(qa2.x, capA);
-                qa2.y = fminf(qa2.y, capA);
-                const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
-                const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
-                const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
-                ca[2 * k] = __float_as_uint(ta.x);
-                ca[2 * k + 1] = __float_as_uint(ta.y);
-                float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
-                qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
-                qb2.y = fminf(fmaxf(qb2.y, -capB), capB);
-                const float2 tb = __fadd2_rn(qb2, f2(12582912.0f));
-                const float2 rb = __fadd2_rn(tb, f2(-12582912.0f));
-                const float2 db = __fadd2_rn(qb2, make_float2(-rb.x, -rb.y));
-                cb[2 * k] = rb.x;
-                cb[2 * k + 1] = rb.y;
-                redo |= (fabsf(da.x) > halfA) | (fabsf(da.y) > halfA) | (fabsf(db.x) > halfB) | (fabsf(db.y) > halfB);
-            }
+                for (int k = 0; k < 4; ++k) {
+                    const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
+                    float2 qa2 = __fmul2_rn(make_float2(ex2_approx(x2.x), ex2_approx(x2.y)), f2(invA));
+                    if constexpr (CL) {
+                        qa2.x = fminf(qa2.x, capA);
+                        qa2.y = fminf(qa2.y, capA);
+                    }
+                    const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
+                    const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
+                    const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
+                    ca[2 * k] = __float_as_uint(ta.x);
+                    ca[2 * k + 1] = __float_as_uint(ta.y);
+                    float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
+                    if constexpr (CL) {
+                        qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
+                        qb2.y = fminf(fmaxf(qb2.y, -capB), capB);
+                    }
+                    const float2 tb = __fadd2_rn(qb2, f2(12582912.0f));
+                    const float2 rb = __fadd2_rn(tb, f2(-12582912.0f));
+                    const float2 db = __fadd2_rn(qb2, make_float2(-rb.x, -rb.y));
+                    cb[2 * k] = rb.x;
+                    cb[2 * k + 1] = rb.y;
+                    redo |= (fabsf(da.x) > halfA) | (fabsf(da.y) > halfA) | (fabsf(db.x) > halfB) |
+                            (fabsf(db.y) > halfB);
+                }
+            };
+            // The clamps can bind only if the largest quotient exceeds the cap: q_b <=
+            // dfb*max|BSf| and q_a <= paf*invA (monotone rounding; the factor covers
+            // ex2.approx's relative error). Warp-uniform choice, both forms are exact.
+            const bool noclip = dfb * ss.BSmaxf <= capB && paf * invA * 1.000001f <= capA;
+            if (__all_sync(0xffffffffu, noclip)) pass1(std::false_type{});
+            else pass1(std::true_type{});
             if (redo) {  // exact f64 codes where the f32 quotient is not certified
                 exact();
 #pragma unroll
@@ -399,18 +423,25 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                 const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
                 float chd[8];  // h codes as exact f32 integers (F2F.F64 balances the XU and FP64 pipes)
                 bool hredo = EXACT;
+                auto hcodes = [&](auto clamp) {
+                    constexpr bool CL = decltype(clamp)::value;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    float2 q = __fmul2_rn(hfv[k], f2(invHf));
-                    q.x = fminf(fmaxf(q.x, -capH), capH);
-                    q.y = fminf(fmaxf(q.y, -capH), capH);
-                    const float2 th = __fadd2_rn(q, f2(12582912.0f));
-                    const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
-                    const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
-                    chd[2 * k] = rh.x;
-                    chd[2 * k + 1] = rh.y;
-                    hredo |= (fabsf(dh.x) > halfH) | (fabsf(dh.y) > halfH);
-                }
+                    for (int k = 0; k < 4; ++k) {
+                        float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                        if constexpr (CL) {
+                            q.x = fminf(fmaxf(q.x, -capH), capH);
+                            q.y = fminf(fmaxf(q.y, -capH), capH);
+                        }
+                        const float2 th = __fadd2_rn(q, f2(12582912.0f));
+                        const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
+                        const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
+                        chd[2 * k] = rh.x;
+                        chd[2 * k + 1] = rh.y;
+                        hredo |= (fabsf(dh.x) > halfH) | (fabsf(dh.y) > halfH);
+                    }
+                };
+                if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});  // |q| <= phf*invHf
+                else hcodes(std::true_type{});
                 if (hredo) {
 #pragma unroll
                     for (int m = 0; m < 8; ++m) {
