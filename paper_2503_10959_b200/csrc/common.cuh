@@ -41,6 +41,18 @@ __device__ __forceinline__ double quant_code_inv(double x, double s, double inv_
     return fmin(fmax(r, -q), q);
 }
 
+// quant_code_inv as an int, without the conversion pipe: 1.5*2^52 + r holds r
+// in its low word (two's complement), the rest is quant_code_inv's test.
+__device__ __forceinline__ int quant_code_int(double x, double s, double inv_s, double q, int qi) {
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    double q2 = dmul(x, inv_s);
+    q2 = fmin(fmax(q2, -(q + 1.0)), q + 1.0);
+    const double t = dadd(q2, kMagic);
+    int c = __double2loint(t);
+    if (fabs(dadd(q2, -dadd(t, -kMagic))) > 0.4999999999990) c = static_cast<int>(round(__ddiv_rn(x, s)));
+    return min(max(c, -qi), qi);
+}
+
 // Same, exact division only (for per-channel outlier scales).
 __device__ __forceinline__ double quant_code_div(double x, double s, double q) {
     double r = round(__ddiv_rn(x, s));

@@ -17,12 +17,12 @@
 // (gemm.cpp:208-216).
 //
 // Two kernels:
-//  * k1_channel (fast path): one thread owns two channels of one (sample,
+//  * k1_channel (fast path): one thread owns four channels of one (sample,
 //    refresh window) and walks the window's tokens. Exact whenever
 //    C(t) = fl(nextafter(theta,+inf)/q_a) > S^I(t) holds (host-checked per
 //    site and step): then O(t) = O_r(t) U {ch: |x| > theta}
 //    and channels never interact. Rows are read as 16-byte vectors, codes
-//    stored as char2; D1's RMSNorm factor comes from k1_rownorm.
+//    stored as char4; D1's RMSNorm factor comes from k1_rownorm.
 //  * k1_literal: one warp owns one (sample, window) with lane l holding
 //    channels l, l+32, ...; the cross-channel maximum of detect_outliers is a
 //    warp reduction, so the reference is followed verbatim (also provides
@@ -42,8 +42,16 @@ __global__ void __launch_bounds__(256) k1_rownorm(const double* __restrict__ x, 
     if (r >= rows) return;
     const double* xr = x + r * E;
     double ps = 0.0;
-    for (int k = lane; k < E; k += 32) {
-        const double v = xr[k];
+    int k = lane;
+    for (; k + 7 * 32 < E; k += 8 * 32) {  // 8 loads in flight, summed in channel order
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(xr + k + 32 * j);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ps = dadd(ps, dmul(v[j], v[j]));
+    }
+    for (; k < E; k += 32) {
+        const double v = __ldg(xr + k);
         ps = dadd(ps, dmul(v, v));
     }
 #pragma unroll
@@ -54,33 +62,38 @@ __global__ void __launch_bounds__(256) k1_rownorm(const double* __restrict__ x, 
     }
 }
 
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+// Layer input of two channels at one token (16-byte loads).
 template <int SRC>
 __device__ __forceinline__ double2 k1_load2(const K1Params& p, size_t src, size_t crow_global) {
     if (SRC == K1_SRC_MERGE) {
         // merged = (0 + o_0) + o_1 (ssm.cpp:214-229), y = merged * gate (ssm.cpp:231)
-        const double2 a = *reinterpret_cast<const double2*>(p.x + src);
-        const double2 g = *reinterpret_cast<const double2*>(p.gate + src);
+        const double2 a = ldg2(p.x + src);
+        const double2 g = ldg2(p.gate + src);
         double m0 = dadd(0.0, a.x), m1 = dadd(0.0, a.y);
         if (p.x2) {
-            const double2 b = *reinterpret_cast<const double2*>(p.x2 + src);
+            const double2 b = ldg2(p.x2 + src);
             m0 = dadd(m0, b.x);
             m1 = dadd(m1, b.y);
         }
         return make_double2(dmul(m0, silu_d(g.x)), dmul(m1, silu_d(g.y)));  // gate = silu(x W_g^T)
     }
-    double2 v = *reinterpret_cast<const double2*>(p.x + src);
+    double2 v = ldg2(p.x + src);
     if (SRC == K1_SRC_RMSNORM) {
-        const double r = p.rs[crow_global];
+        const double r = __ldg(p.rs + crow_global);
         v.x = dmul(v.x, r);
         v.y = dmul(v.y, r);
     }
     return v;
 }
 
+// One thread owns four channels of one (sample, refresh window) and walks the
+// window's tokens; a warp covers 128 channels = 4 mask words (8 lanes x 4 bits).
 template <int SRC>
-__global__ void __launch_bounds__(128) k1_channel(const K1Params p) {
-    const int E = p.E, T = p.T, J = (E + 31) >> 5;
-    const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * 2;  // channels ch, ch+1
+__global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
+    const int E = p.E, T = p.T, J = E >> 5;
+    const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * 4;  // channels ch .. ch+3
     const int lane = threadIdx.x & 31;
     const int win = p.window, nwin = (T + win - 1) / win;
     const int s = blockIdx.y / nwin;
@@ -88,46 +101,61 @@ __global__ void __launch_bounds__(128) k1_channel(const K1Params p) {
     const bool active = ch < E;  // E is a multiple of 32
     const bool dyn = p.mode == MODE_DYNAMIC;
     const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
+    const int qai = static_cast<int>(qa);
     const double theta = p.cal.theta;
-    bool in0 = false, in1 = false;
+    const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
+    const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
+    // maybe_refresh points inside the window (t0 is 0 or a refresh point, where the
+    // state starts clear anyway)
+    int next_ref = (dyn && p.n_refresh > 0) ? t0 + p.n_refresh : 0x7fffffff;
+    unsigned in = 0;  // bit k: channel ch+k is in O
     for (int t = t0; t < t1; ++t) {
-        const int crow = p.order < 0 ? t : (p.order == 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid)));
+        const int crow = p.order <= 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid));
         const size_t cg = static_cast<size_t>(s) * T + crow;
         const size_t row = static_cast<size_t>(s) * T + t;
-        double2 v = make_double2(0.0, 0.0);
-        if (active) v = k1_load2<SRC>(p, cg * E + ch, cg);
-        if (dyn) {
-            if (refresh_at(t, p.n_refresh)) in0 = in1 = false;  // maybe_refresh
-            if (fabs(v.x) > theta) in0 = true;                   // detect_outliers, channel-local form
-            if (fabs(v.y) > theta) in1 = true;
-        }
-        const double S = dyn ? p.cal.s_in[t] : p.cal.s_full[t];
-        const double inv = dyn ? (p.inv_in ? p.inv_in[t] : __ddiv_rn(1.0, S))
-                               : (p.inv_full ? p.inv_full[t] : __ddiv_rn(1.0, S));
-        int c0 = 0, c1 = 0;
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
         if (active) {
-            if (in0) {
-                const double os = scale_from_peak(fabs(v.x), qo);  // scale_for over the 1-value row
-                p.ocode[row * E + ch] = static_cast<int8_t>(static_cast<int>(quant_code_div(v.x, os, qo)));
-                p.oscale[row * E + ch] = os;
-            } else {
-                c0 = static_cast<int>(quant_code_inv(v.x, S, inv, qa));
-            }
-            if (in1) {
-                const double os = scale_from_peak(fabs(v.y), qo);
-                p.ocode[row * E + ch + 1] = static_cast<int8_t>(static_cast<int>(quant_code_div(v.y, os, qo)));
-                p.oscale[row * E + ch + 1] = os;
-            } else {
-                c1 = static_cast<int>(quant_code_inv(v.y, S, inv, qa));
-            }
-            *reinterpret_cast<char2*>(p.codes + row * E + ch) =
-                make_char2(static_cast<signed char>(c0), static_cast<signed char>(c1));
+            const double2 lo = k1_load2<SRC>(p, cg * E + ch, cg), hi = k1_load2<SRC>(p, cg * E + ch + 2, cg);
+            v[0] = lo.x;
+            v[1] = lo.y;
+            v[2] = hi.x;
+            v[3] = hi.y;
         }
-        // mask word of channels 32w..32w+31: 16 lanes x 2 bits
-        unsigned bits = active ? ((in0 ? 1u : 0u) | (in1 ? 2u : 0u)) << ((lane & 15) * 2) : 0u;
+        if (dyn) {
+            if (t == next_ref) {  // maybe_refresh
+                in = 0;
+                next_ref += p.n_refresh;
+            }
 #pragma unroll
-        for (int o = 8; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
-        if (active && (lane & 15) == 0) {
+            for (int k = 0; k < 4; ++k)
+                if (fabs(v[k]) > theta) in |= 1u << k;  // detect_outliers, channel-local form
+        }
+        const double S = s_tab[t];
+        const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
+        if (active) {
+            int c[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                c[k] = 0;
+                if ((in >> k) & 1u) {
+                    const double os = scale_from_peak(fabs(v[k]), qo);  // scale_for over the 1-value row
+                    p.ocode[row * E + ch + k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[k], os, qo)));
+                    p.oscale[row * E + ch + k] = os;
+                } else {
+                    c[k] = quant_code_int(v[k], S, inv, qa, qai);
+                }
+            }
+            *reinterpret_cast<char4*>(p.codes + row * E + ch) =
+                make_char4(static_cast<signed char>(c[0]), static_cast<signed char>(c[1]),
+                           static_cast<signed char>(c[2]), static_cast<signed char>(c[3]));
+        }
+        // mask word of channels 32w..32w+31 from 8 lanes x 4 bits (all zero in the common case)
+        unsigned bits = active ? in << ((lane & 7) * 4) : 0u;
+        if (__any_sync(0xffffffffu, bits != 0u)) {
+#pragma unroll
+            for (int o = 4; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+        }
+        if (active && (lane & 7) == 0) {
             p.omask[row * J + (ch >> 5)] = bits;
             if (bits) atomicAdd(p.ocnt + row, __popc(bits));
         }
@@ -272,8 +300,9 @@ static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
         k1_rownorm<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(p.x, p.rs, rows, p.E);
     }
     const int nwin = (p.T + p.window - 1) / p.window;
-    dim3 grid((p.E / 2 + 127) / 128, p.S * nwin);
-    k1_channel<SRC><<<grid, 128, 0, st>>>(p);
+    const int quads = p.E / 4, threads = quads >= 256 ? 256 : ((quads + 31) / 32) * 32;
+    dim3 grid((quads + threads - 1) / threads, p.S * nwin);
+    k1_channel<SRC><<<grid, threads, 0, st>>>(p);
     return cudaGetLastError();
 }
 

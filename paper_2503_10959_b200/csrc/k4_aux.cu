@@ -128,8 +128,52 @@ __global__ void k4_conv(const double* __restrict__ u0, const double* __restrict_
     }
 }
 
+// Fast form for W = 4 and even E: a thread owns two channels of a run of kRun
+// tokens; the run's inputs (plus W-1 halo tokens) are loaded once, as 16-byte
+// vectors, before any output is formed. Same per-output order as k4_conv.
+template <int W>
+__global__ void __launch_bounds__(128) k4_conv_run(const double* __restrict__ u0, const double* __restrict__ taps,
+                                                   double* __restrict__ u, int S, int T, int E) {
+    constexpr int kRun = 14;
+    const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (ch >= E) return;
+    const int nrun = (T + kRun - 1) / kRun;
+    const int s = blockIdx.y / nrun, t0 = (blockIdx.y % nrun) * kRun, t1 = min(T, t0 + kRun);
+    double2 tp[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) tp[k] = make_double2(__ldg(taps + ch * W + k), __ldg(taps + (ch + 1) * W + k));
+    const double* base = u0 + static_cast<size_t>(s) * T * E + ch;
+    double2 in[kRun + W - 1];  // in[j] = token t0 - (W-1) + j
+#pragma unroll
+    for (int j = 0; j < kRun + W - 1; ++j) {
+        const int tok = t0 - (W - 1) + j;
+        in[j] = (tok >= 0 && tok < t1) ? __ldg(reinterpret_cast<const double2*>(base + static_cast<size_t>(tok) * E))
+                                       : make_double2(0.0, 0.0);
+    }
+    double* out = u + static_cast<size_t>(s) * T * E + ch;
+#pragma unroll
+    for (int i = 0; i < kRun; ++i) {
+        const int t = t0 + i;
+        if (t >= t1) break;
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            if (t - (W - 1 - k) < 0) continue;  // ssm.cpp:200-212 skips taps before the sequence start
+            a = dadd(a, dmul(tp[k].x, in[i + k].x));
+            b = dadd(b, dmul(tp[k].y, in[i + k].y));
+        }
+        *reinterpret_cast<double2*>(out + static_cast<size_t>(t) * E) = make_double2(a, b);
+    }
+}
+
 cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, int T, int E, int W, cudaStream_t st) {
-    k4_conv<<<2368, 256, 0, st>>>(u0, taps, u, S, T, E, W);
+    if (W == 4 && E % 2 == 0 && (reinterpret_cast<uintptr_t>(u0) & 15) == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0) {
+        const int nrun = (T + 13) / 14;
+        dim3 grid((E / 2 + 127) / 128, S * nrun);
+        k4_conv_run<4><<<grid, 128, 0, st>>>(u0, taps, u, S, T, E);
+    } else {
+        k4_conv<<<2368, 256, 0, st>>>(u0, taps, u, S, T, E, W);
+    }
     return cudaGetLastError();
 }
 
