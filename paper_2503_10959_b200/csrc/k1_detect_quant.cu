@@ -88,6 +88,41 @@ __device__ __forceinline__ double2 k1_load2(const K1Params& p, size_t src, size_
     return v;
 }
 
+// Merge source, certified form. v = m * silu(g) with m = (0 + o_0) + o_1 exact
+// in f64; v is evaluated in f32 with a relative error bound, and the detector
+// decision and inlier code are taken from it only when the bound keeps them
+// away from theta and from half-integers; otherwise (and for outlier channels)
+// the exact f64 value is used. Bound: g and m rounded to f32 (2 x 2^-24),
+// the ex2 argument (3|g| 2^-24 relative in e), ex2.approx (2^-22), the
+// sigmoid's add and quotient (2 x 2^-24, doubled for g < 0 where e/(1+e)
+// carries e's error in full), two products: |vf/v - 1| <= (6|g| + 15) 2^-24;
+// the code adds 1/s rounded to f32 and one product. Below g = -80 ex2 flushes,
+// so those elements always take the exact path.
+struct MergeApprox {
+    float v, eps;
+};
+// exact merged value y = merged * silu(gate) (ssm.cpp:231): the rare path, kept out of line
+__device__ __noinline__ double merge_exact(double m, double g) { return dmul(m, silu_d(g)); }
+__device__ __forceinline__ MergeApprox merge_approx(double m, double g) {
+    const float gf = __double2float_rn(g), mf = __double2float_rn(m);
+    const float ag = fabsf(gf);
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-ag * 1.44269504f));
+    const float den = 1.0f + e;
+    const float sig = (gf >= 0.0f ? 1.0f : e) / den;
+    MergeApprox r;
+    r.v = (mf * gf) * sig;
+    if (m == 0.0 || g == 0.0) {  // v = +-0 exactly: code 0, never an outlier (frequent: all-zero h codes)
+        r.v = 0.0f;
+        r.eps = 0.0f;
+        return r;
+    }
+    // f32 subnormals (relative error unbounded), the ex2 flush and overflow take the exact path
+    const bool ok = gf >= -80.0f && ag >= 1e-30f && fabsf(mf) >= 1e-30f && fabsf(r.v) < 1e30f;
+    r.eps = ok ? fmaf(ag, 6.0f, 24.0f) * 5.9604645e-8f : 1.0f;
+    return r;
+}
+
 // One thread owns four channels of one (sample, refresh window) and walks the
 // window's tokens; a warp covers 128 channels = 4 mask words (8 lanes x 4 bits).
 template <int SRC>
@@ -103,6 +138,7 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
     const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
     const int qai = static_cast<int>(qa);
     const double theta = p.cal.theta;
+    const float thetaf = __double2float_rn(theta);
     const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
     const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
     // maybe_refresh points inside the window (t0 is 0 or a refresh point, where the
@@ -114,33 +150,85 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
         const size_t cg = static_cast<size_t>(s) * T + crow;
         const size_t row = static_cast<size_t>(s) * T + t;
         double v[4] = {0.0, 0.0, 0.0, 0.0};
+        double mg[4], gg[4];  // merge source: merged scan output and gate pre-activation
+        MergeApprox ap[4];
         if (active) {
-            const double2 lo = k1_load2<SRC>(p, cg * E + ch, cg), hi = k1_load2<SRC>(p, cg * E + ch + 2, cg);
-            v[0] = lo.x;
-            v[1] = lo.y;
-            v[2] = hi.x;
-            v[3] = hi.y;
+            if (SRC == K1_SRC_MERGE) {
+                const size_t src = cg * E + ch;
+                const double2 a0 = ldg2(p.x + src), a1 = ldg2(p.x + src + 2);
+                const double2 g0 = ldg2(p.gate + src), g1 = ldg2(p.gate + src + 2);
+                mg[0] = dadd(0.0, a0.x);  // (0 + o_0) + o_1, ssm.cpp:214-229
+                mg[1] = dadd(0.0, a0.y);
+                mg[2] = dadd(0.0, a1.x);
+                mg[3] = dadd(0.0, a1.y);
+                if (p.x2) {
+                    const double2 b0 = ldg2(p.x2 + src), b1 = ldg2(p.x2 + src + 2);
+                    mg[0] = dadd(mg[0], b0.x);
+                    mg[1] = dadd(mg[1], b0.y);
+                    mg[2] = dadd(mg[2], b1.x);
+                    mg[3] = dadd(mg[3], b1.y);
+                }
+                gg[0] = g0.x;
+                gg[1] = g0.y;
+                gg[2] = g1.x;
+                gg[3] = g1.y;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ap[k] = merge_approx(mg[k], gg[k]);
+            } else {
+                const double2 lo = k1_load2<SRC>(p, cg * E + ch, cg), hi = k1_load2<SRC>(p, cg * E + ch + 2, cg);
+                v[0] = lo.x;
+                v[1] = lo.y;
+                v[2] = hi.x;
+                v[3] = hi.y;
+            }
         }
+        unsigned have = 0;  // merge: bit k = v[k] holds the exact value
         if (dyn) {
             if (t == next_ref) {  // maybe_refresh
                 in = 0;
                 next_ref += p.n_refresh;
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (fabs(v[k]) > theta) in |= 1u << k;  // detect_outliers, channel-local form
+            for (int k = 0; k < 4; ++k) {  // detect_outliers, channel-local form
+                if (SRC == K1_SRC_MERGE) {
+                    if (!active || ((in >> k) & 1u)) continue;
+                    const float av = fabsf(ap[k].v);
+                    if (av * (1.0f - ap[k].eps) > thetaf * 1.0000003f) {
+                        in |= 1u << k;
+                    } else if (av * (1.0f + ap[k].eps) >= thetaf * 0.9999997f) {
+                        v[k] = merge_exact(mg[k], gg[k]);
+                        have |= 1u << k;
+                        if (fabs(v[k]) > theta) in |= 1u << k;
+                    }
+                } else {
+                    if (fabs(v[k]) > theta) in |= 1u << k;
+                }
+            }
         }
         const double S = s_tab[t];
         const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
         if (active) {
             int c[4];
+            const float invf = __double2float_rn(inv), capf = static_cast<float>(qa) + 1.0f;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 c[k] = 0;
                 if ((in >> k) & 1u) {
+                    if (SRC == K1_SRC_MERGE && !((have >> k) & 1u)) v[k] = merge_exact(mg[k], gg[k]);
                     const double os = scale_from_peak(fabs(v[k]), qo);  // scale_for over the 1-value row
                     p.ocode[row * E + ch + k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[k], os, qo)));
                     p.oscale[row * E + ch + k] = os;
+                } else if (SRC == K1_SRC_MERGE) {
+                    // certified f32 quotient: |dq| <= (|q| + 1) (eps + 3 2^-24)
+                    const float q = fminf(fmaxf(ap[k].v * invf, -capf), capf);
+                    const float r = rintf(q);
+                    if (!((have >> k) & 1u) &&
+                        fabsf(q - r) < 0.5f - fmaf(fabsf(q) + 1.0f, ap[k].eps + 1.8e-7f, 1e-6f)) {
+                        c[k] = min(max(static_cast<int>(r), -qai), qai);
+                    } else {
+                        if (!((have >> k) & 1u)) v[k] = merge_exact(mg[k], gg[k]);
+                        c[k] = quant_code_int(v[k], S, inv, qa, qai);
+                    }
                 } else {
                     c[k] = quant_code_int(v[k], S, inv, qa, qai);
                 }

@@ -149,3 +149,53 @@ def test_detect_quantize_sources(oracle_checker, gpu_ctx, src):
     m = _unpack(a["omask"], E).astype(bool)
     assert m.any()
     assert np.array_equal(a["ocode"][m], b["ocode"][m]) and np.array_equal(a["oscale"][m], b["oscale"][m])
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_detect_quantize_merge_edges(gpu_ctx, seed):
+    """Merge source: the certified f32 evaluation of merged * silu(gate) == the
+    exact f64 kernel on the cases that stress it: exact zeros (all-zero h codes
+    give o = 0), zero gates, gates past +-80 (ex2 flush), subnormals, and values
+    placed on / near half-integer quotients and near theta."""
+    import torch
+    S, T, E = 4, 30, 128
+    rng = np.random.default_rng(seed)
+    s_val, theta = 0.35, 2.4
+    g = rng.normal(size=(S, T, E)) * 2.0
+    o0 = rng.normal(size=(S, T, E))
+    o1 = rng.normal(size=(S, T, E))
+    sig = 1.0 / (1.0 + np.exp(-g))
+    silu = g * sig
+    kind = rng.integers(0, 8, size=(S, T, E))
+    # 1: merged exactly zero; 2: gate zero; 3: gate far negative / positive; 4: subnormal merged
+    o1[kind == 1] = -o0[kind == 1]
+    g[kind == 2] = 0.0
+    g[kind == 3] = rng.choice([-95.0, -81.0, 85.0, 300.0], size=int((kind == 3).sum()))
+    o0[kind == 4] = 1e-310
+    o1[kind == 4] = 0.0
+    # 5/6: merged * silu(gate) / s on a half-integer (+- tiny) -> certification must refuse or be right
+    silu = g * (1.0 / (1.0 + np.exp(-g)))
+    target = (rng.integers(-6, 7, size=(S, T, E)) + 0.5) * s_val
+    off = np.where(kind == 5, 0.0, rng.choice([1e-9, -1e-9, 1e-5, -1e-5, 3e-4], size=(S, T, E)))
+    sel = (kind >= 5) & (kind <= 6) & (np.abs(silu) > 1e-3)
+    m_target = (target + off * s_val) / np.where(sel, silu, 1.0)
+    o0[sel] = m_target[sel]
+    o1[sel] = 0.0
+    # 7: close to theta
+    sel7 = (kind == 7) & (np.abs(silu) > 1e-3)
+    o0[sel7] = (theta * (1 + rng.choice([1e-12, -1e-12, 1e-6, -1e-6], size=int(sel7.sum())))) / silu[sel7]
+    o1[sel7] = 0.0
+    x, x2, gate = _dev(o0), _dev(o1), _dev(g)
+    s_in = _dev(np.full(T, s_val))
+    outs = []
+    for lit in (False, True):
+        r = gpu_ctx.detect_quantize(x, S=S, T=T, E=E, theta=theta, s_in=s_in, s_full=s_in, n_refresh=5, act_bits=4,
+                                    outlier_bits=8, mode=1, src=2, x2=x2, gate=gate, literal=lit)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in r.items()})
+    a, b = outs
+    for k in ("codes", "s_row", "ocnt", "omask"):
+        assert np.array_equal(a[k], b[k]), k
+    m = _unpack(a["omask"], E).astype(bool)
+    assert m.any() and (~m).any()
+    assert np.array_equal(a["ocode"][m], b["ocode"][m]) and np.array_equal(a["oscale"][m], b["oscale"][m])
