@@ -30,17 +30,32 @@
 
 namespace ob {
 
-constexpr int kBM = 128, kBK = 128, kStages = 4, kEpiWarps = 8, kThreads = 128 + 32 * kEpiWarps;
+constexpr int kBM = 128, kBK = 128, kStages = 3, kEpiWarps = 8, kThreads = 128 + 32 * kEpiWarps;
+constexpr int kStgBufs = 1;  // epilogue staging buffers per warp
+// (K <= a few thousand: the MMA main loop of a tile is short next to its f64
+// epilogue, so shared memory goes to double-buffered epilogue staging instead
+// of deeper operand pipelining.)
 
 template <int BN>
 struct K2Smem {
     static constexpr int kABytes = kBM * kBK;
     static constexpr int kBBytes = BN * kBK;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kEpiOff = kStages * kStageBytes;  // per-warp 32 x 32 f64 output tiles (2 TMA boxes)
-    static constexpr int kBarOff = kEpiOff + kEpiWarps * 8192;
+    static constexpr int kEpiOff = kStages * kStageBytes;  // per warp: 2 x (32 x 32 f64 output tile = 2 TMA boxes)
+    static constexpr int kWsOff = kEpiOff + kEpiWarps * kStgBufs * 8192;  // per warp: the chunk's 32 column scales
+    // row metadata ring (2 tiles ahead, filled by warp 3): S_m, |O|, mask words (J <= 32)
+    static constexpr int kMetaS = 0, kMetaCnt = kBM * 8, kMetaMask = kMetaCnt + kBM * 4;
+    static constexpr int kMetaBytes = kMetaMask + kBM * 32 * 4;
+    static constexpr int kMetaOff = kWsOff + kEpiWarps * 256;
+    static constexpr int kBarOff = kMetaOff + 2 * kMetaBytes;
     static constexpr int kTotal = kBarOff + 256 + 1024;  // barriers + tmem slot + alignment slack
 };
+
+// int32 -> f64, exact, without the conversion pipe (I2F.F64 is slow on sm_100):
+// 2^52 + (v + 2^31) assembled from words, minus 2^52 + 2^31.
+__device__ __forceinline__ double i32_to_f64(uint32_t v) {
+    return __hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)) - 4503601774854144.0;
+}
 
 template <int BN, int POST, bool PLANES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -53,8 +68,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + kStages;
     uint64_t* acc_full = empty + kStages;
     uint64_t* acc_empty = acc_full + 2;
-    uint64_t* res_bar = acc_empty + 2;  // per epilogue warp: residual tile loads
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + kEpiWarps);
+    uint64_t* res_bar = acc_empty + 2;  // per epilogue warp and staging buffer: residual tile loads
+    uint64_t* meta_full = res_bar + 2 * kEpiWarps;
+    uint64_t* meta_empty = meta_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(meta_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.R + BN - 1) / BN;
@@ -72,7 +89,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(acc_full + s, 1);
             ptx::mbar_init(acc_empty + s, kEpiWarps);  // one arrive per epilogue warp
         }
-        for (int w = 0; w < kEpiWarps; ++w) ptx::mbar_init(res_bar + w, 1);
+        for (int w = 0; w < 2 * kEpiWarps; ++w) ptx::mbar_init(res_bar + w, 1);
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(meta_full + s, 1);
+            ptx::mbar_init(meta_empty + s, kEpiWarps);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<2 * BN>(tmem_slot);
@@ -130,37 +151,84 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mma_commit(acc_full + buf);
             }
         }
+    } else if (warp == 3) {  // ---- row metadata producer: S_m, |O| and mask words of upcoming tiles
+        const int J = p.a.J;
+        const bool bulk_ok = ((reinterpret_cast<uintptr_t>(p.a.s_row) | reinterpret_cast<uintptr_t>(p.a.ocnt) |
+                               reinterpret_cast<uintptr_t>(p.a.omask)) & 15) == 0;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+            const int slot = it & 1;
+            ptx::mbar_wait(meta_empty + slot, ((it >> 1) & 1) ^ 1);
+            uint8_t* mb = smem + L::kMetaOff + slot * L::kMetaBytes;
+            double* ms = reinterpret_cast<double*>(mb + L::kMetaS);
+            int* mc = reinterpret_cast<int*>(mb + L::kMetaCnt);
+            uint32_t* mm = reinterpret_cast<uint32_t*>(mb + L::kMetaMask);
+            const int m0 = (tile / n_tiles) * kBM;
+            const int nrows = min(kBM, p.M - m0);
+            if (nrows == kBM && bulk_ok) {  // full tile: three contiguous bulk copies onto the slot's barrier
+                if (lane == 0) {
+                    const uint32_t mbytes = static_cast<uint32_t>(kBM * J * 4);
+                    ptx::mbar_arrive_expect_tx(meta_full + slot, kBM * 8 + kBM * 4 + mbytes);
+                    ptx::bulk_g2s(ms, p.a.s_row + m0, kBM * 8, meta_full + slot);
+                    ptx::bulk_g2s(mc, p.a.ocnt + m0, kBM * 4, meta_full + slot);
+                    ptx::bulk_g2s(mm, p.a.omask + static_cast<size_t>(m0) * J, mbytes, meta_full + slot);
+                }
+                continue;
+            }
+#pragma unroll
+            for (int i = lane; i < kBM; i += 32) {  // ragged last tile
+                const bool v = i < nrows;
+                ms[i] = v ? __ldg(p.a.s_row + m0 + i) : 0.0;
+                mc[i] = v ? __ldg(p.a.ocnt + m0 + i) : 0;
+            }
+            {
+                const uint32_t* src = p.a.omask + static_cast<size_t>(m0) * J;
+                const int n = nrows * J;
+                for (int i = lane; i < n; i += 32) mm[i] = __ldg(src + i);
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(meta_full + slot);
+        }
     } else if (warp >= 4) {  // ---- epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
         const int ew = warp - 4;
         const int q = warp & 3;       // TMEM lanes 32q..32q+31 (a warp may only touch its quarter)
         const int chalf = ew >> 2;    // which half of the BN columns
-        // per-warp output tile: two 32-row x 16-double boxes, 128B-swizzled (TMA layout)
-        uint8_t* stg = smem + L::kEpiOff + ew * 8192;
-        uint64_t* rbar = res_bar + ew;
-        uint32_t rphase = 0;
+        // per-warp output tiles (double-buffered): two 32-row x 16-double boxes each, 128B-swizzled
+        uint8_t* stg0 = smem + L::kEpiOff + ew * kStgBufs * 8192;
+        double* wss = reinterpret_cast<double*>(smem + L::kWsOff + ew * 256);
+
         constexpr bool resid = POST == POST_RESID;
-        int it = 0;
+        int it = 0, cs = 0;  // tile and chunk sequence of this warp
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             const int m0 = (tile / n_tiles) * kBM, n0 = (tile % n_tiles) * BN;
-            ptx::mbar_wait(acc_full + buf, aphase);
-            ptx::tc_fence_after();
             const int rbase = m0 + q * 32;
             const int row = rbase + lane;
             const bool rv = row < p.M;
-            const double S = rv ? p.a.s_row[row] : 0.0;
-            const int cnt = rv ? p.a.ocnt[row] : 0;
+            const int mslot = it & 1;
+            ptx::mbar_wait(meta_full + mslot, (it >> 1) & 1);
+            const uint8_t* mb = smem + L::kMetaOff + mslot * L::kMetaBytes;
+            const double S = reinterpret_cast<const double*>(mb + L::kMetaS)[q * 32 + lane];
+            const int cnt = reinterpret_cast<const int*>(mb + L::kMetaCnt)[q * 32 + lane];
+            const uint32_t* msk = reinterpret_cast<const uint32_t*>(mb + L::kMetaMask) + (q * 32) * p.a.J;
+            ptx::mbar_wait(acc_full + buf, aphase);
+            ptx::tc_fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < BN / 64; ++cc) {
+            for (int cc = 0; cc < BN / 64; ++cc, ++cs) {
                 const int c = chalf * (BN / 64) + cc;
                 const int r0 = n0 + c * 32;
                 if (r0 >= p.R) break;  // uniform across the warp
                 const bool to2 = POST == POST_INPROJ && r0 >= p.epi.split;
                 const CUtensorMap* om = to2 ? &tmO2 : &tmO;
                 const int oc0 = to2 ? r0 - p.epi.split : r0;
+                const int sb = kStgBufs == 2 ? (cs & 1) : 0;
+                uint8_t* stg = stg0 + sb * 8192;
+                uint64_t* rbar = res_bar + 2 * ew + sb;
+                const double wsl = __ldg(p.ws + r0 + lane);  // R % 32 == 0: in range
                 if (lane == 0) {
-                    ptx::bulk_wait_read0();  // the previous tile's store has left the staging buffer
+                    if (kStgBufs == 2) ptx::bulk_wait_read1();  // this buffer's store (two chunks ago) has left it
+                    else ptx::bulk_wait_read0();
                     if (resid) {             // D1 residual: bring x[rows][r0..r0+31] into the staging tile
                         ptx::mbar_arrive_expect_tx(rbar, 8192);
                         ptx::tma_load_2d(stg, om, rbar, oc0, rbase);
@@ -174,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // order (gemm.cpp:208-216), ws[r] * y (gemm.cpp:218-219), post-op
                 double y[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) y[j] = dmul(S, static_cast<double>(static_cast<int32_t>(acc[j])));
+                for (int j = 0; j < 32; ++j) y[j] = dmul(S, i32_to_f64(acc[j]));
                 int32_t aout[PLANES ? 32 : 1];
                 if (PLANES)
 #pragma unroll
@@ -183,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int word = -1;
                 unsigned bits = 0;
                 for (int o = 0; o < cnt; ++o) {
-                    while (bits == 0) bits = p.a.omask[static_cast<size_t>(row) * p.a.J + (++word)];
+                    while (bits == 0) bits = msk[lane * p.a.J + (++word)];
                     const int ch = word * 32 + (__ffs(bits) - 1);
                     bits &= bits - 1;
                     const size_t oi = static_cast<size_t>(row) * p.K + ch;
@@ -209,17 +277,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         p.epi.acc_out[static_cast<size_t>(row) * p.R + r0 + j] = aout[j];
                     }
                 }
-                if (resid) {
-                    ptx::mbar_wait(rbar, rphase);
-                    rphase ^= 1;
-                }
+                wss[lane] = wsl;
+                __syncwarp();
+                if (resid) ptx::mbar_wait(rbar, (kStgBufs == 2 ? cs >> 1 : cs) & 1);
 #pragma unroll
                 for (int j2 = 0; j2 < 16; ++j2) {  // 16-byte chunk j2 = columns 2*j2, 2*j2+1
                     double2* cell = reinterpret_cast<double2*>(stg + (j2 >> 3) * 4096 + lane * 128 +
                                                                (((j2 & 7) ^ (lane & 7)) << 4));
                     double v0 = y[2 * j2], v1 = y[2 * j2 + 1];
-                    const int ca = r0 + 2 * j2;  // R % 32 == 0: the chunk is in range
-                    const double2 w2 = __ldg(reinterpret_cast<const double2*>(p.ws + ca));
+                    const int ca = r0 + 2 * j2;
+                    const double2 w2 = reinterpret_cast<const double2*>(wss)[j2];
                     v0 = dmul(w2.x, v0);
                     v1 = dmul(w2.y, v1);
                     if (POST == POST_XPROJ) {
@@ -243,7 +310,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(acc_empty + buf);
+            if (lane == 0) {
+                ptx::mbar_arrive(acc_empty + buf);
+                ptx::mbar_arrive(meta_empty + mslot);
+            }
         }
         if (lane == 0) ptx::bulk_wait0();
     }
@@ -320,6 +390,7 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.M < 1 || p.R < 1 || p.K < 1 || (p.K % 16) != 0 || (p.R % 16) != 0) return cudaErrorInvalidValue;
     if (p.epi.post == POST_INPROJ && (p.epi.split % 32) != 0) return cudaErrorInvalidValue;
     if ((p.epi.ld_out % 2) != 0 || (p.R % 32) != 0) return cudaErrorInvalidValue;  // TMA pitch, whole chunks
+    if (p.a.J < (p.K + 31) / 32 || p.a.J > 32) return cudaErrorInvalidValue;  // mask rows staged in smem: K <= 1024
     const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
     if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
 #define K2_CASE(P)                                                                                       \

@@ -106,12 +106,6 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
                  "r"(valid ? 8 : 0)
                  : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     ptx::smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
-                 : "memory");
-}
 
 // Per (direction, sample, scan step) tables the scan consumes: B, C, the
 // calibrated scales and their f32 inverses, the b_bar quotients per unit delta
@@ -224,7 +218,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
         if (lane == 0) {
             const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
             ptx::mbar_arrive_expect_tx(&sh.bar[buf], bytes);
-            bulk_g2s(&sh.st[buf][0], wsteps + t0, bytes, &sh.bar[buf]);
+            ptx::bulk_g2s(&sh.st[buf][0], wsteps + t0, bytes, &sh.bar[buf]);
         }
     };
     issue(0, 0);
