@@ -55,8 +55,10 @@ struct __align__(16) StepShared {
     float invSaf, invSbf, invShf, Bmaxf;
     float LA;  // ln2 * (1 + max(0, log2(1/S_a))): bound of ln2*|log2 a_bar| where inlier rounding matters
     float BSmaxf;  // max_m |BSf[m]|: no b_bar quotient of a channel exceeds delta * BSmaxf
-    int refresh;
-    int crow;  // canonical token of this scan step (ssm.cpp:30-46)
+    float hA0, hA1;  // inlier a_bar certification margin = hA0 - hA1 * eps_delta (see the step loop)
+    int keep;        // outlier flags kept at this step: 0 at a maybe_refresh point (quant.cpp:303-311), else ~0
+    int ocol;        // crow * E: canonical token of this scan step (ssm.cpp:30-46), as an output offset
+    int pad[2];
 };
 
 static_assert(sizeof(StepShared) % 16 == 0, "bulk-copied step tables");
@@ -80,15 +82,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Codes travel as the f32 bit pattern of q + 1.5*2^23 = 0x4B400000 + code (the
-// round-to-nearest magic); that word under the exponent of 2^52 is
-// 2^52 + 0x4B400000 + code exactly, and one DADD recovers the code as a double.
-// (The conversion pipe, I2F.F64, is quarter rate: 1.7x slower scan when measured.)
+// Round to nearest via the magic 1.5*2^23: the f32 bit pattern of q + 1.5*2^23 is
+// 0x4B400000 + code. Integer -> f64 avoids the conversion pipe (I2F.F64 measured
+// 1.7x slower here): a_bar codes (>= 0) go under the exponent of 2^52 into one
+// DFMA; b_bar and h codes use F2F.F64.F32 of the exact f32 integer, which
+// balances the XU against the FP64/ALU issue slots.
 constexpr unsigned kMagicBits = 0x4B400000u;
-__device__ __forceinline__ double code_bits_to_double(unsigned bits) {
-    return __hiloint2double(0x43300000, bits) - (4503599627370496.0 + 1262485504.0);
-}
-__device__ __forceinline__ unsigned code_to_bits(int code) { return kMagicBits + static_cast<unsigned>(code); }
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
 // f32 softplus(x) = max(x,0) + log1p(exp(-|x|)) and its relative error bound:
@@ -152,8 +151,11 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         ss.invSbf = invSbf;
         ss.invShf = __double2float_rn(ih ? ih[t] : __ddiv_rn(1.0, Sh));
         ss.LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(Sa))));
-        ss.refresh = refresh_at(t, p.n_refresh) ? 1 : 0;
-        ss.crow = scan_perm(p.order, t, p.grid);
+        ss.keep = refresh_at(t, p.n_refresh) ? 0 : ~0;
+        ss.ocol = scan_perm(p.order, t, p.grid) * p.E;
+        const float qa1 = static_cast<float>((1 << (p.abits - 1)) - 1) + 1.0f;
+        ss.hA1 = qa1 * ss.LA;
+        ss.hA0 = 0.5f - fmaf(qa1, fmaf(ss.LA, 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
     }
 }
 
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
     constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
     const double* __restrict__ proj = p.proj;
     const double* __restrict__ uin = p.u;
-    double* __restrict__ oout = p.o;
+    double* __restrict__ obase = p.o + static_cast<size_t>(s) * T * E + (active ? i : 0);
     const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
     float2 A2f[4];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
     double Amax = -1e300;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
     double h[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) h[m] = 0.0;
-    bool inA = false, inB = false, inH = false;
+    unsigned fl = 0;  // channel in O: bit 0 a_bar, bit 1 b_bar, bit 2 h
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
     // chunk staging: lane -> (step, channel) = (lane >> 4 + 2k, lane & 15)
@@ -260,62 +262,61 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             };
             // inlier scales (static mode; dynamic steps where neither tensor is an outlier)
             double sA = ss.Sa, sB = ss.Sb;
-            float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf, LA = ss.LA;
+            float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
+            // Certification margins (in units of q) where rounding matters (|q| <= qmax+1):
+            // a_bar: |dq| <= q (ln2 |x2| (ed + 2^-23) + 2^-21), ln2 |x2| <= LA there;
+            // b_bar: |dq| <= |q| (ed + 8 2^-24). Inlier forms folded to h0 - h1*ed.
+            float halfA = fmaf(-ss.hA1, ed, ss.hA0);
+            float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
             // f32 a_bar peak: the detector's certified estimate and the clipping bound below
             const float x2m = df * Amax2f;
             const float paf = ex2_approx(x2m);
             if (dyn) {
-                const bool rf = ss.refresh != 0;  // maybe_refresh, quant.cpp:303-311
-                inA = inA && !rf;
-                inB = inB && !rf;
-                inH = inH && !rf;
+                fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh, quant.cpp:303-311
                 // detect_outliers, channel-local form, on certified f32 peaks
                 const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
                 const float pbf = df * ss.Bmaxf;
                 const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
                 // one branch off the inlier path: outlier channels and decisions within the bound
-                if (inA | inB | (paf >= thAf * (1.0f - ea)) | (pbf >= thBf * (1.0f - eb))) {
-                    if (!inA) {
+                if ((fl & 3u) | (paf >= thAf * (1.0f - ea)) | (pbf >= thBf * (1.0f - eb))) {
+                    if (!(fl & 1u)) {
                         if (paf > thAf * (1.0f + ea)) {
-                            inA = true;
+                            fl |= 1u;
                         } else if (paf >= thAf * (1.0f - ea)) {
                             exact();
-                            if (pa > thA) inA = true;
+                            if (pa > thA) fl |= 1u;
                         }
                     }
-                    if (!inB) {
+                    if (!(fl & 2u)) {
                         if (pbf > thBf * (1.0f + eb)) {
-                            inB = true;
+                            fl |= 2u;
                         } else if (pbf >= thBf * (1.0f - eb)) {
                             exact();
-                            if (pb > thB) inB = true;
+                            if (pb > thB) fl |= 2u;
                         }
                     }
-                    if (inA || inB) exact();
-                    if (inA) {
+                    if (fl & 3u) exact();
+                    if (fl & 1u) {
                         sA = scale_from_peak(pa, qo);
                         invA = __double2float_rn(__ddiv_rn(1.0, sA));
                         qAf = qof;
-                        LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                        const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                        halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
                     }
-                    if (inB) {
+                    if (fl & 2u) {
                         sB = scale_from_peak(pb, qo);
                         kB = __double2float_rn(__ddiv_rn(1.0, sB)) / ss.invSbf;
                         qBf = qof;
+                        halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
                     }
                 }
             }
             const float dfb = df * kB;
-            // Certification margins (in units of q) where rounding matters (|q| <= qmax+1):
-            // a_bar: |dq| <= q (ln2 |x2| (ed + 2^-23) + 2^-21), ln2 |x2| <= LA there;
-            // b_bar: |dq| <= |q| (ed + 8 2^-24).
-            const float halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
-            const float halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
             // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23), clamped
             // before rounding so the integer is the reference's clipped code. Two elements
             // per packed f32x2 instruction; codes are kept as magic bit patterns.
-            unsigned ca[8];  // a_bar codes as magic bits, b_bar codes as exact f32 integers
+            unsigned ca[8];  // a_bar codes (>= 0) as integers, b_bar codes as exact f32 integers
             float cb[8];
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
             const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
@@ -332,8 +333,8 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                     const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
                     const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
                     const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
-                    ca[2 * k] = __float_as_uint(ta.x);
-                    ca[2 * k + 1] = __float_as_uint(ta.y);
+                    ca[2 * k] = __float_as_uint(ta.x) - kMagicBits;
+                    ca[2 * k + 1] = __float_as_uint(ta.y) - kMagicBits;
                     float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
                     if constexpr (CL) {
                         qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                     const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
                     if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
-                        ca[m] = code_to_bits(static_cast<int>(
+                        ca[m] = static_cast<unsigned>(static_cast<int>(
                             quant_code_div(exp(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
@@ -369,10 +370,13 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
                             quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
                 }
             }
-            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update
+            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update.
+            // a_bar codes are >= 0: fma(2^52 + c, sA, -2^52 sA) = c sA before its one rounding,
+            // i.e. exactly dmul(c, sA).
+            const double nKA = dmul(sA, -4503599627370496.0);
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                const double a_q = dmul(code_bits_to_double(ca[m]), sA);
+                const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
                 const double b_q = dmul(static_cast<double>(cb[m]), sB);
                 h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
             }
@@ -390,19 +394,19 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
             phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
             double sH = ss.Sh, qH = qa;
             float invHf = ss.invShf;
-            if (dyn && (inH | (phf >= thHf))) {
-                if (!inH) {
+            if (dyn && ((fl & 4u) | (phf >= thHf))) {
+                if (!(fl & 4u)) {
                     if (phf > thHf) {
-                        inH = true;
+                        fl |= 4u;
                     } else {  // phf == fl32(theta): the exact peak decides
                         double ph = 0.0;
 #pragma unroll
                         for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
                         ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
-                        if (ph > thH) inH = true;
+                        if (ph > thH) fl |= 4u;
                     }
                 }
-                if (inH) {
+                if (fl & 4u) {
                     double ph = 0.0;
 #pragma unroll
                     for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
@@ -463,13 +467,13 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
 #pragma unroll
                 for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
                 if (active) {
-                    oout[(static_cast<size_t>(s) * T + ss.crow) * E + i] = o;
+                    obase[ss.ocol] = o;
                     if (p.masks) {
                         const size_t b = (static_cast<size_t>(s) * T + t) * E + i;
                         const size_t kst = static_cast<size_t>(p.S) * T * E;
-                        p.masks[b] = inA;
-                        p.masks[kst + b] = inB;
-                        p.masks[2 * kst + b] = inH;
+                        p.masks[b] = fl & 1u;
+                        p.masks[kst + b] = (fl >> 1) & 1u;
+                        p.masks[2 * kst + b] = (fl >> 2) & 1u;
                     }
                 }
             }
