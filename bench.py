@@ -276,8 +276,10 @@ def run_ours(args):
         # Peak: the measured f64 lane-op rate of this GPU (one DFMA = 1 op).
         ops_per_elem = 28.0
         elem = B * L * E * N
-        achieved = elem * ops_per_elem / (scan_ms / scan_n * 1e-3) / 1e12
+        # one scan op per block (its launches: the step-table prep + the scan kernel)
+        achieved = elem * ops_per_elem / (scan_ms / dims.blocks * 1e-3) / 1e12
         peak_ops = fp64_peak / 2.0
+        traffic = scan_traffic_bytes()
         cfg = dict(CONFIG, global_batch=B * world, parallelism=f"dp{world}")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -288,7 +290,8 @@ def run_ours(args):
                 "gpu_launches": int(launches_per_fwd * args.steps),
                 "roofline": {"kernel": "k3_scan", "bound": "fp64", "achieved": achieved, "peak": peak_ops,
                              "unit": "Tops (f64 lane-ops/s)", "frac": achieved / peak_ops if peak_ops else None,
-                             "traffic": None,
+                             "traffic": traffic,
+                             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01/ncu_traffic_r01d.json)",
                              "peak_source": "measured in-process: DFMA probe (1 op per DFMA lane)",
                              "work": f"{ops_per_elem:.0f} f64 lane-ops x S*T*E*N state-element-steps per launch"},
                 "kernels_ms_per_step": {k: v[0] for k, v in fam.items()},
@@ -303,6 +306,18 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def scan_traffic_bytes():
+    """DRAM bytes (read + write) of one k3_scan_fast launch from the committed
+    `ncu --set full` capture of this workload, or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_traffic_r01d.json")
+    try:
+        with open(path) as f:
+            k = json.load(f)["kernels"]
+        return [v for n, v in k.items() if n.startswith("k3_scan_fast")][0][0]["traffic_bytes"]
+    except Exception:
+        return None
 
 
 def main():

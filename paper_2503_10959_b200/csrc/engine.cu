@@ -653,11 +653,12 @@ void Model::tick_begin(int fam) {
     cuda_check(cudaEventCreate(&b), "event");
     cuda_check(cudaEventRecord(a, ctx->stream), "event record");
     timing.ev.push_back({fam, {a, b}});
+    timing.k0 = kernel_launch_counter();
 }
 void Model::tick_end(int fam) {
     if (!timing.on) return;
     cuda_check(cudaEventRecord(timing.ev.back().second.second, ctx->stream), "event record");
-    timing.launches[fam] += 1;
+    timing.launches[fam] += static_cast<int>(kernel_launch_counter() - timing.k0);  // kernels, not ops
 }
 void Model::timing_collect() {
     cuda_check(cudaStreamSynchronize(ctx->stream), "timing sync");

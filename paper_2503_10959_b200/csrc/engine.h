@@ -166,6 +166,7 @@ class Model {
         double ms[FAM_COUNT] = {0, 0, 0, 0, 0};
         int launches[FAM_COUNT] = {0, 0, 0, 0, 0};
         bool keep_list = false;
+        long k0 = 0;  // kernel_launch_counter() at tick_begin
         std::vector<std::pair<int, double>> list;  // (family, ms) per launch, in order
     } timing;
     void tick_begin(int fam);

@@ -376,6 +376,7 @@ static cudaError_t launch_literal(const K1Params& p, cudaStream_t st) {
     else if (J <= 24) k1_literal<24, SRC><<<blocks, threads, 0, st>>>(p);
     else if (J <= 32) k1_literal<32, SRC><<<blocks, threads, 0, st>>>(p);
     else return cudaErrorInvalidValue;
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 
@@ -386,11 +387,13 @@ static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
     if (SRC == K1_SRC_RMSNORM) {
         const long rows = static_cast<long>(p.S) * p.T;
         k1_rownorm<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(p.x, p.rs, rows, p.E);
+        ++kernel_launch_counter();
     }
     const int nwin = (p.T + p.window - 1) / p.window;
     const int quads = p.E / 4, threads = quads >= 256 ? 256 : ((quads + 31) / 32) * 32;
     dim3 grid((quads + threads - 1) / threads, p.S * nwin);
     k1_channel<SRC><<<grid, threads, 0, st>>>(p);
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 

@@ -383,6 +383,7 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
     k2_qlinear<BN, POST, PLANES><<<grid, kThreads, smem, st>>>(ta, tb, to, to2, p);
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 

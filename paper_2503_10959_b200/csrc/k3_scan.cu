@@ -128,9 +128,11 @@ cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal
         if (p.E > 1024) return cudaErrorInvalidValue;
         const int threads = ((p.E + 31) / 32) * 32;
         k3_scan<true, 16><<<dim3(1, p.S), threads, 0, st>>>(p);
+        ++kernel_launch_counter();
     } else {
         const int threads = 128;
         k3_scan<false, 16><<<dim3((p.E + threads - 1) / threads, p.S), threads, 0, st>>>(p);
+        ++kernel_launch_counter();
     }
     return cudaGetLastError();
 }

@@ -493,6 +493,7 @@ static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* s
     }
     dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
     k3_scan_fast<EXACT, ABITS><<<grid, kThr, smem, st>>>(P, steps);
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 
@@ -518,6 +519,7 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     StepShared* steps = static_cast<StepShared*>(work);
     const int warps = ndirs * S * T;
     k3_step_tables<<<(warps + 7) / 8, 256, 0, st>>>(P, ndirs, steps);
+    ++kernel_launch_counter();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     switch (dirs[0].abits) {

@@ -80,6 +80,7 @@ cudaError_t launch_dgemm(const DGemmParams& p, cudaStream_t st) {
     if (p.M < 1 || p.R < 1 || p.K < 1) return cudaErrorInvalidValue;
     dim3 grid((p.R + DG_BN - 1) / DG_BN, (p.M + DG_BM - 1) / DG_BM);
     k4_dgemm<<<grid, 256, 0, st>>>(p);
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 
@@ -105,6 +106,7 @@ __global__ void k4_patch_gather(const double* __restrict__ img, double* __restri
 cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,
                                 cudaStream_t st) {
     k4_patch_gather<<<1184, 256, 0, st>>>(img, patches, S, image, channels, patch);
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 
@@ -171,8 +173,10 @@ cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, 
         const int nrun = (T + 13) / 14;
         dim3 grid((E / 2 + 127) / 128, S * nrun);
         k4_conv_run<4><<<grid, 128, 0, st>>>(u0, taps, u, S, T, E);
+        ++kernel_launch_counter();
     } else {
         k4_conv<<<2368, 256, 0, st>>>(u0, taps, u, S, T, E, W);
+        ++kernel_launch_counter();
     }
     return cudaGetLastError();
 }
@@ -189,6 +193,7 @@ __global__ void k4_meanpool(const double* __restrict__ x, double* __restrict__ p
 
 cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st) {
     k4_meanpool<<<dim3((E + 127) / 128, S), 128, 0, st>>>(x, pooled, S, T, E);
+    ++kernel_launch_counter();
     return cudaGetLastError();
 }
 

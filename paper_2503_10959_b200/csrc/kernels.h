@@ -7,6 +7,13 @@
 
 namespace ob {
 
+// Kernels launched by the calling host thread (every launch_* wrapper counts its
+// <<<>>> launches; the engine reports per-op deltas as gpu_launches).
+inline long& kernel_launch_counter() {
+    static thread_local long n = 0;
+    return n;
+}
+
 enum Mode { MODE_FP = 0, MODE_DYNAMIC = 1, MODE_STATIC = 2 };  // quant.hpp:101 (FP == bypass)
 enum K1Src { K1_SRC_PLAIN = 0, K1_SRC_RMSNORM = 1, K1_SRC_MERGE = 2 };
 

@@ -6,7 +6,7 @@ import csv, collections, subprocess, sys
 
 rep = sys.argv[1]
 norm = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + (["-k", sys.argv[3]] if len(sys.argv) > 3 else []),
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr, fname = None, None
