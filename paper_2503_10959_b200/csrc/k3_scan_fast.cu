@@ -6,8 +6,9 @@
 // adjacent lanes own one channel, 8 of its N = 16 states each, so a warp
 // covers 16 channels. Warps are independent: each stages its own copy of the
 // per-step values in its own shared-memory slice and synchronises only with
-// __syncwarp, so a warp delayed by a rare exact fallback never stalls the others. The two halves of a channel exchange two values per step
-// through shuffles: the h peak (max is order-free) and the running output sum —
+// __syncwarp, so a warp delayed by a rare exact fallback never stalls the
+// others. The two halves of a channel exchange two values per step through
+// shuffles: the h peak (max is order-free) and the running output sum —
 // the first half computes 0 + C_0 h_0 + ... + C_7 h_7 in order and the second
 // half continues the same chain with C_8 h_8 ... C_15 h_15, which is the
 // reference's sequential sum (ssm.cpp:170-174) bit-for-bit.
