@@ -15,6 +15,9 @@ lst = m.forward_profile_launches(imgs, cal, ob.MODE_DYNAMIC)
 names = ["patch_gather", "patch_embed"]
 per_block = ["K1 in_proj", "K2 in_proj", "conv", "K1 x_proj d0", "K2 x_proj d0", "K1 x_proj d1", "K2 x_proj d1",
              "K3 scan", "K1 out_proj", "K2 out_proj"]
+if (len(lst) - 4) == 8 * blocks:  # conv fused with both x_proj K1s
+    per_block = ["K1 in_proj", "K2 in_proj", "conv+K1 x_proj", "K2 x_proj d0", "K2 x_proj d1", "K3 scan",
+                 "K1 out_proj", "K2 out_proj"]
 for b in range(blocks): names += per_block
 names += ["meanpool", "head"]
 agg = collections.defaultdict(float)
