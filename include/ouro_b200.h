@@ -192,6 +192,11 @@ ouro_status ouro_b200_forward_profile_launches(ouro_b200_model* m, ouro_b200_cal
  * the roofline denominator of the f64 scan (no vendor figure is used). */
 ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops);
 
+/* Measured dense int8 tensor throughput (TOP/s, 2 ops per MAC) of this device:
+ * back-to-back tcgen05.mma.kind::i8 M=128 N=256 K=32 on every SM, the K2
+ * roofline denominator. */
+ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops);
+
 /* Parity harness: run a forward over host images and keep every
  * intermediate of one block (keys documented in DESIGN.md §5). */
 ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,

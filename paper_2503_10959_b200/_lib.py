@@ -55,6 +55,7 @@ _SIGS = {
     "ouro_b200_forward_profile":([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P], _I),
     "ouro_b200_forward_profile_launches": ([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
+    "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_trace_run": ([_P, _P, _I, _I, _I, _P, _SZ, _SZ, C.POINTER(_P)], _I),
     "ouro_b200_trace_get": ([_P, C.c_char_p, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_trace_free": ([_P], None),

@@ -529,6 +529,14 @@ ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops) {
     });
 }
 
+ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops) {
+    return guarded([&] {
+        require(ctx && tops, "measure_i8_peak: NULL argument");
+        *tops = ob::measure_i8_peak(ctx->c->stream, ctx->c->num_sms);
+        ob::require(*tops > 0.0, "measure_i8_peak: probe failed");
+    });
+}
+
 ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
                                 const double* images_host, size_t B, size_t block, ouro_b200_trace** out) {
     return guarded([&] {

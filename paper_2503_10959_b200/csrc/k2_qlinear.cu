@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 3) {  // ---- row metadata producer: S_m, |O| and mask words of upcoming tiles
         const int J = p.a.J;
+        const bool smask = J <= 32;  // mask rows fit the slot (K <= 1024); else the epilogue reads them globally
         const bool bulk_ok = ((reinterpret_cast<uintptr_t>(p.a.s_row) | reinterpret_cast<uintptr_t>(p.a.ocnt) |
                                reinterpret_cast<uintptr_t>(p.a.omask)) & 15) == 0;
         int it = 0;
@@ -167,11 +168,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nrows = min(kBM, p.M - m0);
             if (nrows == kBM && bulk_ok) {  // full tile: three contiguous bulk copies onto the slot's barrier
                 if (lane == 0) {
-                    const uint32_t mbytes = static_cast<uint32_t>(kBM * J * 4);
+                    const uint32_t mbytes = smask ? static_cast<uint32_t>(kBM * J * 4) : 0u;
                     ptx::mbar_arrive_expect_tx(meta_full + slot, kBM * 8 + kBM * 4 + mbytes);
                     ptx::bulk_g2s(ms, p.a.s_row + m0, kBM * 8, meta_full + slot);
                     ptx::bulk_g2s(mc, p.a.ocnt + m0, kBM * 4, meta_full + slot);
-                    ptx::bulk_g2s(mm, p.a.omask + static_cast<size_t>(m0) * J, mbytes, meta_full + slot);
+                    if (smask) ptx::bulk_g2s(mm, p.a.omask + static_cast<size_t>(m0) * J, mbytes, meta_full + slot);
                 }
                 continue;
             }
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ms[i] = v ? __ldg(p.a.s_row + m0 + i) : 0.0;
                 mc[i] = v ? __ldg(p.a.ocnt + m0 + i) : 0;
             }
-            {
+            if (smask) {
                 const uint32_t* src = p.a.omask + static_cast<size_t>(m0) * J;
                 const int n = nrows * J;
                 for (int i = lane; i < n; i += 32) mm[i] = __ldg(src + i);
@@ -211,7 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint8_t* mb = smem + L::kMetaOff + mslot * L::kMetaBytes;
             const double S = reinterpret_cast<const double*>(mb + L::kMetaS)[q * 32 + lane];
             const int cnt = reinterpret_cast<const int*>(mb + L::kMetaCnt)[q * 32 + lane];
-            const uint32_t* msk = reinterpret_cast<const uint32_t*>(mb + L::kMetaMask) + (q * 32) * p.a.J;
+            const uint32_t* msk = p.a.J <= 32 ? reinterpret_cast<const uint32_t*>(mb + L::kMetaMask) + (q * 32) * p.a.J
+                                              : p.a.omask + static_cast<size_t>(rbase) * p.a.J;
             ptx::mbar_wait(acc_full + buf, aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     bits &= bits - 1;
                     const size_t oi = static_cast<size_t>(row) * p.K + ch;
                     const int xo_i = p.a.ocode[oi];
-                    const double xo = static_cast<double>(xo_i);
+                    const double xo = i32_to_f64(static_cast<uint32_t>(xo_i));
                     const double osc = p.a.oscale[oi];
                     const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(ch) * p.R + r0);
                     int4 w01 = __ldg(wp), w23 = __ldg(wp + 1);
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const int wq = j < 16 ? wv[j] : wv2[j - 16];
-                        const double coeff = dmul(osc, static_cast<double>(wq));
+                        const double coeff = dmul(osc, i32_to_f64(static_cast<uint32_t>(wq)));
                         y[j] = dadd(y[j], dmul(coeff, xo));
                         if (PLANES) aout[j] += wq * xo_i;
                     }
@@ -319,6 +321,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     if (warp == 2) ptx::tmem_dealloc<2 * BN>(tmem_base);
+}
+
+// ---- int8 tensor-pipe probe (the INT8 peak is measured, not assumed) ----
+// One CTA per SM; one thread issues `iters` x 4 back-to-back
+// tcgen05.mma.cta_group::1.kind::i8 (M=128, N=256, K=32) on shared-memory
+// operands into a TMEM accumulator, then commits once.
+__global__ void __launch_bounds__(128, 1) k2_i8_probe(int iters) {
+    __shared__ __align__(1024) uint8_t sb[256 * 128];  // operand values are irrelevant here:
+    uint8_t* sa = sb;                                  // A aliases B's first 128 rows
+    __shared__ uint64_t done;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&done, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<256>(&slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t d = slot;
+    if (threadIdx.x == 0) {
+        constexpr uint32_t idesc = ptx::idesc_i8(128, 256);
+        const uint64_t da = ptx::smem_desc_sw128(sa), db = ptx::smem_desc_sw128(sb);
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ptx::mma_i8(d, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
+        ptx::mma_commit(&done);
+        ptx::mbar_wait(&done, 0);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<256>(d);
+}
+
+double measure_i8_peak(cudaStream_t st, int num_sms) {
+    const int iters = 8192;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k2_i8_probe<<<num_sms, 128, 0, st>>>(iters);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0, st);
+        k2_i8_probe<<<num_sms, 128, 0, st>>>(iters);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess) return 0.0;
+    const double ops = 2.0 * 128 * 256 * 32 * 4.0 * iters * num_sms;
+    return ops / (best * 1e-3) / 1e12;
 }
 
 // ---- host side -------------------------------------------------------------
@@ -391,7 +449,7 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.M < 1 || p.R < 1 || p.K < 1 || (p.K % 16) != 0 || (p.R % 16) != 0) return cudaErrorInvalidValue;
     if (p.epi.post == POST_INPROJ && (p.epi.split % 32) != 0) return cudaErrorInvalidValue;
     if ((p.epi.ld_out % 2) != 0 || (p.R % 32) != 0) return cudaErrorInvalidValue;  // TMA pitch, whole chunks
-    if (p.a.J < (p.K + 31) / 32 || p.a.J > 32) return cudaErrorInvalidValue;  // mask rows staged in smem: K <= 1024
+    if (p.a.J < (p.K + 31) / 32) return cudaErrorInvalidValue;
     const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
     if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
 #define K2_CASE(P)                                                                                       \

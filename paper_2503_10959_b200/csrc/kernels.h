@@ -144,6 +144,7 @@ cudaError_t launch_patch_gather(const double* img, double* patches, int S, int i
 cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, int T, int E, int W,
                         cudaStream_t st);
 double measure_fp64_peak(cudaStream_t st, int num_sms);  // TFLOP/s (DFMA = 2 flops)
+double measure_i8_peak(cudaStream_t st, int num_sms);    // dense int8 tensor TOP/s (tcgen05 kind::i8)
 cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st);
 
 }  // namespace ob

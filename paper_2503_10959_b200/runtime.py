@@ -125,6 +125,12 @@ class Context:
         L.check(self.lib.ouro_b200_measure_fp64_peak(self.h, C.byref(v)))
         return v.value
 
+    def measure_i8_peak(self) -> float:
+        """Measured dense int8 tensor-core throughput of this device in TOP/s."""
+        v = C.c_double()
+        L.check(self.lib.ouro_b200_measure_i8_peak(self.h, C.byref(v)))
+        return v.value
+
     # ---- operators (device tensors) --------------------------------------------
     def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
                         mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, literal=False,

@@ -30,7 +30,7 @@ def _unpack(words: np.ndarray, K: int) -> np.ndarray:
 
 
 @pytest.mark.parametrize("M,R,K,n_o", [(128, 128, 128, 0), (300, 160, 256, 5), (1000, 800, 768, 12),
-                                       (77, 1536, 192, 3), (4096, 768, 768, 8)])
+                                       (77, 1536, 192, 3), (4096, 768, 768, 8), (260, 96, 2048, 40)])
 def test_quant_linear_shared_outliers_bit_exact(oracle_checker, gpu_ctx, M, R, K, n_o):
     """hybrid_gemm with one outlier list for all columns (gemm.cpp:181-225):
     acc_inlier / acc_outlier bit-exact, output bit-exact (same f64 op order)."""

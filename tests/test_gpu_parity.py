@@ -217,3 +217,25 @@ def test_scan_variants_identical(pair, abits):
         outs.append(gm.forward_host(imgs, gcal, 1))
     gm.set_option("scan_variant", 0)
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("abits,n_refresh", [(4, 10), (8, 7)])
+def test_long_sequence_c4(oracle_checker, gpu_ctx, abits, n_refresh):
+    """C4-shaped sequence length (448x448 / 16 -> L = 784, scan grid 28) at a
+    small width: FP and quantized logits match the oracle, per-block traces are
+    bit-exact for the quantized operands (refresh windows not dividing L)."""
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    dims = dict(image=112, channels=3, patch=4, embed=64, state=16, blocks=1, classes=10, conv_width=4)
+    om = oracle_checker.model(O.Dims(**dims), SEED)
+    gm = ob.Model(gpu_ctx, ob.Dims(**dims), SEED)
+    od = O.Dims(**dims)
+    assert od.image // od.patch == 28
+    imgs = oracle_checker.normal(11, 2 * od.pix).reshape(2, od.image, od.image, od.channels)
+    cimgs = oracle_checker.normal(12, 2 * od.pix).reshape(2, od.image, od.image, od.channels)
+    assert rel_err(gm.forward_host(imgs, None, 0), om.forward(imgs, None, 0)) <= RTOL_F64
+    spec = _spec(abits, n_refresh=n_refresh, rho=0.02)
+    ocal = om.calibrate(cimgs, spec)
+    gcal = _import_calib(gm, ocal.export(), spec)
+    for mode in (1, 2):
+        assert rel_err(gm.forward_host(imgs, gcal, mode), om.forward(imgs, ocal, mode)) <= RTOL_F64, mode
