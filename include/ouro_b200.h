@@ -149,6 +149,20 @@ ouro_status ouro_b200_calib_create(ouro_b200_model* m, const unsigned* bits /* w
 ouro_status ouro_b200_calibrate(ouro_b200_model* m, const double* images_dev, size_t B, const unsigned* bits,
                                 size_t n_refresh, double rho, int d1, int d2, size_t chunk, ouro_b200_calib** out);
 void ouro_b200_calib_free(ouro_b200_calib* c);
+/* Calibration directories in the reference's on-disk format
+ * (save_calibration / load_calibration, quant.cpp:179-290): calibration.txt
+ * plus one <name>_scales.ouro f64 [2][tokens] file per scan tensor
+ * block<b>.dir<d>.{a_bar,b_bar,h}. The D2 linear-site tables go to
+ * d2_linear_sites.txt (+ scale files), which the reference ignores. Load
+ * checks the directory against the model's dims; d2 = 1 needs the D2 file
+ * (a reference-written directory loads with d2 = 0). Missing or malformed
+ * files -> OURO_ERR_IO. */
+ouro_status ouro_b200_calib_save(ouro_b200_calib* c, ouro_b200_model* m, const char* dir);
+ouro_status ouro_b200_calib_load(ouro_b200_model* m, const char* dir, int d1, int d2, ouro_b200_calib** out);
+/* The spec a calibration carries: bits = {weight, act, outlier}, n_refresh, rho, d1, d2. */
+ouro_status ouro_b200_calib_spec(ouro_b200_calib* c, unsigned* bits, size_t* n_refresh, double* rho, int* d1,
+                                 int* d2);
+
 ouro_status ouro_b200_calib_count(ouro_b200_calib* c, int which, size_t* out);
 ouro_status ouro_b200_calib_get(ouro_b200_calib* c, int which, size_t idx, double* theta, double* s_in,
                                 double* s_full, uint8_t* excluded);

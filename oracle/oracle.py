@@ -148,6 +148,8 @@ class Checker:
             L.ref_pin_fp_forward.argtypes = [_P, _P, _SZ, _P]
             L.ref_pin_calibrate.argtypes = [_P, _P, _SZ, _P, _SZ, C.c_double, C.POINTER(_P)]
             L.ref_pin_quantized_forward.argtypes = [_P, _P, C.c_int, _P, _SZ, _P, _P]
+            L.ref_pin_save_calibration.argtypes = [_P, C.c_char_p]
+            L.ref_pin_load_calibration.argtypes = [C.c_char_p, C.POINTER(_P)]
 
     def _check(self, st: int) -> None:
         if st != 0:
@@ -316,6 +318,16 @@ class Model:
         self.chk._check(self.chk.lib.ref_pin_quantized_forward(self.h, calib.h, mode, _ptr(images), B, _ptr(lq),
                                                                _ptr(lf)))
         return lq, lf
+
+    def ref_save_calibration(self, calib: "CalibHandle", directory: str) -> None:
+        """The reference's own save_calibration (quant.cpp:179-216) of a handle's scan tensors."""
+        self.chk._check(self.chk.lib.ref_pin_save_calibration(calib.h, str(directory).encode()))
+
+    def ref_load_calibration(self, directory: str, spec: Spec) -> "CalibHandle":
+        """The reference's own load_calibration (quant.cpp:218-290)."""
+        h = C.c_void_p()
+        self.chk._check(self.chk.lib.ref_pin_load_calibration(str(directory).encode(), C.byref(h)))
+        return CalibHandle(self, h, spec)
 
 
 class CalibHandle:

@@ -302,4 +302,64 @@ int ref_pin_quantized_forward(void* m, void* c, int mode, const double* images, 
     });
 }
 
+// save_calibration (quant.cpp:179-216) of a calibration handle's scan tensors,
+// named block<b>.dir<d>.<kind> as calibrate names them (quant.cpp:150-151).
+int ref_pin_save_calibration(void* c, const char* dir) {
+    return guarded([&] {
+        const oro::Calib& k = static_cast<CalibH*>(c)->c;
+        ouro::CalibrationResult cr;
+        cr.spec.weight_bits = k.spec.wbits;
+        cr.spec.act_bits = k.spec.abits;
+        cr.spec.outlier_bits = k.spec.obits;
+        cr.spec.n_refresh = k.spec.n_refresh;
+        cr.spec.rho = k.spec.rho;
+        cr.tokens = k.tokens;
+        cr.embed = k.embed;
+        cr.state = k.state;
+        cr.blocks = k.blocks;
+        cr.ndirs = k.ndirs;
+        const char* kinds[3] = {"a_bar", "b_bar", "h"};
+        for (std::size_t b = 0; b < k.blocks; ++b)
+            for (std::size_t d = 0; d < k.ndirs; ++d)
+                for (int q = 0; q < 3; ++q) {
+                    const oro::TCal& t = k.at(b, d, q);
+                    ouro::TensorCalib tc;
+                    tc.name = "block" + std::to_string(b) + ".dir" + std::to_string(d) + "." + kinds[q];
+                    tc.theta = t.theta;
+                    tc.scale_inlier = t.s_in;
+                    tc.scale_full = t.s_full;
+                    tc.excluded.assign(t.excluded.begin(), t.excluded.end());
+                    cr.tensors.push_back(std::move(tc));
+                }
+        ouro::save_calibration(dir, cr);
+    });
+}
+
+// load_calibration (quant.cpp:218-290) into a calibration handle (scan tensors).
+int ref_pin_load_calibration(const char* dir, void** out) {
+    return guarded([&] {
+        ouro::CalibrationResult cr = ouro::load_calibration(dir);
+        auto h = std::make_unique<CalibH>();
+        oro::Calib& c = h->c;
+        const unsigned bits[3] = {cr.spec.weight_bits, cr.spec.act_bits, cr.spec.outlier_bits};
+        c.spec = make_spec(bits, cr.spec.n_refresh, cr.spec.rho);
+        c.tokens = cr.tokens;
+        c.embed = cr.embed;
+        c.state = cr.state;
+        c.blocks = cr.blocks;
+        c.ndirs = cr.ndirs;
+        c.d1 = false;
+        c.d2 = false;
+        for (const auto& t : cr.tensors) {
+            oro::TCal tc;
+            tc.theta = t.theta;
+            tc.s_in = t.scale_inlier;
+            tc.s_full = t.scale_full;
+            tc.excluded = t.excluded;
+            c.scan.push_back(std::move(tc));
+        }
+        *out = h.release();
+    });
+}
+
 }  // extern "C"

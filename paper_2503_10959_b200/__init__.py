@@ -6,9 +6,9 @@ sm_100a kernels of ``libouro_b200.so``. Names mirror the reference's C++
 operator API (``/root/reference/proj/src/ouro/{quant,gemm,ssm}.hpp``).
 """
 from ._lib import (MODE_DYNAMIC, MODE_FP, MODE_STATIC, POST_BIAS, POST_INPROJ, POST_RESID, POST_STORE, SRC_MERGE,
-                   SRC_PLAIN, SRC_RMSNORM, NumericError, OuroError, ValidationError, load)
+                   SRC_PLAIN, SRC_RMSNORM, IoError, NumericError, OuroError, ValidationError, load)
 from .runtime import Calibration, Context, Dims, Model, QuantSpec, TensorCal, Trace
 
 __all__ = ["Context", "Model", "Calibration", "TensorCal", "QuantSpec", "Dims", "Trace", "load", "OuroError",
-           "ValidationError", "NumericError", "MODE_FP", "MODE_DYNAMIC", "MODE_STATIC", "POST_STORE", "POST_INPROJ",
+           "ValidationError", "NumericError", "IoError", "MODE_FP", "MODE_DYNAMIC", "MODE_STATIC", "POST_STORE", "POST_INPROJ",
            "POST_RESID", "POST_BIAS", "SRC_PLAIN", "SRC_RMSNORM", "SRC_MERGE"]

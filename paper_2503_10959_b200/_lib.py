@@ -56,6 +56,10 @@ _SIGS = {
     "ouro_b200_forward_profile_launches": ([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
+    "ouro_b200_calib_save": ([_P, _P, C.c_char_p], _I),
+    "ouro_b200_calib_load": ([_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], _I),
+    "ouro_b200_calib_spec": ([_P, C.POINTER(C.c_uint), C.POINTER(C.c_size_t), C.POINTER(_D), C.POINTER(C.c_int),
+                              C.POINTER(C.c_int)], _I),
     "ouro_b200_trace_run": ([_P, _P, _I, _I, _I, _P, _SZ, _SZ, C.POINTER(_P)], _I),
     "ouro_b200_trace_get": ([_P, C.c_char_p, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_trace_free": ([_P], None),
@@ -75,6 +79,10 @@ class ValidationError(OuroError):
 
 
 class NumericError(OuroError):
+    pass
+
+
+class IoError(OuroError):
     pass
 
 
@@ -105,4 +113,6 @@ def check(status: int) -> None:
         raise ValidationError(status, msg)
     if status == ERR_NUMERIC:
         raise NumericError(status, msg)
+    if status == ERR_IO:
+        raise IoError(status, msg)
     raise OuroError(status, msg)

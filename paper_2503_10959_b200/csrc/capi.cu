@@ -26,6 +26,9 @@ ouro_status guarded(Fn&& fn) {
     } catch (const ob::NumericError& e) {
         g_last_error = e.what();
         return OURO_ERR_NUMERIC;
+    } catch (const ob::IoError& e) {
+        g_last_error = e.what();
+        return OURO_ERR_IO;
     } catch (const std::exception& e) {
         g_last_error = std::string("internal error: ") + e.what();
         return OURO_ERR_VALIDATION;
@@ -337,6 +340,46 @@ ouro_status ouro_b200_calibrate(ouro_b200_model* m, const double* images_dev, si
     });
 }
 void ouro_b200_calib_free(ouro_b200_calib* c) { delete c; }
+
+ouro_status ouro_b200_calib_save(ouro_b200_calib* c, ouro_b200_model* m, const char* dir) {
+    return guarded([&] {
+        require(c && m && dir, "calib_save: NULL argument");
+        ob::save_calibration_dir(*c->c, m->m->d.state, dir);
+    });
+}
+
+ouro_status ouro_b200_calib_load(ouro_b200_model* m, const char* dir, int d1, int d2, ouro_b200_calib** out) {
+    return guarded([&] {
+        require(m && dir && out, "calib_load: NULL argument");
+        auto h = std::make_unique<ouro_b200_calib>();
+        h->c = std::make_unique<ob::Calibration>();
+        ob::Calibration& c = *h->c;
+        const ob::Dims& d = m->m->d;
+        c.d1 = d1 != 0;
+        c.tokens = d.tokens();
+        c.embed = d.embed;
+        c.blocks = d.blocks;
+        c.ndirs = static_cast<int>(m->m->host.orders.size());
+        ob::load_calibration_dir(c, d.state, dir, d2 != 0);
+        require(c.spec.abits <= 8 && c.spec.wbits <= 4, "calib_load: bit widths outside this build's operands");
+        *out = h.release();
+    });
+}
+
+ouro_status ouro_b200_calib_spec(ouro_b200_calib* c, unsigned* bits, size_t* n_refresh, double* rho, int* d1,
+                                 int* d2) {
+    return guarded([&] {
+        require(c && bits && n_refresh && rho && d1 && d2, "calib_spec: NULL argument");
+        const ob::Calibration& k = *c->c;
+        bits[0] = k.spec.wbits;
+        bits[1] = k.spec.abits;
+        bits[2] = k.spec.obits;
+        *n_refresh = static_cast<size_t>(k.spec.n_refresh);
+        *rho = k.spec.rho;
+        *d1 = k.d1 ? 1 : 0;
+        *d2 = k.d2 ? 1 : 0;
+    });
+}
 
 ouro_status ouro_b200_calib_count(ouro_b200_calib* c, int which, size_t* out) {
     return guarded([&] {

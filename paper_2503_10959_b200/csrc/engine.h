@@ -21,6 +21,9 @@ struct ValidationError : std::runtime_error {
 struct NumericError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 inline void require(bool c, const std::string& m) {
     if (!c) throw ValidationError(m);
 }
@@ -108,6 +111,10 @@ class Calibration {
     const double* inv_in_dev(bool is_lin, size_t idx) const;
     const double* inv_full_dev(bool is_lin, size_t idx) const;
 };
+
+// Calibration directories in the reference's format (calib_io.cpp).
+void save_calibration_dir(const Calibration& c, int state, const std::string& dir);
+void load_calibration_dir(Calibration& c, int state, const std::string& dir, bool want_d2);
 
 class Model {
   public:

@@ -231,6 +231,11 @@ class Calibration:
     def export(self):
         return ([self.get(0, i) for i in range(self.count(0))], [self.get(1, i) for i in range(self.count(1))])
 
+    def save(self, directory: str) -> None:
+        """Write the reference's calibration directory (save_calibration,
+        quant.cpp:179-216) plus the D2 linear-site tables (d2_linear_sites.txt)."""
+        L.check(self.lib.ouro_b200_calib_save(self.h, self.model.h, str(directory).encode()))
+
 
 class Trace:
     def __init__(self, lib, h):
@@ -295,6 +300,18 @@ class Model:
         for i, t in enumerate(lin):
             cal.set(1, i, t)
         return cal
+
+    def load_calibration(self, directory: str, d1: bool = True, d2: bool = True) -> Calibration:
+        """Read a calibration directory (load_calibration, quant.cpp:218-290);
+        d2 needs the D2 tables this library writes (reference-written: d2=False)."""
+        h = C.c_void_p()
+        L.check(self.lib.ouro_b200_calib_load(self.h, str(directory).encode(), int(d1), int(d2), C.byref(h)))
+        bits = (C.c_uint * 3)()
+        nr, rho, k1, k2 = C.c_size_t(), C.c_double(), C.c_int(), C.c_int()
+        L.check(self.lib.ouro_b200_calib_spec(h, bits, C.byref(nr), C.byref(rho), C.byref(k1), C.byref(k2)))
+        spec = QuantSpec(int(bits[0]), int(bits[1]), int(bits[2]), int(nr.value), float(rho.value), bool(k1.value),
+                         bool(k2.value))
+        return Calibration(self, h, spec)
 
     def calibrate(self, images, spec: QuantSpec, chunk: int = 0) -> Calibration:
         """calibrate (quant.cpp:129-177) on the GPU; images: device f64 tensor [B, H, W, C]."""
