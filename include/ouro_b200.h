@@ -149,6 +149,13 @@ ouro_status ouro_b200_calib_create(ouro_b200_model* m, const unsigned* bits /* w
 ouro_status ouro_b200_calibrate(ouro_b200_model* m, const double* images_dev, size_t B, const unsigned* bits,
                                 size_t n_refresh, double rho, int d1, int d2, size_t chunk, ouro_b200_calib** out);
 void ouro_b200_calib_free(ouro_b200_calib* c);
+/* Dequantized weight operand (quantize_weights + dequantize_rows,
+ * quant.cpp:355-384) at `bits`: "patch_w", "head_w", "block<b>.in" (w_in|w_gate),
+ * "block<b>.out_proj", "block<b>.conv", "block<b>.dir<d>.xp" (w_delta|w_b|w_c).
+ * out == NULL queries the size into *n. Host memory. */
+ouro_status ouro_b200_model_get_qweight(ouro_b200_model* m, const char* name, unsigned bits, double* out,
+                                       size_t cap, size_t* n);
+
 /* Calibration directories in the reference's on-disk format
  * (save_calibration / load_calibration, quant.cpp:179-290): calibration.txt
  * plus one <name>_scales.ouro f64 [2][tokens] file per scan tensor

@@ -149,6 +149,8 @@ class Checker:
             L.ref_pin_calibrate.argtypes = [_P, _P, _SZ, _P, _SZ, C.c_double, C.POINTER(_P)]
             L.ref_pin_quantized_forward.argtypes = [_P, _P, C.c_int, _P, _SZ, _P, _P]
             L.ref_pin_save_calibration.argtypes = [_P, C.c_char_p]
+            L.ref_pin_quant_eval.argtypes = [_P, _P, C.c_int, _P, _SZ, _P, _P, C.POINTER(C.c_double),
+                                             C.POINTER(_SZ), _P]
             L.ref_pin_load_calibration.argtypes = [C.c_char_p, C.POINTER(_P)]
 
     def _check(self, st: int) -> None:
@@ -318,6 +320,18 @@ class Model:
         self.chk._check(self.chk.lib.ref_pin_quantized_forward(self.h, calib.h, mode, _ptr(images), B, _ptr(lq),
                                                                _ptr(lf)))
         return lq, lf
+
+    def ref_quant_eval(self, images: np.ndarray, calib: "CalibHandle", mode: int) -> dict:
+        """The reference's quantized_forward (quant.cpp:505-579) and its metrics."""
+        images = np.ascontiguousarray(images, np.float64)
+        B = images.size // self.dims.pix
+        lq = np.zeros((B, self.dims.classes), np.float64)
+        lf = np.zeros((B, self.dims.classes), np.float64)
+        mse, agree = C.c_double(), _SZ()
+        lm = np.zeros(self.dims.blocks * len(self.orders), np.float64)
+        self.chk._check(self.chk.lib.ref_pin_quant_eval(self.h, calib.h, mode, _ptr(images), B, _ptr(lq), _ptr(lf),
+                                                        C.byref(mse), C.byref(agree), _ptr(lm)))
+        return dict(logits_q=lq, logits_fp=lf, logits_mse=mse.value, argmax_agree=agree.value, layer_mse=lm)
 
     def ref_save_calibration(self, calib: "CalibHandle", directory: str) -> None:
         """The reference's own save_calibration (quant.cpp:179-216) of a handle's scan tensors."""

@@ -302,6 +302,46 @@ int ref_pin_quantized_forward(void* m, void* c, int mode, const double* images, 
     });
 }
 
+// quantized_forward (quant.cpp:505-579) with its metrics: logits_mse, argmax
+// agreement and the teacher-forced per-(block, dir) scan MSE (no spikes).
+int ref_pin_quant_eval(void* m, void* c, int mode, const double* images, std::size_t B, double* logits_q,
+                       double* logits_fp, double* logits_mse, std::size_t* argmax_agree, double* layer_mse) {
+    return guarded([&] {
+        const oro::ModelW& w = static_cast<ModelH*>(m)->w;
+        const oro::Calib& k = static_cast<CalibH*>(c)->c;
+        ouro::ToyVmmModel rm = oro::to_ref(w);
+        std::size_t pix = w.d.image * w.d.image * w.d.channels;
+        ouro::CalibrationResult cr;
+        cr.spec.weight_bits = k.spec.wbits;
+        cr.spec.act_bits = k.spec.abits;
+        cr.spec.outlier_bits = k.spec.obits;
+        cr.spec.n_refresh = k.spec.n_refresh;
+        cr.spec.rho = k.spec.rho;
+        cr.tokens = k.tokens;
+        cr.embed = k.embed;
+        cr.state = k.state;
+        cr.blocks = k.blocks;
+        cr.ndirs = k.ndirs;
+        for (const oro::TCal& t : k.scan) {
+            ouro::TensorCalib tc;
+            tc.theta = t.theta;
+            tc.scale_inlier = t.s_in;
+            tc.scale_full = t.s_full;
+            tc.excluded.assign(t.excluded.begin(), t.excluded.end());
+            cr.tensors.push_back(std::move(tc));
+        }
+        ouro::QuantMode qm = mode == 1 ? ouro::QuantMode::Dynamic
+                                       : (mode == 2 ? ouro::QuantMode::Static : ouro::QuantMode::Bypass);
+        ouro::QuantEvalResult r = ouro::quantized_forward(rm, std::vector<double>(images, images + B * pix), B, cr, qm,
+                                                          ouro::SpikeSettings{});
+        std::memcpy(logits_q, r.logits_q.data(), r.logits_q.size() * sizeof(double));
+        std::memcpy(logits_fp, r.logits_fp.data(), r.logits_fp.size() * sizeof(double));
+        *logits_mse = r.logits_mse;
+        *argmax_agree = r.argmax_agree;
+        for (std::size_t i = 0; i < r.layer_mse.size(); ++i) layer_mse[i] = r.layer_mse[i].second;
+    });
+}
+
 // save_calibration (quant.cpp:179-216) of a calibration handle's scan tensors,
 // named block<b>.dir<d>.<kind> as calibrate names them (quant.cpp:150-151).
 int ref_pin_save_calibration(void* c, const char* dir) {

@@ -57,6 +57,7 @@ _SIGS = {
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_calib_save": ([_P, _P, C.c_char_p], _I),
+    "ouro_b200_model_get_qweight": ([_P, C.c_char_p, C.c_uint, _P, C.c_size_t, C.POINTER(C.c_size_t)], _I),
     "ouro_b200_calib_load": ([_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], _I),
     "ouro_b200_calib_spec": ([_P, C.POINTER(C.c_uint), C.POINTER(C.c_size_t), C.POINTER(_D), C.POINTER(C.c_int),
                               C.POINTER(C.c_int)], _I),

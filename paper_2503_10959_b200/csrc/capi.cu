@@ -303,6 +303,20 @@ static ob::QuantSpec spec_from(const unsigned* bits, size_t n_refresh, double rh
     return s;
 }
 
+ouro_status ouro_b200_model_get_qweight(ouro_b200_model* m, const char* name, unsigned bits, double* out,
+                                       size_t cap, size_t* n) {
+    return guarded([&] {
+        require(m && name && n, "model_get_qweight: NULL argument");
+        require(bits >= 2 && bits <= 8, "model_get_qweight: bits must be in [2, 8]");
+        const std::vector<double> v = m->m->host.dequantized(name, bits);
+        *n = v.size();
+        if (out) {
+            require(cap >= v.size(), "model_get_qweight: output buffer too small");
+            std::memcpy(out, v.data(), v.size() * sizeof(double));
+        }
+    });
+}
+
 ouro_status ouro_b200_calib_create(ouro_b200_model* m, const unsigned* bits, size_t n_refresh, double rho, int d1,
                                    int d2, ouro_b200_calib** out) {
     return guarded([&] {

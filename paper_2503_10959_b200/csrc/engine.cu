@@ -232,6 +232,28 @@ void Model::upload_fp() {
     fp_dirty = false;
 }
 
+std::vector<double> HostModel::dequantized(const std::string& name, unsigned bits) const {
+    // quantize_weights + dequantize_rows (quant.cpp:355-384) of one weight matrix; the
+    // fused operands are the row concatenations the engine multiplies by
+    const int E = d.embed, N = d.state;
+    auto at = [&](const std::string& k) -> const std::vector<double>& {
+        auto it = t.find(k);
+        require(it != t.end(), "qweight: unknown tensor '" + k + "'");
+        return it->second;
+    };
+    const size_t p = name.rfind('.');
+    const std::string pre = p == std::string::npos ? "" : name.substr(0, p + 1), leaf = name.substr(p + 1);
+    if (name == "patch_w") return quantize_rows(at("patch_w"), E, bits).deq;
+    if (name == "head_w") return quantize_rows(at("head_w"), d.classes, bits).deq;
+    if (leaf == "in") return quantize_rows(cat({&at(pre + "w_in"), &at(pre + "w_gate")}), 2 * E, bits).deq;
+    if (leaf == "out_proj") return quantize_rows(at(name), E, bits).deq;
+    if (leaf == "conv") return quantize_rows(at(name), E, bits).deq;
+    if (leaf == "xp")
+        return quantize_rows(cat({&at(pre + "w_delta"), &at(pre + "w_b"), &at(pre + "w_c")}), E + 2 * N, bits).deq;
+    throw ValidationError("qweight: '" + name + "' is not a quantized weight (patch_w, head_w, block<b>.in, "
+                          "block<b>.out_proj, block<b>.conv, block<b>.dir<d>.xp)");
+}
+
 void Model::quantize(unsigned bits) {
     if (qbits == bits) return;
     upload_fp();

@@ -82,6 +82,8 @@ struct HostModel {  // ToyVmmModel tensors in f64 (ssm.hpp:58-66)
     Dims d;
     std::vector<int> orders;
     std::map<std::string, std::vector<double>> t;
+    // W4 dequantized operand of a quantized weight (quantize_weights/dequantize_rows)
+    std::vector<double> dequantized(const std::string& name, unsigned bits) const;
 };
 HostModel make_toy_model(const Dims& d, const std::vector<int>& orders, uint64_t seed);
 

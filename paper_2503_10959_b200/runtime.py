@@ -259,6 +259,14 @@ class Trace:
         return self.lib.ouro_b200_trace_get(self.h, key.encode(), None, 0, C.byref(n)) == 0
 
 
+def _scan_perm(order: int, T: int, grid: int) -> np.ndarray:
+    """scan_permutation (ssm.cpp:30-46): canonical token visited at scan step t."""
+    t = np.arange(T)
+    fast, slow = t % grid, t // grid
+    return {0: slow * grid + fast, 1: T - 1 - (slow * grid + fast), 2: fast * grid + slow,
+            3: T - 1 - (fast * grid + slow)}[order]
+
+
 class Model:
     """Toy Vim model (ToyVmmModel, ssm.hpp:58-66) resident on one B200."""
 
@@ -377,6 +385,53 @@ class Model:
         L.check(self.lib.ouro_b200_forward_host(self.h, calib.h if calib else None, mode, int(d1), int(d2),
                                                 _ptr(images), B, _ptr(logits)))
         return logits
+
+    def qweight(self, name: str, bits: int = 4) -> np.ndarray:
+        """W4 dequantized operand (quantize_weights + dequantize_rows, quant.cpp:355-384):
+        patch_w, head_w, block<b>.in, block<b>.out_proj, block<b>.conv, block<b>.dir<d>.xp."""
+        n = C.c_size_t()
+        L.check(self.lib.ouro_b200_model_get_qweight(self.h, name.encode(), bits, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        L.check(self.lib.ouro_b200_model_get_qweight(self.h, name.encode(), bits, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def quant_eval(self, images: np.ndarray, calib: Calibration, mode: int, *, d1=True, d2=True) -> dict:
+        """quantized_forward (quant.cpp:505-579) on the GPU: the FP pass and the
+        quantized pass over host images, logits_mse over all logits, argmax
+        agreement, and the teacher-forced scan-output MSE per (block, dir) -- each
+        direction's quantized scan re-run on the FP pass's own scan input with the
+        W4 x_proj weights (quant.cpp:548-577). Spike injection is not modelled."""
+        import torch
+        images = np.ascontiguousarray(images, np.float64)
+        d = self.dims
+        S, T, E, N = images.size // d.pix, d.tokens, d.embed, d.state
+        lq = self.forward_host(images, calib, mode, d1=d1, d2=d2)
+        lf = self.forward_host(images, None, L.MODE_FP, d1=d1, d2=d2)
+        diff = lf - lq
+        out = dict(logits_fp=lf, logits_q=lq, logits_mse=float(np.sum(diff * diff) / diff.size),
+                   argmax_agree=int(np.sum(np.argmax(lf, axis=1) == np.argmax(lq, axis=1))), batch=S, layer_mse=[])
+        scan, _ = calib.export()
+        nd = len(self.orders)
+        dev = torch.device("cuda", self.ctx.device)
+        tdev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        for b in range(d.blocks):
+            tr = self.trace(images, None, L.MODE_FP, b, d1=d1, d2=d2)
+            u = tr.get("u", np.float64).reshape(S, T, E)
+            for k, order in enumerate(self.orders):
+                perm = _scan_perm(order, T, d.grid)
+                w = tdev(self.qweight(f"block{b}.dir{k}.xp", calib.spec.wbits).reshape(E + 2 * N, E))
+                proj = self.ctx.dgemm(tdev(u[:, perm, :].reshape(S * T, E)), w)  # k-ascending dots, as s6_scan
+                o_tf = torch.empty(S * T * E, dtype=torch.float64, device=dev)
+                tabs = [scan[(b * nd + k) * 3 + q] for q in range(3)]
+                self.ctx.quant_scan(S=S, T=T, E=E, order=order, grid=d.grid, u=tdev(u), proj=proj,
+                                    a=tdev(self.get_tensor(f"block{b}.dir{k}.a")),
+                                    b_delta=tdev(self.get_tensor(f"block{b}.dir{k}.b_delta")), o=o_tf, mode=mode,
+                                    n_refresh=calib.spec.n_refresh, act_bits=calib.spec.abits,
+                                    outlier_bits=calib.spec.obits, theta=[t.theta for t in tabs],
+                                    s_in=[tdev(t.s_in) for t in tabs], s_full=[tdev(t.s_full) for t in tabs])
+                e = tr.get(f"dir{k}.o", np.float64) - o_tf.cpu().numpy()
+                out["layer_mse"].append((f"block{b}.dir{k}", float(np.sum(e * e) / e.size)))
+        return out
 
     def trace(self, images: np.ndarray, calib: Calibration | None, mode: int, block: int, *, d1=True,
               d2=True) -> Trace:

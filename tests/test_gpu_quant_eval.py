@@ -1,0 +1,40 @@
+"""GPU quant-eval == the reference's quantized_forward (quant.cpp:505-579):
+FP and quantized logits, logits_mse, argmax agreement and the teacher-forced
+per-(block, dir) scan-output MSE (run_quant_eval's metrics,
+pipeline.cpp:115-167)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DIMS = dict(image=32, channels=3, patch=8, embed=64, state=16, blocks=2, classes=10, conv_width=4)
+SEED = 9
+
+
+@pytest.mark.parametrize("abits,mode", [(4, 1), (4, 2), (8, 1)])
+def test_quant_eval_matches_reference(ref_checker, gpu_ctx, abits, mode):
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    od = O.Dims(**DIMS)
+    rm = ref_checker.model(od, SEED)
+    cimgs = ref_checker.normal(21, 3 * od.pix).reshape(3, od.image, od.image, od.channels)
+    imgs = ref_checker.normal(22, 4 * od.pix).reshape(4, od.image, od.image, od.channels)
+    spec = O.Spec(wbits=4, abits=abits, obits=8, n_refresh=5, rho=0.05, d1=False, d2=False)
+    rcal = rm.ref_calibrate(cimgs, spec)
+    want = rm.ref_quant_eval(imgs, rcal, mode)
+
+    gm = ob.Model(gpu_ctx, ob.Dims(**DIMS), SEED)
+    conv = lambda t: ob.TensorCal(t.theta, t.s_in, t.s_full, t.excluded)
+    gcal = gm.calibration_from([conv(t) for t in rcal.export().scan], [],
+                               ob.QuantSpec(4, abits, 8, 5, 0.05, False, False))
+    got = gm.quant_eval(imgs, gcal, mode, d1=False, d2=False)
+
+    rel = lambda a, b: float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300))
+    assert rel(got["logits_fp"], want["logits_fp"]) <= 1e-9
+    assert rel(got["logits_q"], want["logits_q"]) <= 1e-9
+    assert got["argmax_agree"] == want["argmax_agree"]
+    assert abs(got["logits_mse"] - want["logits_mse"]) <= 1e-6 * want["logits_mse"]
+    names = [n for n, _ in got["layer_mse"]]
+    assert names == [f"block{b}.dir{d}" for b in range(DIMS["blocks"]) for d in range(2)]
+    lm = np.array([v for _, v in got["layer_mse"]])
+    assert np.all(np.abs(lm - want["layer_mse"]) <= 1e-6 * np.abs(want["layer_mse"]) + 1e-300)
