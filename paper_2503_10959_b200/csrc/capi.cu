@@ -56,8 +56,15 @@ struct ouro_b200_model {
     GraphKey key{};
     int key_hits = 0;
     cudaGraphExec_t exec = nullptr;
+    // end-to-end (host buffer) path: its own graph slot and the H2D copy stream
+    GraphKey hkey{};
+    int hkey_hits = 0;
+    cudaGraphExec_t hexec = nullptr;
+    cudaStream_t copy = nullptr;
     ~ouro_b200_model() {
         if (exec) cudaGraphExecDestroy(exec);
+        if (hexec) cudaGraphExecDestroy(hexec);
+        if (copy) cudaStreamDestroy(copy);
     }
 };
 struct ouro_b200_calib {
@@ -277,6 +284,10 @@ ouro_status ouro_b200_model_set_tensor(ouro_b200_model* m, const char* name, con
             cudaGraphExecDestroy(m->exec);
             m->exec = nullptr;
         }
+        if (m->hexec) {
+            cudaGraphExecDestroy(m->hexec);
+            m->hexec = nullptr;
+        }
     });
 }
 ouro_status ouro_b200_model_get_tensor(ouro_b200_model* m, const char* name, double* host, size_t cap,
@@ -437,6 +448,10 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on) {
             cudaGraphExecDestroy(m->exec);
             m->exec = nullptr;
         }
+        if (!m->graphs && m->hexec) {
+            cudaGraphExecDestroy(m->hexec);
+            m->hexec = nullptr;
+        }
     });
 }
 
@@ -492,18 +507,72 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
                                    const double* images_host, size_t B, double* logits_host) {
     return guarded([&] {
         require(m && images_host && logits_host, "forward_host: NULL argument");
+        require(mode == ob::MODE_FP || c != nullptr, "forward_host: quantized modes need a calibration");
         ob::Model& mm = *m->m;
+        ob::Calibration* cal = c ? c->c.get() : nullptr;
         const size_t pix = static_cast<size_t>(mm.d.image) * mm.d.image * mm.d.channels;
         cudaStream_t st = m->ctx->c->stream;
         mm.w.img.ensure(B * pix);
         mm.w.logits.ensure(B * mm.d.classes);
-        ob::cuda_check(cudaMemcpyAsync(mm.w.img.p, images_host, B * pix * sizeof(double), cudaMemcpyHostToDevice, st),
-                       "H2D images");
-        ouro_status s = ouro_b200_forward(m, c, mode, d1, d2, mm.w.img.p, B, mm.w.logits.p);
-        if (s != OURO_OK) throw ob::ValidationError(g_last_error);
-        ob::cuda_check(cudaMemcpyAsync(logits_host, mm.w.logits.p, B * mm.d.classes * sizeof(double),
-                                       cudaMemcpyDeviceToHost, st),
-                       "D2H logits");
+        const size_t lbytes = B * mm.d.classes * sizeof(double);
+        cudaPointerAttributes attr{};
+        const bool pinned = cudaPointerGetAttributes(&attr, images_host) == cudaSuccess &&
+                            attr.type == cudaMemoryTypeHost;
+        cudaGetLastError();  // clear a benign "not a device pointer" status
+        if (!pinned || st == nullptr) {  // pageable images: staged copy, no overlap
+            ob::cuda_check(cudaMemcpyAsync(mm.w.img.p, images_host, B * pix * sizeof(double), cudaMemcpyHostToDevice, st),
+                           "H2D images");
+            ouro_status s = ouro_b200_forward(m, c, mode, d1, d2, mm.w.img.p, B, mm.w.logits.p);
+            if (s != OURO_OK) throw ob::ValidationError(g_last_error);
+            ob::cuda_check(cudaMemcpyAsync(logits_host, mm.w.logits.p, lbytes, cudaMemcpyDeviceToHost, st), "D2H logits");
+            ob::cuda_check(cudaStreamSynchronize(st), "forward_host sync");
+            return;
+        }
+        if (!m->copy) ob::cuda_check(cudaStreamCreateWithFlags(&m->copy, cudaStreamNonBlocking), "copy stream");
+        // pinned images: the H2D copy runs in 4 chunks on the copy stream, each chunk's
+        // patch gather + embedding waits only for its own chunk (Model::HostFeed)
+        ob::Model::HostFeed feed;
+        feed.host = images_host;
+        feed.copy = m->copy;
+        feed.chunks = B >= 64 ? 4 : 1;
+        auto body = [&] {
+            mm.forward(cal, mode, d1 != 0, d2 != 0, mm.w.img.p, static_cast<int>(B), mm.w.logits.p, nullptr, nullptr,
+                       &feed);
+            ob::cuda_check(cudaMemcpyAsync(logits_host, mm.w.logits.p, lbytes, cudaMemcpyDeviceToHost, st), "D2H logits");
+        };
+        ouro_b200_model::GraphKey key{cal, mode, d1, d2, images_host, B, logits_host};
+        const bool stale = cal && cal->dirty;
+        if (m->graphs && !stale && m->hexec && m->hkey == key) {
+            ob::cuda_check(cudaGraphLaunch(m->hexec, st), "graph launch");
+        } else if (m->graphs && !stale && m->hkey == key && m->hkey_hits >= 1) {
+            cudaGraph_t g = nullptr;
+            ob::cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            try {
+                body();
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ob::cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+            if (m->hexec) cudaGraphExecDestroy(m->hexec);
+            m->hexec = nullptr;
+            ob::cuda_check(cudaGraphInstantiate(&m->hexec, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            ob::cuda_check(cudaGraphLaunch(m->hexec, st), "graph launch");
+        } else {
+            body();
+            if (m->hkey == key) {
+                ++m->hkey_hits;
+            } else {
+                m->hkey = key;
+                m->hkey_hits = 1;
+                if (m->hexec) {
+                    cudaGraphExecDestroy(m->hexec);
+                    m->hexec = nullptr;
+                }
+            }
+        }
         ob::cuda_check(cudaStreamSynchronize(st), "forward_host sync");
     });
 }
@@ -524,6 +593,10 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         if (m->exec) {
             cudaGraphExecDestroy(m->exec);
             m->exec = nullptr;
+        }
+        if (m->hexec) {
+            cudaGraphExecDestroy(m->hexec);
+            m->hexec = nullptr;
         }
     });
 }

@@ -382,7 +382,7 @@ void grab(Model::TraceSink* tr, const std::string& key, const T* dev, size_t n, 
 }  // namespace
 
 void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S, double* logits,
-                    TraceSink* trace, unsigned long long* calib_peaks) {
+                    TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed) {
     require(S >= 1, "forward: batch must be >= 1");
     require(d.state == 16, "this build keeps N = 16 scan states in registers (ModelDims.state must be 16)");
     require(d.embed % 32 == 0 && d.embed <= 1024, "embed must be a multiple of 32 and <= 1024");
@@ -407,20 +407,46 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
     const bool tr_on = trace != nullptr;
     auto tb = [&](int b) { return tr_on && trace->block == b; };
 
-    // patch embed: x = patches . W^T + b (ssm.cpp:253-256), FP or W4-dequantized weights
-    tick_begin(FAM_AUX);
-    cuda_check(launch_patch_gather(images, w.patches.p, S, d.image, d.channels, d.patch, st), "patch gather");
-    tick_end(FAM_AUX);
-    {
+    // patch embed: x = patches . W^T + b (ssm.cpp:253-256), FP or W4-dequantized weights;
+    // per-sample work, so with a host feed it runs chunk by chunk behind the H2D copies
+    const size_t pix = static_cast<size_t>(d.image) * d.image * d.channels;
+    const int nchunk = feed ? std::max(1, std::min(feed->chunks, S)) : 1;
+    if (feed) {
+        while (static_cast<int>(feed_events.size()) < nchunk + 1) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            feed_events.push_back(e);
+        }
+        cuda_check(cudaEventRecord(feed_events[nchunk], st), "feed fork");  // copies start after prior work
+        cuda_check(cudaStreamWaitEvent(feed->copy, feed_events[nchunk], 0), "feed fork");
+        for (int k = 0; k < nchunk; ++k) {
+            const int s0 = static_cast<int>(static_cast<long>(S) * k / nchunk);
+            const int s1 = static_cast<int>(static_cast<long>(S) * (k + 1) / nchunk);
+            cuda_check(cudaMemcpyAsync(const_cast<double*>(images) + s0 * pix, feed->host + s0 * pix,
+                                       (s1 - s0) * pix * sizeof(double), cudaMemcpyHostToDevice, feed->copy),
+                       "H2D images");
+            cuda_check(cudaEventRecord(feed_events[k], feed->copy), "feed event");
+        }
+    }
+    for (int k = 0; k < nchunk; ++k) {
+        const int s0 = static_cast<int>(static_cast<long>(S) * k / nchunk);
+        const int s1 = static_cast<int>(static_cast<long>(S) * (k + 1) / nchunk);
+        if (feed) cuda_check(cudaStreamWaitEvent(st, feed_events[k], 0), "feed wait");
+        const size_t r0 = static_cast<size_t>(s0) * L, nr = static_cast<size_t>(s1 - s0) * L;
+        tick_begin(FAM_AUX);
+        cuda_check(launch_patch_gather(images + s0 * pix, w.patches.p + r0 * d.patch_vals(), s1 - s0, d.image,
+                                       d.channels, d.patch, st),
+                   "patch gather");
+        tick_end(FAM_AUX);
         DGemmParams g;
-        g.M = static_cast<int>(rows);
+        g.M = static_cast<int>(nr);
         g.R = E;
         g.K = d.patch_vals();
-        g.a = w.patches.p;
+        g.a = w.patches.p + r0 * d.patch_vals();
         g.lda = d.patch_vals();
         g.w = quant ? patch_deq.p : patch_w.p;
         g.epi.post = POST_BIAS;
-        g.epi.out = w.x.p;
+        g.epi.out = w.x.p + r0 * E;
         g.epi.ld_out = E;
         g.epi.bias = patch_b.p;
         tick_begin(FAM_DGEMM);

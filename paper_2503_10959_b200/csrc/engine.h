@@ -187,8 +187,16 @@ class Model {
         std::map<std::string, std::vector<char>> blobs;
     };
     // Runs the whole forward on `ctx` stream; images/logits are device pointers.
+    // Host-image feed for the end-to-end call: the H2D copy of chunk k+1 (copy
+    // stream) overlaps the patch gather + embedding of chunk k (main stream).
+    struct HostFeed {
+        const double* host = nullptr;  // pinned host images (B x pix)
+        cudaStream_t copy = nullptr;
+        int chunks = 1;
+    };
     void forward(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S, double* logits,
-                 TraceSink* trace, unsigned long long* calib_peaks);
+                 TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed = nullptr);
+    std::vector<cudaEvent_t> feed_events;  // one per chunk, created on first use
     std::unique_ptr<Calibration> calibrate(const double* images_dev, int S, const QuantSpec& spec, bool d1, bool d2,
                                            int chunk);
 };
