@@ -529,12 +529,12 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
             return;
         }
         if (!m->copy) ob::cuda_check(cudaStreamCreateWithFlags(&m->copy, cudaStreamNonBlocking), "copy stream");
-        // pinned images: the H2D copy runs in 4 chunks on the copy stream, each chunk's
+        // pinned images: the H2D copy runs in 8 chunks on the copy stream, each chunk's
         // patch gather + embedding waits only for its own chunk (Model::HostFeed)
         ob::Model::HostFeed feed;
         feed.host = images_host;
         feed.copy = m->copy;
-        feed.chunks = B >= 64 ? 4 : 1;
+        feed.chunks = B >= 64 ? 8 : 1;
         auto body = [&] {
             mm.forward(cal, mode, d1 != 0, d2 != 0, mm.w.img.p, static_cast<int>(B), mm.w.logits.p, nullptr, nullptr,
                        &feed);
