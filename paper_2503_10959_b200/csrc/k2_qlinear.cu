@@ -431,13 +431,8 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
                       inproj ? p.epi.split : p.epi.ld_out))
         return cudaErrorInvalidValue;
     const int smem = K2Smem<BN>::kTotal;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k2_qlinear<BN, POST, PLANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, POST, PLANES>>(smem);
+    if (e != cudaSuccess) return e;
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
     k2_qlinear<BN, POST, PLANES><<<grid, kThreads, smem, st>>>(ta, tb, to, to2, p);

@@ -484,14 +484,9 @@ __global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const 
 
 template <bool EXACT, int ABITS>
 static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
-    static bool attr = false;
     const int smem = static_cast<int>(sizeof(WarpSmem)) * (kThr / 32);
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k3_scan_fast<EXACT, ABITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = ensure_smem_attr<k3_scan_fast<EXACT, ABITS>>(smem);
+    if (e != cudaSuccess) return e;
     dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
     k3_scan_fast<EXACT, ABITS><<<grid, kThr, smem, st>>>(P, steps);
     ++kernel_launch_counter();

@@ -1,6 +1,7 @@
 // Kernel parameter blocks and launchers (host/device shared, internal to the
 // library; the public boundary is include/ouro_b200.h).
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -12,6 +13,21 @@ namespace ob {
 inline long& kernel_launch_counter() {
     static thread_local long n = 0;
     return n;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, and contexts on several devices may share a process.
+template <auto Kernel>
+cudaError_t ensure_smem_attr(int bytes) {
+    static std::atomic<unsigned long long> done{0};  // bit d: set on device d
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
 }
 
 enum Mode { MODE_FP = 0, MODE_DYNAMIC = 1, MODE_STATIC = 2 };  // quant.hpp:101 (FP == bypass)
