@@ -30,14 +30,25 @@
 
 namespace ob {
 
-constexpr int kBM = 128, kBK = 128, kStages = 3, kEpiWarps = 8, kThreads = 128 + 32 * kEpiWarps;
+constexpr int kBM = 128, kBK = 128;
 constexpr int kStgBufs = 1;  // epilogue staging buffers per warp
-// (K <= a few thousand: the MMA main loop of a tile is short next to its f64
-// epilogue, so shared memory goes to double-buffered epilogue staging instead
-// of deeper operand pipelining.)
+// Two shapes of the same kernel, chosen per call (launch_qlinear):
+//  * EW = 8 epilogue warps, 3 operand stages: main-loop-heavy calls (wide R);
+//  * EW = 16 epilogue warps, 2 operand stages, setmaxnreg moving registers from
+//    warpgroup 0 to the epilogue: epilogue-heavy calls (residual post-op,
+//    outlier terms; the f64 epilogue, not the int8 main loop, bounds those —
+//    main loop alone 0.039 ms of 0.135 for the Vim-B out_proj).
+template <int EW>
+struct K2Cfg {
+    static constexpr int kEpiWarps = EW;
+    static constexpr int kThreads = 128 + 32 * EW;
+    static constexpr int kStages = EW >= 16 ? 2 : 3;
+    static constexpr int kMaskWords = EW >= 16 ? 24 : 32;  // mask words per row staged in shared memory
+};
 
-template <int BN>
+template <int BN, int EW>
 struct K2Smem {
+    static constexpr int kStages = K2Cfg<EW>::kStages, kEpiWarps = EW, kMaskWords = K2Cfg<EW>::kMaskWords;
     static constexpr int kABytes = kBM * kBK;
     static constexpr int kBBytes = BN * kBK;
     static constexpr int kStageBytes = kABytes + kBBytes;
@@ -45,10 +56,10 @@ struct K2Smem {
     static constexpr int kWsOff = kEpiOff + kEpiWarps * kStgBufs * 8192;  // per warp: the chunk's 32 column scales
     // row metadata ring (2 tiles ahead, filled by warp 3): S_m, |O|, mask words (J <= 32)
     static constexpr int kMetaS = 0, kMetaCnt = kBM * 8, kMetaMask = kMetaCnt + kBM * 4;
-    static constexpr int kMetaBytes = kMetaMask + kBM * 32 * 4;
+    static constexpr int kMetaBytes = kMetaMask + kBM * kMaskWords * 4;
     static constexpr int kMetaOff = kWsOff + kEpiWarps * 256;
     static constexpr int kBarOff = kMetaOff + 2 * kMetaBytes;
-    static constexpr int kTotal = kBarOff + 256 + 1024;  // barriers + tmem slot + alignment slack
+    static constexpr int kTotal = kBarOff + 512 + 1024;  // barriers + tmem slot + alignment slack
 };
 
 // int32 -> f64, exact, without the conversion pipe (I2F.F64 is slow on sm_100):
@@ -57,11 +68,12 @@ __device__ __forceinline__ double i32_to_f64(uint32_t v) {
     return __hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)) - 4503601774854144.0;
 }
 
-template <int BN, int POST, bool PLANES>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int EW, int POST, bool PLANES>
+__global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
     k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, const QLinParams p) {
-    using L = K2Smem<BN>;
+    using L = K2Smem<BN, EW>;
+    constexpr int kStages = L::kStages, kEpiWarps = EW, kMaskWords = L::kMaskWords;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -102,6 +114,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    // warpgroup 0 (TMA, MMA, TMEM allocator, row metadata) needs few registers: it hands
+    // them to the four epilogue warpgroups (register budgets per role region)
+    if (warp < 4) {
+    if constexpr (EW >= 16) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
             int stage = 0;
@@ -153,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 3) {  // ---- row metadata producer: S_m, |O| and mask words of upcoming tiles
         const int J = p.a.J;
-        const bool smask = J <= 32;  // mask rows fit the slot (K <= 1024); else the epilogue reads them globally
+        const bool smask = J <= kMaskWords;  // mask rows fit the slot; else the epilogue reads them globally
         const bool bulk_ok = ((reinterpret_cast<uintptr_t>(p.a.s_row) | reinterpret_cast<uintptr_t>(p.a.ocnt) |
                                reinterpret_cast<uintptr_t>(p.a.omask)) & 15) == 0;
         int it = 0;
@@ -190,10 +206,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(meta_full + slot);
         }
-    } else if (warp >= 4) {  // ---- epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
+    }
+    } else {  // ---- epilogue: 16 warps = 4 TMEM lane quarters x 4 column groups
+        if constexpr (EW >= 16) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
         const int ew = warp - 4;
         const int q = warp & 3;       // TMEM lanes 32q..32q+31 (a warp may only touch its quarter)
-        const int chalf = ew >> 2;    // which half of the BN columns
+        const int cgrp = ew >> 2;     // which quarter of the BN columns
         // per-warp output tiles (double-buffered): two 32-row x 16-double boxes each, 128B-swizzled
         uint8_t* stg0 = smem + L::kEpiOff + ew * kStgBufs * 8192;
         double* wss = reinterpret_cast<double*>(smem + L::kWsOff + ew * 256);
@@ -212,13 +230,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint8_t* mb = smem + L::kMetaOff + mslot * L::kMetaBytes;
             const double S = reinterpret_cast<const double*>(mb + L::kMetaS)[q * 32 + lane];
             const int cnt = reinterpret_cast<const int*>(mb + L::kMetaCnt)[q * 32 + lane];
-            const uint32_t* msk = p.a.J <= 32 ? reinterpret_cast<const uint32_t*>(mb + L::kMetaMask) + (q * 32) * p.a.J
+            const uint32_t* msk = p.a.J <= kMaskWords
+                                      ? reinterpret_cast<const uint32_t*>(mb + L::kMetaMask) + (q * 32) * p.a.J
                                               : p.a.omask + static_cast<size_t>(rbase) * p.a.J;
             ptx::mbar_wait(acc_full + buf, aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < BN / 64; ++cc, ++cs) {
-                const int c = chalf * (BN / 64) + cc;
+            constexpr int kChunksPerWarp = BN / 32 / (EW / 4);
+            for (int cc = 0; cc < kChunksPerWarp; ++cc, ++cs) {
+                const int c = cgrp * kChunksPerWarp + cc;
                 const int r0 = n0 + c * 32;
                 if (r0 >= p.R) break;  // uniform across the warp
                 const bool to2 = POST == POST_INPROJ && r0 >= p.epi.split;
@@ -420,7 +440,7 @@ static bool make_map_f64(CUtensorMap* m, const double* base, int rows, int cols,
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int POST, bool PLANES>
+template <int BN, int EW, int POST, bool PLANES>
 static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) {
     CUtensorMap ta, tb, to, to2;
     if (!make_map(&ta, p.a.codes, p.M, p.K, kBM) || !make_map(&tb, p.w, p.R, p.K, BN)) return cudaErrorInvalidValue;
@@ -430,12 +450,12 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
     if (!make_map_f64(&to2, inproj ? p.epi.out2 : p.epi.out, p.M, inproj ? p.R - p.epi.split : ocols,
                       inproj ? p.epi.split : p.epi.ld_out))
         return cudaErrorInvalidValue;
-    const int smem = K2Smem<BN>::kTotal;
-    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, POST, PLANES>>(smem);
+    const int smem = K2Smem<BN, EW>::kTotal;
+    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, EW, POST, PLANES>>(smem);
     if (e != cudaSuccess) return e;
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
-    k2_qlinear<BN, POST, PLANES><<<grid, kThreads, smem, st>>>(ta, tb, to, to2, p);
+    k2_qlinear<BN, EW, POST, PLANES><<<grid, K2Cfg<EW>::kThreads, smem, st>>>(ta, tb, to, to2, p);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }
@@ -447,9 +467,13 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.a.J < (p.K + 31) / 32) return cudaErrorInvalidValue;
     const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
     if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
+    // main-loop-heavy calls (wide outputs, no residual) keep the 8-warp / 3-stage shape
+    const bool wide = p.epi.post != POST_RESID && (p.R > 1024 || p.K > 1024);
 #define K2_CASE(P)                                                                                       \
     case P:                                                                                              \
-        return planes ? launch_bn<128, P, true>(p, st, num_sms) : launch_bn<128, P, false>(p, st, num_sms);
+        if (wide)                                                                                        \
+            return planes ? launch_bn<128, 8, P, true>(p, st, num_sms) : launch_bn<128, 8, P, false>(p, st, num_sms); \
+        return planes ? launch_bn<128, 16, P, true>(p, st, num_sms) : launch_bn<128, 16, P, false>(p, st, num_sms);
     switch (p.epi.post) {
         K2_CASE(POST_STORE)
         K2_CASE(POST_INPROJ)
