@@ -239,3 +239,29 @@ def test_long_sequence_c4(oracle_checker, gpu_ctx, abits, n_refresh):
     gcal = _import_calib(gm, ocal.export(), spec)
     for mode in (1, 2):
         assert rel_err(gm.forward_host(imgs, gcal, mode), om.forward(imgs, ocal, mode)) <= RTOL_F64, mode
+
+
+@pytest.mark.parametrize("embed,abits", [(192, 8), (384, 4)])
+def test_vim_t_s_widths(oracle_checker, gpu_ctx, embed, abits):
+    """The C1 (Vim-T, E=192, W4A8) and C2 (Vim-S, E=384, W4A4) channel widths at
+    a small image: FP and quantized (dynamic, static) logits vs the oracle, and
+    the fast scan == its all-exact variant."""
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    dims = dict(image=32, channels=3, patch=8, embed=embed, state=16, blocks=2, classes=10, conv_width=4)
+    od = O.Dims(**dims)
+    om = oracle_checker.model(od, SEED)
+    gm = ob.Model(gpu_ctx, ob.Dims(**dims), SEED)
+    imgs = oracle_checker.normal(31, 3 * od.pix).reshape(3, od.image, od.image, od.channels)
+    cimgs = oracle_checker.normal(32, 3 * od.pix).reshape(3, od.image, od.image, od.channels)
+    assert rel_err(gm.forward_host(imgs, None, 0), om.forward(imgs, None, 0)) <= RTOL_F64
+    spec = _spec(abits, n_refresh=4, rho=0.02)
+    ocal = om.calibrate(cimgs, spec)
+    gcal = _import_calib(gm, ocal.export(), spec)
+    for mode in (1, 2):
+        assert rel_err(gm.forward_host(imgs, gcal, mode), om.forward(imgs, ocal, mode)) <= RTOL_F64, mode
+    a = gm.forward_host(imgs, gcal, 1)
+    gm.set_option("scan_variant", 2)
+    b = gm.forward_host(imgs, gcal, 1)
+    gm.set_option("scan_variant", 0)
+    assert np.array_equal(a, b)
