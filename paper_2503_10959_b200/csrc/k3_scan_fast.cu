@@ -2,9 +2,9 @@
 // where the channel-local detector is exact, both scan
 // directions in one launch.
 //
-// Work split. A CTA owns 128 channels of one (sample, direction); two
-// adjacent lanes own one channel, 8 of its N = 16 states each, so a warp
-// covers 16 channels. Warps are independent: each stages its own copy of the
+// Work split. A CTA owns 32 channels of one (sample, direction) (small CTAs
+// keep the last wave's tail short: 8 of them share an SM); two adjacent lanes
+// own one channel, 8 of its N = 16 states each, so a warp covers 16 channels. Warps are independent: each stages its own copy of the
 // per-step values in its own shared-memory slice and synchronises only with
 // __syncwarp, so a warp delayed by a rare exact fallback never stalls the
 // others. The two halves of a channel exchange two values per step through
@@ -41,7 +41,7 @@
 
 namespace ob {
 
-constexpr int kCh = 128;       // channels per CTA
+constexpr int kCh = 32;        // channels per CTA
 constexpr int kThr = 2 * kCh;  // two threads per channel
 constexpr int kChunk = 8;      // steps staged per chunk
 
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
 }
 
 template <bool EXACT, int ABITS>
-__global__ void __launch_bounds__(kThr, 2) k3_scan_fast(const ScanDirs P, const StepShared* __restrict__ steps) {
+__global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t scan_smem_raw[];
     const int warp = threadIdx.x >> 5;
     WarpSmem& sh = reinterpret_cast<WarpSmem*>(scan_smem_raw)[warp];
