@@ -9,46 +9,67 @@
 namespace ob {
 
 // Y[m][r] = 0.0 + sum_{k ascending} A[m][k] * W[r][k]  (detail::mm !ta,tb;
-// tensor.cpp:373-382), 64x64 output tile per CTA, 4x4 per thread, k staged
-// through shared memory 16 at a time. Every output keeps its own sequential
-// k order, so tiling does not change a bit of the result.
-constexpr int DG_BM = 64, DG_BN = 64, DG_BK = 16;
+// tensor.cpp:373-382), 128x64 output tile per CTA, 8x4 per thread, k staged
+// through shared memory 16 at a time, the next k tile loaded into registers
+// while the current one is multiplied. Every output keeps its own sequential
+// k order, so tiling does not change a bit of the result. FP64-bound: a MAC is a
+// separately rounded DMUL + DADD (the reference builds with -ffp-contract=off).
+constexpr int DG_BM = 128, DG_BN = 64, DG_BK = 16, DG_TM = 8;
 
 __global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
     __shared__ double sa[DG_BK][DG_BM + 1];
     __shared__ double sw[DG_BK][DG_BN + 1];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int m0 = blockIdx.y * DG_BM, r0 = blockIdx.x * DG_BN;
-    double acc[4][4];
+    double acc[DG_TM][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < DG_TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    // k-tile element idx = threadIdx.x + 256 * u: row idx / 16, k idx % 16 (128 B runs)
+    double ra[DG_BM * DG_BK / 256], rw[DG_BN * DG_BK / 256];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < DG_BM * DG_BK / 256; ++u) {
+            const int idx = threadIdx.x + 256 * u, r = idx / DG_BK, gk = k0 + idx % DG_BK, gm = m0 + r;
+            ra[u] = (gm < p.M && gk < p.K) ? __ldg(p.a + static_cast<size_t>(gm) * p.lda + gk) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < DG_BN * DG_BK / 256; ++u) {
+            const int idx = threadIdx.x + 256 * u, r = idx / DG_BK, gk = k0 + idx % DG_BK, gr = r0 + r;
+            rw[u] = (gr < p.R && gk < p.K) ? __ldg(p.w + static_cast<size_t>(gr) * p.K + gk) : 0.0;
+        }
+    };
+    fetch(0);
     for (int k0 = 0; k0 < p.K; k0 += DG_BK) {
-        for (int idx = threadIdx.x; idx < DG_BM * DG_BK; idx += 256) {
-            const int r = idx / DG_BK, k = idx % DG_BK;
-            const int gm = m0 + r, gk = k0 + k;
-            sa[k][r] = (gm < p.M && gk < p.K) ? p.a[static_cast<size_t>(gm) * p.lda + gk] : 0.0;
-            const int gr = r0 + r;
-            sw[k][r] = (gr < p.R && gk < p.K) ? p.w[static_cast<size_t>(gr) * p.K + gk] : 0.0;
+#pragma unroll
+        for (int u = 0; u < DG_BM * DG_BK / 256; ++u) {
+            const int idx = threadIdx.x + 256 * u;
+            sa[idx % DG_BK][idx / DG_BK] = ra[u];
+        }
+#pragma unroll
+        for (int u = 0; u < DG_BN * DG_BK / 256; ++u) {
+            const int idx = threadIdx.x + 256 * u;
+            sw[idx % DG_BK][idx / DG_BK] = rw[u];
         }
         __syncthreads();
+        if (k0 + DG_BK < p.K) fetch(k0 + DG_BK);  // in flight during this tile's products
         const int kk = min(DG_BK, p.K - k0);
         for (int k = 0; k < kk; ++k) {
-            double av[4], wv[4];
+            double av[DG_TM], wv[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = sa[k][ty + 16 * i];
+            for (int i = 0; i < DG_TM; ++i) av[i] = sa[k][ty + 16 * i];
 #pragma unroll
             for (int j = 0; j < 4; ++j) wv[j] = sw[k][tx + 16 * j];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < DG_TM; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = dadd(acc[i][j], dmul(av[i], wv[j]));
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < DG_TM; ++i) {
         const int m = m0 + ty + 16 * i;
         if (m >= p.M) continue;
 #pragma unroll
