@@ -15,8 +15,10 @@ inline long& kernel_launch_counter() {
     return n;
 }
 
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
-// the attribute is per device, and contexts on several devices may share a process.
+// Allow a kernel the device's opt-in shared-memory maximum, once per (kernel,
+// device): the attribute caps what launches may request (so it is set to the
+// device limit, not to one launch's size) and is per device (contexts on
+// several devices may share a process).
 template <auto Kernel>
 cudaError_t ensure_smem_attr(int bytes) {
     static std::atomic<unsigned long long> done{0};  // bit d: set on device d
@@ -25,7 +27,11 @@ cudaError_t ensure_smem_attr(int bytes) {
     if (e != cudaSuccess) return e;
     const unsigned long long bit = 1ull << (dev & 63);
     if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
-    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    if (bytes > optin) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
     return e;
 }
