@@ -218,6 +218,13 @@ ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops);
  * roofline denominator. */
 ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops);
 
+/* Diagnostic: y[i] = f(x[i]) on the device for the path's transcendental
+ * functions, fn = 0 exp, 1 log1p, 2 softplus, 3 silu (tensor.hpp:146-154);
+ * x and y are device pointers of n doubles. The device forms restate glibc's
+ * exp/log1p so they equal the reference's std::exp/std::log1p bit for bit;
+ * the tests hold them to that against the host libm. */
+ouro_status ouro_b200_math_eval(ouro_b200_ctx* ctx, int fn, const double* x_dev, double* y_dev, size_t n);
+
 /* Parity harness: run a forward over host images and keep every
  * intermediate of one block (keys documented in DESIGN.md §5). */
 ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,

@@ -1,0 +1,579 @@
+// C++ host API over the C ABI (ouro_b200.h), mirroring the reference's operator
+// API (namespace ouro: gemm.hpp, quant.hpp, ssm.hpp) for the quantized VMM
+// inference path: same type names, argument meaning and error types, so a
+// caller of ouro::hybrid_gemm / ouro::calibrate / ouro::quantized_forward can
+// switch to ouro_b200:: by changing the namespace. Every computation runs in
+// the library's sm_100a kernels; this header only moves host data to and from
+// the device and adapts layouts.
+//
+//   ouro::X (reference)                                   ouro_b200::X
+//   ------------------------------------------------------------------------------
+//   PackedInt4, pack_int4, unpack_int4 (gemm.hpp:19-30)    same storage layout
+//   OutlierBuffer, GemmResult (gemm.hpp:34-76)             same fields
+//   hybrid_gemm, gemm_i4, gemm_i4xi8 (gemm.hpp:61-85)      K2 (tcgen05 kind::i8 + fused epilogue)
+//   round_f16 (gemm.hpp:93)                                IEEE binary16 round trip
+//   QuantSpec, TensorCalib, CalibrationResult (quant.hpp)  same fields
+//   ModelDims, ScanOrder, make_toy_model (ssm.hpp)         GPU-resident model, same seeded weights
+//   calibrate (quant.cpp:129-177)                          GPU calibration
+//   quantized_forward, QuantEvalResult (quant.cpp:505-579) GPU passes + teacher-forced layer MSE
+//
+// Link with -louro_b200 -lcudart. Kernels run on a per-thread default context
+// (device 0) unless a Context is passed.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ouro_b200.h"
+
+namespace ouro_b200 {
+
+// ---- errors (common.hpp:13-25 -> status codes of the C ABI) -------------------
+struct Error : std::runtime_error {
+    ouro_status status;
+    Error(ouro_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+struct ValidationError : Error {
+    explicit ValidationError(const std::string& m) : Error(OURO_ERR_VALIDATION, m) {}
+};
+struct NumericError : Error {
+    explicit NumericError(const std::string& m) : Error(OURO_ERR_NUMERIC, m) {}
+};
+struct IoError : Error {
+    explicit IoError(const std::string& m) : Error(OURO_ERR_IO, m) {}
+};
+
+inline void check(ouro_status s) {
+    if (s == OURO_OK) return;
+    const std::string m = ouro_b200_last_error();
+    if (s == OURO_ERR_VALIDATION) throw ValidationError(m);
+    if (s == OURO_ERR_IO) throw IoError(m);
+    throw NumericError(m);
+}
+inline void require(bool c, const std::string& m) {
+    if (!c) throw ValidationError(m);
+}
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw NumericError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- device plumbing ----------------------------------------------------------
+class Context {
+  public:
+    explicit Context(int device = 0) : dev_(device) { check(ouro_b200_ctx_create(device, &h_)); }
+    ~Context() { ouro_b200_ctx_free(h_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    ouro_b200_ctx* handle() const { return h_; }
+    int device() const { return dev_; }
+    void synchronize() const { check(ouro_b200_ctx_synchronize(h_)); }
+
+  private:
+    ouro_b200_ctx* h_ = nullptr;
+    int dev_ = 0;
+};
+
+inline Context& default_context(int device = 0) {
+    thread_local std::map<int, std::unique_ptr<Context>> ctxs;
+    auto& c = ctxs[device];
+    if (!c) c = std::make_unique<Context>(device);
+    return *c;
+}
+
+template <class T>
+class DeviceBuffer {
+  public:
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(size_t n) : n_(n) {
+        if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+    }
+    DeviceBuffer(const T* host, size_t n) : DeviceBuffer(n) { upload(host, n); }
+    explicit DeviceBuffer(const std::vector<T>& v) : DeviceBuffer(v.data(), v.size()) {}
+    ~DeviceBuffer() {
+        if (p_) cudaFree(p_);
+    }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    void upload(const T* host, size_t n) {
+        if (n) cuda_check(cudaMemcpy(p_, host, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    }
+    void zero() {
+        if (n_) cuda_check(cudaMemset(p_, 0, n_ * sizeof(T)), "memset");
+    }
+    std::vector<T> download() const {
+        std::vector<T> v(n_);
+        if (n_) cuda_check(cudaMemcpy(v.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+        return v;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+
+  private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// ---- quant-linear (gemm.hpp) --------------------------------------------------
+// Two signed 4-bit codes per byte, low nibble = even column (gemm.hpp:19-26).
+struct PackedInt4 {
+    size_t rows = 0, cols = 0;
+    size_t stride = 0;  // bytes per row = ceil(cols / 2)
+    std::vector<uint8_t> bytes;
+    int8_t get(size_t r, size_t c) const {
+        const uint8_t b = bytes[r * stride + c / 2];
+        const uint8_t nib = (c & 1) ? static_cast<uint8_t>(b >> 4) : static_cast<uint8_t>(b & 0x0F);
+        return static_cast<int8_t>(static_cast<int8_t>(nib << 4) >> 4);  // sign-extend the nibble
+    }
+};
+
+inline PackedInt4 pack_int4(const int8_t* codes, size_t rows, size_t cols) {
+    PackedInt4 p;
+    p.rows = rows;
+    p.cols = cols;
+    p.stride = (cols + 1) / 2;
+    p.bytes.assign(rows * p.stride, 0);
+    for (size_t r = 0; r < rows; ++r)
+        for (size_t c = 0; c < cols; ++c) {
+            const int8_t v = codes[r * cols + c];
+            require(v >= -7 && v <= 7, "pack_int4: code outside [-7, 7]");
+            const uint8_t nib = static_cast<uint8_t>(v) & 0x0F;
+            p.bytes[r * p.stride + c / 2] |= static_cast<uint8_t>((c & 1) ? nib << 4 : nib);
+        }
+    return p;
+}
+
+inline std::vector<int8_t> unpack_int4(const PackedInt4& p) {
+    std::vector<int8_t> out(p.rows * p.cols);
+    for (size_t r = 0; r < p.rows; ++r)
+        for (size_t c = 0; c < p.cols; ++c) out[r * p.cols + c] = p.get(r, c);
+    return out;
+}
+
+struct OutlierBuffer {
+    std::vector<size_t> channels;  // strictly increasing
+    std::vector<int8_t> codes;     // channels.size() x cols
+    std::vector<double> scales;    // per channel
+    size_t cols = 0;
+};
+
+struct GemmResult {
+    size_t rows = 0, cols = 0;
+    std::vector<int32_t> acc_inlier;
+    std::vector<int32_t> acc_outlier;  // unscaled integer sum over outlier channels
+    std::vector<double> output;
+};
+
+constexpr size_t kMaxInnerI4 = (size_t{1} << 31) / (7 * 7);
+constexpr size_t kMaxInnerI4xI8 = (size_t{1} << 31) / (7 * 127);
+
+// IEEE binary16 round trip (round to nearest even, overflow to infinity).
+inline double round_f16(double v) { return static_cast<double>(static_cast<_Float16>(v)); }
+
+namespace detail {
+inline size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+// One K2 launch over the reference's orientation: y[m][c] = sum_k w[m][k] x[k][c].
+// The kernel is token-major (rows = the C columns), so the planes are transposed
+// on the way in and out; K is padded to a multiple of 16 and the output rows to a
+// multiple of 32 with zero codes, which leaves every sum and product unchanged.
+inline GemmResult run_k2(Context& ctx, const PackedInt4& w, const std::vector<double>& w_scales,
+                         const PackedInt4* x_inlier, double inlier_scale, const OutlierBuffer& outliers, size_t cols) {
+    const size_t M = w.rows, K = w.cols, C = cols;
+    const size_t Kp = round_up(std::max<size_t>(K, 1), 16), Mp = round_up(std::max<size_t>(M, 1), 32);
+    const size_t J = (Kp + 31) / 32, n_o = outliers.channels.size();
+    GemmResult res;
+    res.rows = M;
+    res.cols = C;
+    if (M == 0 || C == 0) return res;
+    std::vector<int8_t> codes(C * Kp, 0), wc(Mp * Kp, 0), wt(Kp * Mp, 0), ocode(C * Kp, 0);
+    std::vector<double> ws(Mp, 0.0), s_row(C, inlier_scale), oscale(C * Kp, 0.0);
+    std::vector<int32_t> ocnt(C, static_cast<int32_t>(n_o));
+    std::vector<uint32_t> word(J, 0u);
+    if (x_inlier)
+        for (size_t k = 0; k < K; ++k)
+            for (size_t c = 0; c < C; ++c) codes[c * Kp + k] = x_inlier->get(k, c);
+    for (size_t m = 0; m < M; ++m) {
+        ws[m] = w_scales[m];
+        for (size_t k = 0; k < K; ++k) wt[k * Mp + m] = wc[m * Kp + k] = w.get(m, k);
+    }
+    for (size_t j = 0; j < n_o; ++j) {
+        const size_t ch = outliers.channels[j];
+        word[ch / 32] |= 1u << (ch % 32);
+        for (size_t c = 0; c < C; ++c) {
+            ocode[c * Kp + ch] = outliers.codes[j * C + c];
+            oscale[c * Kp + ch] = outliers.scales[j];
+        }
+    }
+    std::vector<uint32_t> omask(C * J);
+    for (size_t c = 0; c < C; ++c) std::copy(word.begin(), word.end(), omask.begin() + c * J);
+    DeviceBuffer<int8_t> d_codes(codes), d_w(wc), d_wt(wt), d_ocode(ocode);
+    DeviceBuffer<double> d_ws(ws), d_srow(s_row), d_oscale(oscale), d_out(C * Mp);
+    DeviceBuffer<int32_t> d_ocnt(ocnt), d_ain(C * Mp), d_aout(C * Mp);
+    DeviceBuffer<uint32_t> d_omask(omask);
+    check(ouro_b200_quant_linear(ctx.handle(), C, Mp, Kp, d_codes.get(), d_srow.get(), d_ocnt.get(),
+                                 d_omask.get(), d_ocode.get(), d_oscale.get(), d_w.get(), d_wt.get(), d_ws.get(),
+                                 OURO_B200_POST_STORE, d_out.get(), Mp, nullptr, 0, nullptr, d_ain.get(),
+                                 d_aout.get()));
+    ctx.synchronize();
+    const std::vector<double> out = d_out.download();
+    const std::vector<int32_t> ain = d_ain.download(), aout = d_aout.download();
+    res.acc_inlier.resize(M * C);
+    res.acc_outlier.resize(M * C);
+    res.output.resize(M * C);
+    for (size_t m = 0; m < M; ++m)
+        for (size_t c = 0; c < C; ++c) {
+            res.acc_inlier[m * C + c] = ain[c * Mp + m];
+            res.acc_outlier[m * C + c] = aout[c * Mp + m];
+            res.output[m * C + c] = out[c * Mp + m];
+        }
+    return res;
+}
+
+inline void check_outliers(const OutlierBuffer& o, size_t k, const char* who) {
+    require(o.channels.size() <= kMaxInnerI4xI8, std::string(who) + ": outlier channel count exceeds the no-overflow bound");
+    for (size_t j = 0; j < o.channels.size(); ++j) {
+        require(o.channels[j] < k, std::string(who) + ": outlier channel outside the weight contraction dim");
+        require(j == 0 || o.channels[j] > o.channels[j - 1], std::string(who) + ": outlier channels must increase");
+    }
+    require(o.codes.size() == o.channels.size() * o.cols, std::string(who) + ": outlier code plane has the wrong size");
+}
+}  // namespace detail
+
+// output[m][c] = w_scales[m] * (S_in * acc_inlier[m][c] + sum_j (s_j * w[m][ch_j]) * xo[j][c]),
+// outlier terms in ascending channel order (gemm.cpp:181-225), bit-exact. `threads`
+// is accepted for signature compatibility; f16_output rounds through binary16.
+inline GemmResult hybrid_gemm(Context& ctx, const PackedInt4& w, const std::vector<double>& w_scales,
+                              const PackedInt4& x_inlier, double inlier_scale, const OutlierBuffer& outliers,
+                              int threads = 1, bool f16_output = false) {
+    (void)threads;
+    require(w_scales.size() == w.rows, "hybrid_gemm: one weight scale per output row");
+    require(outliers.channels.empty() || outliers.cols == x_inlier.cols,
+            "hybrid_gemm: outlier buffer width disagrees with the inlier plane");
+    require(outliers.scales.size() == outliers.channels.size(), "hybrid_gemm: one scale per outlier channel");
+    require(inlier_scale > 0.0, "hybrid_gemm: inlier scale must be positive");
+    require(w.cols == x_inlier.rows, "gemm_i4: inner dimensions disagree");
+    require(w.cols <= kMaxInnerI4, "gemm_i4: contraction dim exceeds the no-overflow bound");
+    detail::check_outliers(outliers, w.cols, "hybrid_gemm");
+    GemmResult r = detail::run_k2(ctx, w, w_scales, &x_inlier, inlier_scale, outliers, x_inlier.cols);
+    if (f16_output)
+        for (double& v : r.output) v = round_f16(v);
+    return r;
+}
+inline GemmResult hybrid_gemm(const PackedInt4& w, const std::vector<double>& w_scales, const PackedInt4& x_inlier,
+                              double inlier_scale, const OutlierBuffer& outliers, int threads = 1,
+                              bool f16_output = false) {
+    return hybrid_gemm(default_context(), w, w_scales, x_inlier, inlier_scale, outliers, threads, f16_output);
+}
+
+// acc[m][c] = sum_k w[m][k] x[k][c] (gemm.cpp:137-158), int32, exact.
+inline std::vector<int32_t> gemm_i4(const PackedInt4& w, const PackedInt4& x, int threads = 1) {
+    (void)threads;
+    require(w.cols == x.rows, "gemm_i4: inner dimensions disagree");
+    require(w.cols <= kMaxInnerI4, "gemm_i4: contraction dim exceeds the no-overflow bound");
+    return detail::run_k2(default_context(), w, std::vector<double>(w.rows, 1.0), &x, 1.0, OutlierBuffer{}, x.cols)
+        .acc_inlier;
+}
+
+// acc[m][c] = sum_j w[m][ch_j] xo[j][c] (gemm.cpp:160-179), int32, exact.
+inline std::vector<int32_t> gemm_i4xi8(const PackedInt4& w, const OutlierBuffer& outliers, int threads = 1) {
+    (void)threads;
+    detail::check_outliers(outliers, w.cols, "gemm_i4xi8");
+    OutlierBuffer o = outliers;
+    if (o.scales.size() != o.channels.size()) o.scales.assign(o.channels.size(), 1.0);
+    return detail::run_k2(default_context(), w, std::vector<double>(w.rows, 1.0), nullptr, 1.0, o, outliers.cols)
+        .acc_outlier;
+}
+
+// ---- quantization config and calibration (quant.hpp) -------------------------
+struct QuantSpec {
+    unsigned weight_bits = 4;
+    unsigned act_bits = 8;
+    unsigned outlier_bits = 8;
+    size_t n_refresh = 10;
+    double rho = 0.01;
+    void validate() const {  // quant.cpp:54-60
+        require(weight_bits >= 2, "weight bits must be >= 2");
+        require(act_bits >= 2, "activation bits must be >= 2");
+        require(outlier_bits >= 2 && outlier_bits <= 8, "outlier bits must be in [2, 8]");
+        require(act_bits <= outlier_bits, "inlier activation bits must not exceed outlier bits");
+        require(rho >= 0.0 && rho < 1.0, "rho must be in [0, 1)");
+    }
+};
+
+struct TensorCalib {
+    std::string name;  // "block<b>.dir<d>.<kind>"
+    double theta = 0.0;
+    std::vector<double> scale_inlier;
+    std::vector<double> scale_full;
+    std::vector<char> excluded;
+};
+
+struct CalibrationResult {
+    QuantSpec spec;
+    size_t tokens = 0, embed = 0, state = 0, blocks = 0, ndirs = 0;
+    std::vector<TensorCalib> tensors;  // [block][dir][kind]
+};
+
+enum class QuantMode { Dynamic, Static, Bypass };
+enum class ScanOrder { RowForward, RowBackward, ColForward, ColBackward };
+
+struct ModelDims {
+    size_t image = 32, channels = 3, patch = 4, embed = 16, state = 4, blocks = 2, classes = 10, conv_width = 3;
+    size_t grid() const { return image / patch; }
+    size_t tokens() const { return grid() * grid(); }
+    size_t patch_vals() const { return patch * patch * channels; }
+};
+
+struct SpikeSettings {  // spike injection is not modelled on the GPU: rate must be 0
+    double rate = 0.0;
+    double gain = 100.0;
+    size_t channels = 1;
+    uint64_t salt = 0;
+};
+
+struct QuantEvalResult {
+    std::vector<double> logits_fp, logits_q;
+    std::vector<std::pair<std::string, double>> layer_mse;  // teacher-forced, per (block, dir)
+    double logits_mse = 0.0;
+    size_t argmax_agree = 0;
+    size_t batch = 0;
+};
+
+// The toy Vim model of make_toy_model (ssm.cpp:88-120), resident on the GPU:
+// equal seeds give the reference's bit-identical weights.
+class ToyVmmModel {
+  public:
+    ToyVmmModel(Context& ctx, const ModelDims& dims, const std::vector<ScanOrder>& orders, uint64_t seed)
+        : ctx_(&ctx), dims_(dims), orders_(orders) {
+        const size_t d[8] = {dims.image, dims.channels, dims.patch, dims.embed,
+                             dims.state, dims.blocks,   dims.classes, dims.conv_width};
+        std::vector<int> o;
+        for (ScanOrder s : orders) o.push_back(static_cast<int>(s));
+        check(ouro_b200_model_create(ctx.handle(), d, o.data(), o.size(), seed, &h_));
+    }
+    ~ToyVmmModel() { ouro_b200_model_free(h_); }
+    ToyVmmModel(const ToyVmmModel&) = delete;
+    ToyVmmModel& operator=(const ToyVmmModel&) = delete;
+    ouro_b200_model* handle() const { return h_; }
+    Context& context() const { return *ctx_; }
+    const ModelDims& dims() const { return dims_; }
+    const std::vector<ScanOrder>& orders() const { return orders_; }
+    std::vector<double> tensor(const std::string& name) const {
+        size_t n = 0;
+        check(ouro_b200_model_get_tensor(h_, name.c_str(), nullptr, 0, &n));
+        std::vector<double> v(n);
+        check(ouro_b200_model_get_tensor(h_, name.c_str(), v.data(), n, &n));
+        return v;
+    }
+    std::vector<double> qweight(const std::string& name, unsigned bits) const {
+        size_t n = 0;
+        check(ouro_b200_model_get_qweight(h_, name.c_str(), bits, nullptr, 0, &n));
+        std::vector<double> v(n);
+        check(ouro_b200_model_get_qweight(h_, name.c_str(), bits, v.data(), n, &n));
+        return v;
+    }
+
+  private:
+    Context* ctx_;
+    ModelDims dims_;
+    std::vector<ScanOrder> orders_;
+    ouro_b200_model* h_ = nullptr;
+};
+
+inline std::unique_ptr<ToyVmmModel> make_toy_model(const ModelDims& dims, const std::vector<ScanOrder>& orders,
+                                                   uint64_t seed) {
+    return std::make_unique<ToyVmmModel>(default_context(), dims, orders, seed);
+}
+
+namespace detail {
+inline const char* kind_name(size_t k) { return k == 0 ? "a_bar" : (k == 1 ? "b_bar" : "h"); }
+
+// RAII calibration handle built from a CalibrationResult (scan tensors only: the
+// reference's quantized pass, no D1/D2).
+struct CalibHandle {
+    ouro_b200_calib* h = nullptr;
+    CalibHandle(const ToyVmmModel& m, const CalibrationResult& c) {
+        const ModelDims& d = m.dims();
+        require(c.blocks == d.blocks && c.ndirs == m.orders().size() && c.tokens == d.tokens() && c.embed == d.embed,
+                "calibration does not match the model geometry");
+        require(c.tensors.size() == c.blocks * c.ndirs * 3, "calibration record: tensor count does not match dims");
+        c.spec.validate();
+        const unsigned bits[3] = {c.spec.weight_bits, c.spec.act_bits, c.spec.outlier_bits};
+        check(ouro_b200_calib_create(m.handle(), bits, c.spec.n_refresh, c.spec.rho, 0, 0, &h));
+        for (size_t i = 0; i < c.tensors.size(); ++i) {
+            const TensorCalib& t = c.tensors[i];
+            require(t.scale_inlier.size() == c.tokens && t.scale_full.size() == c.tokens && t.excluded.size() == c.embed,
+                    "calibration record: tensor " + t.name + " has the wrong length");
+            std::vector<uint8_t> ex(t.excluded.begin(), t.excluded.end());
+            check(ouro_b200_calib_set(h, 0, i, t.theta, t.scale_inlier.data(), t.scale_full.data(), ex.data()));
+        }
+    }
+    ~CalibHandle() { ouro_b200_calib_free(h); }
+    CalibHandle(const CalibHandle&) = delete;
+    CalibHandle& operator=(const CalibHandle&) = delete;
+};
+
+inline std::vector<int> scan_permutation(ScanOrder o, size_t grid) {  // ssm.cpp:30-46
+    const size_t m = grid * grid;
+    std::vector<int> p(m);
+    for (size_t t = 0; t < m; ++t) {
+        const size_t fast = t % grid, slow = t / grid;
+        size_t v = 0;
+        switch (o) {
+            case ScanOrder::RowForward: v = slow * grid + fast; break;
+            case ScanOrder::RowBackward: v = m - 1 - (slow * grid + fast); break;
+            case ScanOrder::ColForward: v = fast * grid + slow; break;
+            default: v = m - 1 - (fast * grid + slow); break;
+        }
+        p[t] = static_cast<int>(v);
+    }
+    return p;
+}
+
+inline std::vector<double> trace_get(ouro_b200_trace* t, const std::string& key) {
+    size_t bytes = 0;
+    check(ouro_b200_trace_get(t, key.c_str(), nullptr, 0, &bytes));
+    std::vector<double> v(bytes / sizeof(double));
+    check(ouro_b200_trace_get(t, key.c_str(), v.data(), bytes, &bytes));
+    return v;
+}
+}  // namespace detail
+
+// calibrate (quant.cpp:129-177) on the GPU: per-step peaks of every scan tensor,
+// quantile on the host. images: batch x (image*image*channels), row-major.
+inline CalibrationResult calibrate(const ToyVmmModel& model, const std::vector<double>& images, size_t batch,
+                                   const QuantSpec& spec) {
+    spec.validate();
+    const ModelDims& d = model.dims();
+    require(images.size() == batch * d.image * d.image * d.channels, "calibrate: image buffer size mismatch");
+    DeviceBuffer<double> img(images);
+    const unsigned bits[3] = {spec.weight_bits, spec.act_bits, spec.outlier_bits};
+    ouro_b200_calib* h = nullptr;
+    check(ouro_b200_calibrate(model.handle(), img.get(), batch, bits, spec.n_refresh, spec.rho, 0, 0, 0, &h));
+    std::unique_ptr<ouro_b200_calib, void (*)(ouro_b200_calib*)> guard(h, ouro_b200_calib_free);
+    CalibrationResult c;
+    c.spec = spec;
+    c.tokens = d.tokens();
+    c.embed = d.embed;
+    c.state = d.state;
+    c.blocks = d.blocks;
+    c.ndirs = model.orders().size();
+    size_t n = 0;
+    check(ouro_b200_calib_count(h, 0, &n));
+    for (size_t i = 0; i < n; ++i) {
+        TensorCalib t;
+        const size_t b = i / (c.ndirs * 3), dir = (i / 3) % c.ndirs, k = i % 3;
+        t.name = "block" + std::to_string(b) + ".dir" + std::to_string(dir) + "." + detail::kind_name(k);
+        t.scale_inlier.resize(c.tokens);
+        t.scale_full.resize(c.tokens);
+        std::vector<uint8_t> ex(c.embed);
+        check(ouro_b200_calib_get(h, 0, i, &t.theta, t.scale_inlier.data(), t.scale_full.data(), ex.data()));
+        t.excluded.assign(ex.begin(), ex.end());
+        c.tensors.push_back(std::move(t));
+    }
+    return c;
+}
+
+// quantized_forward (quant.cpp:505-579): the reference pass and the quantized pass
+// (W4 weights + the QuantHook policy) over the same images, their logits,
+// logits_mse, argmax agreement and the teacher-forced scan-output MSE per
+// (block, dir): each direction's quantized scan re-run on the reference pass's
+// own scan input with the quantized x_proj weights.
+inline QuantEvalResult quantized_forward(const ToyVmmModel& model, const std::vector<double>& images, size_t batch,
+                                         const CalibrationResult& calib, QuantMode mode,
+                                         const SpikeSettings& spikes = SpikeSettings{}) {
+    require(spikes.rate == 0.0, "quantized_forward: spike injection is not available on the GPU path");
+    const ModelDims& d = model.dims();
+    require(images.size() == batch * d.image * d.image * d.channels, "quantized_forward: image buffer size mismatch");
+    detail::CalibHandle cal(model, calib);
+    QuantEvalResult out;
+    out.batch = batch;
+    out.logits_fp.resize(batch * d.classes);
+    out.logits_q.resize(batch * d.classes);
+    check(ouro_b200_forward_host(model.handle(), nullptr, OURO_B200_MODE_FP, 0, 0, images.data(), batch,
+                                 out.logits_fp.data()));
+    if (mode == QuantMode::Bypass) {
+        out.logits_q = out.logits_fp;
+    } else {
+        const int m = mode == QuantMode::Dynamic ? OURO_B200_MODE_DYNAMIC : OURO_B200_MODE_STATIC;
+        check(ouro_b200_forward_host(model.handle(), cal.h, m, 0, 0, images.data(), batch, out.logits_q.data()));
+    }
+    double lm = 0.0;
+    for (size_t i = 0; i < out.logits_fp.size(); ++i) {
+        const double e = out.logits_fp[i] - out.logits_q[i];
+        lm += e * e;
+    }
+    out.logits_mse = lm / static_cast<double>(out.logits_fp.size());
+    for (size_t b = 0; b < batch; ++b) {
+        const double* f = out.logits_fp.data() + b * d.classes;
+        const double* q = out.logits_q.data() + b * d.classes;
+        if (std::max_element(f, f + d.classes) - f == std::max_element(q, q + d.classes) - q) ++out.argmax_agree;
+    }
+    // teacher-forced per-layer MSE
+    Context& ctx = model.context();
+    const size_t T = d.tokens(), E = d.embed, N = d.state, P = E + 2 * N, nd = model.orders().size();
+    const int qmode = mode == QuantMode::Static ? OURO_B200_MODE_STATIC
+                                                : (mode == QuantMode::Dynamic ? OURO_B200_MODE_DYNAMIC : OURO_B200_MODE_FP);
+    for (size_t b = 0; b < d.blocks; ++b) {
+        ouro_b200_trace* tr = nullptr;
+        check(ouro_b200_trace_run(model.handle(), nullptr, OURO_B200_MODE_FP, 0, 0, images.data(), batch, b, &tr));
+        std::unique_ptr<ouro_b200_trace, void (*)(ouro_b200_trace*)> tguard(tr, ouro_b200_trace_free);
+        const std::vector<double> u = detail::trace_get(tr, "u");
+        DeviceBuffer<double> d_u(u);
+        for (size_t dir = 0; dir < nd; ++dir) {
+            const std::string pd = "block" + std::to_string(b) + ".dir" + std::to_string(dir);
+            const std::vector<int> perm = detail::scan_permutation(model.orders()[dir], d.grid());
+            std::vector<double> us(batch * T * E);
+            for (size_t s = 0; s < batch; ++s)
+                for (size_t t = 0; t < T; ++t)
+                    std::memcpy(us.data() + (s * T + t) * E, u.data() + (s * T + perm[t]) * E, E * sizeof(double));
+            DeviceBuffer<double> d_us(us), d_w(model.qweight(pd + ".xp", calib.spec.weight_bits)),
+                d_proj(batch * T * P), d_a(model.tensor(pd + ".a")), d_bd(model.tensor(pd + ".b_delta")),
+                d_o(batch * T * E);
+            check(ouro_b200_dgemm(ctx.handle(), batch * T, P, E, d_us.get(), E, d_w.get(), OURO_B200_POST_STORE,
+                                  d_proj.get(), P, nullptr, 0, nullptr));
+            std::vector<std::unique_ptr<DeviceBuffer<double>>> tabs;
+            double theta[3];
+            const double* si[3];
+            const double* sf[3];
+            for (size_t k = 0; k < 3; ++k) {
+                const TensorCalib& tc = calib.tensors[(b * nd + dir) * 3 + k];
+                theta[k] = tc.theta;
+                tabs.push_back(std::make_unique<DeviceBuffer<double>>(tc.scale_inlier));
+                si[k] = tabs.back()->get();
+                tabs.push_back(std::make_unique<DeviceBuffer<double>>(tc.scale_full));
+                sf[k] = tabs.back()->get();
+            }
+            if (qmode == OURO_B200_MODE_FP) {  // bypass: the hook is a no-op, so the re-run is the FP scan
+                out.layer_mse.emplace_back(pd, 0.0);
+                continue;
+            }
+            check(ouro_b200_quant_scan(ctx.handle(), batch, T, E, N, static_cast<int>(model.orders()[dir]),
+                                       static_cast<int>(d.grid()), d_u.get(), d_proj.get(), d_a.get(), d_bd.get(),
+                                       d_o.get(), qmode, calib.spec.n_refresh, calib.spec.act_bits,
+                                       calib.spec.outlier_bits, theta, si, sf, nullptr, 0, nullptr));
+            ctx.synchronize();
+            const std::vector<double> o_tf = d_o.download();
+            const std::vector<double> o_fp = detail::trace_get(tr, "dir" + std::to_string(dir) + ".o");
+            double acc = 0.0;
+            for (size_t i = 0; i < o_fp.size(); ++i) {
+                const double e = o_fp[i] - o_tf[i];
+                acc += e * e;
+            }
+            out.layer_mse.emplace_back(pd, acc / static_cast<double>(o_fp.size()));
+        }
+    }
+    return out;
+}
+
+}  // namespace ouro_b200

@@ -36,6 +36,9 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir(REF_SRC)
     if ref:
         subprocess.run(["make", "-s", "-C", HERE, "ref", f"REF={REF_SRC}"], check=True)
+        # the C++ host API checked against the reference (needs libouro_b200.so built first)
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2503_10959_b200", "libouro_b200.so")):
+            subprocess.run(["make", "-s", "-C", HERE, "cpp-api-test", f"REF={REF_SRC}"], check=True)
 
 
 def ref_available() -> bool:

@@ -56,6 +56,7 @@ _SIGS = {
     "ouro_b200_forward_profile_launches": ([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
+    "ouro_b200_math_eval": ([_P, _I, _P, _P, _SZ], _I),
     "ouro_b200_calib_save": ([_P, _P, C.c_char_p], _I),
     "ouro_b200_model_get_qweight": ([_P, C.c_char_p, C.c_uint, _P, C.c_size_t, C.POINTER(C.c_size_t)], _I),
     "ouro_b200_calib_load": ([_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], _I),

@@ -667,6 +667,15 @@ ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops) {
     });
 }
 
+ouro_status ouro_b200_math_eval(ouro_b200_ctx* ctx, int fn, const double* x_dev, double* y_dev, size_t n) {
+    return guarded([&] {
+        require(ctx != nullptr, "math_eval: ctx is NULL");
+        require(fn >= 0 && fn <= 3, "math_eval: fn must be 0 (exp), 1 (log1p), 2 (softplus) or 3 (silu)");
+        require(n == 0 || (x_dev && y_dev), "math_eval: NULL buffer");
+        ob::cuda_check(ob::launch_math_eval(fn, x_dev, y_dev, n, ctx->c->stream), "math_eval");
+    });
+}
+
 ouro_status ouro_b200_trace_run(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
                                 const double* images_host, size_t B, size_t block, ouro_b200_trace** out) {
     return guarded([&] {

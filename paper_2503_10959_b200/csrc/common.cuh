@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "glibc_math.cuh"
+
 namespace ob {
 
 constexpr int kMaxN = 16;  // state size N the scan keeps in registers
@@ -65,13 +67,14 @@ __device__ __forceinline__ double scale_from_peak(double peak, double q) {
     return peak == 0.0 ? 1.0 : __ddiv_rn(peak, q);
 }
 
-// softplus_val / sigmoid_val / silu_val, tensor.hpp:146-154.
+// softplus_val / sigmoid_val / silu_val, tensor.hpp:146-154, with glibc's exp and
+// log1p (glibc_math.cuh) so the values equal the reference's bit for bit.
 __device__ __forceinline__ double softplus_d(double x) {
-    return dadd(fmax(x, 0.0), log1p(exp(-fabs(x))));
+    return dadd(fmax(x, 0.0), gl::log1p(gl::exp(-fabs(x))));
 }
 __device__ __forceinline__ double sigmoid_d(double x) {
-    if (x >= 0.0) return __ddiv_rn(1.0, dadd(1.0, exp(-x)));
-    double e = exp(x);
+    if (x >= 0.0) return __ddiv_rn(1.0, dadd(1.0, gl::exp(-x)));
+    double e = gl::exp(x);
     return __ddiv_rn(e, dadd(1.0, e));
 }
 __device__ __forceinline__ double silu_d(double x) { return dmul(x, sigmoid_d(x)); }

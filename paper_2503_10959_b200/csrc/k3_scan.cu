@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(LITERAL ? 1024 : 128) k3_scan(const ScanParams
         double a[N], b[N];
 #pragma unroll
         for (int m = 0; m < N; ++m) {
-            a[m] = exp(dmul(delta, A[m]));
+            a[m] = gl::exp(dmul(delta, A[m]));
             b[m] = dmul(delta, __ldg(pr + E + m));
         }
         quant_row<LITERAL, N>(a, inA, 0, t, p, i, active, lit, qa, qo, red, s);

@@ -67,6 +67,11 @@ constexpr int kWarpCh = 16;  // channels per warp
 // Per-warp slice: step tables and raw per-channel inputs are double-buffered
 // (chunk k+1 is in flight while chunk k is scanned); x / deltaf / epsd hold
 // the current chunk.
+// The exact f64 transcendental values (glibc's algorithms) are needed only on the
+// rare exact paths: out of line, so the certified f32 loop keeps its code size.
+__device__ __noinline__ double exp_call(double x) { return gl::exp(x); }
+__device__ __noinline__ double softplus_call(double x) { return softplus_d(x); }
+
 struct WarpSmem {
     StepShared st[2][kChunk];
     double dp[2][kChunk][kWarpCh];  // x_proj delta pre-activations (raw)
@@ -255,8 +260,8 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
             double delta, pa, pb;
             auto exact = [&]() {
                 if (!have) {
-                    delta = softplus_d(sh.x[tt][c]);
-                    pa = exp(dmul(delta, Amax));
+                    delta = softplus_call(sh.x[tt][c]);
+                    pa = exp_call(dmul(delta, Amax));
                     pb = dmul(delta, ss.Bmax);
                     have = true;
                 }
@@ -364,7 +369,7 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
                     if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
                         ca[m] = static_cast<unsigned>(static_cast<int>(
-                            quant_code_div(exp(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
+                            quant_code_div(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
                         cb[m] = static_cast<float>(

@@ -2,7 +2,9 @@
 // projection GEMM used for patch embedding, the head and the FP (calibration /
 // bypass) linear layers; patch gather; causal depthwise conv; mean pool.
 // Each keeps the reference's per-output operation order so FP results match
-// the CPU reference bit-for-bit (modulo libm ulps in exp/log1p).
+// the CPU reference bit-for-bit (exp/log1p are glibc's, glibc_math.cuh).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -214,6 +216,24 @@ __global__ void k4_meanpool(const double* __restrict__ x, double* __restrict__ p
 
 cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st) {
     k4_meanpool<<<dim3((E + 127) / 128, S), 128, 0, st>>>(x, pooled, S, T, E);
+    ++kernel_launch_counter();
+    return cudaGetLastError();
+}
+
+// The device transcendental functions of the path (glibc's exp / log1p and the
+// softplus / SiLU built on them, common.cuh) over a vector, for the tests that pin
+// them to the reference's libm.
+__global__ void k4_math_eval(int fn, const double* __restrict__ x, double* __restrict__ y, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double v = x[i];
+        y[i] = fn == 0 ? gl::exp(v) : fn == 1 ? gl::log1p(v) : fn == 2 ? softplus_d(v) : silu_d(v);
+    }
+}
+cudaError_t launch_math_eval(int fn, const double* x, double* y, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 16));
+    k4_math_eval<<<blocks, 256, 0, st>>>(fn, x, y, n);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }

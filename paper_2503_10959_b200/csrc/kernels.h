@@ -167,6 +167,8 @@ cudaError_t launch_conv(const double* u0, const double* taps, double* u, int S, 
                         cudaStream_t st);
 double measure_fp64_peak(cudaStream_t st, int num_sms);  // TFLOP/s (DFMA = 2 flops)
 double measure_i8_peak(cudaStream_t st, int num_sms);    // dense int8 tensor TOP/s (tcgen05 kind::i8)
+// fn: 0 exp, 1 log1p, 2 softplus, 3 silu (device forms, glibc-identical)
+cudaError_t launch_math_eval(int fn, const double* x, double* y, size_t n, cudaStream_t st);
 cudaError_t launch_meanpool(const double* x, double* pooled, int S, int T, int E, cudaStream_t st);
 
 }  // namespace ob

@@ -131,6 +131,15 @@ class Context:
         L.check(self.lib.ouro_b200_measure_i8_peak(self.h, C.byref(v)))
         return v.value
 
+    def math_eval(self, fn: str, x):
+        """Device exp / log1p / softplus / silu of a float64 CUDA tensor: the forms the
+        kernels use, which restate glibc's so they equal the reference's bit for bit."""
+        code = {"exp": 0, "log1p": 1, "softplus": 2, "silu": 3}[fn]
+        x = x.contiguous()
+        y = x.new_empty(x.shape)
+        L.check(self.lib.ouro_b200_math_eval(self.h, code, _ptr(x), _ptr(y), x.numel()))
+        return y
+
     # ---- operators (device tensors) --------------------------------------------
     def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
                         mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, literal=False,

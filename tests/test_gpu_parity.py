@@ -1,9 +1,10 @@
 """GPU parity: the sm_100a path against the CPU oracle (oracle/, pinned to the
 reference build) on identical seeded inputs.
 
-Bar (north star): bit-exact outlier masks, quantized codes and int32
-accumulators; f64 floating outputs within 1e-9 relative (libm exp/log1p on
-the GPU differ from glibc by <= 1 ulp, nothing else differs).
+Bar: bit-exact outlier masks, quantized codes and int32 accumulators (the
+north star), and f64 outputs bit-identical too: every f64 operation follows
+the reference's order and the device exp/log1p restate glibc's
+(csrc/glibc_math.cuh), so RTOL_F64 is 0 (north star allows 1e-3 on logits).
 """
 import numpy as np
 import pytest
@@ -13,7 +14,7 @@ pytestmark = pytest.mark.gpu
 DIMS = dict(image=32, channels=3, patch=8, embed=64, state=16, blocks=2, classes=10, conv_width=4)
 SEED = 1234
 B = 3
-RTOL_F64 = 1e-9
+RTOL_F64 = 0.0
 
 
 def rel_err(a, b):

@@ -11,14 +11,18 @@ DIMS = dict(image=32, channels=3, patch=8, embed=64, state=16, blocks=2, classes
 SEED = 9
 
 
-@pytest.mark.parametrize("abits,mode", [(4, 1), (4, 2), (8, 1)])
-def test_quant_eval_matches_reference(ref_checker, gpu_ctx, abits, mode):
+# data seeds (calibration, eval): 31/32 is the case whose block-1 scan put a value
+# within an ulp of a code boundary when the device used CUDA's exp; with glibc's
+# algorithms on the device every case is bit-identical.
+@pytest.mark.parametrize("abits,mode,seeds", [(4, 1, (21, 22)), (4, 2, (21, 22)), (8, 1, (21, 22)),
+                                              (4, 1, (31, 32)), (4, 2, (31, 32))])
+def test_quant_eval_matches_reference(ref_checker, gpu_ctx, abits, mode, seeds):
     from oracle import oracle as O
     import paper_2503_10959_b200 as ob
     od = O.Dims(**DIMS)
     rm = ref_checker.model(od, SEED)
-    cimgs = ref_checker.normal(21, 3 * od.pix).reshape(3, od.image, od.image, od.channels)
-    imgs = ref_checker.normal(22, 4 * od.pix).reshape(4, od.image, od.image, od.channels)
+    cimgs = ref_checker.normal(seeds[0], 3 * od.pix).reshape(3, od.image, od.image, od.channels)
+    imgs = ref_checker.normal(seeds[1], 4 * od.pix).reshape(4, od.image, od.image, od.channels)
     spec = O.Spec(wbits=4, abits=abits, obits=8, n_refresh=5, rho=0.05, d1=False, d2=False)
     rcal = rm.ref_calibrate(cimgs, spec)
     want = rm.ref_quant_eval(imgs, rcal, mode)
@@ -29,12 +33,11 @@ def test_quant_eval_matches_reference(ref_checker, gpu_ctx, abits, mode):
                                ob.QuantSpec(4, abits, 8, 5, 0.05, False, False))
     got = gm.quant_eval(imgs, gcal, mode, d1=False, d2=False)
 
-    rel = lambda a, b: float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300))
-    assert rel(got["logits_fp"], want["logits_fp"]) <= 1e-9
-    assert rel(got["logits_q"], want["logits_q"]) <= 1e-9
+    assert np.array_equal(np.asarray(got["logits_fp"]), np.asarray(want["logits_fp"]))
+    assert np.array_equal(np.asarray(got["logits_q"]), np.asarray(want["logits_q"]))
     assert got["argmax_agree"] == want["argmax_agree"]
-    assert abs(got["logits_mse"] - want["logits_mse"]) <= 1e-6 * want["logits_mse"]
+    assert abs(got["logits_mse"] - want["logits_mse"]) <= 1e-12 * want["logits_mse"]
     names = [n for n, _ in got["layer_mse"]]
     assert names == [f"block{b}.dir{d}" for b in range(DIMS["blocks"]) for d in range(2)]
     lm = np.array([v for _, v in got["layer_mse"]])
-    assert np.all(np.abs(lm - want["layer_mse"]) <= 1e-6 * np.abs(want["layer_mse"]) + 1e-300)
+    assert np.all(np.abs(lm - want["layer_mse"]) <= 1e-12 * np.abs(want["layer_mse"]) + 1e-300)
