@@ -80,8 +80,9 @@ ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out);
  * f64 [S*T], ocnt int32 [S*T] = |O(t)|, omask uint32 [S*T][ceil(E/32)]
  * (bit ch%32 of word ch/32 = channel in O(t)), ocode int8 / oscale f64
  * [S*T][E] written at outlier positions only, optional scanned uint8 [S*T]
- * (DetectResult::scanned; literal kernel). rs_work: dev f64 [S*T] scratch
- * for SRC_RMSNORM on the channel-parallel kernel. */
+ * (DetectResult::scanned; literal kernel). rs_work: ignored (kept for ABI
+ * stability; the staged kernel computes D1 row factors in shared memory), may
+ * be NULL. */
 ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
                                       size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
                                       const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,

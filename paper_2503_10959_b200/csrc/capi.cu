@@ -140,7 +140,7 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
         k.cal.theta = theta;
         k.cal.s_in = s_in;
         k.cal.s_full = s_full;
-        k.rs = rs_work;
+        (void)rs_work;
         k.force_literal = literal;
         k.codes = codes;
         k.s_row = s_row;

@@ -302,14 +302,16 @@ void Model::ensure_work(int S, bool trace) {
     w.pooled.ensure(static_cast<size_t>(S) * E);
     w.proj.ensure(nd * rows * (E + 2 * N));
     w.o.ensure(nd * rows * E);
-    w.codes.ensure(rows * E);
-    w.ocode.ensure(rows * E);
-    w.oscale.ensure(rows * E);
-    w.omask.ensure(rows * ((E + 31) / 32));
-    w.rs.ensure(rows);
-    w.s_row.ensure(rows);
-    w.ocnt.ensure(rows);
-    w.scanned.ensure(rows);
+    // quantized-activation operands: one slot per scan direction (the x_proj K1 of
+    // both directions runs as one launch); slot 0 also serves in_proj / out_proj
+    const size_t slots = std::max<size_t>(1, nd);
+    w.codes.ensure(slots * rows * E);
+    w.ocode.ensure(slots * rows * E);
+    w.oscale.ensure(slots * rows * E);
+    w.omask.ensure(slots * rows * ((E + 31) / 32));
+    w.s_row.ensure(slots * rows);
+    w.ocnt.ensure(slots * rows);
+    w.scanned.ensure(slots * rows);
     w.scan_steps.ensure(scan_fast_workspace_bytes(S, static_cast<int>(L), static_cast<int>(nd)));
     if (trace) {
         w.masks.ensure(2 * 3 * rows * E);
@@ -455,6 +457,8 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
     }
     if (tr_on) grab(trace, "x_embed", w.x.p, rows * E, st);
 
+    int qslot = 0;  // QAct slot the K1 / K2 / trace lambdas address
+    const size_t J = (E + 31) / 32;
     auto k1_base = [&](int src, const double* x, int order, int b, int site, bool record) {
         K1Params k;
         k.S = S;
@@ -476,17 +480,16 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             k.cal.s_full = cal->s_full_dev(true, li);
             k.inv_in = cal->inv_in_dev(true, li);
             k.inv_full = cal->inv_full_dev(true, li);
-            k.rs = w.rs.p;
-            k.codes = w.codes.p;
-            k.s_row = w.s_row.p;
-            k.ocnt = w.ocnt.p;
-            k.omask = w.omask.p;
-            k.ocode = w.ocode.p;
-            k.oscale = w.oscale.p;
+            k.codes = w.codes.p + qslot * rows * E;
+            k.s_row = w.s_row.p + qslot * rows;
+            k.ocnt = w.ocnt.p + qslot * rows;
+            k.omask = w.omask.p + qslot * rows * J;
+            k.ocode = w.ocode.p + qslot * rows * E;
+            k.oscale = w.oscale.p + qslot * rows * E;
             // literal detector where the channel-local form is not exact, on request,
             // and in trace mode (it also reports DetectResult::scanned)
             k.force_literal = (mode == MODE_DYNAMIC && cal->lin_literal[li]) || k1_variant == 1 || tb(b);
-            if (tb(b)) k.scanned = w.scanned.p;
+            if (tb(b)) k.scanned = w.scanned.p + qslot * rows;
         } else {
             k.mode = MODE_FP;
             k.window = 8;
@@ -497,25 +500,25 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
     };
     auto qact = [&]() {
         QAct a;
-        a.codes = w.codes.p;
-        a.s_row = w.s_row.p;
-        a.ocnt = w.ocnt.p;
-        a.omask = w.omask.p;
-        a.ocode = w.ocode.p;
-        a.oscale = w.oscale.p;
-        a.J = (E + 31) / 32;
+        a.codes = w.codes.p + qslot * rows * E;
+        a.s_row = w.s_row.p + qslot * rows;
+        a.ocnt = w.ocnt.p + qslot * rows;
+        a.omask = w.omask.p + qslot * rows * J;
+        a.ocode = w.ocode.p + qslot * rows * E;
+        a.oscale = w.oscale.p + qslot * rows * E;
+        a.J = static_cast<int>(J);
         return a;
     };
     auto trace_lin = [&](int b, int site, int R) {
         if (!tb(b) || !qlin) return;
         std::string p = "lin" + std::to_string(site) + ".";
-        grab(trace, p + "codes", w.codes.p, rows * E, st);
-        grab(trace, p + "s_row", w.s_row.p, rows, st);
-        grab(trace, p + "ocnt", w.ocnt.p, rows, st);
-        grab(trace, p + "ocode", w.ocode.p, rows * E, st);
-        grab(trace, p + "oscale", w.oscale.p, rows * E, st);
-        grab(trace, p + "omask", w.omask.p, rows * ((E + 31) / 32), st);
-        grab(trace, p + "scanned", w.scanned.p, rows, st);
+        grab(trace, p + "codes", w.codes.p + qslot * rows * E, rows * E, st);
+        grab(trace, p + "s_row", w.s_row.p + qslot * rows, rows, st);
+        grab(trace, p + "ocnt", w.ocnt.p + qslot * rows, rows, st);
+        grab(trace, p + "ocode", w.ocode.p + qslot * rows * E, rows * E, st);
+        grab(trace, p + "oscale", w.oscale.p + qslot * rows * E, rows * E, st);
+        grab(trace, p + "omask", w.omask.p + qslot * rows * J, rows * J, st);
+        grab(trace, p + "scanned", w.scanned.p + qslot * rows, rows, st);
         grab(trace, p + "acc_in", w.acc_in.p, rows * R, st);
         grab(trace, p + "acc_out", w.acc_out.p, rows * R, st);
     };
@@ -583,14 +586,31 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         }
         ScanParams sps[2];
         bool any_literal = false;
+        // x_proj inputs of every direction: one K1 launch over the shared rows u
+        // (direction dd quantizes into QAct slot dd), then the x_proj GEMMs. FP mode
+        // materialises rows into the one xin buffer: K1 and GEMM per direction.
+        const bool k1_pair = qlin && nd <= 2;
+        if (k1_pair) {
+            K1Params kx[2];
+            for (int dd = 0; dd < nd; ++dd) {
+                qslot = dd;
+                kx[dd] = k1_base(K1_SRC_PLAIN, w.u.p, host.orders[dd], b, 1 + dd, true);
+            }
+            tick_begin(FAM_K1);
+            cuda_check(launch_k1_dirs(kx, nd, st), "K1 x_proj");
+            tick_end(FAM_K1);
+        }
         for (int dd = 0; dd < nd; ++dd) {
             const int order = host.orders[dd];
             double* proj = w.proj.p + static_cast<size_t>(dd) * rows * P;
             double* o = w.o.p + static_cast<size_t>(dd) * rows * E;
-            K1Params kx = k1_base(K1_SRC_PLAIN, w.u.p, order, b, 1 + dd, true);
-            tick_begin(FAM_K1);
-            cuda_check(launch_k1(kx, st), "K1 x_proj");
-            tick_end(FAM_K1);
+            qslot = k1_pair ? dd : 0;
+            if (!k1_pair) {
+                K1Params kx = k1_base(K1_SRC_PLAIN, w.u.p, order, b, 1 + dd, true);
+                tick_begin(FAM_K1);
+                cuda_check(launch_k1(kx, st), "K1 x_proj");
+                tick_end(FAM_K1);
+            }
             GemmEpi e;  // dpre | B | C (softplus(dpre + b_delta) runs in the scan's chunk pre-pass)
             e.post = POST_STORE;
             e.out = proj;
@@ -656,6 +676,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
                 if (quant && mode == MODE_DYNAMIC) grab(trace, p + "masks", sps[dd].masks, 3 * rows * E, st);
                 trace->blobs[p + "literal"] = std::vector<char>(1, static_cast<char>(lit ? 1 : 0));
             }
+        qslot = 0;
         K1Params km = k1_base(K1_SRC_MERGE, w.o.p, -1, b, nsites - 1, true);
         km.x2 = nd > 1 ? w.o.p + rows * E : nullptr;
         km.gate = w.gate.p;

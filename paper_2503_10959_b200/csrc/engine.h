@@ -158,7 +158,7 @@ class Model {
         DevBuf<double> x, patches, u0, gate, u, xin, pooled, logits, img;
         DevBuf<double> proj, o;  // per dir stacked
         DevBuf<int8_t> codes, ocode;
-        DevBuf<double> s_row, oscale, rs;
+        DevBuf<double> s_row, oscale;
         DevBuf<int> ocnt;
         DevBuf<uint32_t> omask;
         DevBuf<uint8_t> scanned, masks, scan_steps;

@@ -16,9 +16,16 @@
 // channel order, the order the reference adds outlier terms in
 // (gemm.cpp:208-216).
 //
-// Two kernels:
-//  * k1_channel (fast path): one thread owns four channels of one (sample,
-//    refresh window) and walks the window's tokens. Exact whenever
+// Three kernels:
+//  * k1_staged (fast path, plain / RMSNorm sources): a CTA owns one (sample,
+//    refresh window) and all E channels; the window's rows arrive in shared
+//    memory by bulk copies (two-stage ring, any scan order), D1's row factor is
+//    taken from the staged rows, and one thread walks four channels. Both scan
+//    directions' x_proj inputs can share one launch (CTAs interleaved so
+//    mirrored windows read the same rows from L2).
+//  * k1_channel (fast path, merge source): one thread owns four channels of
+//    one (sample, refresh window) and walks the window's tokens. Both fast
+//    kernels are exact whenever
 //    C(t) = fl(nextafter(theta,+inf)/q_a) > S^I(t) holds (host-checked per
 //    site and step): then O(t) = O_r(t) U {ch: |x| > theta}
 //    and channels never interact. Rows are read as 16-byte vectors, codes
@@ -27,40 +34,13 @@
 //    channels l, l+32, ...; the cross-channel maximum of detect_outliers is a
 //    warp reduction, so the reference is followed verbatim (also provides
 //    DetectResult::scanned).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100_ptx.cuh"
 
 namespace ob {
-
-// D1 RMSNorm factor per token row: 1/sqrt(mean(x^2) + 1e-6) with the sum taken
-// as 32 lane-strided partials (channel k -> partial k%32, k ascending) combined
-// by an xor butterfly (oracle/driver.hpp rmsnorm_row).
-__global__ void __launch_bounds__(256) k1_rownorm(const double* __restrict__ x, double* __restrict__ rs, long rows,
-                                                  int E) {
-    const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (r >= rows) return;
-    const double* xr = x + r * E;
-    double ps = 0.0;
-    int k = lane;
-    for (; k + 7 * 32 < E; k += 8 * 32) {  // 8 loads in flight, summed in channel order
-        double v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(xr + k + 32 * j);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) ps = dadd(ps, dmul(v[j], v[j]));
-    }
-    for (; k < E; k += 32) {
-        const double v = __ldg(xr + k);
-        ps = dadd(ps, dmul(v, v));
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) ps = dadd(ps, __shfl_xor_sync(0xffffffffu, ps, o));
-    if (lane == 0) {
-        const double ms = __ddiv_rn(ps, static_cast<double>(E));
-        rs[r] = __ddiv_rn(1.0, __dsqrt_rn(dadd(ms, 1e-6)));
-    }
-}
 
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 
@@ -251,6 +231,182 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
     }
 }
 
+// Staged fast path. Per CTA: one (sample, refresh window) of one direction, all
+// E channels (blockDim = E/4 rounded to warps). Rows of `rc` steps per stage,
+// two stages: chunk c lands in stage c&1 by per-row bulk copies on an mbarrier;
+// chunk c+2 is issued once every thread has finished chunk c.
+constexpr int kK1StageBytes = 32 * 1024;
+constexpr int kK1MaxRc = 16;
+struct K1Dirs {
+    K1Params p[2];
+    int n = 1;       // directions in this launch
+    int mirror = 0;  // direction 1 runs window nwin-1-w (row-reverse of direction 0): same rows, same time
+    int rc = 1;      // steps per stage
+};
+
+__device__ __forceinline__ int k1_row_of(const K1Params& p, int t) {
+    return p.order <= 0 ? t : (p.order == 1 ? p.T - 1 - t : scan_perm(p.order, t, p.grid));
+}
+
+template <int SRC>
+__global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs dirs) {
+    extern __shared__ __align__(128) unsigned char k1_smem[];
+    double* stage = reinterpret_cast<double*>(k1_smem);  // [2][rc][E]
+    __shared__ uint64_t bar[2];
+    __shared__ int cnt[2][kK1MaxRc];     // |O(t)| of the chunk's rows
+    __shared__ double rsv[2][kK1MaxRc];  // D1 row factors of the chunk's rows
+    const int d = dirs.n == 2 ? static_cast<int>(blockIdx.y & 1) : 0;
+    const K1Params& p = dirs.p[d];
+    const int yy = dirs.n == 2 ? static_cast<int>(blockIdx.y >> 1) : static_cast<int>(blockIdx.y);
+    const int E = p.E, T = p.T, J = E >> 5, rc = dirs.rc;
+    const int win = p.window, nwin = (T + win - 1) / win;
+    const int s = yy / nwin;
+    int wi = yy % nwin;
+    if (d == 1 && dirs.mirror) wi = nwin - 1 - wi;
+    const int t0 = wi * win, t1 = min(T, t0 + win);
+    const int nchunks = (t1 - t0 + rc - 1) / rc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int ch = tid * 4;
+    const bool active = ch < E;
+    const uint32_t row_bytes = static_cast<uint32_t>(E) * 8u;
+
+    if (tid == 0) {
+        ptx::mbar_init(&bar[0], 1);
+        ptx::mbar_init(&bar[1], 1);
+        ptx::fence_barrier_init();
+    }
+    if (tid < 2 * kK1MaxRc) cnt[tid / kK1MaxRc][tid % kK1MaxRc] = 0;
+    __syncthreads();
+    auto issue = [&](int c) {  // thread 0
+        const int buf = c & 1, ts = t0 + c * rc, te = min(t1, ts + rc);
+        ptx::mbar_arrive_expect_tx(&bar[buf], static_cast<uint32_t>(te - ts) * row_bytes);
+        for (int t = ts; t < te; ++t)
+            ptx::bulk_g2s(stage + (static_cast<size_t>(buf) * rc + (t - ts)) * E,
+                     p.x + (static_cast<size_t>(s) * T + k1_row_of(p, t)) * E, row_bytes, &bar[buf]);
+    };
+    if (tid == 0) {
+        issue(0);
+        if (nchunks > 1) issue(1);
+    }
+
+    // every field the loop needs, read once (the direction's parameter block is
+    // selected at run time)
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    const int n_refresh = p.n_refresh;
+    const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
+    const int qai = static_cast<int>(qa);
+    const double theta = p.cal.theta;
+    const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
+    const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
+    int8_t* __restrict__ const codes = p.codes;
+    int8_t* __restrict__ const ocode = p.ocode;
+    double* __restrict__ const oscale = p.oscale;
+    uint32_t* __restrict__ const omask = p.omask;
+    double* __restrict__ const s_row = p.s_row;
+    int* __restrict__ const ocnt = p.ocnt;
+    int next_ref = (dyn && n_refresh > 0) ? t0 + n_refresh : 0x7fffffff;
+    unsigned in = 0;  // bit k: channel ch+k is in O
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1, ts = t0 + c * rc, te = min(t1, ts + rc);
+        const double* sb = stage + static_cast<size_t>(buf) * rc * E;
+        ptx::mbar_wait(&bar[buf], static_cast<uint32_t>((c >> 1) & 1));
+        if (SRC == K1_SRC_RMSNORM) {
+            // 1/sqrt(mean(x^2) + 1e-6): 32 lane-strided partials (channel k -> partial
+            // k%32, k ascending) combined by an xor butterfly (oracle/driver.hpp rmsnorm_row)
+            for (int r = warp; r < te - ts; r += nwarps) {
+                const double* xr = sb + static_cast<size_t>(r) * E;
+                double ps = 0.0;
+                for (int k = lane; k < E; k += 32) ps = dadd(ps, dmul(xr[k], xr[k]));
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) ps = dadd(ps, __shfl_xor_sync(0xffffffffu, ps, o));
+                if (lane == 0) rsv[buf][r] = __ddiv_rn(1.0, __dsqrt_rn(dadd(__ddiv_rn(ps, static_cast<double>(E)), 1e-6)));
+            }
+            __syncthreads();
+        }
+        for (int t = ts; t < te; ++t) {
+            const int slot = t - ts;
+            const size_t row = static_cast<size_t>(s) * T + t;
+            const double S = s_tab[t];
+            const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            if (active) {
+                const double2 lo = *reinterpret_cast<const double2*>(sb + static_cast<size_t>(slot) * E + ch);
+                const double2 hi = *reinterpret_cast<const double2*>(sb + static_cast<size_t>(slot) * E + ch + 2);
+                v[0] = lo.x;
+                v[1] = lo.y;
+                v[2] = hi.x;
+                v[3] = hi.y;
+                if (SRC == K1_SRC_RMSNORM) {
+                    const double r = rsv[buf][slot];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v[k] = dmul(v[k], r);
+                }
+            }
+            if (dyn) {
+                if (t == next_ref) {  // maybe_refresh
+                    in = 0;
+                    next_ref += n_refresh;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // detect_outliers, channel-local form
+                    in |= (fabs(v[k]) > theta ? 1u : 0u) << k;
+            }
+            // inlier codes for all four channels: quant_code_int's rounding without its
+            // f64 clamp (round, then clamp the integer: same code for |q| < 2^50); a
+            // quotient near a half-integer or beyond 2^50 is decided exactly below
+            constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+            int cc[4];
+            bool tie = false;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double q2 = dmul(v[k], inv);
+                const double tq = dadd(q2, kMagic);
+                cc[k] = __double2loint(tq);
+                tie |= (fabs(dadd(q2, -dadd(tq, -kMagic))) > 0.4999999999990) | !(fabs(q2) < 0x1p50);
+            }
+            if (tie) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cc[k] = quant_code_int(v[k], S, inv, qa, qai);
+            }
+            if (active) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cc[k] = ((in >> k) & 1u) ? 0 : min(max(cc[k], -qai), qai);
+                *reinterpret_cast<char4*>(codes + row * E + ch) =
+                    make_char4(static_cast<signed char>(cc[0]), static_cast<signed char>(cc[1]),
+                               static_cast<signed char>(cc[2]), static_cast<signed char>(cc[3]));
+                if (in) {  // outlier channels: own scale |x|/q_o, code at o_bits
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if ((in >> k) & 1u) {
+                            const double os = scale_from_peak(fabs(v[k]), qo);  // scale_for over the 1-value row
+                            ocode[row * E + ch + k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[k], os, qo)));
+                            oscale[row * E + ch + k] = os;
+                        }
+                    }
+                }
+            }
+            // mask word of channels 32w..32w+31 from 8 lanes x 4 bits (all zero in the common case)
+            unsigned bits = active ? in << ((lane & 7) * 4) : 0u;
+            if (__any_sync(0xffffffffu, bits != 0u)) {
+#pragma unroll
+                for (int o = 4; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+                if (active && (lane & 7) == 0 && bits) atomicAdd(&cnt[buf][slot], __popc(bits));
+            }
+            if (active && (lane & 7) == 0) omask[row * J + (ch >> 5)] = bits;
+            if (tid == 0) s_row[row] = S;
+        }
+        __syncthreads();  // stage `buf` consumed, counts complete
+        if (tid < te - ts) {
+            ocnt[static_cast<size_t>(s) * T + ts + tid] = cnt[buf][tid];
+            cnt[buf][tid] = 0;
+        }
+        if (tid == 0 && c + 2 < nchunks) {
+            ptx::fence_async_smem();  // generic-proxy reads of the stage before the async refill
+            issue(c + 2);
+        }
+    }
+}
+
 template <int JMAX, int SRC>
 __global__ void __launch_bounds__(256) k1_literal(const K1Params p) {
     const int lane = threadIdx.x & 31;
@@ -384,11 +540,6 @@ template <int SRC>
 static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(p.ocnt, 0, static_cast<size_t>(p.S) * p.T * sizeof(int), st);
     if (e != cudaSuccess) return e;
-    if (SRC == K1_SRC_RMSNORM) {
-        const long rows = static_cast<long>(p.S) * p.T;
-        k1_rownorm<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(p.x, p.rs, rows, p.E);
-        ++kernel_launch_counter();
-    }
     const int nwin = (p.T + p.window - 1) / p.window;
     const int quads = p.E / 4, threads = quads >= 256 ? 256 : ((quads + 31) / 32) * 32;
     dim3 grid((quads + threads - 1) / threads, p.S * nwin);
@@ -397,20 +548,61 @@ static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int SRC>
+static cudaError_t launch_staged(const K1Dirs& dirs, cudaStream_t st) {
+    const K1Params& p = dirs.p[0];
+    const int nwin = (p.T + p.window - 1) / p.window;
+    const int threads = ((p.E / 4 + 31) / 32) * 32;  // E <= 1024: one CTA covers every channel
+    const size_t smem = 2ull * dirs.rc * p.E * sizeof(double);
+    cudaError_t e = ensure_smem_attr<k1_staged<SRC>>(static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    k1_staged<SRC><<<dim3(1, p.S * nwin * dirs.n), threads, smem, st>>>(dirs);
+    ++kernel_launch_counter();
+    return cudaGetLastError();
+}
+
+static K1Dirs k1_dirs(const K1Params* ps, int n) {
+    K1Dirs d;
+    d.n = n;
+    d.p[0] = ps[0];
+    d.p[1] = n > 1 ? ps[1] : ps[0];
+    d.mirror = n > 1 && ps[0].order <= 0 && ps[1].order == 1;
+    const int rows = kK1StageBytes / (ps[0].E * 8);
+    d.rc = std::max(1, std::min({rows, kK1MaxRc, ps[0].window}));
+    return d;
+}
+
+static bool k1_fast(const K1Params& p) {
+    // the channel-parallel kernels need: a quantizing mode, no DetectResult output,
+    // the channel-local detector exact (no literal steps) and E % 32 == 0
+    return p.mode != MODE_FP && !p.scanned && !p.force_literal && (p.E % 32) == 0;
+}
+
 cudaError_t launch_k1(const K1Params& p, cudaStream_t st) {
     if (p.E < 1 || p.E > 1024 || p.T < 1 || p.S < 1 || p.window < 1) return cudaErrorInvalidValue;
-    // the channel-parallel kernel needs: a quantizing mode, no DetectResult
-    // output, the channel-local detector exact (no literal steps), E % 32 == 0
-    // and (RMSNORM) a row-factor buffer
-    const bool fast = p.mode != MODE_FP && !p.scanned && !p.force_literal && (p.E % 32) == 0 &&
-                      (p.src != K1_SRC_RMSNORM || p.rs != nullptr);
+    const bool fast = k1_fast(p);
     switch (p.src) {
-        case K1_SRC_PLAIN: return fast ? launch_channel<K1_SRC_PLAIN>(p, st) : launch_literal<K1_SRC_PLAIN>(p, st);
+        case K1_SRC_PLAIN: return fast ? launch_staged<K1_SRC_PLAIN>(k1_dirs(&p, 1), st) : launch_literal<K1_SRC_PLAIN>(p, st);
         case K1_SRC_RMSNORM:
-            return fast ? launch_channel<K1_SRC_RMSNORM>(p, st) : launch_literal<K1_SRC_RMSNORM>(p, st);
+            return fast ? launch_staged<K1_SRC_RMSNORM>(k1_dirs(&p, 1), st) : launch_literal<K1_SRC_RMSNORM>(p, st);
         case K1_SRC_MERGE: return fast ? launch_channel<K1_SRC_MERGE>(p, st) : launch_literal<K1_SRC_MERGE>(p, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_k1_dirs(const K1Params* ps, int n, cudaStream_t st) {
+    // one staged launch when every direction quantizes the same plain rows on the fast path
+    bool pair = n == 2;
+    for (int i = 0; pair && i < n; ++i)
+        pair = ps[i].src == K1_SRC_PLAIN && k1_fast(ps[i]) && ps[i].x == ps[0].x && ps[i].S == ps[0].S &&
+               ps[i].T == ps[0].T && ps[i].E == ps[0].E && ps[i].window == ps[0].window && ps[i].E <= 1024 &&
+               ps[i].E >= 1;
+    if (pair) return launch_staged<K1_SRC_PLAIN>(k1_dirs(ps, n), st);
+    for (int i = 0; i < n; ++i) {
+        const cudaError_t e = launch_k1(ps[i], st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace ob

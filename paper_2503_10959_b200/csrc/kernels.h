@@ -15,10 +15,10 @@ inline long& kernel_launch_counter() {
     return n;
 }
 
-// Allow a kernel the device's opt-in shared-memory maximum, once per (kernel,
-// device): the attribute caps what launches may request (so it is set to the
-// device limit, not to one launch's size) and is per device (contexts on
-// several devices may share a process).
+// Allow a kernel the device's opt-in shared-memory maximum (less its static
+// shared memory), once per (kernel, device): the attribute caps what launches
+// may request (so it is set to the device limit, not to one launch's size) and
+// is per device (contexts on several devices may share a process).
 template <auto Kernel>
 cudaError_t ensure_smem_attr(int bytes) {
     static std::atomic<unsigned long long> done{0};  // bit d: set on device d
@@ -30,8 +30,12 @@ cudaError_t ensure_smem_attr(int bytes) {
     int optin = 0;
     e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
-    if (bytes > optin) return cudaErrorInvalidValue;
-    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncAttributes fa{};  // static + dynamic shared memory must fit the opt-in limit
+    e = cudaFuncGetAttributes(&fa, Kernel);
+    if (e != cudaSuccess) return e;
+    const int limit = optin - static_cast<int>(fa.sharedSizeBytes);
+    if (bytes > limit) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, limit);
     if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
     return e;
 }
@@ -68,7 +72,7 @@ struct K1Params {
     SiteCal cal;
     const double* inv_in = nullptr;    // optional [T] 1/s_in (host-computed); else divided in-kernel
     const double* inv_full = nullptr;  // optional [T] 1/s_full
-    double* rs = nullptr;              // [S*T] D1 row factors (workspace of the fast RMSNorm path)
+    double* rs = nullptr;              // unused (the staged kernel computes D1 row factors in shared memory)
     int force_literal = 0;             // run the literal detector kernel
     // quantized outputs (rows in step order, row = s*T + t): the QAct operand
     int8_t* codes = nullptr;
@@ -83,6 +87,9 @@ struct K1Params {
     unsigned long long* peaks = nullptr;    // [T][E] running max |x| (f64 bits), calibration
 };
 cudaError_t launch_k1(const K1Params& p, cudaStream_t st);
+// Several scan directions' K1 over the same rows: one launch on the staged fast
+// path (each direction's outputs in its own QAct), else one launch each.
+cudaError_t launch_k1_dirs(const K1Params* ps, int n, cudaStream_t st);
 
 // Post-ops fused into the quant-linear / f64 GEMM epilogues.
 enum PostOp {
