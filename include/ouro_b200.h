@@ -219,6 +219,64 @@ ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops);
  * roofline denominator. */
 ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops);
 
+/* detect_outliers + split_quantize over a stream of `steps` planes of K
+ * channels x C values, x dev f64 [steps][K][C] (channel = row of the plane,
+ * quant.cpp:313-335, gemm.cpp:106-135): maybe_refresh(t, n_refresh) clears the
+ * outlier list, a channel's peak is its max |x| over the C values, the scan
+ * fires when max_{ch not in O} peak / q(act_bits) > s_in[t] and then adds every
+ * channel with peak > theta; inlier values are coded at s_in[t], outlier
+ * channels at their own scale peak / q(outlier_bits). Outputs are the K2
+ * operand with rows r = t*C + i and channel stride Kp >= K (codes 0 beyond K):
+ * codes int8 [steps*C][Kp], s_row f64, ocnt int32 (|O(t)|), omask uint32
+ * [steps*C][ceil(Kp/32)], ocode int8 / oscale f64 [steps*C][Kp] at outlier
+ * positions, optional scanned uint8 [steps] (DetectResult::scanned). K <= 4096. */
+ouro_status ouro_b200_detect_quantize_planes(ouro_b200_ctx* ctx, const double* x, size_t steps, size_t K, size_t C,
+                                             double theta, const double* s_in, size_t n_refresh, unsigned act_bits,
+                                             unsigned outlier_bits, size_t Kp, int8_t* codes, double* s_row,
+                                             int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
+                                             uint8_t* scanned);
+
+/* The gemm-bench stage on the GPU (run_gemm_bench, pipeline.cpp:229-275).
+ * Settings and records mirror SweepSettings / SweepRecord / BenchSettings /
+ * BenchRecord (gemm.hpp:103-138); operands are drawn exactly as the
+ * reference's bench_refresh_sweep / bench_gemm draw them from `seed`, so
+ * mean_o_list and scans_per_step equal the reference's. Times are device time
+ * (CUDA events) per trial, median over trials: the sweep times the plane
+ * detector + quantizer and one K2 launch over all steps per period; the bench
+ * times K2 ("hybrid", path 0) and the f64 GEMM of the dequantized operands
+ * ("f64", path 1). `outputs` (nullable): the sweep's GEMM outputs,
+ * [n_periods][steps][c][m] (the reference's y[m][c] per step). */
+typedef struct {
+    const size_t* periods; /* 0 = never refresh */
+    size_t n_periods;
+    size_t steps, m, k, c, persistent_channels;
+    double transient_rate, spike_gain;
+    size_t trials;
+    uint64_t seed;
+} ouro_b200_sweep_settings;
+typedef struct {
+    size_t period;
+    double median_total_ns, mean_o_list, scans_per_step;
+} ouro_b200_sweep_record;
+ouro_status ouro_b200_refresh_sweep(ouro_b200_ctx* ctx, const ouro_b200_sweep_settings* s,
+                                    ouro_b200_sweep_record* records, double* outputs);
+typedef struct {
+    const size_t* sizes;
+    size_t n_sizes;
+    double outlier_fraction;
+    size_t trials;
+    uint64_t seed;
+    int f16_output;
+} ouro_b200_bench_settings;
+typedef struct {
+    int path; /* 0 hybrid, 1 f64 */
+    size_t size;
+    double median_ns;
+} ouro_b200_bench_record;
+/* records: 2 * n_sizes entries, per size hybrid then f64 */
+ouro_status ouro_b200_gemm_bench(ouro_b200_ctx* ctx, const ouro_b200_bench_settings* s,
+                                 ouro_b200_bench_record* records);
+
 /* Diagnostic: y[i] = f(x[i]) on the device for the path's transcendental
  * functions, fn = 0 exp, 1 log1p, 2 softplus, 3 silu (tensor.hpp:146-154);
  * x and y are device pointers of n doubles. The device forms restate glibc's

@@ -576,4 +576,58 @@ inline QuantEvalResult quantized_forward(const ToyVmmModel& model, const std::ve
     return out;
 }
 
+// ---- gemm-bench stage (gemm.hpp:103-138, gemm.cpp:260-411) on the GPU ----
+struct BenchSettings {
+    std::vector<size_t> sizes = {64, 128, 256};
+    double outlier_fraction = 0.01;
+    size_t trials = 5;
+    int threads = 1;  // accepted for signature parity; the GPU path ignores it
+    uint64_t seed = 1;
+    bool f16_output = false;
+};
+struct BenchRecord {
+    std::string path;  // "hybrid" or "f64"
+    size_t size = 0;
+    double median_ns = 0.0;  // device time
+};
+struct SweepSettings {
+    std::vector<size_t> periods = {1, 5, 10, 20, 0};  // 0 = never refresh
+    size_t steps = 300;
+    size_t m = 8, k = 512, c = 32;
+    size_t persistent_channels = 6;
+    double transient_rate = 0.15;
+    double spike_gain = 40.0;
+    size_t trials = 5;
+    uint64_t seed = 1;
+};
+struct SweepRecord {
+    size_t period = 0;
+    double median_total_ns = 0.0;
+    double mean_o_list = 0.0;
+    double scans_per_step = 0.0;
+};
+
+// bench_gemm: same draws as the reference; "hybrid" = K2, "f64" = the f64 GEMM.
+inline std::vector<BenchRecord> bench_gemm(const BenchSettings& s, Context& ctx = default_context()) {
+    ouro_b200_bench_settings bs{s.sizes.data(), s.sizes.size(), s.outlier_fraction, s.trials, s.seed,
+                                s.f16_output ? 1 : 0};
+    std::vector<ouro_b200_bench_record> r(2 * s.sizes.size());
+    check(ouro_b200_gemm_bench(ctx.handle(), &bs, r.data()));
+    std::vector<BenchRecord> out;
+    for (const auto& x : r) out.push_back({x.path == 0 ? "hybrid" : "f64", x.size, x.median_ns});
+    return out;
+}
+
+// bench_refresh_sweep: same draws as the reference, so mean_o_list and
+// scans_per_step equal the reference's; the timing is device time.
+inline std::vector<SweepRecord> bench_refresh_sweep(const SweepSettings& s, Context& ctx = default_context()) {
+    ouro_b200_sweep_settings ss{s.periods.data(), s.periods.size(), s.steps, s.m, s.k, s.c, s.persistent_channels,
+                                s.transient_rate, s.spike_gain, s.trials, s.seed};
+    std::vector<ouro_b200_sweep_record> r(s.periods.size());
+    check(ouro_b200_refresh_sweep(ctx.handle(), &ss, r.data(), nullptr));
+    std::vector<SweepRecord> out;
+    for (const auto& x : r) out.push_back({x.period, x.median_total_ns, x.mean_o_list, x.scans_per_step});
+    return out;
+}
+
 }  // namespace ouro_b200

@@ -155,6 +155,9 @@ class Checker:
             L.ref_pin_quant_eval.argtypes = [_P, _P, C.c_int, _P, _SZ, _P, _P, C.POINTER(C.c_double),
                                              C.POINTER(_SZ), _P]
             L.ref_pin_load_calibration.argtypes = [C.c_char_p, C.POINTER(_P)]
+            L.ref_pin_refresh_sweep.argtypes = [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_double, C.c_double, _SZ,
+                                                C.c_uint64, _P, _P]
+            L.ref_pin_gemm_bench.argtypes = [_P, _SZ, C.c_double, _SZ, C.c_uint64, _P, _P]
 
     def _check(self, st: int) -> None:
         if st != 0:
@@ -184,6 +187,24 @@ class Checker:
                                               _ptr(np.ascontiguousarray(s_full, np.float64)), n_refresh, abits, obits,
                                               mode, _ptr(masks), _ptr(scanned)))
         return x, masks, scanned
+
+    def ref_refresh_sweep(self, periods, steps, m, k, c, persistent, transient_rate, spike_gain, trials, seed):
+        """The reference's own bench_refresh_sweep (gemm.cpp:326-411): (mean_o_list, scans_per_step) per period."""
+        per = np.ascontiguousarray(periods, np.uint64)
+        mo = np.zeros(len(per))
+        sc = np.zeros(len(per))
+        self._check(self.lib.ref_pin_refresh_sweep(_ptr(per), len(per), steps, m, k, c, persistent, transient_rate,
+                                                   spike_gain, trials, seed, _ptr(mo), _ptr(sc)))
+        return mo, sc
+
+    def ref_gemm_bench(self, sizes, outlier_fraction, trials, seed):
+        """The reference's own bench_gemm (gemm.cpp:260-324): its (path, size) record list."""
+        sz = np.ascontiguousarray(sizes, np.uint64)
+        paths = np.zeros(2 * len(sz), np.int32)
+        out = np.zeros(2 * len(sz), np.uint64)
+        self._check(self.lib.ref_pin_gemm_bench(_ptr(sz), len(sz), outlier_fraction, trials, seed, _ptr(paths),
+                                                _ptr(out)))
+        return list(zip(paths.tolist(), out.tolist()))
 
     def hybrid_gemm(self, w: np.ndarray, w_scales: np.ndarray, x_inlier: np.ndarray, s_in: float,
                     channels: np.ndarray, ocodes: np.ndarray, oscales: np.ndarray):

@@ -342,6 +342,49 @@ int ref_pin_quant_eval(void* m, void* c, int mode, const double* images, std::si
     });
 }
 
+// bench_refresh_sweep (gemm.cpp:326-411) itself: per period, the mean |O| after
+// detection and the scans per step (the GPU sweep draws the same operands).
+int ref_pin_refresh_sweep(const std::size_t* periods, std::size_t n_periods, std::size_t steps, std::size_t m,
+                          std::size_t k, std::size_t c, std::size_t persistent, double transient_rate,
+                          double spike_gain, std::size_t trials, std::uint64_t seed, double* mean_o_list,
+                          double* scans_per_step) {
+    return guarded([&] {
+        ouro::SweepSettings ss;
+        ss.periods.assign(periods, periods + n_periods);
+        ss.steps = steps;
+        ss.m = m;
+        ss.k = k;
+        ss.c = c;
+        ss.persistent_channels = persistent;
+        ss.transient_rate = transient_rate;
+        ss.spike_gain = spike_gain;
+        ss.trials = trials;
+        ss.seed = seed;
+        const auto recs = ouro::bench_refresh_sweep(ss);
+        for (std::size_t i = 0; i < recs.size(); ++i) {
+            mean_o_list[i] = recs[i].mean_o_list;
+            scans_per_step[i] = recs[i].scans_per_step;
+        }
+    });
+}
+
+// bench_gemm (gemm.cpp:260-324): the record list (path 0 hybrid / 1 f64, size).
+int ref_pin_gemm_bench(const std::size_t* sizes, std::size_t n_sizes, double outlier_fraction, std::size_t trials,
+                       std::uint64_t seed, int* paths, std::size_t* out_sizes) {
+    return guarded([&] {
+        ouro::BenchSettings bs;
+        bs.sizes.assign(sizes, sizes + n_sizes);
+        bs.outlier_fraction = outlier_fraction;
+        bs.trials = trials;
+        bs.seed = seed;
+        const auto recs = ouro::bench_gemm(bs);
+        for (std::size_t i = 0; i < recs.size(); ++i) {
+            paths[i] = recs[i].path == "hybrid" ? 0 : 1;
+            out_sizes[i] = recs[i].size;
+        }
+    });
+}
+
 // save_calibration (quant.cpp:179-216) of a calibration handle's scan tensors,
 // named block<b>.dir<d>.<kind> as calibrate names them (quant.cpp:150-151).
 int ref_pin_save_calibration(void* c, const char* dir) {

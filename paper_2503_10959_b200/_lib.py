@@ -57,6 +57,10 @@ _SIGS = {
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_math_eval": ([_P, _I, _P, _P, _SZ], _I),
+    "ouro_b200_detect_quantize_planes": ([_P, _P, _SZ, _SZ, _SZ, _D, _P, _SZ, C.c_uint, C.c_uint, _SZ, _P, _P, _P,
+                                          _P, _P, _P, _P], _I),
+    "ouro_b200_refresh_sweep": ([_P, _P, _P, _P], _I),
+    "ouro_b200_gemm_bench": ([_P, _P, _P], _I),
     "ouro_b200_calib_save": ([_P, _P, C.c_char_p], _I),
     "ouro_b200_model_get_qweight": ([_P, C.c_char_p, C.c_uint, _P, C.c_size_t, C.POINTER(C.c_size_t)], _I),
     "ouro_b200_calib_load": ([_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P)], _I),
@@ -105,6 +109,29 @@ def load(path: str = SO_PATH):
         fn.restype = res
     _lib = lib
     return lib
+
+
+class SweepSettings(C.Structure):
+    """ouro_b200_sweep_settings (SweepSettings, gemm.hpp:122-131)."""
+    _fields_ = [("periods", C.POINTER(C.c_size_t)), ("n_periods", C.c_size_t), ("steps", C.c_size_t),
+                ("m", C.c_size_t), ("k", C.c_size_t), ("c", C.c_size_t), ("persistent_channels", C.c_size_t),
+                ("transient_rate", C.c_double), ("spike_gain", C.c_double), ("trials", C.c_size_t),
+                ("seed", C.c_uint64)]
+
+
+class SweepRecord(C.Structure):
+    _fields_ = [("period", C.c_size_t), ("median_total_ns", C.c_double), ("mean_o_list", C.c_double),
+                ("scans_per_step", C.c_double)]
+
+
+class BenchSettings(C.Structure):
+    """ouro_b200_bench_settings (BenchSettings, gemm.hpp:103-110)."""
+    _fields_ = [("sizes", C.POINTER(C.c_size_t)), ("n_sizes", C.c_size_t), ("outlier_fraction", C.c_double),
+                ("trials", C.c_size_t), ("seed", C.c_uint64), ("f16_output", C.c_int)]
+
+
+class BenchRecord(C.Structure):
+    _fields_ = [("path", C.c_int), ("size", C.c_size_t), ("median_ns", C.c_double)]
 
 
 def check(status: int) -> None:

@@ -8,6 +8,7 @@
 
 #include "../../include/ouro_b200.h"
 #include "engine.h"
+#include "planes.h"
 
 using ob::require;
 
@@ -664,6 +665,81 @@ ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops) {
         require(ctx && tops, "measure_i8_peak: NULL argument");
         *tops = ob::measure_i8_peak(ctx->c->stream, ctx->c->num_sms);
         ob::require(*tops > 0.0, "measure_i8_peak: probe failed");
+    });
+}
+
+ouro_status ouro_b200_detect_quantize_planes(ouro_b200_ctx* ctx, const double* x, size_t steps, size_t K, size_t C,
+                                             double theta, const double* s_in, size_t n_refresh, unsigned act_bits,
+                                             unsigned outlier_bits, size_t Kp, int8_t* codes, double* s_row,
+                                             int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
+                                             uint8_t* scanned) {
+    return guarded([&] {
+        require(ctx && x && s_in && codes && s_row && ocnt && omask && ocode && oscale,
+                "detect_quantize_planes: NULL argument");
+        require(steps >= 1 && C >= 1 && K >= 1 && K <= 4096, "detect_quantize_planes: need steps, C >= 1 and 1 <= K <= 4096");
+        require(Kp >= K && Kp <= (1u << 20), "detect_quantize_planes: Kp must be >= K");
+        require(steps * C <= static_cast<size_t>(INT32_MAX) && steps <= 65535, "detect_quantize_planes: too many rows");
+        require(act_bits >= 2 && act_bits <= outlier_bits && outlier_bits <= 8,
+                "detect_quantize_planes: need 2 <= act_bits <= outlier_bits <= 8");
+        ob::PlaneParams p;
+        p.x = x;
+        p.steps = static_cast<int>(steps);
+        p.K = static_cast<int>(K);
+        p.Kp = static_cast<int>(Kp);
+        p.C = static_cast<int>(C);
+        p.theta = theta;
+        p.s_in = s_in;
+        p.n_refresh = static_cast<int>(n_refresh);
+        p.abits = static_cast<int>(act_bits);
+        p.obits = static_cast<int>(outlier_bits);
+        p.a = ob::QAct{codes, s_row, ocnt, omask, ocode, oscale, static_cast<int>((Kp + 31) / 32)};
+        p.scanned = scanned;
+        void* work = nullptr;
+        cudaStream_t st = ctx->c->stream;
+        ob::cuda_check(cudaMallocAsync(&work, ob::plane_workspace_bytes(p.steps, p.K), st), "workspace");
+        p.work = work;
+        const cudaError_t e = ob::launch_detect_planes(p, st);
+        cudaFreeAsync(work, st);
+        ob::cuda_check(e, "detect_quantize_planes");
+    });
+}
+
+ouro_status ouro_b200_refresh_sweep(ouro_b200_ctx* ctx, const ouro_b200_sweep_settings* s,
+                                    ouro_b200_sweep_record* records, double* outputs) {
+    return guarded([&] {
+        require(ctx && s && records && (s->periods || s->n_periods == 0), "refresh_sweep: NULL argument");
+        ob::SweepSettings ss;
+        ss.periods.assign(s->periods, s->periods + s->n_periods);
+        ss.steps = s->steps;
+        ss.m = s->m;
+        ss.k = s->k;
+        ss.c = s->c;
+        ss.persistent_channels = s->persistent_channels;
+        ss.transient_rate = s->transient_rate;
+        ss.spike_gain = s->spike_gain;
+        ss.trials = s->trials;
+        ss.seed = s->seed;
+        std::vector<double> y;
+        const auto recs = ob::refresh_sweep(ss, ctx->c->stream, ctx->c->num_sms, outputs ? &y : nullptr);
+        for (size_t i = 0; i < recs.size(); ++i)
+            records[i] = {recs[i].period, recs[i].median_total_ns, recs[i].mean_o_list, recs[i].scans_per_step};
+        if (outputs) std::memcpy(outputs, y.data(), y.size() * sizeof(double));
+    });
+}
+
+ouro_status ouro_b200_gemm_bench(ouro_b200_ctx* ctx, const ouro_b200_bench_settings* s,
+                                 ouro_b200_bench_record* records) {
+    return guarded([&] {
+        require(ctx && s && records && (s->sizes || s->n_sizes == 0), "gemm_bench: NULL argument");
+        ob::BenchSettings bs;
+        bs.sizes.assign(s->sizes, s->sizes + s->n_sizes);
+        bs.outlier_fraction = s->outlier_fraction;
+        bs.trials = s->trials;
+        bs.seed = s->seed;
+        bs.f16_output = s->f16_output != 0;
+        const auto recs = ob::gemm_bench(bs, ctx->c->stream, ctx->c->num_sms);
+        for (size_t i = 0; i < recs.size(); ++i)
+            records[i] = {recs[i].path == "hybrid" ? 0 : 1, recs[i].size, recs[i].median_ns};
     });
 }
 

@@ -3,6 +3,7 @@
 // only prepares weights (W4 row quantization, once per model, quant.cpp:355-402),
 // reduces calibration statistics (quantile, quant.cpp:117-177) and launches.
 #include "engine.h"
+#include "seeded_rng.h"
 
 #include <algorithm>
 #include <cmath>
@@ -79,24 +80,6 @@ void Context::set_stream(cudaStream_t s) {
 // ---- seeded model init: make_toy_model (ssm.cpp:88-120) with the reference's
 // SeededRng (rng.cpp: mt19937_64, explicit Box-Muller with a cached spare).
 namespace {
-struct SeededRng {
-    std::mt19937_64 gen;
-    bool have = false;
-    double spare = 0.0;
-    explicit SeededRng(uint64_t s) : gen(s) {}
-    double uniform() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
-    double normal() {
-        if (have) {
-            have = false;
-            return spare;
-        }
-        double u1 = 1.0 - uniform(), u2 = uniform();
-        double r = std::sqrt(-2.0 * std::log(u1)), a = 2.0 * M_PI * u2;
-        spare = r * std::sin(a);
-        have = true;
-        return r * std::cos(a);
-    }
-};
 std::vector<double> gaussian(SeededRng& r, size_t n, size_t fan_in) {
     std::vector<double> v(n);
     double s = 1.0 / std::sqrt(static_cast<double>(fan_in));

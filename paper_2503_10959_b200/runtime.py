@@ -140,6 +140,52 @@ class Context:
         L.check(self.lib.ouro_b200_math_eval(self.h, code, _ptr(x), _ptr(y), x.numel()))
         return y
 
+    def refresh_sweep(self, periods=(1, 5, 10, 20, 0), *, steps=300, m=8, k=512, c=32, persistent_channels=6,
+                      transient_rate=0.15, spike_gain=40.0, trials=5, seed=1, outputs=False):
+        """bench_refresh_sweep (gemm.cpp:326-411) on the GPU: one record per period
+        (period, median_total_ns, mean_o_list, scans_per_step); with outputs=True also
+        the GEMM outputs [n_periods][steps][c][m]."""
+        per = (C.c_size_t * len(periods))(*periods)
+        st = L.SweepSettings(per, len(periods), steps, m, k, c, persistent_channels, transient_rate, spike_gain,
+                             trials, seed)
+        recs = (L.SweepRecord * len(periods))()
+        y = np.zeros((len(periods), steps, c, m)) if outputs else None
+        L.check(self.lib.ouro_b200_refresh_sweep(self.h, C.byref(st), recs, _ptr(y)))
+        out = [dict(period=r.period, median_total_ns=r.median_total_ns, mean_o_list=r.mean_o_list,
+                    scans_per_step=r.scans_per_step) for r in recs]
+        return (out, y) if outputs else out
+
+    def gemm_bench(self, sizes=(64, 128, 256), *, outlier_fraction=0.01, trials=5, seed=1, f16_output=False):
+        """bench_gemm (gemm.cpp:260-324) on the GPU: per size a "hybrid" (K2) and an
+        "f64" record with the median device time in ns."""
+        sz = (C.c_size_t * len(sizes))(*sizes)
+        st = L.BenchSettings(sz, len(sizes), outlier_fraction, trials, seed, int(f16_output))
+        recs = (L.BenchRecord * (2 * len(sizes)))()
+        L.check(self.lib.ouro_b200_gemm_bench(self.h, C.byref(st), recs))
+        return [dict(path="hybrid" if r.path == 0 else "f64", size=r.size, median_ns=r.median_ns) for r in recs]
+
+    def detect_quantize_planes(self, x, *, theta, s_in, n_refresh, act_bits=4, outlier_bits=8, Kp=None):
+        """detect_outliers + split_quantize over a stream of K x C planes (x: float64
+        CUDA tensor [steps][K][C]) into the K2 operand with rows t*C + i; returns the
+        QAct dict plus `scanned` [steps]."""
+        import torch
+        x, s_in = x.contiguous(), s_in.contiguous()  # kept alive until the call returns
+        steps, K, Cc = x.shape
+        Kp = K if Kp is None else Kp
+        rows, J, dev = steps * Cc, (Kp + 31) // 32, x.device
+        out = dict(codes=torch.empty(rows, Kp, dtype=torch.int8, device=dev),
+                   s_row=torch.empty(rows, dtype=torch.float64, device=dev),
+                   ocnt=torch.empty(rows, dtype=torch.int32, device=dev),
+                   omask=torch.zeros(rows, J, dtype=torch.int32, device=dev),
+                   ocode=torch.zeros(rows, Kp, dtype=torch.int8, device=dev),
+                   oscale=torch.zeros(rows, Kp, dtype=torch.float64, device=dev),
+                   scanned=torch.zeros(steps, dtype=torch.uint8, device=dev))
+        L.check(self.lib.ouro_b200_detect_quantize_planes(
+            self.h, _ptr(x), steps, K, Cc, float(theta), _ptr(s_in), n_refresh, act_bits,
+            outlier_bits, Kp, _ptr(out["codes"]), _ptr(out["s_row"]), _ptr(out["ocnt"]), _ptr(out["omask"]),
+            _ptr(out["ocode"]), _ptr(out["oscale"]), _ptr(out["scanned"])))
+        return out
+
     # ---- operators (device tensors) --------------------------------------------
     def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
                         mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, literal=False,

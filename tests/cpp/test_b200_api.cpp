@@ -261,3 +261,43 @@ TEST_CASE("quantized_forward on the GPU == reference quantized_forward (logits a
     CHECK_THROWS_AS(ouro_b200::quantized_forward(*gm, img, 4, to_gpu(cal), ouro_b200::QuantMode::Dynamic, sp),
                     ouro_b200::ValidationError);
 }
+
+TEST_CASE("bench_refresh_sweep and bench_gemm on the GPU == reference records") {
+    ouro::SweepSettings rs;
+    rs.steps = 120;
+    rs.k = 256;
+    rs.c = 16;
+    rs.trials = 1;
+    rs.seed = 4;
+    ouro_b200::SweepSettings gs;
+    gs.steps = 120;
+    gs.k = 256;
+    gs.c = 16;
+    gs.trials = 2;
+    gs.seed = 4;
+    const auto want = ouro::bench_refresh_sweep(rs);
+    const auto got = ouro_b200::bench_refresh_sweep(gs);
+    REQUIRE(got.size() == want.size());
+    for (size_t i = 0; i < want.size(); ++i) {
+        CHECK(got[i].period == want[i].period);
+        CHECK(got[i].mean_o_list == want[i].mean_o_list);
+        CHECK(got[i].scans_per_step == want[i].scans_per_step);
+        CHECK(got[i].median_total_ns > 0.0);
+    }
+    ouro::BenchSettings rb;
+    rb.sizes = {48, 160};
+    rb.trials = 1;
+    ouro_b200::BenchSettings gb;
+    gb.sizes = {48, 160};
+    gb.trials = 2;
+    const auto wb = ouro::bench_gemm(rb);
+    const auto gbr = ouro_b200::bench_gemm(gb);
+    REQUIRE(gbr.size() == wb.size());
+    for (size_t i = 0; i < wb.size(); ++i) {
+        CHECK(gbr[i].path == wb[i].path);
+        CHECK(gbr[i].size == wb[i].size);
+        CHECK(gbr[i].median_ns > 0.0);
+    }
+    gs.spike_gain = 1.0;
+    CHECK_THROWS_AS(ouro_b200::bench_refresh_sweep(gs), ouro_b200::ValidationError);
+}
