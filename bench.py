@@ -271,11 +271,11 @@ def run_ours(args):
         L, E, N = dims.tokens, dims.embed, dims.state
         scan_ms, scan_n = fam["k3_scan"]
         # Algorithmic work of one scan launch:
-        # S*T*E*N state-element-steps x 28 arithmetic lane-ops (discretize 2,
+        # S*T*E*N state-element-steps per direction x 28 arithmetic lane-ops (discretize 2,
         # 3 quantizations x 7, update 2, output 2; the exp is not counted).
         # Peak: the measured f64 lane-op rate of this GPU (one DFMA = 1 op).
         ops_per_elem = 28.0
-        elem = B * L * E * N
+        elem = B * L * E * N * len(model.orders)  # one launch scans every direction
         # one scan op per block (its launches: the step-table prep + the scan kernel)
         achieved = elem * ops_per_elem / (scan_ms / dims.blocks * 1e-3) / 1e12
         peak_ops = fp64_peak / 2.0
@@ -293,7 +293,7 @@ def run_ours(args):
                              "traffic": traffic,
                              "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01/ncu_traffic_r01d.json)",
                              "peak_source": "measured in-process: DFMA probe (1 op per DFMA lane)",
-                             "work": f"{ops_per_elem:.0f} f64 lane-ops x S*T*E*N state-element-steps per launch"},
+                             "work": f"{ops_per_elem:.0f} f64 lane-ops x S*T*E*N*dirs state-element-steps per launch"},
                 "kernels_ms_per_step": {k: v[0] for k, v in fam.items()},
                 "kernels_launches_per_step": {k: v[1] for k, v in fam.items()},
                 "clocks": clk.summary(), "logits_finite": finite}
