@@ -219,6 +219,28 @@ ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops);
  * roofline denominator. */
 ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops);
 
+/* Spike injection (SpikeSettings / SpikeHook, quant.hpp:105-118,
+ * quant.cpp:420-446): at (sample, block, dir, t) positions chosen by the
+ * reference's mix64 chain with probability `rate`, `channels` hashed channels'
+ * b_bar values are multiplied by `gain` before quantization. rate 0 = off;
+ * channels in [1, 64]. */
+typedef struct {
+    double rate, gain;
+    size_t channels;
+    uint64_t salt;
+} ouro_b200_spikes;
+/* Spikes for every later forward / trace of this model (NULL = off); spiked
+ * scans run on the reference-form kernel. Cached graphs are rebuilt. */
+ouro_status ouro_b200_model_set_spikes(ouro_b200_model* m, const ouro_b200_spikes* spikes);
+/* quant_scan with spikes: block, dir and the global index of sample 0 place the
+ * scan in the reference's StepContext (quant.cpp:559). */
+ouro_status ouro_b200_quant_scan_spiked(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order,
+                                        int grid, const double* u, const double* proj, const double* a,
+                                        const double* b_delta, double* o, int mode, size_t n_refresh,
+                                        unsigned act_bits, unsigned outlier_bits, const double* theta,
+                                        const double* const* s_in, const double* const* s_full,
+                                        const ouro_b200_spikes* spikes, size_t block, size_t dir, size_t sample0);
+
 /* detect_outliers + split_quantize over a stream of `steps` planes of K
  * channels x C values, x dev f64 [steps][K][C] (channel = row of the plane,
  * quant.cpp:313-335, gemm.cpp:106-135): maybe_refresh(t, n_refresh) clears the

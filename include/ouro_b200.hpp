@@ -334,7 +334,7 @@ struct ModelDims {
     size_t patch_vals() const { return patch * patch * channels; }
 };
 
-struct SpikeSettings {  // spike injection is not modelled on the GPU: rate must be 0
+struct SpikeSettings {  // SpikeHook (quant.hpp:105-118): channels in [1, 64] when rate > 0
     double rate = 0.0;
     double gain = 100.0;
     size_t channels = 1;
@@ -492,8 +492,15 @@ inline CalibrationResult calibrate(const ToyVmmModel& model, const std::vector<d
 inline QuantEvalResult quantized_forward(const ToyVmmModel& model, const std::vector<double>& images, size_t batch,
                                          const CalibrationResult& calib, QuantMode mode,
                                          const SpikeSettings& spikes = SpikeSettings{}) {
-    require(spikes.rate == 0.0, "quantized_forward: spike injection is not available on the GPU path");
     const ModelDims& d = model.dims();
+    // SpikeHook in all three passes (FP, quantized, teacher-forced), as the reference
+    const ouro_b200_spikes sp{spikes.rate, spikes.gain, spikes.channels, spikes.salt};
+    const bool spiked = spikes.rate > 0.0;
+    check(ouro_b200_model_set_spikes(model.handle(), spiked ? &sp : nullptr));
+    struct SpikeReset {
+        ouro_b200_model* m;
+        ~SpikeReset() { ouro_b200_model_set_spikes(m, nullptr); }
+    } spike_reset{model.handle()};
     require(images.size() == batch * d.image * d.image * d.channels, "quantized_forward: image buffer size mismatch");
     detail::CalibHandle cal(model, calib);
     QuantEvalResult out;
@@ -558,10 +565,11 @@ inline QuantEvalResult quantized_forward(const ToyVmmModel& model, const std::ve
                 out.layer_mse.emplace_back(pd, 0.0);
                 continue;
             }
-            check(ouro_b200_quant_scan(ctx.handle(), batch, T, E, N, static_cast<int>(model.orders()[dir]),
-                                       static_cast<int>(d.grid()), d_u.get(), d_proj.get(), d_a.get(), d_bd.get(),
-                                       d_o.get(), qmode, calib.spec.n_refresh, calib.spec.act_bits,
-                                       calib.spec.outlier_bits, theta, si, sf, nullptr, 0, nullptr));
+            check(ouro_b200_quant_scan_spiked(ctx.handle(), batch, T, E, N, static_cast<int>(model.orders()[dir]),
+                                              static_cast<int>(d.grid()), d_u.get(), d_proj.get(), d_a.get(),
+                                              d_bd.get(), d_o.get(), qmode, calib.spec.n_refresh,
+                                              calib.spec.act_bits, calib.spec.outlier_bits, theta, si, sf,
+                                              spiked ? &sp : nullptr, b, dir, 0));
             ctx.synchronize();
             const std::vector<double> o_tf = d_o.download();
             const std::vector<double> o_fp = detail::trace_get(tr, "dir" + std::to_string(dir) + ".o");

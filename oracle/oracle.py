@@ -155,6 +155,8 @@ class Checker:
             L.ref_pin_quant_eval.argtypes = [_P, _P, C.c_int, _P, _SZ, _P, _P, C.POINTER(C.c_double),
                                              C.POINTER(_SZ), _P]
             L.ref_pin_load_calibration.argtypes = [C.c_char_p, C.POINTER(_P)]
+            L.ref_pin_quant_eval_spiked.argtypes = [_P, _P, C.c_int, _P, _SZ, _P, _P, C.POINTER(C.c_double),
+                                                    C.POINTER(_SZ), _P, C.c_double, C.c_double, _SZ, C.c_uint64]
             L.ref_pin_refresh_sweep.argtypes = [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_double, C.c_double, _SZ,
                                                 C.c_uint64, _P, _P]
             L.ref_pin_gemm_bench.argtypes = [_P, _SZ, C.c_double, _SZ, C.c_uint64, _P, _P]
@@ -345,16 +347,22 @@ class Model:
                                                                _ptr(lf)))
         return lq, lf
 
-    def ref_quant_eval(self, images: np.ndarray, calib: "CalibHandle", mode: int) -> dict:
-        """The reference's quantized_forward (quant.cpp:505-579) and its metrics."""
+    def ref_quant_eval(self, images: np.ndarray, calib: "CalibHandle", mode: int, spikes=None) -> dict:
+        """The reference's quantized_forward (quant.cpp:505-579) and its metrics;
+        spikes = (rate, gain, channels, salt) for its SpikeSettings."""
         images = np.ascontiguousarray(images, np.float64)
         B = images.size // self.dims.pix
         lq = np.zeros((B, self.dims.classes), np.float64)
         lf = np.zeros((B, self.dims.classes), np.float64)
         mse, agree = C.c_double(), _SZ()
         lm = np.zeros(self.dims.blocks * len(self.orders), np.float64)
-        self.chk._check(self.chk.lib.ref_pin_quant_eval(self.h, calib.h, mode, _ptr(images), B, _ptr(lq), _ptr(lf),
-                                                        C.byref(mse), C.byref(agree), _ptr(lm)))
+        if spikes is not None:
+            self.chk._check(self.chk.lib.ref_pin_quant_eval_spiked(self.h, calib.h, mode, _ptr(images), B, _ptr(lq),
+                                                                   _ptr(lf), C.byref(mse), C.byref(agree), _ptr(lm),
+                                                                   *spikes))
+        else:
+            self.chk._check(self.chk.lib.ref_pin_quant_eval(self.h, calib.h, mode, _ptr(images), B, _ptr(lq),
+                                                            _ptr(lf), C.byref(mse), C.byref(agree), _ptr(lm)))
         return dict(logits_q=lq, logits_fp=lf, logits_mse=mse.value, argmax_agree=agree.value, layer_mse=lm)
 
     def ref_save_calibration(self, calib: "CalibHandle", directory: str) -> None:

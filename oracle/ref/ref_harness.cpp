@@ -304,9 +304,10 @@ int ref_pin_quantized_forward(void* m, void* c, int mode, const double* images, 
 
 // quantized_forward (quant.cpp:505-579) with its metrics: logits_mse, argmax
 // agreement and the teacher-forced per-(block, dir) scan MSE (no spikes).
-int ref_pin_quant_eval(void* m, void* c, int mode, const double* images, std::size_t B, double* logits_q,
-                       double* logits_fp, double* logits_mse, std::size_t* argmax_agree, double* layer_mse) {
-    return guarded([&] {
+static void quant_eval_impl(void* m, void* c, int mode, const double* images, std::size_t B, double* logits_q,
+                            double* logits_fp, double* logits_mse, std::size_t* argmax_agree, double* layer_mse,
+                            const ouro::SpikeSettings& spikes) {
+    {
         const oro::ModelW& w = static_cast<ModelH*>(m)->w;
         const oro::Calib& k = static_cast<CalibH*>(c)->c;
         ouro::ToyVmmModel rm = oro::to_ref(w);
@@ -333,12 +334,34 @@ int ref_pin_quant_eval(void* m, void* c, int mode, const double* images, std::si
         ouro::QuantMode qm = mode == 1 ? ouro::QuantMode::Dynamic
                                        : (mode == 2 ? ouro::QuantMode::Static : ouro::QuantMode::Bypass);
         ouro::QuantEvalResult r = ouro::quantized_forward(rm, std::vector<double>(images, images + B * pix), B, cr, qm,
-                                                          ouro::SpikeSettings{});
+                                                          spikes);
         std::memcpy(logits_q, r.logits_q.data(), r.logits_q.size() * sizeof(double));
         std::memcpy(logits_fp, r.logits_fp.data(), r.logits_fp.size() * sizeof(double));
         *logits_mse = r.logits_mse;
         *argmax_agree = r.argmax_agree;
         for (std::size_t i = 0; i < r.layer_mse.size(); ++i) layer_mse[i] = r.layer_mse[i].second;
+    }
+}
+
+int ref_pin_quant_eval(void* m, void* c, int mode, const double* images, std::size_t B, double* logits_q,
+                       double* logits_fp, double* logits_mse, std::size_t* argmax_agree, double* layer_mse) {
+    return guarded([&] {
+        quant_eval_impl(m, c, mode, images, B, logits_q, logits_fp, logits_mse, argmax_agree, layer_mse,
+                        ouro::SpikeSettings{});
+    });
+}
+
+// quantized_forward with SpikeSettings (quant.hpp:105-110, SpikeHook quant.cpp:420-446).
+int ref_pin_quant_eval_spiked(void* m, void* c, int mode, const double* images, std::size_t B, double* logits_q,
+                              double* logits_fp, double* logits_mse, std::size_t* argmax_agree, double* layer_mse,
+                              double rate, double gain, std::size_t channels, std::uint64_t salt) {
+    return guarded([&] {
+        ouro::SpikeSettings sp;
+        sp.rate = rate;
+        sp.gain = gain;
+        sp.channels = channels;
+        sp.salt = salt;
+        quant_eval_impl(m, c, mode, images, B, logits_q, logits_fp, logits_mse, argmax_agree, layer_mse, sp);
     });
 }
 

@@ -7,8 +7,8 @@ operator API (``/root/reference/proj/src/ouro/{quant,gemm,ssm}.hpp``).
 """
 from ._lib import (MODE_DYNAMIC, MODE_FP, MODE_STATIC, POST_BIAS, POST_INPROJ, POST_RESID, POST_STORE, SRC_MERGE,
                    SRC_PLAIN, SRC_RMSNORM, IoError, NumericError, OuroError, ValidationError, load)
-from .runtime import Calibration, Context, Dims, Model, QuantSpec, TensorCal, Trace
+from .runtime import Calibration, Context, Dims, Model, QuantSpec, SpikeSettings, TensorCal, Trace
 
-__all__ = ["Context", "Model", "Calibration", "TensorCal", "QuantSpec", "Dims", "Trace", "load", "OuroError",
+__all__ = ["Context", "Model", "Calibration", "TensorCal", "QuantSpec", "SpikeSettings", "Dims", "Trace", "load", "OuroError",
            "ValidationError", "NumericError", "IoError", "MODE_FP", "MODE_DYNAMIC", "MODE_STATIC", "POST_STORE", "POST_INPROJ",
            "POST_RESID", "POST_BIAS", "SRC_PLAIN", "SRC_RMSNORM", "SRC_MERGE"]

@@ -60,6 +60,9 @@ _SIGS = {
     "ouro_b200_detect_quantize_planes": ([_P, _P, _SZ, _SZ, _SZ, _D, _P, _SZ, C.c_uint, C.c_uint, _SZ, _P, _P, _P,
                                           _P, _P, _P, _P], _I),
     "ouro_b200_refresh_sweep": ([_P, _P, _P, _P], _I),
+    "ouro_b200_model_set_spikes": ([_P, _P], _I),
+    "ouro_b200_quant_scan_spiked": ([_P, _SZ, _SZ, _SZ, _SZ, _I, _I, _P, _P, _P, _P, _P, _I, _SZ, C.c_uint, C.c_uint,
+                                     _P, _P, _P, _P, _SZ, _SZ, _SZ], _I),
     "ouro_b200_gemm_bench": ([_P, _P, _P], _I),
     "ouro_b200_calib_save": ([_P, _P, C.c_char_p], _I),
     "ouro_b200_model_get_qweight": ([_P, C.c_char_p, C.c_uint, _P, C.c_size_t, C.POINTER(C.c_size_t)], _I),
@@ -109,6 +112,11 @@ def load(path: str = SO_PATH):
         fn.restype = res
     _lib = lib
     return lib
+
+
+class Spikes(C.Structure):
+    """ouro_b200_spikes (SpikeSettings, quant.hpp:105-110)."""
+    _fields_ = [("rate", C.c_double), ("gain", C.c_double), ("channels", C.c_size_t), ("salt", C.c_uint64)]
 
 
 class SweepSettings(C.Structure):

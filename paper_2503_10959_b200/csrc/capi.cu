@@ -194,42 +194,80 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
     });
 }
 
+static void quant_scan_impl(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order, int grid,
+                            const double* u, const double* proj, const double* a, const double* b_delta, double* o,
+                            int mode, size_t n_refresh, unsigned act_bits, unsigned outlier_bits, const double* theta,
+                            const double* const* s_in, const double* const* s_full, const uint8_t* literal,
+                            int force_literal, uint8_t* masks, const ob::SpikeCfg& spike) {
+    require(ctx && u && proj && a && b_delta && o, "quant_scan: NULL argument");
+    require(N == 16, "quant_scan: this build keeps N = 16 states per channel");
+    require(mode == ob::MODE_FP || (theta && s_in && s_full), "quant_scan: quantized modes need calibration");
+    ob::ScanParams p;
+    p.S = static_cast<int>(S);
+    p.T = static_cast<int>(T);
+    p.E = static_cast<int>(E);
+    p.N = static_cast<int>(N);
+    p.order = order;
+    p.grid = grid;
+    p.u = u;
+    p.proj = proj;
+    p.a = a;
+    p.b_delta = b_delta;
+    p.o = o;
+    p.mode = mode;
+    p.n_refresh = static_cast<int>(n_refresh);
+    p.abits = act_bits;
+    p.obits = outlier_bits;
+    if (mode != ob::MODE_FP)
+        for (int k = 0; k < 3; ++k) {
+            p.cal[k].theta = theta[k];
+            p.cal[k].s_in = s_in[k];
+            p.cal[k].s_full = s_full[k];
+        }
+    p.literal = literal;
+    p.literal_any = literal != nullptr ? 1 : 0;
+    p.force_literal = force_literal;
+    p.masks = masks;
+    p.spike = spike;
+    ob::cuda_check(ob::launch_scan(p, ctx->c->stream, nullptr), "quant_scan");
+}
+
+static ob::SpikeCfg spike_from(const ouro_b200_spikes* sp) {
+    ob::SpikeCfg c;
+    if (sp == nullptr || !(sp->rate > 0.0)) return c;
+    require(sp->channels >= 1 && sp->channels <= static_cast<size_t>(ob::kMaxSpikeChannels),
+            "spikes: channels must be in [1, 64]");
+    c.rate = sp->rate;
+    c.gain = sp->gain;
+    c.channels = static_cast<int>(sp->channels);
+    c.salt = sp->salt;
+    return c;
+}
+
 ouro_status ouro_b200_quant_scan(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order, int grid,
                                  const double* u, const double* proj, const double* a, const double* b_delta,
                                  double* o, int mode, size_t n_refresh, unsigned act_bits, unsigned outlier_bits,
                                  const double* theta, const double* const* s_in, const double* const* s_full,
                                  const uint8_t* literal, int force_literal, uint8_t* masks) {
     return guarded([&] {
-        require(ctx && u && proj && a && b_delta && o, "quant_scan: NULL argument");
-        require(N == 16, "quant_scan: this build keeps N = 16 states per channel");
-        require(mode == ob::MODE_FP || (theta && s_in && s_full), "quant_scan: quantized modes need calibration");
-        ob::ScanParams p;
-        p.S = static_cast<int>(S);
-        p.T = static_cast<int>(T);
-        p.E = static_cast<int>(E);
-        p.N = static_cast<int>(N);
-        p.order = order;
-        p.grid = grid;
-        p.u = u;
-        p.proj = proj;
-        p.a = a;
-        p.b_delta = b_delta;
-        p.o = o;
-        p.mode = mode;
-        p.n_refresh = static_cast<int>(n_refresh);
-        p.abits = act_bits;
-        p.obits = outlier_bits;
-        if (mode != ob::MODE_FP)
-            for (int k = 0; k < 3; ++k) {
-                p.cal[k].theta = theta[k];
-                p.cal[k].s_in = s_in[k];
-                p.cal[k].s_full = s_full[k];
-            }
-        p.literal = literal;
-        p.literal_any = literal != nullptr ? 1 : 0;
-        p.force_literal = force_literal;
-        p.masks = masks;
-        ob::cuda_check(ob::launch_scan(p, ctx->c->stream, nullptr), "quant_scan");
+        quant_scan_impl(ctx, S, T, E, N, order, grid, u, proj, a, b_delta, o, mode, n_refresh, act_bits,
+                        outlier_bits, theta, s_in, s_full, literal, force_literal, masks, ob::SpikeCfg{});
+    });
+}
+
+ouro_status ouro_b200_quant_scan_spiked(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order,
+                                        int grid, const double* u, const double* proj, const double* a,
+                                        const double* b_delta, double* o, int mode, size_t n_refresh,
+                                        unsigned act_bits, unsigned outlier_bits, const double* theta,
+                                        const double* const* s_in, const double* const* s_full,
+                                        const ouro_b200_spikes* spikes, size_t block, size_t dir, size_t sample0) {
+    return guarded([&] {
+        ob::SpikeCfg c = spike_from(spikes);
+        c.block = static_cast<int>(block);
+        c.dir = static_cast<int>(dir);
+        c.sample0 = static_cast<int>(sample0);
+        quant_scan_impl(ctx, S, T, E, N, order, grid, u, proj, a, b_delta, o, mode, n_refresh, act_bits,
+                        outlier_bits, theta, s_in, s_full, nullptr, 0, nullptr, c);
     });
 }
 
@@ -575,6 +613,21 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
             }
         }
         ob::cuda_check(cudaStreamSynchronize(st), "forward_host sync");
+    });
+}
+
+ouro_status ouro_b200_model_set_spikes(ouro_b200_model* m, const ouro_b200_spikes* spikes) {
+    return guarded([&] {
+        require(m != nullptr, "model_set_spikes: model is NULL");
+        m->m->spikes = spike_from(spikes);
+        if (m->exec) {
+            cudaGraphExecDestroy(m->exec);
+            m->exec = nullptr;
+        }
+        if (m->hexec) {
+            cudaGraphExecDestroy(m->hexec);
+            m->hexec = nullptr;
+        }
     });
 }
 

@@ -641,7 +641,12 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         bool lit = false;
         tick_begin(FAM_K3);
         const bool fast_ok = quant && cal->spec.obits == 8 && (cal->spec.abits == 4 || cal->spec.abits == 8);
-        if (fast_ok && !any_literal && scan_variant != 1) {
+        for (int dd = 0; dd < nd; ++dd) {  // SpikeHook runs in the reference-form kernel
+            sps[dd].spike = spikes;
+            sps[dd].spike.block = b;
+            sps[dd].spike.dir = dd;
+        }
+        if (fast_ok && !any_literal && scan_variant != 1 && !(spikes.rate > 0.0)) {
             cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant == 2 ? 1 : 0), "scan");
         } else {
             for (int dd = 0; dd < nd; ++dd) {

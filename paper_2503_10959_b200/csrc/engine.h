@@ -150,6 +150,7 @@ class Model {
     void quantize(unsigned bits);
     bool fp_dirty = true;
     int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
+    SpikeCfg spikes;       // SpikeHook settings (rate 0 = off); block/dir set per scan
     int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only
 
     // workspace

@@ -76,6 +76,39 @@ __device__ __forceinline__ void quant_row(double (&x)[N], bool& in, int kind, in
         p.masks[((static_cast<size_t>(kind) * p.S + s) * p.T + t) * p.E + i] = in ? 1 : 0;
 }
 
+// SpikeHook::spikes_at (quant.cpp:420-439): the step spikes with probability
+// `rate` from a mix64 chain over (salt, sample, block, dir, t); the channels are
+// the first min(channels, E) distinct picks of a further mix64 chain.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // quant.cpp:20-25
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ bool spike_hits(const SpikeCfg& sp, uint64_t sample, uint64_t t, uint64_t e, uint64_t ch) {
+    uint64_t key = sp.salt;
+    key = mix64(key ^ (0x5151ull + sample));
+    key = mix64(key ^ (static_cast<uint64_t>(sp.block) * 131ull + static_cast<uint64_t>(sp.dir)));
+    key = mix64(key ^ t);
+    const double u = static_cast<double>(key >> 11) * 0x1.0p-53;
+    if (u >= sp.rate) return false;
+    uint64_t picks[kMaxSpikeChannels];
+    const uint64_t want = min(static_cast<uint64_t>(sp.channels), e);
+    uint64_t n = 0, pick = key;
+    bool hit = false;
+    while (n < want) {
+        pick = mix64(pick);
+        const uint64_t c = pick % e;
+        bool dup = false;
+        for (uint64_t j = 0; j < n; ++j) dup |= picks[j] == c;
+        if (!dup) {
+            picks[n++] = c;
+            hit |= c == ch;
+        }
+    }
+    return hit;
+}
+
 template <bool LITERAL, int N>
 __global__ void __launch_bounds__(LITERAL ? 1024 : 128) k3_scan(const ScanParams p) {
     __shared__ double red[32];
@@ -105,6 +138,12 @@ __global__ void __launch_bounds__(LITERAL ? 1024 : 128) k3_scan(const ScanParams
             a[m] = gl::exp(dmul(delta, A[m]));
             b[m] = dmul(delta, __ldg(pr + E + m));
         }
+        if (p.spike.rate > 0.0 && active &&
+            spike_hits(p.spike, static_cast<uint64_t>(p.spike.sample0 + s), static_cast<uint64_t>(t),
+                       static_cast<uint64_t>(E), static_cast<uint64_t>(i))) {
+#pragma unroll
+            for (int m = 0; m < N; ++m) b[m] = dmul(b[m], p.spike.gain);  // SpikeHook::on_inputs, before QuantHook
+        }
         quant_row<LITERAL, N>(a, inA, 0, t, p, i, active, lit, qa, qo, red, s);
         quant_row<LITERAL, N>(b, inB, 1, t, p, i, active, lit, qa, qo, red, s);
 #pragma unroll
@@ -119,6 +158,7 @@ __global__ void __launch_bounds__(LITERAL ? 1024 : 128) k3_scan(const ScanParams
 
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal) {
     if (p.N != 16 || p.E < 1 || p.T < 1 || p.S < 1) return cudaErrorInvalidValue;
+    if (p.spike.rate > 0.0 && (p.spike.channels < 1 || p.spike.channels > kMaxSpikeChannels)) return cudaErrorInvalidValue;
     bool lit = false;
     if (p.mode == MODE_DYNAMIC) {
         lit = p.force_literal != 0 || (p.literal != nullptr && p.literal_any != 0);

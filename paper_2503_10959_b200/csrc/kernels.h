@@ -143,6 +143,17 @@ struct ScanKindCal {
     const double* inv_full = nullptr;
     unsigned long long* peaks = nullptr;  // calibration recording [T][E] (FP mode)
 };
+// SpikeHook (quant.cpp:420-446): at seeded (sample, block, dir, t) positions,
+// multiply `channels` hashed channels' b_bar by `gain`, before quantization.
+struct SpikeCfg {
+    double rate = 0.0;  // 0 = off
+    double gain = 100.0;
+    int channels = 1;   // <= kMaxSpikeChannels
+    uint64_t salt = 0;
+    int block = 0, dir = 0;
+    int sample0 = 0;    // global index of this launch's sample 0
+};
+constexpr int kMaxSpikeChannels = 64;
 struct ScanParams {
     int S = 0, T = 0, E = 0, N = 0;
     int order = 0, grid = 0;          // scan order of this direction
@@ -157,6 +168,7 @@ struct ScanParams {
     int literal_any = 0;              // host summary of `literal`
     int force_literal = 0;
     uint8_t* masks = nullptr;         // optional [3][S][T][E] O(t) after detection (parity)
+    SpikeCfg spike;                   // reference-form kernel only (launch_scan)
 };
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
 // Fast path (dynamic/static, channel-local detector): all directions in one launch.

@@ -7,6 +7,7 @@ the boundary.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -227,11 +228,19 @@ class Context:
 
     def quant_scan(self, *, S, T, E, order, grid, u, proj, a, b_delta, o, mode, n_refresh=10, act_bits=8,
                    outlier_bits=8, theta=None, s_in=None, s_full=None, literal=None, force_literal=False,
-                   masks=None):
-        """K3 for one direction. theta: 3 floats; s_in/s_full: 3 device tensors each."""
+                   masks=None, spikes: "SpikeSettings | None" = None, block=0, dir=0, sample0=0):
+        """K3 for one direction. theta: 3 floats; s_in/s_full: 3 device tensors each.
+        spikes: SpikeHook settings, placed at (sample0 + s, block, dir, t)."""
         th = (C.c_double * 3)(*(theta or (0.0, 0.0, 0.0)))
         si = (C.c_void_p * 3)(*[t.data_ptr() for t in s_in]) if s_in is not None else None
         sf = (C.c_void_p * 3)(*[t.data_ptr() for t in s_full]) if s_full is not None else None
+        if spikes is not None:
+            sp = L.Spikes(spikes.rate, spikes.gain, spikes.channels, spikes.salt)
+            L.check(self.lib.ouro_b200_quant_scan_spiked(
+                self.h, S, T, E, 16, order, grid, _ptr(u), _ptr(proj), _ptr(a), _ptr(b_delta), _ptr(o), mode,
+                n_refresh, act_bits, outlier_bits, th if theta is not None else None, si, sf, C.byref(sp), block, dir,
+                sample0))
+            return o
         L.check(self.lib.ouro_b200_quant_scan(
             self.h, S, T, E, 16, order, grid, _ptr(u), _ptr(proj), _ptr(a), _ptr(b_delta), _ptr(o), mode, n_refresh,
             act_bits, outlier_bits, th if theta is not None else None, si, sf, _ptr(literal), int(force_literal),
@@ -247,6 +256,16 @@ class Context:
         L.check(self.lib.ouro_b200_dgemm(self.h, M, R, K, _ptr(a), a.stride(0), _ptr(w), post, _ptr(out),
                                          out.shape[1], _ptr(out2), split, _ptr(bias)))
         return out
+
+
+@dataclasses.dataclass
+class SpikeSettings:
+    """SpikeSettings (quant.hpp:105-110): per (sample, block, dir, step) probability
+    `rate` of multiplying `channels` hashed channels' b_bar by `gain`."""
+    rate: float = 0.0
+    gain: float = 100.0
+    channels: int = 1
+    salt: int = 0
 
 
 class Calibration:
@@ -450,12 +469,28 @@ class Model:
         L.check(self.lib.ouro_b200_model_get_qweight(self.h, name.encode(), bits, _ptr(out), n.value, C.byref(n)))
         return out
 
-    def quant_eval(self, images: np.ndarray, calib: Calibration, mode: int, *, d1=True, d2=True) -> dict:
+    def set_spikes(self, spikes: "SpikeSettings | None") -> None:
+        """SpikeHook for every later forward / trace (None or rate 0 = off)."""
+        sp = L.Spikes(spikes.rate, spikes.gain, spikes.channels, spikes.salt) if spikes is not None else None
+        L.check(self.lib.ouro_b200_model_set_spikes(self.h, C.byref(sp) if sp is not None else None))
+
+    def quant_eval(self, images: np.ndarray, calib: Calibration, mode: int, *, d1=True, d2=True,
+                   spikes: "SpikeSettings | None" = None) -> dict:
         """quantized_forward (quant.cpp:505-579) on the GPU: the FP pass and the
         quantized pass over host images, logits_mse over all logits, argmax
         agreement, and the teacher-forced scan-output MSE per (block, dir) -- each
         direction's quantized scan re-run on the FP pass's own scan input with the
-        W4 x_proj weights (quant.cpp:548-577). Spike injection is not modelled."""
+        W4 x_proj weights (quant.cpp:548-577). spikes: the SpikeHook of all three
+        passes (rate 0 / None = off)."""
+        if spikes is not None and spikes.rate > 0.0:
+            self.set_spikes(spikes)
+            try:
+                return self._quant_eval(images, calib, mode, d1, d2, spikes)
+            finally:
+                self.set_spikes(None)
+        return self._quant_eval(images, calib, mode, d1, d2, None)
+
+    def _quant_eval(self, images, calib, mode, d1, d2, spikes):
         import torch
         images = np.ascontiguousarray(images, np.float64)
         d = self.dims
@@ -474,7 +509,11 @@ class Model:
             u = tr.get("u", np.float64).reshape(S, T, E)
             for k, order in enumerate(self.orders):
                 perm = _scan_perm(order, T, d.grid)
-                w = tdev(self.qweight(f"block{b}.dir{k}.xp", calib.spec.wbits).reshape(E + 2 * N, E))
+                # bypass re-scans with the unquantized model (quant.cpp:519-520: qmodel = model)
+                pd = f"block{b}.dir{k}."
+                wx = (np.concatenate([self.get_tensor(pd + n) for n in ("w_delta", "w_b", "w_c")]) if mode == L.MODE_FP
+                      else self.qweight(pd + "xp", calib.spec.wbits))
+                w = tdev(np.asarray(wx).reshape(E + 2 * N, E))
                 proj = self.ctx.dgemm(tdev(u[:, perm, :].reshape(S * T, E)), w)  # k-ascending dots, as s6_scan
                 o_tf = torch.empty(S * T * E, dtype=torch.float64, device=dev)
                 tabs = [scan[(b * nd + k) * 3 + q] for q in range(3)]
@@ -483,7 +522,8 @@ class Model:
                                     b_delta=tdev(self.get_tensor(f"block{b}.dir{k}.b_delta")), o=o_tf, mode=mode,
                                     n_refresh=calib.spec.n_refresh, act_bits=calib.spec.abits,
                                     outlier_bits=calib.spec.obits, theta=[t.theta for t in tabs],
-                                    s_in=[tdev(t.s_in) for t in tabs], s_full=[tdev(t.s_full) for t in tabs])
+                                    s_in=[tdev(t.s_in) for t in tabs], s_full=[tdev(t.s_full) for t in tabs],
+                                    spikes=spikes, block=b, dir=k)
                 e = tr.get(f"dir{k}.o", np.float64) - o_tf.cpu().numpy()
                 out["layer_mse"].append((f"block{b}.dir{k}", float(np.sum(e * e) / e.size)))
         return out

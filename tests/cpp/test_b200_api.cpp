@@ -256,9 +256,36 @@ TEST_CASE("quantized_forward on the GPU == reference quantized_forward (logits a
                   1e-12 * want.layer_mse[l].second + 1e-300);
         }
     }
-    ouro_b200::SpikeSettings sp;
-    sp.rate = 0.1;
-    CHECK_THROWS_AS(ouro_b200::quantized_forward(*gm, img, 4, to_gpu(cal), ouro_b200::QuantMode::Dynamic, sp),
+    // SpikeHook in every pass (FP, quantized, teacher-forced), bit for bit
+    const double rates[] = {0.2, 0.5};
+    const size_t chans[] = {1, 3};
+    for (int j = 0; j < 2; ++j) {
+        ouro::SpikeSettings rsp;
+        rsp.rate = rates[j];
+        rsp.gain = 50.0;
+        rsp.channels = chans[j];
+        rsp.salt = 11;
+        ouro_b200::SpikeSettings gsp;
+        gsp.rate = rates[j];
+        gsp.gain = 50.0;
+        gsp.channels = chans[j];
+        gsp.salt = 11;
+        for (int i = 0; i < 3; ++i) {
+            ouro::QuantEvalResult want = ouro::quantized_forward(rm, img, 4, cal, rmodes[i], rsp);
+            ouro_b200::QuantEvalResult got = ouro_b200::quantized_forward(*gm, img, 4, to_gpu(cal), gmodes[i], gsp);
+            CHECK(same_bits(got.logits_fp, want.logits_fp));
+            CHECK(same_bits(got.logits_q, want.logits_q));
+            CHECK(got.argmax_agree == want.argmax_agree);
+            REQUIRE(got.layer_mse.size() == want.layer_mse.size());
+            for (size_t l = 0; l < want.layer_mse.size(); ++l)
+                CHECK(std::fabs(got.layer_mse[l].second - want.layer_mse[l].second) <=
+                      1e-12 * want.layer_mse[l].second + 1e-300);
+        }
+    }
+    ouro_b200::SpikeSettings bad;
+    bad.rate = 0.1;
+    bad.channels = 65;
+    CHECK_THROWS_AS(ouro_b200::quantized_forward(*gm, img, 4, to_gpu(cal), ouro_b200::QuantMode::Dynamic, bad),
                     ouro_b200::ValidationError);
 }
 
