@@ -74,10 +74,12 @@ __device__ __forceinline__ double2 k1_load2(const K1Params& p, size_t src, size_
 // away from theta and from half-integers; otherwise (and for outlier channels)
 // the exact f64 value is used. Bound: g and m rounded to f32 (2 x 2^-24),
 // the ex2 argument (3|g| 2^-24 relative in e), ex2.approx (2^-22), the
-// sigmoid's add and quotient (2 x 2^-24, doubled for g < 0 where e/(1+e)
-// carries e's error in full), two products: |vf/v - 1| <= (6|g| + 15) 2^-24;
-// the code adds 1/s rounded to f32 and one product. Below g = -80 ex2 flushes,
-// so those elements always take the exact path.
+// sigmoid's add (2^-24) and its quotient by __fdividef (2 ulp <= 4 x 2^-24 for
+// a denominator in [1, 2]), both doubled for g < 0 where e/(1+e) carries e's
+// error in full, two products: |vf/v - 1| <= (6|g| + 21) 2^-24, inside the
+// (6|g| + 24) 2^-24 the kernel uses; the code adds 1/s rounded to f32 and one
+// product. Below g = -80 ex2 flushes, so those elements always take the exact
+// path.
 struct MergeApprox {
     float v, eps;
 };
@@ -89,7 +91,7 @@ __device__ __forceinline__ MergeApprox merge_approx(double m, double g) {
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-ag * 1.44269504f));
     const float den = 1.0f + e;
-    const float sig = (gf >= 0.0f ? 1.0f : e) / den;
+    const float sig = __fdividef(gf >= 0.0f ? 1.0f : e, den);
     MergeApprox r;
     r.v = (mf * gf) * sig;
     if (m == 0.0 || g == 0.0) {  // v = +-0 exactly: code 0, never an outlier (frequent: all-zero h codes)
