@@ -42,8 +42,8 @@ template <int EW>
 struct K2Cfg {
     static constexpr int kEpiWarps = EW;
     static constexpr int kThreads = 128 + 32 * EW;
-    static constexpr int kStages = EW >= 16 ? 2 : 3;
-    static constexpr int kMaskWords = EW >= 16 ? 24 : 32;  // mask words per row staged in shared memory
+    static constexpr int kStages = EW >= 16 ? 2 : 4;
+    static constexpr int kMaskWords = 24;  // mask words per row staged in shared memory (K <= 768; else global)
 };
 
 template <int BN, int EW>
