@@ -123,6 +123,9 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
                 "detect_quantize: bit widths must satisfy 2 <= act <= outlier <= 8");
         require(src != ob::K1_SRC_MERGE || gate != nullptr, "detect_quantize: merge source needs the gate");
         require(src >= 0 && src <= 2, "detect_quantize: unknown source");
+        require(order >= -1 && order <= 3, "detect_quantize: order must be -1 (identity) or a scan order 0-3");
+        require(order < 2 || (grid >= 1 && static_cast<size_t>(grid) * grid == T),
+                "detect_quantize: column scan orders need T = grid^2");
         ob::K1Params k;
         k.S = static_cast<int>(S);
         k.T = static_cast<int>(T);
@@ -202,6 +205,9 @@ static void quant_scan_impl(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, si
     require(ctx && u && proj && a && b_delta && o, "quant_scan: NULL argument");
     require(N == 16, "quant_scan: this build keeps N = 16 states per channel");
     require(mode == ob::MODE_FP || (theta && s_in && s_full), "quant_scan: quantized modes need calibration");
+    require(order >= 0 && order <= 3, "quant_scan: order must be a scan order 0-3");
+    require(order < 2 || (grid >= 1 && static_cast<size_t>(grid) * grid == T),
+            "quant_scan: column scan orders need T = grid^2");
     ob::ScanParams p;
     p.S = static_cast<int>(S);
     p.T = static_cast<int>(T);

@@ -95,6 +95,12 @@ __host__ __device__ __forceinline__ int scan_perm(int order, int t, int grid) {
     }
 }
 
+// Canonical row of scan step t for a sequence of T steps: identity (order <= 0),
+// row-backward T-1-t (order 1), or the column orders of scan_perm (T = grid^2).
+__host__ __device__ __forceinline__ int row_at(int order, int t, int T, int grid) {
+    return order <= 0 ? t : (order == 1 ? T - 1 - t : scan_perm(order, t, grid));
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

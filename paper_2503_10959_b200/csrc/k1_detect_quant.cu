@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
     int next_ref = (dyn && p.n_refresh > 0) ? t0 + p.n_refresh : 0x7fffffff;
     unsigned in = 0;  // bit k: channel ch+k is in O
     for (int t = t0; t < t1; ++t) {
-        const int crow = p.order <= 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid));
+        const int crow = row_at(p.order, t, T, p.grid);
         const size_t cg = static_cast<size_t>(s) * T + crow;
         const size_t row = static_cast<size_t>(s) * T + t;
         double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -247,7 +247,7 @@ struct K1Dirs {
 };
 
 __device__ __forceinline__ int k1_row_of(const K1Params& p, int t) {
-    return p.order <= 0 ? t : (p.order == 1 ? p.T - 1 - t : scan_perm(p.order, t, p.grid));
+    return row_at(p.order, t, p.T, p.grid);
 }
 
 template <int SRC>
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256) k1_literal(const K1Params p) {
     unsigned inmask = 0;  // bit j: channel j*32+lane is in O
 
     for (int t = t0; t < t1; ++t) {
-        const int crow = p.order < 0 ? t : scan_perm(p.order, t, p.grid);
+        const int crow = row_at(p.order, t, p.T, p.grid);
         const size_t src = (static_cast<size_t>(s) * p.T + crow) * E;
         const size_t row = static_cast<size_t>(s) * p.T + t;
         double v[JMAX];

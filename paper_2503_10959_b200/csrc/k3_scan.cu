@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(LITERAL ? 1024 : 128) k3_scan(const ScanParams
     const double bd = active ? p.b_delta[i] : 0.0;
     bool inA = false, inB = false, inH = false;
     for (int t = 0; t < T; ++t) {
-        const int c = scan_perm(p.order, t, p.grid);
+        const int c = row_at(p.order, t, T, p.grid);
         const double* pr = p.proj + (static_cast<size_t>(s) * T + t) * P;
         const double dpre = active ? pr[i] : 0.0;
         const double uv = active ? p.u[(static_cast<size_t>(s) * T + c) * E + i] : 0.0;

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         ss.invShf = __double2float_rn(ih ? ih[t] : __ddiv_rn(1.0, Sh));
         ss.LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(Sa))));
         ss.keep = refresh_at(t, p.n_refresh) ? 0 : ~0;
-        ss.ocol = scan_perm(p.order, t, p.grid) * p.E;
+        ss.ocol = row_at(p.order, t, p.T, p.grid) * p.E;
         const float qa1 = static_cast<float>((1 << (p.abits - 1)) - 1) + 1.0f;
         ss.hA1 = qa1 * ss.LA;
         ss.hA0 = 0.5f - fmaf(qa1, fmaf(ss.LA, 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
         for (int k = 0; k < kChunk / 2; ++k) {
             const int tt = (lane >> 4) + 2 * k, t = min(t0 + tt, T - 1);
             const bool ok = tt < nt && sic < E;
-            const int cr = p.order == 0 ? t : (p.order == 1 ? T - 1 - t : scan_perm(p.order, t, p.grid));
+            const int cr = row_at(p.order, t, T, p.grid);
             cp_async8(&sh.dp[buf][tt][sc], proj + (static_cast<size_t>(s) * T + t) * P2 + (ok ? sic : 0), ok);
             cp_async8(&sh.u[buf][tt][sc], uin + (static_cast<size_t>(s) * T + cr) * E + (ok ? sic : 0), ok);
         }

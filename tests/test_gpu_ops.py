@@ -199,3 +199,19 @@ def test_detect_quantize_merge_edges(gpu_ctx, seed):
     m = _unpack(a["omask"], E).astype(bool)
     assert m.any() and (~m).any()
     assert np.array_equal(a["ocode"][m], b["ocode"][m]) and np.array_equal(a["oscale"][m], b["oscale"][m])
+
+
+def test_scan_order_geometry_validated(gpu_ctx):
+    """Column scan orders need T = grid^2; orders outside -1..3 are rejected
+    (detect_quantize) before any kernel runs."""
+    import torch
+    import paper_2503_10959_b200 as ob
+    x = torch.zeros(1, 10, 32, dtype=torch.float64, device="cuda")
+    s = torch.ones(10, dtype=torch.float64, device="cuda")
+    kw = dict(S=1, T=10, E=32, theta=1.0, s_in=s, s_full=s, n_refresh=2, act_bits=4, outlier_bits=8)
+    with pytest.raises(ob.ValidationError, match="T = grid"):
+        gpu_ctx.detect_quantize(x, order=2, grid=3, **kw)
+    with pytest.raises(ob.ValidationError, match="order"):
+        gpu_ctx.detect_quantize(x, order=5, grid=0, **kw)
+    gpu_ctx.detect_quantize(x, order=1, grid=0, **kw)  # row orders need no grid
+    torch.cuda.synchronize()

@@ -266,3 +266,57 @@ def test_vim_t_s_widths(oracle_checker, gpu_ctx, embed, abits):
     b = gm.forward_host(imgs, gcal, 1)
     gm.set_option("scan_variant", 0)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("orders,n_refresh", [((2, 3), 4), ((1, 2), 0), ((3,), 5), ((0, 1), 0)])
+def test_scan_orders_and_refresh_windows(oracle_checker, gpu_ctx, orders, n_refresh):
+    """Column scan orders (scan_perm, ssm.cpp:30-46), a single direction and
+    never-refreshing windows (n_refresh 0: the staged K1's row ring refills
+    across the whole sequence; the x_proj K1 pair runs unmirrored for orders
+    other than (0, 1)): FP and quantized logits bit-identical to the oracle."""
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    dims = dict(image=48, channels=3, patch=8, embed=96, state=16, blocks=2, classes=10, conv_width=4)
+    od = O.Dims(**dims)
+    om = oracle_checker.model(od, SEED, orders=orders)
+    gm = ob.Model(gpu_ctx, ob.Dims(**dims), SEED, orders=orders)
+    imgs = oracle_checker.normal(41, 2 * od.pix).reshape(2, od.image, od.image, od.channels)
+    cimgs = oracle_checker.normal(42, 2 * od.pix).reshape(2, od.image, od.image, od.channels)
+    assert rel_err(gm.forward_host(imgs, None, 0), om.forward(imgs, None, 0)) <= RTOL_F64
+    for abits in (4, 8):
+        spec = _spec(abits, n_refresh=n_refresh, rho=0.02)
+        ocal = om.calibrate(cimgs, spec)
+        gcal = _import_calib(gm, ocal.export(), spec)
+        for mode in (1, 2):
+            assert rel_err(gm.forward_host(imgs, gcal, mode), om.forward(imgs, ocal, mode)) <= RTOL_F64, (abits, mode)
+
+
+@pytest.mark.parametrize("E,T,n_refresh,order,src", [(768, 197, 10, 1, 0), (1024, 60, 0, 2, 0), (32, 33, 7, 3, 1),
+                                                     (768, 50, 0, 1, 1), (256, 120, 25, 0, 1)])
+def test_staged_k1_equals_literal(gpu_ctx, E, T, n_refresh, order, src):
+    """The staged K1 (rows bulk-copied per refresh window, D1 factor from the
+    staged rows) == the literal detector kernel, at Vim-B widths, with a ring
+    that refills (n_refresh 0 or long windows) and every scan order."""
+    import torch
+    S = 2
+    rng = np.random.default_rng(E + T + order)
+    x = rng.normal(size=(S, T, E)) * (3.0 if src == 1 else 1.0)
+    x[rng.random((S, T, E)) < 0.01] *= 25.0
+    xd = torch.from_numpy(x).cuda()
+    s_in = torch.from_numpy(np.full(T, 0.35)).cuda()
+    grid = int(T ** 0.5) if order >= 2 else 0
+    if order >= 2:
+        T2 = grid * grid
+        xd, s_in, T = xd[:, :T2].contiguous(), s_in[:T2].contiguous(), T2
+    outs = []
+    for lit in (False, True):
+        r = gpu_ctx.detect_quantize(xd, S=S, T=T, E=E, theta=2.5, s_in=s_in, s_full=s_in, n_refresh=n_refresh,
+                                    act_bits=4, outlier_bits=8, mode=1, src=src, order=order, grid=grid, literal=lit)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in r.items()})
+    a, b = outs
+    for k in ("codes", "s_row", "ocnt", "omask"):
+        assert np.array_equal(a[k], b[k]), k
+    m = np.unpackbits(a["omask"].view(np.uint8), bitorder="little").reshape(S * T, -1)[:, :E].astype(bool)
+    assert m.any()
+    assert np.array_equal(a["ocode"][m], b["ocode"][m]) and np.array_equal(a["oscale"][m], b["oscale"][m])
