@@ -235,11 +235,13 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
 
 // Staged fast path. Per CTA: one (sample, refresh window) of one direction, all
 // E channels (blockDim = E/4 rounded to warps). Rows of `rc` steps per stage,
-// two stages: chunk c lands in stage c&1 by per-row bulk copies on an mbarrier;
-// chunk c+2 is issued once every thread has finished chunk c. 20 KB stages
+// kK1Stages stages: chunk c lands in stage c % kK1Stages by per-row bulk copies
+// on an mbarrier; chunk c + kK1Stages is issued once every thread has finished
+// chunk c. 20 KB stages
 // (rc = 3 rows at E = 768): 4 CTAs per SM; 32 KB stages (3 CTAs) measured
 // 175 / 120 us vs 155 / 113 us for the x_proj pair / in_proj.
 constexpr int kK1StageBytes = 20 * 1024;
+constexpr int kK1Stages = 2;  // 3 stages (fewer CTAs per SM) measured 165 / 117 us vs 155 / 113
 constexpr int kK1MaxRc = 16;
 struct K1Dirs {
     K1Params p[2];
@@ -255,10 +257,10 @@ __device__ __forceinline__ int k1_row_of(const K1Params& p, int t) {
 template <int SRC>
 __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs dirs) {
     extern __shared__ __align__(128) unsigned char k1_smem[];
-    double* stage = reinterpret_cast<double*>(k1_smem);  // [2][rc][E]
-    __shared__ uint64_t bar[2];
-    __shared__ int cnt[2][kK1MaxRc];     // |O(t)| of the chunk's rows
-    __shared__ double rsv[2][kK1MaxRc];  // D1 row factors of the chunk's rows
+    double* stage = reinterpret_cast<double*>(k1_smem);  // [kK1Stages][rc][E]
+    __shared__ uint64_t bar[kK1Stages];
+    __shared__ int cnt[kK1Stages][kK1MaxRc];     // |O(t)| of the chunk's rows
+    __shared__ double rsv[kK1Stages][kK1MaxRc];  // D1 row factors of the chunk's rows
     const int d = dirs.n == 2 ? static_cast<int>(blockIdx.y & 1) : 0;
     const K1Params& p = dirs.p[d];
     const int yy = dirs.n == 2 ? static_cast<int>(blockIdx.y >> 1) : static_cast<int>(blockIdx.y);
@@ -275,23 +277,20 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     const uint32_t row_bytes = static_cast<uint32_t>(E) * 8u;
 
     if (tid == 0) {
-        ptx::mbar_init(&bar[0], 1);
-        ptx::mbar_init(&bar[1], 1);
+        for (int b = 0; b < kK1Stages; ++b) ptx::mbar_init(&bar[b], 1);
         ptx::fence_barrier_init();
     }
-    if (tid < 2 * kK1MaxRc) cnt[tid / kK1MaxRc][tid % kK1MaxRc] = 0;
+    for (int i = tid; i < kK1Stages * kK1MaxRc; i += blockDim.x) cnt[i / kK1MaxRc][i % kK1MaxRc] = 0;
     __syncthreads();
     auto issue = [&](int c) {  // thread 0
-        const int buf = c & 1, ts = t0 + c * rc, te = min(t1, ts + rc);
+        const int buf = c % kK1Stages, ts = t0 + c * rc, te = min(t1, ts + rc);
         ptx::mbar_arrive_expect_tx(&bar[buf], static_cast<uint32_t>(te - ts) * row_bytes);
         for (int t = ts; t < te; ++t)
             ptx::bulk_g2s(stage + (static_cast<size_t>(buf) * rc + (t - ts)) * E,
                      p.x + (static_cast<size_t>(s) * T + k1_row_of(p, t)) * E, row_bytes, &bar[buf]);
     };
-    if (tid == 0) {
-        issue(0);
-        if (nchunks > 1) issue(1);
-    }
+    if (tid == 0)
+        for (int c = 0; c < kK1Stages && c < nchunks; ++c) issue(c);
 
     // every field the loop needs, read once (the direction's parameter block is
     // selected at run time)
@@ -311,9 +310,9 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     int next_ref = (dyn && n_refresh > 0) ? t0 + n_refresh : 0x7fffffff;
     unsigned in = 0;  // bit k: channel ch+k is in O
     for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1, ts = t0 + c * rc, te = min(t1, ts + rc);
+        const int buf = c % kK1Stages, ts = t0 + c * rc, te = min(t1, ts + rc);
         const double* sb = stage + static_cast<size_t>(buf) * rc * E;
-        ptx::mbar_wait(&bar[buf], static_cast<uint32_t>((c >> 1) & 1));
+        ptx::mbar_wait(&bar[buf], static_cast<uint32_t>((c / kK1Stages) & 1));
         if (SRC == K1_SRC_RMSNORM) {
             // 1/sqrt(mean(x^2) + 1e-6): 32 lane-strided partials (channel k -> partial
             // k%32, k ascending) combined by an xor butterfly (oracle/driver.hpp rmsnorm_row)
@@ -404,9 +403,9 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
             ocnt[static_cast<size_t>(s) * T + ts + tid] = cnt[buf][tid];
             cnt[buf][tid] = 0;
         }
-        if (tid == 0 && c + 2 < nchunks) {
+        if (tid == 0 && c + kK1Stages < nchunks) {
             ptx::fence_async_smem();  // generic-proxy reads of the stage before the async refill
-            issue(c + 2);
+            issue(c + kK1Stages);
         }
     }
 }
@@ -557,7 +556,7 @@ static cudaError_t launch_staged(const K1Dirs& dirs, cudaStream_t st) {
     const K1Params& p = dirs.p[0];
     const int nwin = (p.T + p.window - 1) / p.window;
     const int threads = ((p.E / 4 + 31) / 32) * 32;  // E <= 1024: one CTA covers every channel
-    const size_t smem = 2ull * dirs.rc * p.E * sizeof(double);
+    const size_t smem = static_cast<size_t>(kK1Stages) * dirs.rc * p.E * sizeof(double);
     cudaError_t e = ensure_smem_attr<k1_staged<SRC>>(static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     k1_staged<SRC><<<dim3(1, p.S * nwin * dirs.n), threads, smem, st>>>(dirs);
