@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--blocks", type=int, default=24)
     ap.add_argument("--abits", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-parts", type=int, default=None,
+                    help="independent sub-batches on their own streams (engine default 2)")
     return ap.parse_args()
 
 
@@ -202,6 +204,8 @@ def run_ours(args):
     images = torch.randn(B, dims.image, dims.image, dims.channels, dtype=torch.float64, device="cuda", generator=gen)
     logits = torch.empty(B, dims.classes, dtype=torch.float64, device="cuda")
     gathered = [torch.empty_like(logits) for _ in range(world)] if world > 1 else None
+    if args.split_parts is not None:
+        model.set_option("split_parts", args.split_parts)
     model.use_graphs(True)
 
     def step():

@@ -644,6 +644,9 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         if (k == "scan_variant") {
             require(value >= 0 && value <= 2, "model_set_option: scan_variant must be 0, 1 or 2");
             m->m->scan_variant = static_cast<int>(value);
+        } else if (k == "split_parts") {
+            require(value == 1 || value == 2 || value == 4, "model_set_option: split_parts must be 1, 2 or 4");
+            m->m->split_parts = static_cast<int>(value);
         } else if (k == "k1_variant") {
             require(value >= 0 && value <= 1, "model_set_option: k1_variant must be 0 or 1");
             m->m->k1_variant = static_cast<int>(value);

@@ -272,7 +272,18 @@ void Model::quantize(unsigned bits) {
     qbits = bits;
 }
 
-void Model::ensure_work(int S, bool trace) {
+Model::~Model() {
+    for (cudaEvent_t e : w.feed_events) cudaEventDestroy(e);
+    for (SplitPart& sp : parts) {
+        for (cudaEvent_t e : sp.w.feed_events) cudaEventDestroy(e);
+        if (sp.fork) cudaEventDestroy(sp.fork);
+        if (sp.join) cudaEventDestroy(sp.join);
+        if (sp.st) cudaStreamDestroy(sp.st);
+        if (sp.copy) cudaStreamDestroy(sp.copy);
+    }
+}
+
+void Model::ensure_work(Work& w, int S, bool trace) {
     const size_t L = d.tokens(), E = d.embed, N = d.state, nd = host.orders.size();
     const size_t rows = static_cast<size_t>(S) * L;
     w.S = std::max(w.S, S);
@@ -383,9 +394,50 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         const_cast<Calibration*>(cal)->upload(ctx->stream);
     }
     upload_fp();
+    const int np = std::min(split_parts, kMaxSplit);
+    const bool split = np > 1 && trace == nullptr && calib_peaks == nullptr && !timing.on && S >= np * kSplitMin;
+    if (!split) {
+        forward_impl(cal, mode, d1, d2, images, S, logits, trace, calib_peaks, feed, ctx->stream, w);
+        return;
+    }
+    const size_t pix = static_cast<size_t>(d.image) * d.image * d.channels;
+    for (int k = 1; k < np; ++k) {
+        SplitPart& sp = parts[k];
+        if (sp.st == nullptr) {
+            cuda_check(cudaStreamCreateWithFlags(&sp.st, cudaStreamNonBlocking), "split stream");
+            cuda_check(cudaStreamCreateWithFlags(&sp.copy, cudaStreamNonBlocking), "split copy stream");
+            cuda_check(cudaEventCreateWithFlags(&sp.fork, cudaEventDisableTiming), "split event");
+            cuda_check(cudaEventCreateWithFlags(&sp.join, cudaEventDisableTiming), "split event");
+        }
+        cuda_check(cudaEventRecord(sp.fork, ctx->stream), "split fork");
+        cuda_check(cudaStreamWaitEvent(sp.st, sp.fork, 0), "split fork");
+    }
+    for (int k = 0; k < np; ++k) {
+        const int s0 = static_cast<int>(static_cast<long>(S) * k / np);
+        const int s1 = static_cast<int>(static_cast<long>(S) * (k + 1) / np);
+        HostFeed f;
+        if (feed) {
+            f = *feed;
+            f.chunks = std::max(1, feed->chunks / np);
+            f.host = feed->host + static_cast<size_t>(s0) * pix;
+            if (k > 0) f.copy = parts[k].copy;  // every part's first chunk arrives early (they share PCIe)
+        }
+        forward_impl(cal, mode, d1, d2, images + static_cast<size_t>(s0) * pix, s1 - s0,
+                     logits + static_cast<size_t>(s0) * d.classes, nullptr, nullptr, feed ? &f : nullptr,
+                     k == 0 ? ctx->stream : parts[k].st, k == 0 ? w : parts[k].w);
+    }
+    for (int k = 1; k < np; ++k) {
+        cuda_check(cudaEventRecord(parts[k].join, parts[k].st), "split join");
+        cuda_check(cudaStreamWaitEvent(ctx->stream, parts[k].join, 0), "split join");
+    }
+}
+
+void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S,
+                         double* logits, TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed,
+                         cudaStream_t st, Work& w) {
+    const bool quant = mode != MODE_FP;
     const bool qlin = quant && d2;
-    ensure_work(S, trace != nullptr);
-    cudaStream_t st = ctx->stream;
+    ensure_work(w, S, trace != nullptr);
     const int L = d.tokens(), E = d.embed, N = d.state, nd = static_cast<int>(host.orders.size());
     const int P = E + 2 * N, nsites = nd + 2;
     const size_t rows = static_cast<size_t>(S) * L;
@@ -397,6 +449,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
     const size_t pix = static_cast<size_t>(d.image) * d.image * d.channels;
     const int nchunk = feed ? std::max(1, std::min(feed->chunks, S)) : 1;
     if (feed) {
+        auto& feed_events = w.feed_events;
         while (static_cast<int>(feed_events.size()) < nchunk + 1) {
             cudaEvent_t e;
             cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -410,13 +463,13 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
             cuda_check(cudaMemcpyAsync(const_cast<double*>(images) + s0 * pix, feed->host + s0 * pix,
                                        (s1 - s0) * pix * sizeof(double), cudaMemcpyHostToDevice, feed->copy),
                        "H2D images");
-            cuda_check(cudaEventRecord(feed_events[k], feed->copy), "feed event");
+            cuda_check(cudaEventRecord(w.feed_events[k], feed->copy), "feed event");
         }
     }
     for (int k = 0; k < nchunk; ++k) {
         const int s0 = static_cast<int>(static_cast<long>(S) * k / nchunk);
         const int s1 = static_cast<int>(static_cast<long>(S) * (k + 1) / nchunk);
-        if (feed) cuda_check(cudaStreamWaitEvent(st, feed_events[k], 0), "feed wait");
+        if (feed) cuda_check(cudaStreamWaitEvent(st, w.feed_events[k], 0), "feed wait");
         const size_t r0 = static_cast<size_t>(s0) * L, nr = static_cast<size_t>(s1 - s0) * L;
         tick_begin(FAM_AUX);
         cuda_check(launch_patch_gather(images + s0 * pix, w.patches.p + r0 * d.patch_vals(), s1 - s0, d.image,

@@ -121,6 +121,9 @@ void load_calibration_dir(Calibration& c, int state, const std::string& dir, boo
 class Model {
   public:
     Model(Context* ctx, HostModel hm);
+    ~Model();
+    Model(const Model&) = delete;
+    Model& operator=(const Model&) = delete;
     Context* ctx;
     HostModel host;
     Dims d;
@@ -165,8 +168,22 @@ class Model {
         DevBuf<uint8_t> scanned, masks, scan_steps;
         DevBuf<unsigned long long> peaks;
         DevBuf<int32_t> acc_in, acc_out;
+        std::vector<cudaEvent_t> feed_events;  // host-feed chunk events, created on first use
     } w;
-    void ensure_work(int S, bool trace);
+    void ensure_work(Work& wk, int S, bool trace);
+    // Split forward: a batch of >= parts * kSplitMin samples runs as `split_parts`
+    // independent sub-batches on their own streams (samples never interact), so
+    // each part's kernels fill the others' last-wave tails. Off for traces,
+    // calibration recording and per-family timing.
+    static constexpr int kSplitMin = 32;
+    static constexpr int kMaxSplit = 4;
+    int split_parts = 2;
+    struct SplitPart {
+        Work w;
+        cudaStream_t st = nullptr, copy = nullptr;  // compute / H2D streams of parts >= 1
+        cudaEvent_t fork = nullptr, join = nullptr;
+    };
+    SplitPart parts[kMaxSplit];
 
     // Per-kernel-family device time of one forward (CUDA events on the stream).
     enum Family { FAM_K1 = 0, FAM_K2 = 1, FAM_K3 = 2, FAM_DGEMM = 3, FAM_AUX = 4, FAM_COUNT = 5 };
@@ -197,7 +214,10 @@ class Model {
     };
     void forward(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S, double* logits,
                  TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed = nullptr);
-    std::vector<cudaEvent_t> feed_events;  // one per chunk, created on first use
+    // one (half-)batch on stream st with workspace wk (forward() validates and uploads first)
+    void forward_impl(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S,
+                      double* logits, TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed,
+                      cudaStream_t st, Work& w);
     std::unique_ptr<Calibration> calibrate(const double* images_dev, int S, const QuantSpec& spec, bool d1, bool d2,
                                            int chunk);
 };

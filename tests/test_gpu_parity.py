@@ -320,3 +320,42 @@ def test_staged_k1_equals_literal(gpu_ctx, E, T, n_refresh, order, src):
     m = np.unpackbits(a["omask"].view(np.uint8), bitorder="little").reshape(S * T, -1)[:, :E].astype(bool)
     assert m.any()
     assert np.array_equal(a["ocode"][m], b["ocode"][m]) and np.array_equal(a["oscale"][m], b["oscale"][m])
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_split_forward_identical(oracle_checker, gpu_ctx, graphs):
+    """A batch split into independent sub-batches on their own streams
+    ("split_parts" 2 / 4, uneven halves) gives the single-stream logits bit for
+    bit, through the device forward and the host-feed (e2e) path, with and
+    without CUDA-graph replay; the quantized logits also equal the oracle's."""
+    import torch
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    dims = dict(image=32, channels=3, patch=8, embed=64, state=16, blocks=2, classes=10, conv_width=4)
+    od = O.Dims(**dims)
+    om = oracle_checker.model(od, SEED)
+    gm = ob.Model(gpu_ctx, ob.Dims(**dims), SEED)
+    B = 130
+    imgs = oracle_checker.normal(51, B * od.pix).reshape(B, od.image, od.image, od.channels)
+    cimgs = oracle_checker.normal(52, 2 * od.pix).reshape(2, od.image, od.image, od.channels)
+    spec = _spec(4, n_refresh=5, rho=0.02)
+    ocal = om.calibrate(cimgs, spec)
+    gcal = _import_calib(gm, ocal.export(), spec)
+    gm.use_graphs(graphs)
+    dev = torch.from_numpy(imgs).cuda()
+    res = {}
+    for parts in (1, 2, 4):
+        gm.set_option("split_parts", parts)
+        for mode in (0, 1):
+            cal = gcal if mode else None
+            h = gm.forward_host(imgs, cal, mode)
+            d = gm.forward(dev, cal, mode)
+            torch.cuda.synchronize()
+            res[(parts, mode)] = (h, d.cpu().numpy())
+    for mode in (0, 1):
+        base = res[(1, mode)][0]
+        for parts in (1, 2, 4):
+            for got in res[(parts, mode)]:
+                assert np.array_equal(got, base), (parts, mode)
+    assert rel_err(res[(2, 1)][0], om.forward(imgs, ocal, 1)) <= RTOL_F64
+    gm.set_option("split_parts", 2)
