@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--split-parts", type=int, default=None,
                     help="independent sub-batches on their own streams (engine default 2)")
+    ap.add_argument("--feed-chunks", type=int, default=None,
+                    help="H2D chunks of the e2e host feed (engine default 8)")
     return ap.parse_args()
 
 
@@ -206,6 +208,8 @@ def run_ours(args):
     gathered = [torch.empty_like(logits) for _ in range(world)] if world > 1 else None
     if args.split_parts is not None:
         model.set_option("split_parts", args.split_parts)
+    if args.feed_chunks is not None:
+        model.set_option("feed_chunks", args.feed_chunks)
     model.use_graphs(True)
 
     def step():

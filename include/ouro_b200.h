@@ -196,7 +196,8 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
  * detector kernel everywhere; "split_parts" = 2 (default) or 4 runs a batch of
  * >= 32 * parts samples as that many independent sub-batches on their own
- * streams (results identical), 1 one stream. */
+ * streams (results identical), 1 one stream; "feed_chunks" (default 8) = H2D
+ * chunks of forward_host for batches >= 64. */
 ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long value);
 
 /* One forward with CUDA events around every launch: per kernel family

@@ -579,7 +579,7 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
         ob::Model::HostFeed feed;
         feed.host = images_host;
         feed.copy = m->copy;
-        feed.chunks = B >= 64 ? 8 : 1;
+        feed.chunks = B >= 64 ? m->m->feed_chunks : 1;
         auto body = [&] {
             mm.forward(cal, mode, d1 != 0, d2 != 0, mm.w.img.p, static_cast<int>(B), mm.w.logits.p, nullptr, nullptr,
                        &feed);
@@ -644,6 +644,9 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         if (k == "scan_variant") {
             require(value >= 0 && value <= 2, "model_set_option: scan_variant must be 0, 1 or 2");
             m->m->scan_variant = static_cast<int>(value);
+        } else if (k == "feed_chunks") {
+            require(value >= 1 && value <= 64, "model_set_option: feed_chunks must be in [1, 64]");
+            m->m->feed_chunks = static_cast<int>(value);
         } else if (k == "split_parts") {
             require(value == 1 || value == 2 || value == 4, "model_set_option: split_parts must be 1, 2 or 4");
             m->m->split_parts = static_cast<int>(value);

@@ -178,6 +178,8 @@ class Model {
     static constexpr int kSplitMin = 32;
     static constexpr int kMaxSplit = 4;
     int split_parts = 2;
+    int feed_chunks = 8;  // host-feed H2D chunks per forward (batches >= 64); e2e measured 2/4/8/16/32:
+                          // 2599 / 2776 / 2795 / 2701 / 2682 images/s
     struct SplitPart {
         Work w;
         cudaStream_t st = nullptr, copy = nullptr;  // compute / H2D streams of parts >= 1
