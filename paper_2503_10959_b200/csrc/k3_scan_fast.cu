@@ -71,6 +71,10 @@ constexpr int kWarpCh = 16;  // channels per warp
 // rare exact paths: out of line, so the certified f32 loop keeps its code size.
 __device__ __noinline__ double exp_call(double x) { return gl::exp(x); }
 __device__ __noinline__ double softplus_call(double x) { return softplus_d(x); }
+__device__ __noinline__ double qdiv_call(double x, double sc, double q) { return quant_code_div(x, sc, q); }
+// outlier-channel scale and its reciprocal (rare: a channel's first outlier step)
+__device__ __noinline__ double scale_call(double peak, double q) { return scale_from_peak(peak, q); }
+__device__ __noinline__ double recip_call(double x) { return __ddiv_rn(1.0, x); }
 
 struct WarpSmem {
     StepShared st[2][kChunk];
@@ -303,15 +307,15 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                     }
                     if (fl & 3u) exact();
                     if (fl & 1u) {
-                        sA = scale_from_peak(pa, qo);
-                        invA = __double2float_rn(__ddiv_rn(1.0, sA));
+                        sA = scale_call(pa, qo);
+                        invA = __double2float_rn(recip_call(sA));
                         qAf = qof;
                         const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
                         halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
                     }
                     if (fl & 2u) {
-                        sB = scale_from_peak(pb, qo);
-                        kB = __double2float_rn(__ddiv_rn(1.0, sB)) / ss.invSbf;
+                        sB = scale_call(pb, qo);
+                        kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
                         qBf = qof;
                         halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
                     }
@@ -369,11 +373,11 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
                     if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
                         ca[m] = static_cast<unsigned>(static_cast<int>(
-                            quant_code_div(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
+                            qdiv_call(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
                         cb[m] = static_cast<float>(
-                            quant_code_div(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
+                            qdiv_call(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
                 }
             }
             // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update.
@@ -417,8 +421,8 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
 #pragma unroll
                     for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
                     ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
-                    sH = scale_from_peak(ph, qo);
-                    invHf = __double2float_rn(__ddiv_rn(1.0, sH));
+                    sH = scale_call(ph, qo);
+                    invHf = __double2float_rn(recip_call(sH));
                     qH = qo;
                 }
             }
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                         const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
                         const float q = fminf(fmaxf(hv * invHf, -capH), capH);
                         if (EXACT || fabsf(q - rintf(q)) > halfH)
-                            chd[m] = static_cast<float>(quant_code_div(h[m], sH, qH));
+                            chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
                     }
                 }
 #pragma unroll
