@@ -35,6 +35,7 @@
 //    the output sum in the reference's order.
 #include "common.cuh"
 #include "kernels.h"
+#include "scan_f32.cuh"
 #include "sm100_ptx.cuh"
 
 #include <type_traits>
@@ -86,11 +87,6 @@ struct WarpSmem {
     uint64_t bar[2];
 };
 
-__device__ __forceinline__ float ex2_approx(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 
 // Round to nearest via the magic 1.5*2^23: the f32 bit pattern of q + 1.5*2^23 is
 // 0x4B400000 + code. Integer -> f64 avoids the conversion pipe (I2F.F64 measured
@@ -99,16 +95,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // balances the XU against the FP64/ALU issue slots.
 constexpr unsigned kMagicBits = 0x4B400000u;
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
-
-// f32 softplus(x) = max(x,0) + log1p(exp(-|x|)) and its relative error bound:
-// x rounded to f32 (2^-24), ex2.approx (2^-22 + the argument's rounding,
-// <= 1.4|x| 2^-24 relative), log1pf (1 ulp), one add: <= (12 + 3 max(0,-x)) 2^-24.
-// Below x = -80 ex2.approx.ftz flushes; the bound is then 1 (always exact).
-__device__ __forceinline__ float softplus_f32(float x, float& eps) {
-    const float e = ex2_approx(-fabsf(x) * 1.44269504f);
-    eps = x < -80.0f ? 1.0f : fmaf(fmaxf(0.0f, -x), 3.0f, 12.0f) * 5.9604645e-8f;
-    return fmaxf(x, 0.0f) + log1pf(e);
-}
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(ptx::smem_u32(dst)), "l"(src),
