@@ -4,7 +4,7 @@
 // softplus(x) the exact f64 value (glibc-identical exp/log1p). Prints the largest
 // ratio and the x it occurs at; exit code 1 if the bound fails. The
 // argument-rounding term is max(1, -x) 2^-24 for x < 0 and 2^-24 otherwise. GPU program, built
-// and run by tests/test_gpu_softplus_bound.py.
+// and run by tests/test_gpu_f32_bounds.py.
 #include <cstdio>
 #include <cstdint>
 

@@ -19,3 +19,14 @@ def test_softplus_f32_bound_exhaustive(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_merge_f32_bound_exhaustive(tmp_path):
+    """The merge source's certified v = m * silu(g) (csrc/merge_f32.cuh): every f32
+    gate g >= -80 (tests/cpp/merge_bound_check.cu)."""
+    exe = tmp_path / "merge_bound_check"
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", f"-I{CSRC}",
+                    os.path.join(ROOT, "tests", "cpp", "merge_bound_check.cu"), "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
