@@ -63,3 +63,18 @@ def test_version_and_error_slot_cleared(lib):
     lib.ouro_b200_ctx_free(None)
     assert lib.ouro_b200_ctx_synchronize(None) == 2
     assert lib.ouro_b200_last_error() != b""
+
+
+def test_null_arguments_newer_entry_points(lib):
+    """Every entry point added for the plane stream, the gemm-bench stage, spikes
+    and the math diagnostic rejects NULL handles with the validation status."""
+    P = None
+    assert lib.ouro_b200_math_eval(P, 0, P, P, 4) == 2
+    assert lib.ouro_b200_detect_quantize_planes(P, P, 1, 1, 1, C.c_double(1.0), P, 0, 4, 8, 1, P, P, P, P, P, P,
+                                                P) == 2
+    assert lib.ouro_b200_refresh_sweep(P, P, P, P) == 2
+    assert lib.ouro_b200_gemm_bench(P, P, P) == 2
+    assert lib.ouro_b200_model_set_spikes(P, P) == 2
+    assert lib.ouro_b200_model_set_option(P, b"split_parts", 2) == 2
+    assert lib.ouro_b200_quant_scan_spiked(P, 1, 1, 32, 16, 0, 0, P, P, P, P, P, 0, 0, 4, 8, P, P, P, P, 0, 0, 0) == 2
+    assert b"NULL" in lib.ouro_b200_last_error()
