@@ -109,26 +109,31 @@ cudaError_t launch_dgemm(const DGemmParams& p, cudaStream_t st) {
 
 // patches[s][t][p] = img[s][gather(t,p)] with gather of ssm.cpp:72-84:
 // (grid row, grid col, patch row, patch col, channel).
-__global__ void k4_patch_gather(const double* __restrict__ img, double* __restrict__ patches, int S, int image,
-                                int channels, int patch) {
-    const int g = image / patch, L = g * g, pv = patch * patch * channels;
-    const size_t total = static_cast<size_t>(S) * L * pv;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int pidx = static_cast<int>(i % pv);
-        const size_t st = i / pv;
-        const int t = static_cast<int>(st % L);
-        const size_t s = st / L;
-        const int gr = t / g, gc = t % g;
-        const int ch = pidx % channels, pc = (pidx / channels) % patch, pr = pidx / (channels * patch);
-        const size_t src = (static_cast<size_t>(gr * patch + pr) * image + gc * patch + pc) * channels + ch;
-        patches[i] = img[s * static_cast<size_t>(image) * image * channels + src];
+// One block per patch (sample, token): patch row pr is patch*channels contiguous
+// doubles of image row gr*patch + pr, so reads and writes are coalesced and the
+// index arithmetic is 32-bit within the patch.
+__global__ void __launch_bounds__(256) k4_patch_gather(const double* __restrict__ img, double* __restrict__ patches,
+                                                       int S, int image, int channels, int patch) {
+    const int g = image / patch, L = g * g, rowv = patch * channels, pv = patch * rowv;
+    const size_t st = blockIdx.x;  // sample * L + token
+    const int t = static_cast<int>(st % L);
+    const size_t s = st / L;
+    const int gr = t / g, gc = t % g;
+    const double* src = img + s * static_cast<size_t>(image) * image * channels +
+                        (static_cast<size_t>(gr * patch) * image + gc * patch) * channels;
+    double* dst = patches + st * pv;
+    for (int j = threadIdx.x; j < pv; j += blockDim.x) {
+        const int pr = j / rowv, off = j - pr * rowv;
+        dst[j] = __ldg(src + static_cast<size_t>(pr) * image * channels + off);
     }
 }
 
 cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,
                                 cudaStream_t st) {
-    k4_patch_gather<<<1184, 256, 0, st>>>(img, patches, S, image, channels, patch);
+    const int g = image / patch;
+    const unsigned blocks = static_cast<unsigned>(S) * static_cast<unsigned>(g * g);
+    if (blocks == 0) return cudaSuccess;
+    k4_patch_gather<<<blocks, 256, 0, st>>>(img, patches, S, image, channels, patch);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }
