@@ -31,14 +31,16 @@ def get(r, name, scale_to=None):
 
 kernels, lines = {}, []
 cols = ["smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct"]
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
 for r in data:
     name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("ob::", "")
     rd, wr = get(r, "dram__bytes_read.sum", "bytes"), get(r, "dram__bytes_write.sum", "bytes")
     t = get(r, "gpu__time_duration.sum", "ms")
     kernels.setdefault(name, []).append(dict(dram_read_bytes=rd, dram_write_bytes=wr, traffic_bytes=rd + wr,
                                              ncu_time=t, time_unit="ms"))
-    extra = "  ".join(f"{c.split('.')[0].split('__')[-1]} {get(r, c):5.1f}%" for c in cols if c in hdr)
+    extra = "  ".join(f"{c.split('__')[1].split('.')[0]} {get(r, c):5.1f}%" for c in cols if c in hdr)
     lines.append(f"{name:28s} {t * 1e3:9.1f} us  read {rd / 1e6:8.1f} MB  write {wr / 1e6:8.1f} MB  "
                  f"{(rd + wr) / (t * 1e-3) / 1e12:5.2f} TB/s  {extra}")
 with open(out_json, "w") as f:
