@@ -45,29 +45,6 @@ namespace ob {
 
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 
-// Layer input of two channels at one token (16-byte loads).
-template <int SRC>
-__device__ __forceinline__ double2 k1_load2(const K1Params& p, size_t src, size_t crow_global) {
-    if (SRC == K1_SRC_MERGE) {
-        // merged = (0 + o_0) + o_1 (ssm.cpp:214-229), y = merged * gate (ssm.cpp:231)
-        const double2 a = ldg2(p.x + src);
-        const double2 g = ldg2(p.gate + src);
-        double m0 = dadd(0.0, a.x), m1 = dadd(0.0, a.y);
-        if (p.x2) {
-            const double2 b = ldg2(p.x2 + src);
-            m0 = dadd(m0, b.x);
-            m1 = dadd(m1, b.y);
-        }
-        return make_double2(dmul(m0, silu_d(g.x)), dmul(m1, silu_d(g.y)));  // gate = silu(x W_g^T)
-    }
-    double2 v = ldg2(p.x + src);
-    if (SRC == K1_SRC_RMSNORM) {
-        const double r = __ldg(p.rs + crow_global);
-        v.x = dmul(v.x, r);
-        v.y = dmul(v.y, r);
-    }
-    return v;
-}
 
 // exact merged value y = merged * silu(gate) (ssm.cpp:231): the rare path, kept out of line
 __device__ __noinline__ double merge_exact(double m, double g) { return dmul(m, silu_d(g)); }
@@ -76,6 +53,7 @@ __device__ __noinline__ double merge_exact(double m, double g) { return dmul(m, 
 // window's tokens; a warp covers 128 channels = 4 mask words (8 lanes x 4 bits).
 template <int SRC>
 __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
+    static_assert(SRC == K1_SRC_MERGE, "plain and RMSNorm sources run on k1_staged");
     const int E = p.E, T = p.T, J = E >> 5;
     const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * 4;  // channels ch .. ch+3
     const int lane = threadIdx.x & 31;
@@ -123,12 +101,6 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
                 gg[3] = g1.y;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) ap[k] = merge_approx(mg[k], gg[k]);
-            } else {
-                const double2 lo = k1_load2<SRC>(p, cg * E + ch, cg), hi = k1_load2<SRC>(p, cg * E + ch + 2, cg);
-                v[0] = lo.x;
-                v[1] = lo.y;
-                v[2] = hi.x;
-                v[3] = hi.y;
             }
         }
         unsigned have = 0;  // merge: bit k = v[k] holds the exact value

@@ -72,7 +72,6 @@ struct K1Params {
     SiteCal cal;
     const double* inv_in = nullptr;    // optional [T] 1/s_in (host-computed); else divided in-kernel
     const double* inv_full = nullptr;  // optional [T] 1/s_full
-    double* rs = nullptr;              // unused (the staged kernel computes D1 row factors in shared memory)
     int force_literal = 0;             // run the literal detector kernel
     // quantized outputs (rows in step order, row = s*T + t): the QAct operand
     int8_t* codes = nullptr;
