@@ -424,7 +424,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
         }
         forward_impl(cal, mode, d1, d2, images + static_cast<size_t>(s0) * pix, s1 - s0,
                      logits + static_cast<size_t>(s0) * d.classes, nullptr, nullptr, feed ? &f : nullptr,
-                     k == 0 ? ctx->stream : parts[k].st, k == 0 ? w : parts[k].w);
+                     k == 0 ? ctx->stream : parts[k].st, k == 0 ? w : parts[k].w, s0);
     }
     for (int k = 1; k < np; ++k) {
         cuda_check(cudaEventRecord(parts[k].join, parts[k].st), "split join");
@@ -434,7 +434,7 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
 
 void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S,
                          double* logits, TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed,
-                         cudaStream_t st, Work& w) {
+                         cudaStream_t st, Work& w, int sample0) {
     const bool quant = mode != MODE_FP;
     const bool qlin = quant && d2;
     ensure_work(w, S, trace != nullptr);
@@ -698,6 +698,7 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
             sps[dd].spike = spikes;
             sps[dd].spike.block = b;
             sps[dd].spike.dir = dd;
+            sps[dd].spike.sample0 = sample0;
         }
         if (fast_ok && !any_literal && scan_variant != 1 && !(spikes.rate > 0.0)) {
             cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant == 2 ? 1 : 0), "scan");

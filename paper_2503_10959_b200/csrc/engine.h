@@ -219,7 +219,7 @@ class Model {
     // one (half-)batch on stream st with workspace wk (forward() validates and uploads first)
     void forward_impl(const Calibration* cal, int mode, bool d1, bool d2, const double* images, int S,
                       double* logits, TraceSink* trace, unsigned long long* calib_peaks, const HostFeed* feed,
-                      cudaStream_t st, Work& w);
+                      cudaStream_t st, Work& w, int sample0 = 0);  // sample0: global index of sample 0 (SpikeHook)
     std::unique_ptr<Calibration> calibrate(const double* images_dev, int S, const QuantSpec& spec, bool d1, bool d2,
                                            int chunk);
 };

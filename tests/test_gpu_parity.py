@@ -359,3 +359,31 @@ def test_split_forward_identical(oracle_checker, gpu_ctx, graphs):
                 assert np.array_equal(got, base), (parts, mode)
     assert rel_err(res[(2, 1)][0], om.forward(imgs, ocal, 1)) <= RTOL_F64
     gm.set_option("split_parts", 2)
+
+
+def test_split_forward_with_spikes_identical(oracle_checker, gpu_ctx):
+    """SpikeHook positions use the global sample index, so a spiked batch split
+    into sub-batches gives the single-stream logits bit for bit."""
+    from oracle import oracle as O
+    import paper_2503_10959_b200 as ob
+    dims = dict(image=32, channels=3, patch=8, embed=64, state=16, blocks=2, classes=10, conv_width=4)
+    od = O.Dims(**dims)
+    om = oracle_checker.model(od, SEED)
+    gm = ob.Model(gpu_ctx, ob.Dims(**dims), SEED)
+    B = 130
+    imgs = oracle_checker.normal(61, B * od.pix).reshape(B, od.image, od.image, od.channels)
+    cimgs = oracle_checker.normal(62, 2 * od.pix).reshape(2, od.image, od.image, od.channels)
+    spec = _spec(4, n_refresh=5, rho=0.02)
+    gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
+    gm.set_spikes(ob.SpikeSettings(rate=0.3, gain=20.0, channels=2, salt=5))
+    res = {}
+    for parts in (1, 2, 4):
+        gm.set_option("split_parts", parts)
+        res[parts] = [gm.forward_host(imgs, gcal if mode else None, mode) for mode in (0, 1)]
+    gm.set_spikes(None)
+    gm.set_option("split_parts", 2)
+    plain = gm.forward_host(imgs, None, 0)
+    assert not np.array_equal(plain, res[1][0])  # the hook fired
+    for parts in (2, 4):
+        for a, b in zip(res[parts], res[1]):
+            assert np.array_equal(a, b), parts
