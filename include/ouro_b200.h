@@ -231,6 +231,7 @@ typedef struct {
     double rate, gain;
     size_t channels;
     uint64_t salt;
+    size_t sample0; /* global index of the call's first sample (a batch sharded across GPUs) */
 } ouro_b200_spikes;
 /* Spikes for every later forward / trace of this model (NULL = off); spiked
  * scans run on the reference-form kernel. Cached graphs are rebuilt. */

@@ -494,7 +494,7 @@ inline QuantEvalResult quantized_forward(const ToyVmmModel& model, const std::ve
                                          const SpikeSettings& spikes = SpikeSettings{}) {
     const ModelDims& d = model.dims();
     // SpikeHook in all three passes (FP, quantized, teacher-forced), as the reference
-    const ouro_b200_spikes sp{spikes.rate, spikes.gain, spikes.channels, spikes.salt};
+    const ouro_b200_spikes sp{spikes.rate, spikes.gain, spikes.channels, spikes.salt, 0};
     const bool spiked = spikes.rate > 0.0;
     check(ouro_b200_model_set_spikes(model.handle(), spiked ? &sp : nullptr));
     struct SpikeReset {

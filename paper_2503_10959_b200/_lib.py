@@ -116,7 +116,8 @@ def load(path: str = SO_PATH):
 
 class Spikes(C.Structure):
     """ouro_b200_spikes (SpikeSettings, quant.hpp:105-110)."""
-    _fields_ = [("rate", C.c_double), ("gain", C.c_double), ("channels", C.c_size_t), ("salt", C.c_uint64)]
+    _fields_ = [("rate", C.c_double), ("gain", C.c_double), ("channels", C.c_size_t), ("salt", C.c_uint64),
+                ("sample0", C.c_size_t)]
 
 
 class SweepSettings(C.Structure):

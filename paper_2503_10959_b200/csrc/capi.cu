@@ -247,6 +247,7 @@ static ob::SpikeCfg spike_from(const ouro_b200_spikes* sp) {
     c.gain = sp->gain;
     c.channels = static_cast<int>(sp->channels);
     c.salt = sp->salt;
+    c.sample0 = static_cast<int>(sp->sample0);
     return c;
 }
 
@@ -271,7 +272,7 @@ ouro_status ouro_b200_quant_scan_spiked(ouro_b200_ctx* ctx, size_t S, size_t T, 
         ob::SpikeCfg c = spike_from(spikes);
         c.block = static_cast<int>(block);
         c.dir = static_cast<int>(dir);
-        c.sample0 = static_cast<int>(sample0);
+        c.sample0 += static_cast<int>(sample0);
         quant_scan_impl(ctx, S, T, E, N, order, grid, u, proj, a, b_delta, o, mode, n_refresh, act_bits,
                         outlier_bits, theta, s_in, s_full, nullptr, 0, nullptr, c);
     });

@@ -235,7 +235,7 @@ class Context:
         si = (C.c_void_p * 3)(*[t.data_ptr() for t in s_in]) if s_in is not None else None
         sf = (C.c_void_p * 3)(*[t.data_ptr() for t in s_full]) if s_full is not None else None
         if spikes is not None:
-            sp = L.Spikes(spikes.rate, spikes.gain, spikes.channels, spikes.salt)
+            sp = L.Spikes(spikes.rate, spikes.gain, spikes.channels, spikes.salt, spikes.sample0)
             L.check(self.lib.ouro_b200_quant_scan_spiked(
                 self.h, S, T, E, 16, order, grid, _ptr(u), _ptr(proj), _ptr(a), _ptr(b_delta), _ptr(o), mode,
                 n_refresh, act_bits, outlier_bits, th if theta is not None else None, si, sf, C.byref(sp), block, dir,
@@ -266,6 +266,7 @@ class SpikeSettings:
     gain: float = 100.0
     channels: int = 1
     salt: int = 0
+    sample0: int = 0  # global index of the call's first sample (a batch sharded across GPUs)
 
 
 class Calibration:
@@ -471,7 +472,7 @@ class Model:
 
     def set_spikes(self, spikes: "SpikeSettings | None") -> None:
         """SpikeHook for every later forward / trace (None or rate 0 = off)."""
-        sp = L.Spikes(spikes.rate, spikes.gain, spikes.channels, spikes.salt) if spikes is not None else None
+        sp = L.Spikes(spikes.rate, spikes.gain, spikes.channels, spikes.salt, spikes.sample0) if spikes is not None else None
         L.check(self.lib.ouro_b200_model_set_spikes(self.h, C.byref(sp) if sp is not None else None))
 
     def quant_eval(self, images: np.ndarray, calib: Calibration, mode: int, *, d1=True, d2=True,

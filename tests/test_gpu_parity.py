@@ -380,6 +380,12 @@ def test_split_forward_with_spikes_identical(oracle_checker, gpu_ctx):
     for parts in (1, 2, 4):
         gm.set_option("split_parts", parts)
         res[parts] = [gm.forward_host(imgs, gcal if mode else None, mode) for mode in (0, 1)]
+    # a shard of the batch (as one rank of a multi-GPU run sees it) with its global offset
+    gm.set_option("split_parts", 1)
+    gm.set_spikes(ob.SpikeSettings(rate=0.3, gain=20.0, channels=2, salt=5, sample0=65))
+    shard = [gm.forward_host(imgs[65:], gcal if mode else None, mode) for mode in (0, 1)]
+    for a, b in zip(shard, res[1]):
+        assert np.array_equal(a, b[65:])
     gm.set_spikes(None)
     gm.set_option("split_parts", 2)
     plain = gm.forward_host(imgs, None, 0)
