@@ -194,7 +194,7 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * channel-local detector is exact), 1 per-direction reference scan kernel,
  * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
- * detector kernel everywhere; "split_parts" = 2 (default) or 4 runs a batch of
+ * detector kernel everywhere; "split_parts" in [1, 4] (default 2) runs a batch of
  * >= 32 * parts samples as that many independent sub-batches on their own
  * streams (results identical), 1 one stream; "feed_chunks" (default 8) = H2D
  * chunks of forward_host for batches >= 64. */

@@ -649,7 +649,7 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
             require(value >= 1 && value <= 64, "model_set_option: feed_chunks must be in [1, 64]");
             m->m->feed_chunks = static_cast<int>(value);
         } else if (k == "split_parts") {
-            require(value == 1 || value == 2 || value == 4, "model_set_option: split_parts must be 1, 2 or 4");
+            require(value >= 1 && value <= 4, "model_set_option: split_parts must be in [1, 4]");
             m->m->split_parts = static_cast<int>(value);
         } else if (k == "k1_variant") {
             require(value >= 0 && value <= 1, "model_set_option: k1_variant must be 0 or 1");
