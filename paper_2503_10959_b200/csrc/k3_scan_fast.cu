@@ -106,7 +106,10 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
 // calibrated scales and their f32 inverses, the b_bar quotients per unit delta
 // and max_m |B_m|. One warp per step; lane j holds column E + j of the x_proj row.
 __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndirs, StepShared* __restrict__ out) {
-    const int gw = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    // each warp assembles its record in shared memory, then writes it as 16-byte
+    // coalesced chunks (the fields are scattered scalars)
+    __shared__ StepShared rec[8];
+    const int wi = threadIdx.x >> 5, gw = blockIdx.x * 8 + wi, lane = threadIdx.x & 31;
     const ScanParams& p0 = P.d[0];
     const int S = p0.S, T = p0.T;
     if (gw >= ndirs * S * T) return;
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
     const ScanParams& p = P.d[dd];
     const bool dyn = p.mode == MODE_DYNAMIC;
     const double v = p.proj[static_cast<size_t>(st_idx) * (p.E + 32) + p.E + lane];
-    StepShared& ss = out[gw];
+    StepShared& ss = rec[wi];
     const double Sb = dyn ? p.cal[1].s_in[t] : p.cal[1].s_full[t];
     const double* ib = dyn ? p.cal[1].inv_in : p.cal[1].inv_full;
     const float invSbf = __double2float_rn(ib ? ib[t] : __ddiv_rn(1.0, Sb));
@@ -152,7 +155,13 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         const float qa1 = static_cast<float>((1 << (p.abits - 1)) - 1) + 1.0f;
         ss.hA1 = qa1 * ss.LA;
         ss.hA0 = 0.5f - fmaf(qa1, fmaf(ss.LA, 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+        ss.pad[0] = ss.pad[1] = 0;
     }
+    __syncwarp();
+    constexpr int kChunks16 = static_cast<int>(sizeof(StepShared) / 16);
+    const uint4* src = reinterpret_cast<const uint4*>(&rec[wi]);
+    uint4* dst = reinterpret_cast<uint4*>(out + gw);
+    for (int k = lane; k < kChunks16; k += 32) dst[k] = src[k];
 }
 
 template <bool EXACT, int ABITS>
