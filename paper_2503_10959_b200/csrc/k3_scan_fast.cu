@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
             const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
             auto pass1 = [&](auto clamp) {
                 constexpr bool CL = decltype(clamp)::value;
+                float mda = 0.0f, mdb = 0.0f;  // largest distance to the rounded code (3-input max)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
@@ -350,9 +351,10 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                     const float2 db = __fadd2_rn(qb2, make_float2(-rb.x, -rb.y));
                     cb[2 * k] = rb.x;
                     cb[2 * k + 1] = rb.y;
-                    redo |= (fabsf(da.x) > halfA) | (fabsf(da.y) > halfA) | (fabsf(db.x) > halfB) |
-                            (fabsf(db.y) > halfB);
+                    mda = fmaxf(mda, fmaxf(fabsf(da.x), fabsf(da.y)));
+                    mdb = fmaxf(mdb, fmaxf(fabsf(db.x), fabsf(db.y)));
                 }
+                redo |= (mda > halfA) | (mdb > halfB);
             };
             // The clamps can bind only if the largest quotient exceeds the cap: q_b <=
             // dfb*max|BSf| and q_a <= paf*invA (monotone rounding; the factor covers
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                 bool hredo = EXACT;
                 auto hcodes = [&](auto clamp) {
                     constexpr bool CL = decltype(clamp)::value;
+                    float mdh = 0.0f;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         float2 q = __fmul2_rn(hfv[k], f2(invHf));
@@ -440,8 +443,9 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                         const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
                         chd[2 * k] = rh.x;
                         chd[2 * k + 1] = rh.y;
-                        hredo |= (fabsf(dh.x) > halfH) | (fabsf(dh.y) > halfH);
+                        mdh = fmaxf(mdh, fmaxf(fabsf(dh.x), fabsf(dh.y)));
                     }
+                    hredo |= mdh > halfH;
                 };
                 if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});  // |q| <= phf*invHf
                 else hcodes(std::true_type{});
