@@ -265,15 +265,20 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
             }
             __syncthreads();
         }
-        for (int t = ts; t < te; ++t) {
+        // running pointers (row = s*T + t; the staged row `slot` of this chunk)
+        const double* xr = sb + ch;
+        const size_t row0 = static_cast<size_t>(s) * T + ts;
+        int8_t* cp = codes + row0 * E + ch;
+        uint32_t* mp = omask + row0 * J + (ch >> 5);
+        for (int t = ts; t < te; ++t, xr += E, cp += E, mp += J) {
             const int slot = t - ts;
-            const size_t row = static_cast<size_t>(s) * T + t;
+            const size_t row = row0 + slot;
             const double S = s_tab[t];
             const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
             double v[4] = {0.0, 0.0, 0.0, 0.0};
             if (active) {
-                const double2 lo = *reinterpret_cast<const double2*>(sb + static_cast<size_t>(slot) * E + ch);
-                const double2 hi = *reinterpret_cast<const double2*>(sb + static_cast<size_t>(slot) * E + ch + 2);
+                const double2 lo = *reinterpret_cast<const double2*>(xr);
+                const double2 hi = *reinterpret_cast<const double2*>(xr + 2);
                 v[0] = lo.x;
                 v[1] = lo.y;
                 v[2] = hi.x;
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
             if (active) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) cc[k] = ((in >> k) & 1u) ? 0 : min(max(cc[k], -qai), qai);
-                *reinterpret_cast<char4*>(codes + row * E + ch) =
+                *reinterpret_cast<char4*>(cp) =
                     make_char4(static_cast<signed char>(cc[0]), static_cast<signed char>(cc[1]),
                                static_cast<signed char>(cc[2]), static_cast<signed char>(cc[3]));
                 if (in) {  // outlier channels: own scale |x|/q_o, code at o_bits
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
                 for (int o = 4; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
                 if (active && (lane & 7) == 0 && bits) atomicAdd(&cnt[buf][slot], __popc(bits));
             }
-            if (active && (lane & 7) == 0) omask[row * J + (ch >> 5)] = bits;
+            if (active && (lane & 7) == 0) *mp = bits;
             if (tid == 0) s_row[row] = S;
         }
         __syncthreads();  // stage `buf` consumed, counts complete
