@@ -176,10 +176,10 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
 // E channels (blockDim = E/4 rounded to warps). Rows of `rc` steps per stage,
 // kK1Stages stages: chunk c lands in stage c % kK1Stages by per-row bulk copies
 // on an mbarrier; chunk c + kK1Stages is issued once every thread has finished
-// chunk c. 20 KB stages
-// (rc = 3 rows at E = 768): 4 CTAs per SM; 32 KB stages (3 CTAs) measured
-// 175 / 120 us vs 155 / 113 us for the x_proj pair / in_proj.
-constexpr int kK1StageBytes = 20 * 1024;
+// chunk c. 24 KB stages
+// (rc = 4 rows at E = 768; 4 CTAs per SM, register-limited): x_proj pair / in_proj
+// 147 / 105 us; 20 KB (rc = 3) 152 / 112 us; 32 KB (3 CTAs) was slower still.
+constexpr int kK1StageBytes = 24 * 1024;
 constexpr int kK1Stages = 2;  // 3 stages (fewer CTAs per SM) measured 165 / 117 us vs 155 / 113
 constexpr int kK1MaxRc = 16;
 struct K1Dirs {
