@@ -20,7 +20,10 @@ hdr, units, data = rows[0], rows[1], rows[2:]
 
 def get(r, name, scale_to=None):
     i = hdr.index(name)
-    v = float(r[i].replace(",", ""))
+    try:
+        v = float(r[i].replace(",", ""))
+    except ValueError:  # "no data" for a metric ncu could not collect on this kernel
+        return float("nan")
     u = units[i]
     if scale_to == "bytes":
         v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
