@@ -233,6 +233,29 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
             const uint32_t* msk = p.a.J <= kMaskWords
                                       ? reinterpret_cast<const uint32_t*>(mb + L::kMetaMask) + (q * 32) * p.a.J
                                               : p.a.omask + static_cast<size_t>(rbase) * p.a.J;
+            // the row's outlier channels, codes and scales are the same for every column chunk
+            // of the tile: fetched once (up to kHoist), before the accumulator wait hides their
+            // latency
+            // (8-epilogue-warp shape only: the 16-warp shape's register budget would spill)
+            constexpr int kHoist = EW >= 16 ? 1 : 4;
+            int hch[kHoist], hxo[kHoist];
+            double hosc[kHoist];
+            const bool hoisted = EW < 16 && cnt <= kHoist;
+            if (cnt > 0 && hoisted) {
+                int word = -1;
+                unsigned bits = 0;
+#pragma unroll
+                for (int o = 0; o < kHoist; ++o) {
+                    if (o < cnt) {
+                        while (bits == 0) bits = msk[lane * p.a.J + (++word)];
+                        hch[o] = word * 32 + (__ffs(bits) - 1);
+                        bits &= bits - 1;
+                        const size_t oi = static_cast<size_t>(row) * p.K + hch[o];
+                        hxo[o] = p.a.ocode[oi];
+                        hosc[o] = p.a.oscale[oi];
+                    }
+                }
+            }
             ptx::mbar_wait(acc_full + buf, aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -269,17 +292,9 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
                 if (PLANES)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) aout[j] = 0;
-                // walk O(t) in ascending channel order: mask word by word, bit by bit
-                int word = -1;
-                unsigned bits = 0;
-                for (int o = 0; o < cnt; ++o) {
-                    while (bits == 0) bits = msk[lane * p.a.J + (++word)];
-                    const int ch = word * 32 + (__ffs(bits) - 1);
-                    bits &= bits - 1;
-                    const size_t oi = static_cast<size_t>(row) * p.K + ch;
-                    const int xo_i = p.a.ocode[oi];
+                // outlier terms in ascending channel order (gemm.cpp:208-216)
+                auto outlier_term = [&](int ch, int xo_i, double osc) {
                     const double xo = i32_to_f64(static_cast<uint32_t>(xo_i));
-                    const double osc = p.a.oscale[oi];
                     const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(ch) * p.R + r0);
                     int4 w01 = __ldg(wp), w23 = __ldg(wp + 1);
                     const int8_t* wv = reinterpret_cast<const int8_t*>(&w01);
@@ -290,6 +305,21 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
                         const double coeff = dmul(osc, i32_to_f64(static_cast<uint32_t>(wq)));
                         y[j] = dadd(y[j], dmul(coeff, xo));
                         if (PLANES) aout[j] += wq * xo_i;
+                    }
+                };
+                if (hoisted) {
+#pragma unroll
+                    for (int o = 0; o < kHoist; ++o)
+                        if (o < cnt) outlier_term(hch[o], hxo[o], hosc[o]);
+                } else {  // more than kHoist: mask word by word, bit by bit
+                    int word = -1;
+                    unsigned bits = 0;
+                    for (int o = 0; o < cnt; ++o) {
+                        while (bits == 0) bits = msk[lane * p.a.J + (++word)];
+                        const int ch = word * 32 + (__ffs(bits) - 1);
+                        bits &= bits - 1;
+                        const size_t oi = static_cast<size_t>(row) * p.K + ch;
+                        outlier_term(ch, p.a.ocode[oi], p.a.oscale[oi]);
                     }
                 }
                 if (PLANES && rv) {  // the reference's integer planes (parity path)
