@@ -300,7 +300,7 @@ def run_ours(args):
                 "roofline": {"kernel": "k3_scan", "bound": "fp64", "achieved": achieved, "peak": peak_ops,
                              "unit": "Tops (f64 lane-ops/s)", "frac": achieved / peak_ops if peak_ops else None,
                              "traffic": traffic,
-                             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01/ncu_traffic_r01k.json)",
+                             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01/ncu_traffic_r01l.json)",
                              "peak_source": "measured in-process: DFMA probe (1 op per DFMA lane)",
                              "work": f"{ops_per_elem:.0f} f64 lane-ops x S*T*E*N*dirs state-element-steps per launch"},
                 "kernels_ms_per_step": {k: v[0] for k, v in fam.items()},
@@ -320,7 +320,7 @@ def run_ours(args):
 def scan_traffic_bytes():
     """DRAM bytes (read + write) of one k3_scan_fast launch from the committed
     `ncu --set full` capture of this workload, or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_traffic_r01k.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_traffic_r01l.json")
     try:
         with open(path) as f:
             k = json.load(f)["kernels"]
