@@ -7,17 +7,21 @@ classes, conv 4, row-forward + row-backward scans, D1 pre-norm residual),
 W4A4 dynamic OuroMamba-Quant (outliers int8, n_refresh=10, rho=0.01,
 D2 quantized linear inputs), batch 256 per GPU, synthetic N(0,1) f64 images,
 random-init weights (make_toy_model, seed 1234). One step = one forward of the
-batch on every rank (+ the NCCL logits all-gather when N > 1).
+batch on every rank + the NCCL all-gather of the logits (the only collective,
+SURVEY.md §8(e)).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one process per GPU). Rank 0 prints one JSON line.
+`--gpus N` (N > 1) outside torchrun re-launches itself under
+`torch.distributed.run --nproc-per-node N` (one process per GPU); under
+torchrun the world comes from the environment. Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,9 +40,12 @@ CONFIG = dict(workload="Vim-B W4A4 dynamic forward (OuroMamba-Quant), 224x224, b
 METRIC = "W4A4 Vim-B images/sec"
 UNIT = "images/s"
 SEED = 1234
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+FP32_LANES_PER_CLK_SM = 128  # SURVEY.md §8(d) K3 model: FP32 lane-ops per clock per SM
+K3_OPS_PER_ELEM = 28         # discretize 2, 3 quantizations x 7, update 2, output 1 (+ sum)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -47,20 +54,88 @@ def parse():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--embed", type=int, default=768)
     ap.add_argument("--blocks", type=int, default=24)
+    ap.add_argument("--image", type=int, default=224)
     ap.add_argument("--abits", type=int, default=4)
+    ap.add_argument("--rho", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-images", type=int, default=None,
+                    help="images of the full-depth CPU reference sample (default: one per host core)")
     ap.add_argument("--split-parts", type=int, default=None,
                     help="independent sub-batches on their own streams (engine default 2)")
     ap.add_argument("--feed-chunks", type=int, default=None,
                     help="H2D chunks of the e2e host feed (engine default 8)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
+
+# ---- multi-process plumbing (one process per GPU) ----------------------------
 
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(argv, n: int) -> int:
+    """Re-run this script as n ranks under torch.distributed.run (the driver's
+    own launch shape), streaming the ranks' output through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def shard_bounds(global_batch: int, rank: int, world: int):
+    """Contiguous batch slice of a rank: samples never
+    interact (fresh detector state per sample, quant.cpp:477-481)."""
+    s0 = global_batch * rank // world
+    s1 = global_batch * (rank + 1) // world
+    return s0, s1
+
+
+def gather_logits(dist, logits, world: int):
+    """All-gather the per-rank logits [B, classes] into the global [world*B, classes]
+    (rank order = global sample order): the forward's only collective."""
+    if world == 1:
+        return logits
+    import torch
+    parts = [torch.empty_like(logits) for _ in range(world)]
+    dist.all_gather(parts, logits)
+    return torch.cat(parts)
+
+
+def max_over_ranks(dist, value: float, world: int, device) -> float:
+    if world == 1:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed_steps(step, steps: int, world: int, dist, sync, timer) -> float:
+    """K steps bracketed by barrier + sync on both sides; returns the elapsed
+    milliseconds, max over ranks. `timer()` returns (start, stop) callables and
+    a reader (CUDA events on the launching stream on the GPU)."""
+    sync()
+    if world > 1:
+        dist.barrier()
+    start, stop, read = timer()
+    start()
+    for _ in range(steps):
+        step()
+    stop()
+    sync()
+    if world > 1:
+        dist.barrier()
+    return read()
 
 
 class ClockSampler:
@@ -111,44 +186,159 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(model_dims, cal_export, images_np, abits, steps=1, warmup=0):
-    """The reference's CPU implementation (oracle/_ref: the reference's own
-    compiled primitives under the shared driver), all host threads, on a
-    bounded sample: `threads` images through the first 2 of 24 blocks,
-    extrapolated x12 to the 24-block forward. Returns (img/s, cores, sample)."""
+# ---- roofline model ----------------------------
+
+def measured_peaks():
+    """MEASURED_PEAKS.json (driver-written) or the profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "sm_max_mhz": float(p.get("sm_max_mhz", 1965.0)),
+                "source": "of measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "sm_max_mhz": 1965.0, "source": "of fallback (B200_PROFILING.md)"}
+
+
+def op_names(blocks: int, ndirs: int = 2):
+    """Issue order of the ops of one single-stream quantized forward (engine.cu
+    forward_impl): patch gather + embed, per block 9 ops, mean pool + head."""
+    blk = ["k1.in_proj", "k2.in_proj", "aux.conv", "k1.x_proj_pair"] + [f"k2.x_proj{d}" for d in range(ndirs)] + \
+          ["k3.scan", "k1.merge_out_proj", "k2.out_proj"]
+    return ["aux.patch_gather", "f64.patch_embed"] + blk * blocks + ["aux.meanpool", "f64.head"]
+
+
+def op_model(name: str, *, rows: int, E: int, N: int, abits: int):
+    """Algorithmic HBM bytes (and int8 tensor ops) of one op, SURVEY.md §8(d):
+    f64 activations (8 B), codes at their bit width (A4 0.5 B, A8 1 B), one
+    mask bit per channel, s_row (8 B) + |O(t)| (4 B) per row, W4 weights 0.5 B
+    plus f64 row scales; outlier side buffers (< 1 % of channels) excluded."""
+    cb = 0.5 if abits <= 4 else 1.0
+    meta = cb * E + E / 8 + 12  # per quantized row written by K1 / read by K2
+    P = E + 2 * N
+    if name == "k1.in_proj":
+        return rows * (8 * E + meta), 0
+    if name == "k1.x_proj_pair":
+        return rows * (8 * E + 2 * meta), 0
+    if name == "k1.merge_out_proj":
+        return rows * (24 * E + meta), 0
+    if name.startswith("k2."):
+        R = {"k2.in_proj": 2 * E, "k2.out_proj": E}.get(name, P)
+        out_b = rows * R * 8 * (2 if name == "k2.out_proj" else 1)  # out_proj also reads the D1 residual
+        return rows * meta + R * E * 0.5 + R * 8 + out_b, 2 * rows * R * E
+    if name == "aux.conv":
+        return rows * E * 16, 0
+    if name == "k3.scan":  # both directions: u, dpre|B|C in, o out
+        return 2 * rows * (8 * E + 8 * P + 8 * E), 0
+    return None, 0
+
+
+def kernel_rooflines(launches, *, B, L, E, N, blocks, abits, peaks, i8_tops, fp64_tflops, sms):
+    """Per-op and per-family achieved rates from the per-op CUDA-event list of
+    one single-stream forward (forward_profile_launches)."""
+    names = op_names(blocks)
+    if len(launches) != len(names):
+        return None
+    rows = B * L
+    hbm = peaks["hbm_gbs"]
+    fam = {}
+    for nm, (_, ms) in zip(names, launches):
+        byts, ops = op_model(nm, rows=rows, E=E, N=N, abits=abits)
+        f = fam.setdefault(nm, {"ms": 0.0, "n": 0, "bytes": byts or 0.0, "ops": ops})
+        f["ms"] += ms
+        f["n"] += 1
+    out = {}
+    for nm, f in fam.items():
+        if nm.startswith(("aux.patch", "aux.mean", "f64.")) or f["n"] == 0:
+            continue
+        t = f["ms"] / f["n"] * 1e-3  # mean seconds per launch
+        e = {"us_per_launch": round(t * 1e6, 2), "launches_per_fwd": f["n"]}
+        if nm == "k3.scan":
+            work = 2 * rows * E * N * K3_OPS_PER_ELEM
+            fp32_peak = FP32_LANES_PER_CLK_SM * sms * peaks["sm_max_mhz"] * 1e6 / 1e12
+            e.update(bound="fp32", unit="T lane-op/s", achieved=work / t / 1e12, peak=fp32_peak,
+                     frac=work / t / 1e12 / fp32_peak,
+                     model=f"{K3_OPS_PER_ELEM} FP32 lane-ops x 2 dirs x S*T*E*N state-element-steps "
+                           f"(SURVEY §8d); peak = {FP32_LANES_PER_CLK_SM} lanes/clk/SM x {sms} SMs x "
+                           f"{peaks['sm_max_mhz']:.0f} MHz",
+                     hbm_gbs=f["bytes"] / t / 1e9, hbm_frac=f["bytes"] / t / 1e9 / hbm)
+            if fp64_tflops:
+                dfma_lane_ops = fp64_tflops / 2.0
+                e["secondary_f64"] = {"achieved": work / t / 1e12, "peak": dfma_lane_ops,
+                                      "frac": work / t / 1e12 / dfma_lane_ops,
+                                      "unit": "T f64 lane-op/s (same 28-op count vs the in-process DFMA probe)"}
+        else:
+            e.update(bound="hbm", unit="GB/s", achieved=f["bytes"] / t / 1e9, peak=hbm,
+                     frac=f["bytes"] / t / 1e9 / hbm, bytes_per_launch=f["bytes"])
+            if f["ops"]:
+                e.update(tensor_tops=f["ops"] / t / 1e12, tensor_peak_tops=i8_tops,
+                         tensor_frac=(f["ops"] / t / 1e12 / i8_tops) if i8_tops else None)
+        out[nm] = e
+    for grp in ("k1", "k2"):
+        mine = [(fam[n], n) for n in fam if n.startswith(grp + ".")]
+        ms = sum(f["ms"] for f, _ in mine)
+        byts = sum(f["bytes"] * f["n"] for f, _ in mine)
+        ops = sum(f["ops"] * f["n"] for f, _ in mine)
+        g = {"ms_per_fwd": ms, "achieved_gbs": byts / (ms * 1e-3) / 1e9, "frac": byts / (ms * 1e-3) / 1e9 / hbm}
+        if ops and i8_tops:
+            g["tensor_frac"] = ops / (ms * 1e-3) / 1e12 / i8_tops
+        out[grp + ".all"] = g
+    return out
+
+
+def ncu_summary():
+    """Per-launch DRAM traffic and pipe utilisation of the dominant kernel from
+    the newest committed `ncu --set full` capture summary (profiles/r*/k3_ncu.json)."""
+    for rnd in ("r02", "r01"):
+        p = os.path.join(ROOT, "profiles", rnd, "k3_ncu.json")
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            d["file"] = os.path.relpath(p, ROOT)
+            return d
+    return None
+
+
+# ---- the reference's CPU path (oracle/_ref) ----------------------------------
+
+def _ref_setup(dims, blocks, cal_export, abits, rho):
+    """The reference build's model (seeded like make_toy_model) with `blocks`
+    blocks and the given calibration tables (the first `blocks` blocks')."""
+    from oracle import oracle as O
+    chk = O.Checker(O.REF_SO)
+    d = O.Dims(image=dims.image, channels=dims.channels, patch=dims.patch, embed=dims.embed, state=dims.state,
+               blocks=blocks, classes=dims.classes, conv_width=dims.conv_width)
+    m = chk.model(d, SEED)
+    scan, lin = cal_export
+    spec = O.Spec(wbits=4, abits=abits, obits=8, n_refresh=10, rho=rho, d1=True, d2=True)
+    cal = O.Calibration(spec, scan=[O.TensorCal(t.theta, t.s_in, t.s_full, t.excluded) for t in scan[:blocks * 6]],
+                        lin=[O.TensorCal(t.theta, t.s_in, t.s_full, t.excluded) for t in lin[:blocks * 4]])
+    return chk, m, m.calib_from(cal)
+
+
+def cpu_full_forward(dims, cal_export, images_np, abits, rho, n_img):
+    """The reference's CPU implementation (the reference's own compiled
+    primitives under the shared driver, oracle/_ref) on n_img images through
+    ALL blocks, one image per host thread. Returns (images/s, cores, sample,
+    logits). No extrapolation: the timed call is the whole forward."""
     from oracle import oracle as O
     if not O.ref_available():
         return None
-    chk = O.Checker(O.REF_SO)
+    chk, m, ch = _ref_setup(dims, dims.blocks, cal_export, abits, rho)
     cores = os.cpu_count() or 1
-    nblk = 2
-    d = O.Dims(image=model_dims.image, channels=model_dims.channels, patch=model_dims.patch,
-               embed=model_dims.embed, state=model_dims.state, blocks=nblk, classes=model_dims.classes,
-               conv_width=model_dims.conv_width)
-    m = chk.model(d, SEED)
-    scan, lin = cal_export
-    nd = 2
-    spec = O.Spec(wbits=4, abits=abits, obits=8, n_refresh=10, rho=0.01, d1=True, d2=True)
-    cal = O.Calibration(spec, scan=[O.TensorCal(t.theta, t.s_in, t.s_full, t.excluded) for t in scan[:nblk * nd * 3]],
-                        lin=[O.TensorCal(t.theta, t.s_in, t.s_full, t.excluded) for t in lin[:nblk * (nd + 2)]])
-    ch = m.calib_from(cal)
-    n_img = min(cores, images_np.shape[0])
     imgs = np.ascontiguousarray(images_np[:n_img])
-    for _ in range(warmup):
-        m.forward(imgs, ch, 1, threads=cores)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        m.forward(imgs, ch, 1, threads=cores)
-        times.append(time.perf_counter() - t0)
-    t = float(np.median(times))
-    per_img_full = t * (model_dims.blocks / nblk) / n_img
-    sample = (f"{n_img} images x {nblk} of {model_dims.blocks} blocks (x{model_dims.blocks // nblk} to the full "
-              f"forward), W4A4 dynamic D1+D2, {cores} threads, median of {steps}")
-    return 1.0 / per_img_full, cores, sample
+    t0 = time.perf_counter()
+    logits = m.forward(imgs, ch, 1, threads=min(cores, n_img))
+    t = time.perf_counter() - t0
+    sample = (f"{n_img} images through all {dims.blocks} blocks (full forward, no extrapolation), W4A4 dynamic "
+              f"D1+D2, one image per thread on {min(cores, n_img)} of {cores} host threads, one timed run "
+              f"of {t:.1f} s")
+    return n_img / t, min(cores, n_img), sample, logits
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path on this box's host cores, each
+    step a bounded sample (one image per core through 2 of the 24 blocks;
+    images/s extrapolated to the full depth, ms_per_step = the sample's time)."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
@@ -157,22 +347,31 @@ def run_reference(args):
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference build) missing"}))
         return 0
-    dims = ob.Dims(embed=args.embed, blocks=args.blocks)
+    dims = ob.Dims(embed=args.embed, blocks=args.blocks, image=args.image)
+    nblk = min(2, dims.blocks)
     chk = O.Checker(O.REF_SO)
-    # calibration of the first 2 blocks on the CPU (FP forward with the recorder)
     d2 = O.Dims(image=dims.image, channels=dims.channels, patch=dims.patch, embed=dims.embed, state=dims.state,
-                blocks=2, classes=dims.classes, conv_width=dims.conv_width)
+                blocks=nblk, classes=dims.classes, conv_width=dims.conv_width)
     m = chk.model(d2, SEED)
     cores = os.cpu_count() or 1
-    spec = O.Spec(wbits=4, abits=args.abits, obits=8, n_refresh=10, rho=0.01)
-    cimgs = chk.normal(SEED + 7, 2 * dims.pix)
-    cal = m.calibrate(cimgs, spec, threads=cores).export()
-    imgs = chk.normal(SEED + 100, cores * dims.pix).reshape(cores, dims.image, dims.image, dims.channels)
-    ips, cores, sample = cpu_baseline(dims, (cal.scan, cal.lin), imgs, args.abits, steps=args.steps,
-                                      warmup=min(args.warmup, 1))
+    spec = O.Spec(wbits=4, abits=args.abits, obits=8, n_refresh=10, rho=args.rho)
+    cal = m.calibrate(chk.normal(SEED + 7, 2 * dims.pix), spec, threads=cores)  # FP forward + recorder, on the CPU
+    n_img = max(1, min(cores, args.batch))
+    imgs = chk.normal(SEED + 100, n_img * dims.pix).reshape(n_img, dims.image, dims.image, dims.channels)
+    for _ in range(args.warmup):
+        m.forward(imgs, cal, 1, threads=cores)
+    times = []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        m.forward(imgs, cal, 1, threads=cores)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    ips = n_img / (t * dims.blocks / nblk)
+    sample = (f"{n_img} images x {nblk} of {dims.blocks} blocks per step (x{dims.blocks / nblk:g} to the full "
+              f"forward), W4A4 dynamic D1+D2, {cores} threads, median of {len(times)} steps")
     cfg = dict(CONFIG, global_batch=args.batch * max(args.gpus, 1), parallelism=f"dp{max(args.gpus, 1)}")
-    line = {"metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * args.batch / ips, "higher_is_better": True,
+    line = {"metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": args.gpus, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8/f64", "data": "synthetic", "config": cfg,
             "impl": "reference",
             "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
@@ -181,6 +380,8 @@ def run_reference(args):
     return 0
 
 
+# ---- our arm --------------------------------------------------------------------
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -188,73 +389,64 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = ob.Context(local, stream=stream)
-    dims = ob.Dims(embed=args.embed, blocks=args.blocks)
-    B = args.batch
+    dims = ob.Dims(embed=args.embed, blocks=args.blocks, image=args.image)
+    B = args.batch  # per rank (weak scaling); rank r holds samples [r*B, (r+1)*B) of the global batch
     model = ob.Model(ctx, dims, SEED)
-    spec = ob.QuantSpec(wbits=4, abits=args.abits, obits=8, n_refresh=10, rho=0.01, d1=True, d2=True)
-    gcal = torch.Generator(device="cuda").manual_seed(SEED + 7)
-    cal_imgs = torch.randn(8, dims.image, dims.image, dims.channels, dtype=torch.float64, device="cuda",
-                           generator=gcal)
+    spec = ob.QuantSpec(wbits=4, abits=args.abits, obits=8, n_refresh=10, rho=args.rho, d1=True, d2=True)
+    gcal = torch.Generator(device=dev).manual_seed(SEED + 7)  # the same calibration batch on every rank
+    cal_imgs = torch.randn(8, dims.image, dims.image, dims.channels, dtype=torch.float64, device=dev, generator=gcal)
     cal = model.calibrate(cal_imgs, spec, chunk=8)
     del cal_imgs
-    gen = torch.Generator(device="cuda").manual_seed(SEED + 100 + rank)
-    images = torch.randn(B, dims.image, dims.image, dims.channels, dtype=torch.float64, device="cuda", generator=gen)
-    logits = torch.empty(B, dims.classes, dtype=torch.float64, device="cuda")
-    gathered = [torch.empty_like(logits) for _ in range(world)] if world > 1 else None
+    gen = torch.Generator(device=dev).manual_seed(SEED + 100 + rank)
+    images = torch.randn(B, dims.image, dims.image, dims.channels, dtype=torch.float64, device=dev, generator=gen)
+    logits = torch.empty(B, dims.classes, dtype=torch.float64, device=dev)
     if args.split_parts is not None:
         model.set_option("split_parts", args.split_parts)
     if args.feed_chunks is not None:
         model.set_option("feed_chunks", args.feed_chunks)
-    model.use_graphs(True)
 
     def step():
         model.forward(images, cal, ob.MODE_DYNAMIC, logits=logits)
-        if world > 1:
-            dist.all_gather(gathered, logits)
+        gather_logits(dist, logits, world)
 
-    for _ in range(max(args.warmup, 3)):
+    # kernels per step: one eager forward (graph replays launch the same kernels)
+    c0 = ctx.launch_count()
+    model.forward(images, cal, ob.MODE_DYNAMIC, logits=logits)
+    launches_per_step = ctx.launch_count() - c0
+    model.use_graphs(True)
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def cuda_timer():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        return (lambda: e0.record(stream)), (lambda: e1.record(stream)), (lambda: e0.elapsed_time(e1))
+
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = timed_steps(step, args.steps, world, dist, torch.cuda.synchronize, cuda_timer)
+    ms = max_over_ranks(dist, ms, world, dev)
     ms_per_step = ms / args.steps
     value = world * B * args.steps / (ms / 1e3)
     finite = bool(torch.isfinite(logits).all().item())
 
-    # per-kernel device time of one forward (CUDA events around every launch)
+    # per-op device time of one single-stream forward (CUDA events around every op)
+    launches = model.forward_profile_launches(images, cal, ob.MODE_DYNAMIC, logits=logits)
     _, fam = model.forward_profile(images, cal, ob.MODE_DYNAMIC, logits=logits)
-    launches_per_fwd = sum(n for _, n in fam.values())
     fp64_peak = ctx.measure_fp64_peak()
+    i8_peak = ctx.measure_i8_peak()
 
-    # e2e: the C-ABI call with host buffers (H2D images + forward + D2H logits inside)
-    # pinned host buffers (what a serving front end hands the library)
+    # e2e: the C-ABI call with pinned host buffers (H2D images + forward + D2H logits inside)
     host_imgs = torch.empty(images.shape, dtype=torch.float64, pin_memory=True)
     host_imgs.copy_(images)
     host_imgs = host_imgs.numpy()
     host_logits = torch.empty((B, dims.classes), dtype=torch.float64, pin_memory=True).numpy()
-    for _ in range(max(args.warmup, 3)):  # graph capture of the host-feed path, pinned-page warm-up
+    for _ in range(warm):  # graph capture of the host-feed path, pinned-page warm-up
         model.forward_host(host_imgs, cal, ob.MODE_DYNAMIC, logits=host_logits)
     n_e2e = max(1, args.steps)
     if world > 1:
@@ -262,75 +454,79 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(n_e2e):
         model.forward_host(host_imgs, cal, ob.MODE_DYNAMIC, logits=host_logits)
-    e2e_s = (time.perf_counter() - t0) / n_e2e
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(dist, (time.perf_counter() - t0) / n_e2e, world, dev)
     e2e_val = world * B / e2e_s
+    dev_logits = logits.cpu().numpy()
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # the reference's CPU path on rank 0 (any N): full-depth forward of the first
+    # images of this rank's batch, timed, and its logits compared with ours
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(dims, cal.export(), host_imgs, args.abits)
+            n_img = args.cpu_images or (os.cpu_count() or 1)
+            r = cpu_full_forward(dims, cal.export(), host_imgs, args.abits, args.rho, min(n_img, B))
+            if r is not None:
+                ips, cores, sample, ref_logits = r
+                cpu = {"value": ips, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
+                n = ref_logits.shape[0]
+                diff = float(np.max(np.abs(host_logits[:n] - ref_logits)))
+                parity = {"images": n, "max_abs_diff": diff,
+                          "max_rel_diff": diff / float(np.max(np.abs(ref_logits))),
+                          "bit_identical": bool(np.array_equal(host_logits[:n], ref_logits)),
+                          "device_path_equals_e2e": bool(np.array_equal(dev_logits, host_logits)),
+                          "against": "reference build (oracle/_ref): same images, same GPU calibration, all blocks",
+                          "tolerance": "north star <= 1e-3 relative on logits; this build targets 0"}
         except Exception as exc:  # reported, never fatal for the GPU number
-            cpu = ("error", str(exc))
+            cpu = {"error": str(exc)}
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         L, E, N = dims.tokens, dims.embed, dims.state
-        scan_ms, scan_n = fam["k3_scan"]
-        # Algorithmic work of one scan launch:
-        # S*T*E*N state-element-steps per direction x 28 arithmetic lane-ops (discretize 2,
-        # 3 quantizations x 7, update 2, output 2; the exp is not counted).
-        # Peak: the measured f64 lane-op rate of this GPU (one DFMA = 1 op).
-        ops_per_elem = 28.0
-        elem = B * L * E * N * len(model.orders)  # one launch scans every direction
-        # one scan op per block (its launches: the step-table prep + the scan kernel)
-        achieved = elem * ops_per_elem / (scan_ms / dims.blocks * 1e-3) / 1e12
-        peak_ops = fp64_peak / 2.0
-        traffic = scan_traffic_bytes()
-        cfg = dict(CONFIG, global_batch=B * world, parallelism=f"dp{world}")
+        peaks = measured_peaks()
+        kern = kernel_rooflines(launches, B=B, L=L, E=E, N=N, blocks=dims.blocks, abits=args.abits, peaks=peaks,
+                                i8_tops=i8_peak, fp64_tflops=fp64_peak, sms=ctx.num_sms())
+        cfg = dict(CONFIG, global_batch=B * world, parallelism=f"dp{world}", image=dims.image, seq_len=L,
+                   embed=E, blocks=dims.blocks)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "warmup": warm, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int8/f64", "data": "synthetic",
                 "config": cfg,
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(host_imgs.nbytes),
                         "d2h_bytes_per_step": int(host_logits.nbytes)},
-                "gpu_launches": int(launches_per_fwd * args.steps),
-                "roofline": {"kernel": "k3_scan", "bound": "fp64", "achieved": achieved, "peak": peak_ops,
-                             "unit": "Tops (f64 lane-ops/s)", "frac": achieved / peak_ops if peak_ops else None,
-                             "traffic": traffic,
-                             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r01/ncu_traffic_r01l.json)",
-                             "peak_source": "measured in-process: DFMA probe (1 op per DFMA lane)",
-                             "work": f"{ops_per_elem:.0f} f64 lane-ops x S*T*E*N*dirs state-element-steps per launch"},
-                "kernels_ms_per_step": {k: v[0] for k, v in fam.items()},
-                "kernels_launches_per_step": {k: v[1] for k, v in fam.items()},
-                "clocks": clk.summary(), "logits_finite": finite}
-        if cpu and cpu[0] != "error":
-            line["cpu_baseline"] = {"value": cpu[0], "unit": UNIT, "cores": cpu[1], "kind": "reference",
-                                    "sample": cpu[2]}
-        elif cpu:
-            line["cpu_baseline"] = {"error": cpu[1]}
+                "gpu_launches": int(launches_per_step * args.steps),
+                "gpu_launches_per_step": int(launches_per_step)}
+        if kern:
+            k3 = kern["k3.scan"]
+            nc = ncu_summary()
+            line["roofline"] = {"kernel": "k3_scan_fast (both directions + step tables)", "bound": k3["bound"],
+                                "achieved": k3["achieved"], "peak": k3["peak"], "unit": k3["unit"],
+                                "frac": k3["frac"], "model": k3["model"],
+                                "traffic": nc.get("dram_bytes_per_launch") if nc else None,
+                                "traffic_source": nc["file"] if nc else None,
+                                "ncu": {k: v for k, v in (nc or {}).items() if k not in ("file",)},
+                                "secondary_f64": k3.get("secondary_f64"),
+                                "peaks": peaks["source"]}
+            line["kernels"] = kern
+        line["kernels_ms_per_step"] = {k: v[0] for k, v in fam.items()}
+        line["clocks"] = clk.summary()
+        line["logits_finite"] = finite
+        if parity:
+            line["parity"] = parity
+        if cpu:
+            line["cpu_baseline"] = cpu
+        line["peaks_measured_in_process"] = {"i8_tensor_tops": i8_peak, "fp64_tflops": fp64_peak}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
-def scan_traffic_bytes():
-    """DRAM bytes (read + write) of one k3_scan_fast launch from the committed
-    `ncu --set full` capture of this workload, or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_traffic_r01l.json")
-    try:
-        with open(path) as f:
-            k = json.load(f)["kernels"]
-        return [v for n, v in k.items() if n.startswith("k3_scan_fast")][0][0]["traffic_bytes"]
-    except Exception:
-        return None
-
-
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(argv, args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -222,6 +222,13 @@ ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops);
  * roofline denominator. */
 ouro_status ouro_b200_measure_i8_peak(ouro_b200_ctx* ctx, double* tops);
 
+/* Number of this library's kernels launched so far by the calling host thread
+ * (every launcher counts its <<<>>> launches; CUDA-graph replays are not
+ * host launches and do not count). The delta over one eager forward is the
+ * kernels per step a graph replay of that forward launches (bench.py
+ * `gpu_launches`). */
+ouro_status ouro_b200_launch_count(long long* out);
+
 /* Spike injection (SpikeSettings / SpikeHook, quant.hpp:105-118,
  * quant.cpp:420-446): at (sample, block, dir, t) positions chosen by the
  * reference's mix64 chain with probability `rate`, `channels` hashed channels'

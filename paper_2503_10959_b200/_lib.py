@@ -56,6 +56,7 @@ _SIGS = {
     "ouro_b200_forward_profile_launches": ([_P, _P, _I, _I, _I, _P, _SZ, _P, _P, _P, _SZ, C.POINTER(_SZ)], _I),
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
+    "ouro_b200_launch_count": ([C.POINTER(C.c_longlong)], _I),
     "ouro_b200_math_eval": ([_P, _I, _P, _P, _SZ], _I),
     "ouro_b200_detect_quantize_planes": ([_P, _P, _SZ, _SZ, _SZ, _D, _P, _SZ, C.c_uint, C.c_uint, _SZ, _P, _P, _P,
                                           _P, _P, _P, _P], _I),

@@ -272,6 +272,17 @@ void load_calibration_dir(Calibration& c, int state, const std::string& dir_s, b
                                  "block" + std::to_string(b) + ".dir" + std::to_string(d) + "." + kKinds[k], c.scan[i]);
     c.lin.clear();
     c.d2 = false;
+    // A repo-written directory records whether its peaks were taken on the D1
+    // (RMSNorm pre-norm) activations; a forward with the other setting would run
+    // on thresholds of a different distribution, so a mismatch is rejected here
+    // (and Model::forward checks cal.d1 against its own d1).
+    if (fs::exists(dir / "d2_linear_sites.txt")) {
+        const Record l = parse(read_file(dir / "d2_linear_sites.txt"), "D2 record");
+        auto it = l.kv.find("d1");
+        if (it != l.kv.end() && (std::stoul(it->second) != 0) != c.d1)
+            throw ValidationError("calibration directory " + dir.string() + " was recorded with d1 = " + it->second +
+                                  " but loaded with d1 = " + (c.d1 ? "1" : "0"));
+    }
     if (want_d2) {
         if (!fs::exists(dir / "d2_linear_sites.txt"))
             throw ValidationError("calibration directory " + dir.string() +

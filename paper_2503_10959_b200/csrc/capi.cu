@@ -44,16 +44,31 @@ struct ouro_b200_model {
     ouro_b200_ctx* ctx = nullptr;
     std::unique_ptr<ob::Model> m;
     bool graphs = false;
+    // A captured graph bakes in raw pointers (workspace, weights, calibration
+    // tables) and by-value kernel parameters (thresholds, literal routing), so
+    // it is keyed on everything those depend on: the calibration's version (new
+    // on create and on every edit; a freed-and-reallocated handle never matches),
+    // the device allocation epoch (any DevBuf (re)allocation), and the call's
+    // own arguments.
     struct GraphKey {
         const void* cal;
+        uint64_t cal_version;
         int mode, d1, d2;
         const double* img;
         size_t B;
         double* logits;
+        uint64_t epoch;
         bool operator==(const GraphKey& o) const {
-            return std::tie(cal, mode, d1, d2, img, B, logits) == std::tie(o.cal, o.mode, o.d1, o.d2, o.img, o.B, o.logits);
+            return std::tie(cal, cal_version, mode, d1, d2, img, B, logits, epoch) ==
+                   std::tie(o.cal, o.cal_version, o.mode, o.d1, o.d2, o.img, o.B, o.logits, o.epoch);
         }
     };
+    void drop_graphs() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (hexec) cudaGraphExecDestroy(hexec);
+        exec = hexec = nullptr;
+        key_hits = hkey_hits = 0;
+    }
     GraphKey key{};
     int key_hits = 0;
     cudaGraphExec_t exec = nullptr;
@@ -74,6 +89,72 @@ struct ouro_b200_calib {
 struct ouro_b200_trace {
     ob::Model::TraceSink sink;
 };
+
+namespace {
+// Capture `body` on stream st into a fresh executable graph (replacing *exec)
+// and launch it once.
+template <class Fn>
+void capture_and_launch(cudaStream_t st, cudaGraphExec_t* exec, Fn&& body) {
+    cudaGraph_t g = nullptr;
+    ob::cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+        body();
+    } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    ob::cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+    if (*exec) cudaGraphExecDestroy(*exec);
+    *exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(exec, g, 0);
+    cudaGraphDestroy(g);
+    ob::cuda_check(e, "graph instantiate");
+    ob::cuda_check(cudaGraphLaunch(*exec, st), "graph launch");
+}
+
+// Graph policy shared by the device-buffer and host-buffer entry points: the
+// first call with a key runs eagerly (it may allocate workspace or upload a
+// calibration), the second identical call captures, later ones replay. The key's
+// epoch is re-read after an eager run so allocations made by that run count.
+template <class Fn>
+void run_with_graph(ouro_b200_model* m, cudaStream_t st, ouro_b200_model::GraphKey key,
+                    ouro_b200_model::GraphKey* slot, int* hits, cudaGraphExec_t* exec, Fn&& body) {
+    if (!m->graphs || st == nullptr) {  // graphs need a capturable (non-legacy) stream
+        body();
+        return;
+    }
+    key.epoch = ob::alloc_epoch();
+    if (*exec && *slot == key) {
+        ob::cuda_check(cudaGraphLaunch(*exec, st), "graph launch");
+        return;
+    }
+    if (*slot == key && *hits >= 1) {
+        capture_and_launch(st, exec, body);
+        require(ob::alloc_epoch() == key.epoch, "internal error: device memory was reallocated during graph capture");
+        return;
+    }
+    if (*exec) {
+        cudaGraphExecDestroy(*exec);
+        *exec = nullptr;
+    }
+    body();
+    key.epoch = ob::alloc_epoch();
+    if (*slot == key) {
+        ++*hits;
+    } else {
+        *slot = key;
+        *hits = 1;
+    }
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // clear a benign "not a device pointer" status
+    return pinned;
+}
+}  // namespace
 
 extern "C" {
 
@@ -326,14 +407,7 @@ ouro_status ouro_b200_model_set_tensor(ouro_b200_model* m, const char* name, con
     return guarded([&] {
         require(m && name && host, "model_set_tensor: NULL argument");
         m->m->set_tensor(name, host, n);
-        if (m->exec) {
-            cudaGraphExecDestroy(m->exec);
-            m->exec = nullptr;
-        }
-        if (m->hexec) {
-            cudaGraphExecDestroy(m->hexec);
-            m->hexec = nullptr;
-        }
+        m->drop_graphs();  // weights are uploaded by forward()'s host code, which a replay skips
     });
 }
 ouro_status ouro_b200_model_get_tensor(ouro_b200_model* m, const char* name, double* host, size_t cap,
@@ -483,6 +557,7 @@ ouro_status ouro_b200_calib_set(ouro_b200_calib* c, int which, size_t idx, doubl
         if (s_full) std::memcpy(t.s_full.data(), s_full, t.s_full.size() * sizeof(double));
         if (excluded) std::memcpy(t.excluded.data(), excluded, t.excluded.size());
         c->c->dirty = true;
+        c->c->version = ob::next_calib_version();
     });
 }
 
@@ -490,16 +565,10 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on) {
     return guarded([&] {
         require(m != nullptr, "model_use_graphs: model is NULL");
         m->graphs = on != 0;
-        if (!m->graphs && m->exec) {
-            cudaGraphExecDestroy(m->exec);
-            m->exec = nullptr;
-        }
-        if (!m->graphs && m->hexec) {
-            cudaGraphExecDestroy(m->hexec);
-            m->hexec = nullptr;
-        }
+        if (!m->graphs) m->drop_graphs();
     });
 }
+
 
 ouro_status ouro_b200_forward(ouro_b200_model* m, ouro_b200_calib* c, int mode, int d1, int d2,
                               const double* images_dev, size_t B, double* logits_dev) {
@@ -508,44 +577,11 @@ ouro_status ouro_b200_forward(ouro_b200_model* m, ouro_b200_calib* c, int mode, 
         require(mode == ob::MODE_FP || c != nullptr, "forward: quantized modes need a calibration");
         ob::Calibration* cal = c ? c->c.get() : nullptr;
         cudaStream_t st = m->ctx->c->stream;
-        ouro_b200_model::GraphKey key{cal, mode, d1, d2, images_dev, B, logits_dev};
-        // graphs need a capturable stream (not the legacy default stream)
-        const bool stale = (cal && cal->dirty) || st == nullptr;
-        if (m->graphs && !stale && m->exec && m->key == key) {
-            ob::cuda_check(cudaGraphLaunch(m->exec, st), "graph launch");
-            return;
-        }
-        if (m->graphs && !stale && m->key == key && m->key_hits >= 1) {
-            // second identical call: capture the launch sequence once, replay from now on
-            cudaGraph_t g = nullptr;
-            ob::cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-            try {
-                m->m->forward(cal, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev, nullptr,
-                              nullptr);
-            } catch (...) {
-                cudaStreamEndCapture(st, &g);
-                if (g) cudaGraphDestroy(g);
-                throw;
-            }
-            ob::cuda_check(cudaStreamEndCapture(st, &g), "end capture");
-            if (m->exec) cudaGraphExecDestroy(m->exec);
-            m->exec = nullptr;
-            ob::cuda_check(cudaGraphInstantiate(&m->exec, g, 0), "graph instantiate");
-            cudaGraphDestroy(g);
-            ob::cuda_check(cudaGraphLaunch(m->exec, st), "graph launch");
-            return;
-        }
-        m->m->forward(cal, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev, nullptr, nullptr);
-        if (m->key == key) {
-            ++m->key_hits;
-        } else {
-            m->key = key;
-            m->key_hits = 1;
-            if (m->exec) {
-                cudaGraphExecDestroy(m->exec);
-                m->exec = nullptr;
-            }
-        }
+        ouro_b200_model::GraphKey key{cal, cal ? cal->version : 0, mode, d1, d2, images_dev, B, logits_dev, 0};
+        run_with_graph(m, st, key, &m->key, &m->key_hits, &m->exec, [&] {
+            m->m->forward(cal, mode, d1 != 0, d2 != 0, images_dev, static_cast<int>(B), logits_dev, nullptr,
+                          nullptr);
+        });
     });
 }
 
@@ -561,11 +597,9 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
         mm.w.img.ensure(B * pix);
         mm.w.logits.ensure(B * mm.d.classes);
         const size_t lbytes = B * mm.d.classes * sizeof(double);
-        cudaPointerAttributes attr{};
-        const bool pinned = cudaPointerGetAttributes(&attr, images_host) == cudaSuccess &&
-                            attr.type == cudaMemoryTypeHost;
-        cudaGetLastError();  // clear a benign "not a device pointer" status
-        if (!pinned || st == nullptr) {  // pageable images: staged copy, no overlap
+        // The overlapped (and capturable) path needs both host buffers pinned: a
+        // pageable copy can neither overlap nor be captured into a graph.
+        if (!is_pinned(images_host) || !is_pinned(logits_host) || st == nullptr) {
             ob::cuda_check(cudaMemcpyAsync(mm.w.img.p, images_host, B * pix * sizeof(double), cudaMemcpyHostToDevice, st),
                            "H2D images");
             ouro_status s = ouro_b200_forward(m, c, mode, d1, d2, mm.w.img.p, B, mm.w.logits.p);
@@ -575,50 +609,18 @@ ouro_status ouro_b200_forward_host(ouro_b200_model* m, ouro_b200_calib* c, int m
             return;
         }
         if (!m->copy) ob::cuda_check(cudaStreamCreateWithFlags(&m->copy, cudaStreamNonBlocking), "copy stream");
-        // pinned images: the H2D copy runs in 8 chunks on the copy stream, each chunk's
+        // pinned images: the H2D copy runs in chunks on the copy stream, each chunk's
         // patch gather + embedding waits only for its own chunk (Model::HostFeed)
         ob::Model::HostFeed feed;
         feed.host = images_host;
         feed.copy = m->copy;
         feed.chunks = B >= 64 ? m->m->feed_chunks : 1;
-        auto body = [&] {
+        ouro_b200_model::GraphKey key{cal, cal ? cal->version : 0, mode, d1, d2, images_host, B, logits_host, 0};
+        run_with_graph(m, st, key, &m->hkey, &m->hkey_hits, &m->hexec, [&] {
             mm.forward(cal, mode, d1 != 0, d2 != 0, mm.w.img.p, static_cast<int>(B), mm.w.logits.p, nullptr, nullptr,
                        &feed);
             ob::cuda_check(cudaMemcpyAsync(logits_host, mm.w.logits.p, lbytes, cudaMemcpyDeviceToHost, st), "D2H logits");
-        };
-        ouro_b200_model::GraphKey key{cal, mode, d1, d2, images_host, B, logits_host};
-        const bool stale = cal && cal->dirty;
-        if (m->graphs && !stale && m->hexec && m->hkey == key) {
-            ob::cuda_check(cudaGraphLaunch(m->hexec, st), "graph launch");
-        } else if (m->graphs && !stale && m->hkey == key && m->hkey_hits >= 1) {
-            cudaGraph_t g = nullptr;
-            ob::cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-            try {
-                body();
-            } catch (...) {
-                cudaStreamEndCapture(st, &g);
-                if (g) cudaGraphDestroy(g);
-                throw;
-            }
-            ob::cuda_check(cudaStreamEndCapture(st, &g), "end capture");
-            if (m->hexec) cudaGraphExecDestroy(m->hexec);
-            m->hexec = nullptr;
-            ob::cuda_check(cudaGraphInstantiate(&m->hexec, g, 0), "graph instantiate");
-            cudaGraphDestroy(g);
-            ob::cuda_check(cudaGraphLaunch(m->hexec, st), "graph launch");
-        } else {
-            body();
-            if (m->hkey == key) {
-                ++m->hkey_hits;
-            } else {
-                m->hkey = key;
-                m->hkey_hits = 1;
-                if (m->hexec) {
-                    cudaGraphExecDestroy(m->hexec);
-                    m->hexec = nullptr;
-                }
-            }
-        }
+        });
         ob::cuda_check(cudaStreamSynchronize(st), "forward_host sync");
     });
 }
@@ -627,14 +629,7 @@ ouro_status ouro_b200_model_set_spikes(ouro_b200_model* m, const ouro_b200_spike
     return guarded([&] {
         require(m != nullptr, "model_set_spikes: model is NULL");
         m->m->spikes = spike_from(spikes);
-        if (m->exec) {
-            cudaGraphExecDestroy(m->exec);
-            m->exec = nullptr;
-        }
-        if (m->hexec) {
-            cudaGraphExecDestroy(m->hexec);
-            m->hexec = nullptr;
-        }
+        m->drop_graphs();
     });
 }
 
@@ -657,14 +652,7 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         } else {
             throw ob::ValidationError("model_set_option: unknown option '" + k + "'");
         }
-        if (m->exec) {
-            cudaGraphExecDestroy(m->exec);
-            m->exec = nullptr;
-        }
-        if (m->hexec) {
-            cudaGraphExecDestroy(m->hexec);
-            m->hexec = nullptr;
-        }
+        m->drop_graphs();
     });
 }
 
@@ -723,6 +711,13 @@ ouro_status ouro_b200_measure_fp64_peak(ouro_b200_ctx* ctx, double* tflops) {
     return guarded([&] {
         require(ctx && tflops, "measure_fp64_peak: NULL argument");
         *tflops = ob::measure_fp64_peak(ctx->c->stream, ctx->c->num_sms);
+    });
+}
+
+ouro_status ouro_b200_launch_count(long long* out) {
+    return guarded([&] {
+        require(out != nullptr, "launch_count: out is NULL");
+        *out = ob::kernel_launch_counter();
     });
 }
 

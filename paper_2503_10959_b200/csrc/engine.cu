@@ -2,6 +2,7 @@
 // Every arithmetic step of the forward runs in the K1-K4 kernels; the host
 // only prepares weights (W4 row quantization, once per model, quant.cpp:355-402),
 // reduces calibration statistics (quantile, quant.cpp:117-177) and launches.
+#include <atomic>
 #include "engine.h"
 #include "seeded_rng.h"
 
@@ -30,9 +31,19 @@ void QuantSpec::validate() const {  // quant.cpp:54-60
     require(n_refresh >= 0, "n_refresh must be >= 0");
 }
 
+namespace {
+std::atomic<uint64_t> g_alloc_epoch{1};
+std::atomic<uint64_t> g_calib_version{1};
+}  // namespace
+uint64_t alloc_epoch() { return g_alloc_epoch.load(std::memory_order_acquire); }
+uint64_t next_calib_version() { return g_calib_version.fetch_add(1, std::memory_order_relaxed); }
+
 template <class T>
 void DevBuf<T>::release() {
-    if (p) cudaFree(p);
+    if (p) {
+        cudaFree(p);
+        g_alloc_epoch.fetch_add(1, std::memory_order_release);
+    }
     p = nullptr;
     n = 0;
 }
@@ -41,6 +52,7 @@ void DevBuf<T>::ensure(size_t count) {
     if (count <= n) return;
     release();
     cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    g_alloc_epoch.fetch_add(1, std::memory_order_release);
     n = count;
 }
 template <class T>

@@ -28,6 +28,13 @@ inline void require(bool c, const std::string& m) {
     if (!c) throw ValidationError(m);
 }
 void cuda_check(cudaError_t e, const char* what);
+// Process-wide counter bumped by every device (re)allocation or free of a
+// DevBuf. A captured CUDA graph holds raw workspace/weight pointers, so the C
+// ABI keys its graphs on this epoch and re-captures after any reallocation.
+uint64_t alloc_epoch();
+// Fresh id for a calibration's contents: assigned at creation and on every
+// edit, so a graph never replays thresholds (passed by value) of an older version.
+uint64_t next_calib_version();
 
 struct Dims {  // ModelDims, ssm.hpp:42-56
     int image = 32, channels = 3, patch = 4, embed = 16, state = 4, blocks = 2, classes = 10, conv_width = 3;
@@ -107,6 +114,7 @@ class Calibration {
     std::vector<int> literal_any;     // [block][dir]
     std::vector<int> lin_literal;     // [block][site]: some step fails the channel-local check
     bool dirty = true;
+    uint64_t version = next_calib_version();
     void upload(cudaStream_t st);
     const double* s_in_dev(bool is_lin, size_t idx) const;
     const double* s_full_dev(bool is_lin, size_t idx) const;

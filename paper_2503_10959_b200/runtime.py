@@ -132,6 +132,12 @@ class Context:
         L.check(self.lib.ouro_b200_measure_i8_peak(self.h, C.byref(v)))
         return v.value
 
+    def launch_count(self) -> int:
+        """Kernels this library launched from the calling thread so far (graph replays excluded)."""
+        v = C.c_longlong()
+        L.check(self.lib.ouro_b200_launch_count(C.byref(v)))
+        return v.value
+
     def math_eval(self, fn: str, x):
         """Device exp / log1p / softplus / silu of a float64 CUDA tensor: the forms the
         kernels use, which restate glibc's so they equal the reference's bit for bit."""
