@@ -485,7 +485,7 @@ def run_ours(args):
         L, E, N = dims.tokens, dims.embed, dims.state
         peaks = measured_peaks()
         kern = kernel_rooflines(launches, B=B, L=L, E=E, N=N, blocks=dims.blocks, abits=args.abits, peaks=peaks,
-                                i8_tops=i8_peak, fp64_tflops=fp64_peak, sms=ctx.num_sms())
+                                i8_tops=i8_peak, fp64_tflops=fp64_peak, sms=ctx.num_sms)
         cfg = dict(CONFIG, global_batch=B * world, parallelism=f"dp{world}", image=dims.image, seq_len=L,
                    embed=E, blocks=dims.blocks)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -402,6 +402,10 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
                 "calibration does not match the model geometry");  // quant.cpp:508-510
         if (d2) require(cal->d2 && cal->lin.size() == static_cast<size_t>(cal->blocks) * cal->nsites(),
                         "calibration lacks linear-input records (D2)");
+        // thresholds and scales were recorded on the D1 (pre-norm) or the raw
+        // activation distribution; the other one would be silently miscalibrated
+        require(cal->d1 == d1, "calibration was recorded with d1 = " + std::to_string(cal->d1 ? 1 : 0) +
+                                   " but the forward runs with d1 = " + std::to_string(d1 ? 1 : 0));
         quantize(cal->spec.wbits);
         const_cast<Calibration*>(cal)->upload(ctx->stream);
     }
