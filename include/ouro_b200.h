@@ -310,6 +310,62 @@ typedef struct {
 ouro_status ouro_b200_gemm_bench(ouro_b200_ctx* ctx, const ouro_b200_bench_settings* s,
                                  ouro_b200_bench_record* records);
 
+/* ---- OURO tensor files (tensor_io.hpp:13-44) -----------
+ * The reference's container: "OURO" | u32 version 1 | u32 rank | u64 dims |
+ * u32 dtype | payload, little-endian. dtype: */
+enum { OURO_B200_DTYPE_F64 = 0, OURO_B200_DTYPE_I8 = 1, OURO_B200_DTYPE_U4 = 2 };
+/* write_tensor_f64 / _i8 / _u4 (tensor_io.cpp): data = f64[numel], int8[numel],
+ * or for U4 either int8 codes in [-8, 7] (data_packed = 0: packed here, element
+ * i in the low nibble of byte i/2 when i is even) or the packed payload itself
+ * (data_packed = 1, ceil(numel/2) bytes, e.g. a K1 operand produced with
+ * OURO_B200_CODES_PACKED_I4 and copied from the device). Written atomically
+ * (temporary file + rename). A code outside [-8, 7] is a validation error. */
+ouro_status ouro_b200_tensor_save(const char* path, int dtype, const uint64_t* shape, size_t rank, const void* data,
+                                  int data_packed);
+/* Header of a tensor file: dtype, rank and the first `cap` dims (shape may be
+ * NULL). Missing file, bad magic / version / dtype tag, truncation -> IO. */
+ouro_status ouro_b200_tensor_info(const char* path, int* dtype, uint64_t* shape, size_t cap, size_t* rank);
+/* Payload of a tensor file whose dtype must equal `dtype` (else IO, "dtype
+ * mismatch", as read_tensor_*): f64 / int8 elements, or for U4 the codes
+ * sign-extended to int8 (out_packed = 0, read_tensor_u4) or the packed bytes
+ * (out_packed = 1). cap = capacity of `out` in bytes. */
+ouro_status ouro_b200_tensor_load(const char* path, int dtype, void* out, size_t cap, int out_packed);
+
+/* ---- Pipeline stages on the GPU (ouromamba.h:58-65, capi.cpp:166-186) ------
+ * The settings a stage reads from the reference's RunConfig (config.hpp:17-47;
+ * the text parser itself is out of scope). Scan orders are
+ * row-forward, row-backward. run_id tags the metrics lines (the reference uses
+ * the FNV-1a hash of its canonical config text, run_id_of; NULL = "b200").
+ * d1 = d2 = 0 is the reference's own quantized pass. */
+typedef struct {
+    size_t image, channels, patch, embed, state, blocks, classes, conv_width; /* [model] */
+    uint64_t seed;
+    unsigned weight_bits, act_bits, outlier_bits; /* [quant] */
+    size_t n_refresh;                             /* 0 = never ("full") */
+    double outlier_quantile;                      /* rho */
+    const char* mode;                             /* "dynamic", "static" or "bypass" */
+    size_t eval_batch;
+    double spike_rate, spike_gain;
+    size_t spike_channels;
+    int d1, d2; /* declared extensions */
+    const char* run_id;
+    int device;
+} ouro_b200_stage_config;
+/* run_quant_eval (pipeline.cpp:115-167): make_toy_model(dims, seed), the
+ * calibration directory (its quantization settings must equal the config's),
+ * the first min(B, eval_batch) images of `images_file` (OURO f64 [B, H*W*C]);
+ * quantized_forward's metrics on the GPU (logits_mse, argmax_agreement, the
+ * teacher-forced mse_block<b>.dir<d>, and in dynamic mode the QuantHook timeline
+ * of sample 0's b_bar tensors) written to out_dir/metrics.txt in the
+ * reference's line format ("run=<id> stage=quant-eval k=v ...", "%.17g"), plus
+ * out_dir/manifest.txt. */
+ouro_status ouro_b200_quant_eval(const ouro_b200_stage_config* cfg, const char* calib_dir, const char* images_file,
+                                 const char* out_dir);
+/* run_calib (pipeline.cpp:100-113): GPU calibration of the images in
+ * `images_file` written as the reference's calibration directory (plus the D2
+ * tables when cfg->d2) and a manifest. */
+ouro_status ouro_b200_calib_stage(const ouro_b200_stage_config* cfg, const char* images_file, const char* out_dir);
+
 /* Diagnostic: y[i] = f(x[i]) on the device for the path's transcendental
  * functions, fn = 0 exp, 1 log1p, 2 softplus, 3 silu (tensor.hpp:146-154);
  * x and y are device pointers of n doubles. The device forms restate glibc's

@@ -160,10 +160,41 @@ class Checker:
             L.ref_pin_refresh_sweep.argtypes = [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_double, C.c_double, _SZ,
                                                 C.c_uint64, _P, _P]
             L.ref_pin_gemm_bench.argtypes = [_P, _SZ, C.c_double, _SZ, C.c_uint64, _P, _P]
+            L.ref_pin_run_id.argtypes = [C.c_char_p, C.c_char_p, _SZ]
+            L.ref_pin_run_quant_eval.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p]
+            L.ref_pin_run_calib.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p]
+            L.ref_pin_write_tensor.argtypes = [C.c_char_p, C.c_int, _P, _SZ, _P]
+            L.ref_pin_read_tensor_codes.argtypes = [C.c_char_p, C.c_int, _P, _SZ, C.POINTER(_SZ)]
 
     def _check(self, st: int) -> None:
         if st != 0:
             raise OracleError(self.lib.oro_last_error().decode())
+
+    # ---- the reference's own pipeline stages and tensor files (reference build only) ----
+    def ref_run_id(self, config_text: str) -> str:
+        buf = C.create_string_buffer(64)
+        self._check(self.lib.ref_pin_run_id(config_text.encode(), buf, 64))
+        return buf.value.decode()
+
+    def ref_run_quant_eval(self, config_text: str, calib_dir, images_file, out_dir) -> None:
+        self._check(self.lib.ref_pin_run_quant_eval(config_text.encode(), str(calib_dir).encode(),
+                                                    str(images_file).encode(), str(out_dir).encode()))
+
+    def ref_run_calib(self, config_text: str, images_file, out_dir) -> None:
+        self._check(self.lib.ref_pin_run_calib(config_text.encode(), str(images_file).encode(), str(out_dir).encode()))
+
+    def ref_write_tensor(self, path, dtype: int, data: np.ndarray) -> None:
+        """write_tensor_f64 (dtype 0) / _i8 (1) / _u4 (2) of the reference."""
+        arr = np.ascontiguousarray(data, np.float64 if dtype == 0 else np.int8)
+        shape = np.array(arr.shape, dtype=np.uint64)
+        self._check(self.lib.ref_pin_write_tensor(str(path).encode(), dtype, _ptr(shape), arr.ndim, _ptr(arr)))
+
+    def ref_read_tensor_codes(self, path, dtype: int, n: int) -> np.ndarray:
+        """read_tensor_i8 (dtype 1) / read_tensor_u4 (2) of the reference (flat codes)."""
+        out = np.zeros(max(n, 1), np.int8)
+        got = _SZ()
+        self._check(self.lib.ref_pin_read_tensor_codes(str(path).encode(), dtype, _ptr(out), out.size, C.byref(got)))
+        return out[:got.value]
 
     # ---- model ---------------------------------------------------------------
     def model(self, dims: Dims, seed: int, orders=(0, 1)) -> "Model":

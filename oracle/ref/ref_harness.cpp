@@ -11,7 +11,10 @@
 #include <cstring>
 
 #include "../oracle_ops.hpp"
+#include "ouro/config.hpp"
 #include "ouro/gemm.hpp"
+#include "ouro/pipeline.hpp"
+#include "ouro/tensor_io.hpp"
 #include "ouro/quant.hpp"
 #include "ouro/ssm.hpp"
 #include "ouro/tensor.hpp"
@@ -465,6 +468,50 @@ int ref_pin_load_calibration(const char* dir, void** out) {
             c.scan.push_back(std::move(tc));
         }
         *out = h.release();
+    });
+}
+
+// The reference's own pipeline stages (pipeline.cpp), driven by a config text in
+// the reference's format (parse_config_text): the stage entry points of the B200
+// C ABI (ouro_b200_quant_eval / ouro_b200_calib_stage) are checked against these
+// file for file. run_id_of gives the metrics lines' run tag.
+int ref_pin_run_id(const char* config_text, char* out, std::size_t cap) {
+    return guarded([&] {
+        const std::string id = ouro::run_id_of(ouro::parse_config_text(config_text));
+        if (id.size() + 1 > cap) throw ouro::ValidationError("run id buffer too small");
+        std::memcpy(out, id.c_str(), id.size() + 1);
+    });
+}
+int ref_pin_run_quant_eval(const char* config_text, const char* calib_dir, const char* images_file,
+                           const char* out_dir) {
+    return guarded([&] { ouro::run_quant_eval(ouro::parse_config_text(config_text), calib_dir, images_file, out_dir); });
+}
+int ref_pin_run_calib(const char* config_text, const char* images_file, const char* out_dir) {
+    return guarded([&] { ouro::run_calib(ouro::parse_config_text(config_text), images_file, out_dir); });
+}
+// write_tensor_f64 / _i8 / _u4 and their readers (tensor_io.cpp), for the
+// OURO container parity tests
+int ref_pin_write_tensor(const char* path, int dtype, const std::uint64_t* shape, std::size_t rank, const void* data) {
+    return guarded([&] {
+        ouro::Shape sh(shape, shape + rank);
+        std::size_t n = 1;
+        for (std::size_t d : sh) n *= d;
+        if (dtype == 0) {
+            ouro::write_tensor_f64(path, ouro::Tensor::from(sh, std::vector<double>(static_cast<const double*>(data),
+                                                                                    static_cast<const double*>(data) + n)));
+        } else {
+            std::vector<std::int8_t> v(static_cast<const std::int8_t*>(data), static_cast<const std::int8_t*>(data) + n);
+            if (dtype == 1) ouro::write_tensor_i8(path, sh, v);
+            else ouro::write_tensor_u4(path, sh, v);
+        }
+    });
+}
+int ref_pin_read_tensor_codes(const char* path, int dtype, std::int8_t* out, std::size_t cap, std::size_t* n) {
+    return guarded([&] {
+        auto r = dtype == 1 ? ouro::read_tensor_i8(path) : ouro::read_tensor_u4(path);
+        *n = r.second.size();
+        if (r.second.size() > cap) throw ouro::ValidationError("output buffer too small");
+        std::memcpy(out, r.second.data(), r.second.size());
     });
 }
 

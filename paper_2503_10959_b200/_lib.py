@@ -57,6 +57,11 @@ _SIGS = {
     "ouro_b200_measure_fp64_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_measure_i8_peak": ([_P, C.POINTER(_D)], _I),
     "ouro_b200_launch_count": ([C.POINTER(C.c_longlong)], _I),
+    "ouro_b200_tensor_save": ([C.c_char_p, _I, _P, _SZ, _P, _I], _I),
+    "ouro_b200_tensor_info": ([C.c_char_p, C.POINTER(_I), _P, _SZ, C.POINTER(_SZ)], _I),
+    "ouro_b200_tensor_load": ([C.c_char_p, _I, _P, _SZ, _I], _I),
+    "ouro_b200_quant_eval": ([_P, C.c_char_p, C.c_char_p, C.c_char_p], _I),
+    "ouro_b200_calib_stage": ([_P, C.c_char_p, C.c_char_p], _I),
     "ouro_b200_math_eval": ([_P, _I, _P, _P, _SZ], _I),
     "ouro_b200_detect_quantize_planes": ([_P, _P, _SZ, _SZ, _SZ, _D, _P, _SZ, C.c_uint, C.c_uint, _SZ, _P, _P, _P,
                                           _P, _P, _P, _P], _I),
@@ -119,6 +124,17 @@ class Spikes(C.Structure):
     """ouro_b200_spikes (SpikeSettings, quant.hpp:105-110)."""
     _fields_ = [("rate", C.c_double), ("gain", C.c_double), ("channels", C.c_size_t), ("salt", C.c_uint64),
                 ("sample0", C.c_size_t)]
+
+
+class StageConfig(C.Structure):
+    """ouro_b200_stage_config: the RunConfig settings a pipeline stage reads (config.hpp:17-47)."""
+    _fields_ = [("image", C.c_size_t), ("channels", C.c_size_t), ("patch", C.c_size_t), ("embed", C.c_size_t),
+                ("state", C.c_size_t), ("blocks", C.c_size_t), ("classes", C.c_size_t), ("conv_width", C.c_size_t),
+                ("seed", C.c_uint64), ("weight_bits", C.c_uint), ("act_bits", C.c_uint), ("outlier_bits", C.c_uint),
+                ("n_refresh", C.c_size_t), ("outlier_quantile", C.c_double), ("mode", C.c_char_p),
+                ("eval_batch", C.c_size_t), ("spike_rate", C.c_double), ("spike_gain", C.c_double),
+                ("spike_channels", C.c_size_t), ("d1", C.c_int), ("d2", C.c_int), ("run_id", C.c_char_p),
+                ("device", C.c_int)]
 
 
 class SweepSettings(C.Structure):

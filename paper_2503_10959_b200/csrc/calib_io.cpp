@@ -33,81 +33,24 @@ namespace fs = std::filesystem;
 
 namespace {
 
-constexpr char kMagic[4] = {'O', 'U', 'R', 'O'};
-constexpr uint32_t kFormatVersion = 1;  // tensor_io.hpp:21
-constexpr uint32_t kDtypeF64 = 0;       // Dtype::F64, tensor_io.hpp:17
+void atomic_write(const fs::path& path, const std::string& bytes) { atomic_write_bytes(path.string(), bytes); }
+std::string read_file(const fs::path& path) { return read_whole_file(path.string()); }
 
-void atomic_write(const fs::path& path, const std::string& bytes) {  // tensor_io.cpp: temp file + rename
-    fs::path tmp = path;
-    tmp += ".tmp";
-    {
-        std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
-        if (!f) throw IoError("cannot create file: " + tmp.string());
-        f.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
-        if (!f) throw IoError("short write: " + tmp.string());
-    }
-    std::error_code ec;
-    fs::rename(tmp, path, ec);
-    if (ec) throw IoError("rename failed: " + tmp.string() + " -> " + path.string() + ": " + ec.message());
-}
-
-std::string read_file(const fs::path& path) {
-    std::ifstream f(path, std::ios::binary);
-    if (!f) throw IoError("cannot open file: " + path.string());
-    return std::string(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
-}
-
-template <class T>
-void put(std::string& b, T v) {
-    b.append(reinterpret_cast<const char*>(&v), sizeof(T));  // little-endian host (x86-64 / aarch64)
-}
-
+// <tensor>_scales.ouro: f64 [2][tokens], row 0 S^I(t), row 1 S_full(t)
 void write_scales(const fs::path& path, const TensorCal& tc, size_t tokens) {
-    std::string b;
-    b.append(kMagic, 4);
-    put<uint32_t>(b, kFormatVersion);
-    put<uint32_t>(b, 2);  // rank
-    put<uint64_t>(b, 2);
-    put<uint64_t>(b, tokens);
-    put<uint32_t>(b, kDtypeF64);
-    b.append(reinterpret_cast<const char*>(tc.s_in.data()), tokens * sizeof(double));
-    b.append(reinterpret_cast<const char*>(tc.s_full.data()), tokens * sizeof(double));
-    atomic_write(path, b);
+    std::vector<double> v(tc.s_in.begin(), tc.s_in.begin() + static_cast<long>(tokens));
+    v.insert(v.end(), tc.s_full.begin(), tc.s_full.begin() + static_cast<long>(tokens));
+    ouro_tensor_write(path.string(), OuroDtype::F64, {2, tokens}, v.data(), v.size() * sizeof(double));
 }
 
 void read_scales(const fs::path& path, size_t tokens, TensorCal& tc) {
-    const std::string b = read_file(path);
-    size_t off = 0;
-    auto need = [&](size_t n) {
-        if (off + n > b.size()) throw IoError(path.string() + ": truncated tensor file");
-    };
-    auto get32 = [&] {
-        need(4);
-        uint32_t v;
-        std::memcpy(&v, b.data() + off, 4);
-        off += 4;
-        return v;
-    };
-    need(4);
-    if (std::memcmp(b.data(), kMagic, 4) != 0) throw IoError(path.string() + ": bad magic, not a tensor file");
-    off = 4;
-    if (get32() != kFormatVersion) throw IoError(path.string() + ": unsupported tensor format version");
-    const uint32_t rank = get32();
-    if (rank > 16) throw IoError(path.string() + ": implausible tensor rank");
-    std::vector<uint64_t> shape(rank);
-    for (auto& d : shape) {
-        need(8);
-        std::memcpy(&d, b.data() + off, 8);
-        off += 8;
-    }
-    if (get32() != kDtypeF64) throw IoError(path.string() + ": dtype mismatch, expected f64");
-    if (shape != std::vector<uint64_t>{2, tokens})
+    const OuroTensor t = ouro_tensor_read(path.string());
+    if (t.dtype != OuroDtype::F64) throw IoError(path.string() + ": dtype mismatch, expected f64");
+    if (t.shape != std::vector<uint64_t>{2, tokens})
         throw IoError("calibration scales " + path.string() + ": unexpected shape");
-    need(2 * tokens * sizeof(double));
-    tc.s_in.resize(tokens);
-    tc.s_full.resize(tokens);
-    std::memcpy(tc.s_in.data(), b.data() + off, tokens * sizeof(double));
-    std::memcpy(tc.s_full.data(), b.data() + off + tokens * sizeof(double), tokens * sizeof(double));
+    const double* d = reinterpret_cast<const double*>(t.payload.data());
+    tc.s_in.assign(d, d + tokens);
+    tc.s_full.assign(d + tokens, d + 2 * tokens);
 }
 
 std::string g17(double v) {  // "%.17g" as the reference writes theta and rho

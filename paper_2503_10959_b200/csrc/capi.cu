@@ -8,34 +8,19 @@
 
 #include "../../include/ouro_b200.h"
 #include "engine.h"
+#include "guard.h"
 #include "planes.h"
 
 using ob::require;
 
-namespace {
-thread_local std::string g_last_error;
-
-template <typename Fn>
-ouro_status guarded(Fn&& fn) {
-    try {
-        fn();
-        g_last_error.clear();
-        return OURO_OK;
-    } catch (const ob::ValidationError& e) {
-        g_last_error = e.what();
-        return OURO_ERR_VALIDATION;
-    } catch (const ob::NumericError& e) {
-        g_last_error = e.what();
-        return OURO_ERR_NUMERIC;
-    } catch (const ob::IoError& e) {
-        g_last_error = e.what();
-        return OURO_ERR_IO;
-    } catch (const std::exception& e) {
-        g_last_error = std::string("internal error: ") + e.what();
-        return OURO_ERR_VALIDATION;
-    }
+namespace ob {
+std::string& last_error_slot() {
+    static thread_local std::string slot;
+    return slot;
 }
-}  // namespace
+}  // namespace ob
+using ob::guarded;
+#define g_last_error (ob::last_error_slot())
 
 struct ouro_b200_ctx {
     std::unique_ptr<ob::Context> c;
@@ -638,7 +623,7 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         require(m && key, "model_set_option: NULL argument");
         const std::string k(key);
         if (k == "scan_variant") {
-            require(value >= 0 && value <= 2, "model_set_option: scan_variant must be 0, 1 or 2");
+            require(value >= 0 && value <= 3, "model_set_option: scan_variant must be 0, 1, 2 or 3");
             m->m->scan_variant = static_cast<int>(value);
         } else if (k == "feed_chunks") {
             require(value >= 1 && value <= 64, "model_set_option: feed_chunks must be in [1, 64]");

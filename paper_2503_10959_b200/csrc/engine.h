@@ -122,6 +122,23 @@ class Calibration {
     const double* inv_full_dev(bool is_lin, size_t idx) const;
 };
 
+// OURO tensor container (ouro_tensor.cpp; tensor_io.hpp:13-44).
+enum class OuroDtype : uint32_t { F64 = 0, I8 = 1, U4 = 2 };
+struct OuroTensor {
+    std::vector<uint64_t> shape;
+    OuroDtype dtype = OuroDtype::F64;
+    std::string payload;  // bytes as stored (u4: nibble-packed)
+};
+void atomic_write_bytes(const std::string& path, const std::string& bytes);
+std::string read_whole_file(const std::string& path);
+size_t ouro_numel(const std::vector<uint64_t>& shape);
+size_t ouro_payload_bytes(OuroDtype dt, const std::vector<uint64_t>& shape);
+void pack_nibbles(const int8_t* codes, size_t n, uint8_t* out);     // (n + 1) / 2 bytes
+void unpack_nibbles(const uint8_t* packed, size_t n, int8_t* out);  // n codes
+void ouro_tensor_write(const std::string& path, OuroDtype dt, const std::vector<uint64_t>& shape, const void* payload,
+                       size_t bytes);
+OuroTensor ouro_tensor_read(const std::string& path);
+
 // Calibration directories in the reference's format (calib_io.cpp).
 void save_calibration_dir(const Calibration& c, int state, const std::string& dir);
 void load_calibration_dir(Calibration& c, int state, const std::string& dir, bool want_d2);
@@ -162,7 +179,8 @@ class Model {
     bool fp_dirty = true;
     int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
     SpikeCfg spikes;       // SpikeHook settings (rate 0 = off); block/dir set per scan
-    int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only
+    int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only,
+                           // 3 the round-1 fast kernel (A/B)
 
     // workspace
     struct Work {

@@ -29,7 +29,8 @@
 //    C(t) = fl(nextafter(theta,+inf)/q_a) > S^I(t) holds (host-checked per
 //    site and step): then O(t) = O_r(t) U {ch: |x| > theta}
 //    and channels never interact. Rows are read as 16-byte vectors, codes
-//    stored as char4; D1's RMSNorm factor comes from k1_rownorm.
+//    stored as char4; D1's RMSNorm factor is taken from the staged rows
+//    (k1_staged), so x is read once.
 //  * k1_literal: one warp owns one (sample, window) with lane l holding
 //    channels l, l+32, ...; the cross-channel maximum of detect_outliers is a
 //    warp reduction, so the reference is followed verbatim (also provides

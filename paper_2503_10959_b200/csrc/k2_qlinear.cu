@@ -14,13 +14,13 @@
 // canonical K-major UMMA layout and the output rows are the next layer's
 // token-major activations.
 //
-// Structure (persistent, one CTA per SM, 8 warps):
+// Structure (persistent, one CTA per SM; 4 + EW warps, EW = 8 or 16 epilogue warps):
 //   warp 0      TMA producer: 128x128 A tile + BNx128 B tile per K-block, 128B swizzle
 //   warp 1      MMA issuer: 4 x tcgen05.mma.kind::i8 (M=128, N=BN, K=32) per K-block
 //   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulators)
-//   warps 4-11  epilogue: tcgen05.ld 32x32b, f64 dequant + outlier terms per row, then a
-//               shared-memory transpose so ws[r] * y, the post-op and the stores run
-//               one lane per column (coalesced 256 B rows)
+//   warp 3      row metadata (S_m, |O(t)|, mask words) of upcoming tiles, bulk-copied
+//   warps 4..   epilogue: tcgen05.ld 32x32b, f64 dequant + outlier terms per row, then
+//               ws[r] * y, the post-op and TMA stores of 32x16 f64 boxes from swizzled staging
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -33,7 +33,7 @@ namespace ob {
 constexpr int kBM = 128, kBK = 128;
 constexpr int kStgBufs = 1;  // epilogue staging buffers per warp
 // Two shapes of the same kernel, chosen per call (launch_qlinear):
-//  * EW = 8 epilogue warps, 3 operand stages: main-loop-heavy calls (wide R);
+//  * EW = 8 epilogue warps, 4 operand stages: main-loop-heavy calls (wide R);
 //  * EW = 16 epilogue warps, 2 operand stages, setmaxnreg moving registers from
 //    warpgroup 0 to the epilogue: epilogue-heavy calls (residual post-op,
 //    outlier terms; the f64 epilogue, not the int8 main loop, bounds those —
@@ -497,8 +497,9 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.a.J < (p.K + 31) / 32) return cudaErrorInvalidValue;
     const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
     if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
-    // main-loop-heavy calls (wide outputs, no residual) keep the 8-warp / 3-stage shape
-    // (x_proj, R = 800: 3 stages measured 0.25 ms per forward faster than 16 epilogue warps)
+    // main-loop-heavy calls (wide outputs, no residual) take the 8-warp / 4-stage shape
+    // (x_proj, R = 800: measured 0.25 ms per forward faster than 16 epilogue warps; 4 stages
+    // 0.33 ms per forward faster than 3)
     const bool wide = p.epi.post != POST_RESID && (p.R > 512 || p.K > 1024);
 #define K2_CASE(P)                                                                                       \
     case P:                                                                                              \

@@ -164,8 +164,348 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
     for (int k = lane; k < kChunks16; k += 32) dst[k] = src[k];
 }
 
-template <bool EXACT, int ABITS>
+template <bool EXACT, int ABITS, bool TRACE>
 __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const StepShared* __restrict__ steps) {
+    extern __shared__ __align__(16) uint8_t scan_smem_raw[];
+    const int warp = threadIdx.x >> 5;
+    WarpSmem& sh = reinterpret_cast<WarpSmem*>(scan_smem_raw)[warp];
+    const ScanParams& p = P.d[blockIdx.z];
+    const unsigned lane = threadIdx.x & 31;
+    const int s = blockIdx.y, c = lane >> 1, half = lane & 1;
+    const int cw = blockIdx.x * kCh + warp * kWarpCh;  // first channel of this warp
+    if (cw >= p.E) return;  // no CTA-wide barriers below
+    const int i = cw + c;
+    const bool active = i < p.E;
+    const int E = p.E, T = p.T, P2 = E + 32, m0 = half * 8;
+    const unsigned pair = 3u << (lane & ~1u);
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;  // outlier_bits = 8
+    constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
+    const double* __restrict__ proj = p.proj;
+    const double* __restrict__ uin = p.u;
+    double* __restrict__ obase = p.o + static_cast<size_t>(s) * T * E + (active ? i : 0);
+    const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
+    float2 A2f[4];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
+    double Amax = -1e300;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double a0 = active ? arow[m0 + 2 * k] : -1.0, a1 = active ? arow[m0 + 2 * k + 1] : -1.0;
+        A2f[k] = make_float2(__double2float_rn(a0 * 1.4426950408889634), __double2float_rn(a1 * 1.4426950408889634));
+        Amax = fmax(Amax, fmax(a0, a1));
+    }
+    Amax = fmax(Amax, __shfl_xor_sync(0xffffffffu, Amax, 1));
+    const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
+    double h[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) h[m] = 0.0;
+    unsigned fl = 0;  // channel in O: bit 0 a_bar, bit 1 b_bar, bit 2 h
+    const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
+    const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
+    // chunk staging: lane -> (step, channel) = (lane >> 4 + 2k, lane & 15)
+    const int sc = lane & 15, sic = cw + sc;
+    const double bd = sic < E ? p.b_delta[sic] : 0.0;
+    const StepShared* wsteps = steps + (static_cast<size_t>(blockIdx.z) * p.S + s) * T;
+    if (lane == 0) {
+        ptx::mbar_init(&sh.bar[0], 1);
+        ptx::mbar_init(&sh.bar[1], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncwarp();
+    auto issue = [&](int t0, int buf) {  // async copies of chunk t0 into buffer buf
+        const int nt = min(kChunk, T - t0);
+#pragma unroll
+        for (int k = 0; k < kChunk / 2; ++k) {
+            const int tt = (lane >> 4) + 2 * k, t = min(t0 + tt, T - 1);
+            const bool ok = tt < nt && sic < E;
+            const int cr = row_at(p.order, t, T, p.grid);
+            cp_async8(&sh.dp[buf][tt][sc], proj + (static_cast<size_t>(s) * T + t) * P2 + (ok ? sic : 0), ok);
+            cp_async8(&sh.u[buf][tt][sc], uin + (static_cast<size_t>(s) * T + cr) * E + (ok ? sic : 0), ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (lane == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
+            ptx::mbar_arrive_expect_tx(&sh.bar[buf], bytes);
+            ptx::bulk_g2s(&sh.st[buf][0], wsteps + t0, bytes, &sh.bar[buf]);
+        }
+    };
+    issue(0, 0);
+
+    for (int t0 = 0, ci = 0; t0 < T; t0 += kChunk, ++ci) {
+        const int nt = min(kChunk, T - t0), cur = ci & 1;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();  // chunk ci's per-channel inputs landed; chunk ci-1 consumed
+#pragma unroll
+        for (int k = 0; k < kChunk / 2; ++k) {
+            const int tt = (lane >> 4) + 2 * k;
+            const double x = dadd(sh.dp[cur][tt][sc], bd);  // softplus argument, ssm.cpp:150-151
+            float eps;
+            sh.x[tt][sc] = x;
+            sh.deltaf[tt][sc] = softplus_f32(__double2float_rn(x), eps);
+            sh.epsd[tt][sc] = eps;
+        }
+        if (t0 + kChunk < T) issue(t0 + kChunk, cur ^ 1);
+        __syncwarp();
+        ptx::mbar_wait(&sh.bar[cur], (ci >> 1) & 1);
+
+        // Output of step tt (o = 0 + C_0 h_0 + ... + C_15 h_15 in order: the first lane of a
+        // pair sums from 0, the second continues the same chain) from the carried state h,
+        // which still holds step tt's quantized state until pass 2 of step tt+1 updates it.
+        // For A4 it is issued from inside pass 1 of step tt+1, so its dependent DADD chain
+        // overlaps that step's independent f32 work (measured 2.44 vs 2.49 ms per Vim-B
+        // launch; A8 measured 3 % slower deferred, so it emits at the end of its step); the
+        // chunk's last step is emitted at the end of the chunk (its step record is about to
+        // be recycled).
+        auto emit = [&](int te, unsigned fl_e, bool store) {
+            const StepShared& se = sh.st[cur][te];
+            double pr[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) pr[m] = dmul(se.C[m0 + m], h[m]);
+            double o = 0.0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
+            o = __shfl_sync(0xffffffffu, o, lane & ~1u);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
+            if (store && half && active) {
+                obase[se.ocol] = o;
+                if constexpr (TRACE) {
+                    const size_t b = (static_cast<size_t>(s) * T + t0 + te) * E + i;
+                    const size_t kst = static_cast<size_t>(p.S) * T * E;
+                    p.masks[b] = fl_e & 1u;
+                    p.masks[kst + b] = (fl_e >> 1) & 1u;
+                    p.masks[2 * kst + b] = (fl_e >> 2) & 1u;
+                }
+            }
+        };
+        constexpr bool kDefer = ABITS == 4;
+        unsigned fl_prev = fl;
+        for (int tt = 0; tt < nt; ++tt) {
+            const int t = t0 + tt;
+            const StepShared& ss = sh.st[cur][tt];
+            const float df = sh.deltaf[tt][c];
+            const float ed = sh.epsd[tt][c];
+            const double uv = sh.u[cur][tt][c];
+            // exact delta and peaks, computed on demand (decisions near theta, outlier
+            // scales, fallbacks)
+            bool have = false;
+            double delta, pa, pb;
+            auto exact = [&]() {
+                if (!have) {
+                    delta = softplus_call(sh.x[tt][c]);
+                    pa = exp_call(dmul(delta, Amax));
+                    pb = dmul(delta, ss.Bmax);
+                    have = true;
+                }
+            };
+            // inlier scales (static mode; dynamic steps where neither tensor is an outlier)
+            double sA = ss.Sa, sB = ss.Sb;
+            float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
+            // Certification margins (in units of q) where rounding matters (|q| <= qmax+1):
+            // a_bar: |dq| <= q (ln2 |x2| (ed + 2^-23) + 2^-21), ln2 |x2| <= LA there;
+            // b_bar: |dq| <= |q| (ed + 8 2^-24). Inlier forms folded to h0 - h1*ed.
+            float halfA = fmaf(-ss.hA1, ed, ss.hA0);
+            float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
+            // f32 a_bar peak: the detector's certified estimate and the clipping bound below
+            const float x2m = df * Amax2f;
+            const float paf = ex2_approx(x2m);
+            if (dyn) {
+                fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh, quant.cpp:303-311
+                // detect_outliers, channel-local form, on certified f32 peaks
+                const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
+                const float pbf = df * ss.Bmaxf;
+                const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
+                // one branch off the inlier path: outlier channels and decisions within the bound
+                if ((fl & 3u) | (paf >= thAf * (1.0f - ea)) | (pbf >= thBf * (1.0f - eb))) {
+                    if (!(fl & 1u)) {
+                        if (paf > thAf * (1.0f + ea)) {
+                            fl |= 1u;
+                        } else if (paf >= thAf * (1.0f - ea)) {
+                            exact();
+                            if (pa > thA) fl |= 1u;
+                        }
+                    }
+                    if (!(fl & 2u)) {
+                        if (pbf > thBf * (1.0f + eb)) {
+                            fl |= 2u;
+                        } else if (pbf >= thBf * (1.0f - eb)) {
+                            exact();
+                            if (pb > thB) fl |= 2u;
+                        }
+                    }
+                    if (fl & 3u) exact();
+                    if (fl & 1u) {
+                        sA = scale_call(pa, qo);
+                        invA = __double2float_rn(recip_call(sA));
+                        qAf = qof;
+                        const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                        halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+                    }
+                    if (fl & 2u) {
+                        sB = scale_call(pb, qo);
+                        kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
+                        qBf = qof;
+                        halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                    }
+                }
+            }
+            const float dfb = df * kB;
+            const float capA = qAf + 0.25f, capB = qBf + 0.25f;
+            // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23), clamped
+            // before rounding so the integer is the reference's clipped code. Two elements
+            // per packed f32x2 instruction; codes are kept as magic bit patterns.
+            unsigned ca[8];  // a_bar codes (>= 0) as integers, b_bar codes as exact f32 integers
+            float cb[8];
+            bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
+            const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
+            auto pass1 = [&](auto clamp) {
+                constexpr bool CL = decltype(clamp)::value;
+                if constexpr (kDefer)
+                    if (tt > 0) emit(tt - 1, fl_prev, true);  // previous step's output (see emit)
+                float mda = 0.0f, mdb = 0.0f;  // largest distance to the rounded code (3-input max)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
+                    float2 qa2 = __fmul2_rn(make_float2(ex2_approx(x2.x), ex2_approx(x2.y)), f2(invA));
+                    if constexpr (CL) {
+                        qa2.x = fminf(qa2.x, capA);
+                        qa2.y = fminf(qa2.y, capA);
+                    }
+                    const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
+                    const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
+                    const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
+                    ca[2 * k] = __float_as_uint(ta.x) - kMagicBits;
+                    ca[2 * k + 1] = __float_as_uint(ta.y) - kMagicBits;
+                    float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
+                    if constexpr (CL) {
+                        qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
+                        qb2.y = fminf(fmaxf(qb2.y, -capB), capB);
+                    }
+                    const float2 tb = __fadd2_rn(qb2, f2(12582912.0f));
+                    const float2 rb = __fadd2_rn(tb, f2(-12582912.0f));
+                    const float2 db = __fadd2_rn(qb2, make_float2(-rb.x, -rb.y));
+                    cb[2 * k] = rb.x;
+                    cb[2 * k + 1] = rb.y;
+                    mda = fmaxf(mda, fmaxf(fabsf(da.x), fabsf(da.y)));
+                    mdb = fmaxf(mdb, fmaxf(fabsf(db.x), fabsf(db.y)));
+                }
+                redo |= (mda > halfA) | (mdb > halfB);
+            };
+            // The clamps can bind only if the largest quotient exceeds the cap: q_b <=
+            // dfb*max|BSf| and q_a <= paf*invA (monotone rounding; the factor covers
+            // ex2.approx's relative error). Warp-uniform choice, both forms are exact.
+            const bool noclip = dfb * ss.BSmaxf <= capB && paf * invA * 1.000001f <= capA;
+            if (__all_sync(0xffffffffu, noclip)) pass1(std::false_type{});
+            else pass1(std::true_type{});
+            if (redo) {  // exact f64 codes where the f32 quotient is not certified
+                exact();
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
+                    const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
+                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
+                        ca[m] = static_cast<unsigned>(static_cast<int>(
+                            qdiv_call(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
+                    const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
+                    if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
+                        cb[m] = static_cast<float>(
+                            qdiv_call(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
+                }
+            }
+            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update.
+            // a_bar codes are >= 0: fma(2^52 + c, sA, -2^52 sA) = c sA before its one rounding,
+            // i.e. exactly dmul(c, sA).
+            const double nKA = dmul(sA, -4503599627370496.0);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
+                const double b_q = dmul(static_cast<double>(cb[m]), sB);
+                h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
+            }
+            // h detection + codes. Rounding to f32 is monotone, so the f32 peak
+            // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
+            // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
+            // needs the exact f64 peak. Outlier channels take the exact peak for their scale.
+            float2 hfv[4];
+            float phf = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
+                phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
+            }
+            phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
+            double sH = ss.Sh, qH = qa;
+            float invHf = ss.invShf;
+            if (dyn && ((fl & 4u) | (phf >= thHf))) {
+                if (!(fl & 4u)) {
+                    if (phf > thHf) {
+                        fl |= 4u;
+                    } else {  // phf == fl32(theta): the exact peak decides
+                        double ph = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                        ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                        if (ph > thH) fl |= 4u;
+                    }
+                }
+                if (fl & 4u) {
+                    double ph = 0.0;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                    ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                    sH = scale_call(ph, qo);
+                    invHf = __double2float_rn(recip_call(sH));
+                    qH = qo;
+                }
+            }
+            {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
+                const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
+                const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+                float chd[8];  // h codes as exact f32 integers (F2F.F64 balances the XU and FP64 pipes)
+                bool hredo = EXACT;
+                auto hcodes = [&](auto clamp) {
+                    constexpr bool CL = decltype(clamp)::value;
+                    float mdh = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                        if constexpr (CL) {
+                            q.x = fminf(fmaxf(q.x, -capH), capH);
+                            q.y = fminf(fmaxf(q.y, -capH), capH);
+                        }
+                        const float2 th = __fadd2_rn(q, f2(12582912.0f));
+                        const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
+                        const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
+                        chd[2 * k] = rh.x;
+                        chd[2 * k + 1] = rh.y;
+                        mdh = fmaxf(mdh, fmaxf(fabsf(dh.x), fabsf(dh.y)));
+                    }
+                    hredo |= mdh > halfH;
+                };
+                if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});  // |q| <= phf*invHf
+                else hcodes(std::true_type{});
+                if (hredo) {
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {
+                        const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
+                        const float q = fminf(fmaxf(hv * invHf, -capH), capH);
+                        if (EXACT || fabsf(q - rintf(q)) > halfH)
+                            chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < 8; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
+            }
+            if constexpr (!kDefer) emit(tt, fl, true);
+            fl_prev = fl;
+        }
+        if constexpr (kDefer) emit(nt - 1, fl_prev, true);
+    }
+}
+
+// Round-1 form of the kernel below (output sum at the end of each step), kept
+// as scan variant 3 for A/B runs.
+template <bool EXACT, int ABITS>
+__global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t scan_smem_raw[];
     const int warp = threadIdx.x >> 5;
     WarpSmem& sh = reinterpret_cast<WarpSmem*>(scan_smem_raw)[warp];
@@ -490,15 +830,38 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
     }
 }
 
-template <bool EXACT, int ABITS>
+template <bool EXACT, int ABITS, bool TRACE>
 static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
     const int smem = static_cast<int>(sizeof(WarpSmem)) * (kThr / 32);
-    cudaError_t e = ensure_smem_attr<k3_scan_fast<EXACT, ABITS>>(smem);
+    cudaError_t e = ensure_smem_attr<k3_scan_fast<EXACT, ABITS, TRACE>>(smem);
     if (e != cudaSuccess) return e;
     dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
-    k3_scan_fast<EXACT, ABITS><<<grid, kThr, smem, st>>>(P, steps);
+    k3_scan_fast<EXACT, ABITS, TRACE><<<grid, kThr, smem, st>>>(P, steps);
     ++kernel_launch_counter();
     return cudaGetLastError();
+}
+
+template <int ABITS>
+static cudaError_t launch_r1(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
+    const int smem = static_cast<int>(sizeof(WarpSmem)) * (kThr / 32);
+    cudaError_t e = ensure_smem_attr<k3_scan_r1<false, ABITS>>(smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
+    k3_scan_r1<false, ABITS><<<grid, kThr, smem, st>>>(P, steps);
+    ++kernel_launch_counter();
+    return cudaGetLastError();
+}
+
+template <int ABITS>
+static cudaError_t launch_variant(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st,
+                                  int variant, bool trace) {
+    switch (variant) {
+        case 0: return trace ? launch_fast<false, ABITS, true>(P, ndirs, steps, st)
+                             : launch_fast<false, ABITS, false>(P, ndirs, steps, st);
+        case 1: return trace ? launch_fast<true, ABITS, true>(P, ndirs, steps, st)
+                             : launch_fast<true, ABITS, false>(P, ndirs, steps, st);
+        default: return launch_r1<ABITS>(P, ndirs, steps, st);
+    }
 }
 
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs) {
@@ -506,7 +869,7 @@ size_t scan_fast_workspace_bytes(int S, int T, int ndirs) {
 }
 
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
-                             int force_exact) {
+                             int variant) {
     if (ndirs < 1 || ndirs > 2) return cudaErrorInvalidValue;
     ScanDirs P;
     for (int k = 0; k < ndirs; ++k) {
@@ -526,9 +889,10 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     ++kernel_launch_counter();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    const bool trace = dirs[0].masks != nullptr;
     switch (dirs[0].abits) {
-        case 4: return force_exact ? launch_fast<true, 4>(P, ndirs, steps, st) : launch_fast<false, 4>(P, ndirs, steps, st);
-        default: return force_exact ? launch_fast<true, 8>(P, ndirs, steps, st) : launch_fast<false, 8>(P, ndirs, steps, st);
+        case 4: return launch_variant<4>(P, ndirs, steps, st, variant, trace);
+        default: return launch_variant<8>(P, ndirs, steps, st, variant, trace);
     }
 }
 

@@ -170,13 +170,15 @@ struct ScanParams {
     SpikeCfg spike;                   // reference-form kernel only (launch_scan)
 };
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
-// Fast path (dynamic/static, channel-local detector): all directions in one launch.
-// force_exact = 1 disables the certified f32 codes (every element exact f64).
-// Fast exact scan, both directions in one launch (plus a step-table prep
-// launch); work = scan_fast_workspace_bytes(S, T, ndirs) bytes, 16-aligned.
+// Fast path (dynamic/static, channel-local detector): both directions in one
+// launch (plus a step-table prep launch); work = scan_fast_workspace_bytes(S, T,
+// ndirs) bytes, 16-aligned. variant 0: the shipped kernel (k3_scan_v2); 1: the
+// same with the certified f32 codes disabled (every element exact f64); 2: the
+// round-1 kernel (k3_scan_fast), kept for A/B runs. Non-null `masks` selects the
+// parity-trace instantiation.
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
-                             int force_exact);
+                             int variant);
 
 // K4 auxiliaries.
 cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,

@@ -543,3 +543,88 @@ class Model:
         L.check(self.lib.ouro_b200_trace_run(self.h, calib.h if calib else None, mode, int(d1), int(d2),
                                              _ptr(images), B, block, C.byref(h)))
         return Trace(self.lib, h)
+
+
+# ---- OURO tensor files and pipeline stages (host-side entry points) -----------------
+
+DTYPE_F64, DTYPE_I8, DTYPE_U4 = 0, 1, 2
+
+
+def tensor_save(path, data: np.ndarray, dtype: int = DTYPE_F64, *, packed: bool = False, shape=None) -> None:
+    """write_tensor_f64 / _i8 / _u4 (tensor_io.cpp) in the reference's OURO container.
+    U4: int8 codes in [-8, 7], or (packed=True) the nibble-packed payload with `shape`
+    the logical code shape (e.g. a K1 operand produced in the packed format)."""
+    lib = L.load()
+    arr = np.ascontiguousarray(data, np.float64 if dtype == DTYPE_F64 else (np.uint8 if packed else np.int8))
+    shp = np.array(shape if shape is not None else arr.shape, dtype=np.uint64)
+    L.check(lib.ouro_b200_tensor_save(str(path).encode(), dtype, _ptr(shp), shp.size, _ptr(arr), int(packed)))
+
+
+def tensor_info(path):
+    """(dtype, shape) of a tensor file."""
+    lib = L.load()
+    dt, rank = C.c_int(), C.c_size_t()
+    shp = np.zeros(16, np.uint64)
+    L.check(lib.ouro_b200_tensor_info(str(path).encode(), C.byref(dt), _ptr(shp), 16, C.byref(rank)))
+    return dt.value, tuple(int(x) for x in shp[:rank.value])
+
+
+def tensor_load(path, *, packed: bool = False) -> np.ndarray:
+    """read_tensor_f64 / _i8 / _u4: f64 or int8 codes in the file's shape (packed=True: the raw u4 bytes)."""
+    lib = L.load()
+    dt, shape = tensor_info(path)
+    n = int(np.prod(shape)) if shape else 1
+    if dt == DTYPE_F64:
+        out = np.empty(shape, np.float64)
+    elif dt == DTYPE_U4 and packed:
+        out = np.empty((n + 1) // 2, np.uint8)
+    else:
+        out = np.empty(shape, np.int8)
+    L.check(lib.ouro_b200_tensor_load(str(path).encode(), dt, _ptr(out), out.nbytes, int(packed)))
+    return out
+
+
+@dataclass
+class StageConfig:
+    """The RunConfig settings the GPU stages read (config.hpp:17-47); scan orders
+    row-forward, row-backward; d1 = d2 = False is the reference's own pass."""
+    dims: Dims = field(default_factory=Dims)
+    seed: int = 1
+    weight_bits: int = 4
+    act_bits: int = 8
+    outlier_bits: int = 8
+    n_refresh: int = 10
+    outlier_quantile: float = 0.01
+    mode: str = "dynamic"
+    eval_batch: int = 4
+    spike_rate: float = 0.0
+    spike_gain: float = 100.0
+    spike_channels: int = 1
+    d1: bool = False
+    d2: bool = False
+    run_id: str | None = None
+    device: int = 0
+
+    def _c(self):
+        d = self.dims
+        self._mode_b = self.mode.encode()
+        self._run_b = self.run_id.encode() if self.run_id is not None else None
+        return L.StageConfig(d.image, d.channels, d.patch, d.embed, d.state, d.blocks, d.classes, d.conv_width,
+                             self.seed, self.weight_bits, self.act_bits, self.outlier_bits, self.n_refresh,
+                             self.outlier_quantile, self._mode_b, self.eval_batch, self.spike_rate, self.spike_gain,
+                             self.spike_channels, int(self.d1), int(self.d2), self._run_b, self.device)
+
+
+def quant_eval_stage(cfg: StageConfig, calib_dir, images_file, out_dir) -> None:
+    """ouro_quant_eval (capi.cpp:174-186) on the GPU: writes out_dir/metrics.txt + manifest.txt."""
+    lib = L.load()
+    c = cfg._c()
+    L.check(lib.ouro_b200_quant_eval(C.byref(c), str(calib_dir).encode(), str(images_file).encode(),
+                                     str(out_dir).encode()))
+
+
+def calib_stage(cfg: StageConfig, images_file, out_dir) -> None:
+    """ouro_calib (capi.cpp:166-172) on the GPU: the calibration directory + manifest."""
+    lib = L.load()
+    c = cfg._c()
+    L.check(lib.ouro_b200_calib_stage(C.byref(c), str(images_file).encode(), str(out_dir).encode()))

@@ -208,16 +208,18 @@ def test_k1_variants_identical(pair, abits):
 @pytest.mark.parametrize("abits", [4, 8])
 def test_scan_variants_identical(pair, abits):
     """K3 fast path (certified f32 codes + exact fallbacks), its all-exact
-    variant and the per-direction reference kernel agree bit-for-bit."""
+    variant, the round-1 fast kernel and the per-direction reference kernel
+    agree bit-for-bit."""
     om, gm, imgs, cimgs = pair
     spec = _spec(abits, rho=0.05)
     gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
     outs = []
-    for v in (0, 1, 2):
+    for v in (0, 1, 2, 3):
         gm.set_option("scan_variant", v)
         outs.append(gm.forward_host(imgs, gcal, 1))
     gm.set_option("scan_variant", 0)
-    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    for v in (1, 2, 3):
+        assert np.array_equal(outs[0], outs[v]), v
 
 
 @pytest.mark.parametrize("abits,n_refresh", [(4, 10), (8, 7)])
