@@ -257,11 +257,18 @@ EvalOut quant_eval(Model& m, Calibration& cal, int mode, bool d1, bool d2, const
             cuda_check(launch_scan(sp, st, nullptr), "teacher-forced scan");
             const std::vector<double> oh = to_host(o_tf.p, rows * E, st);
             const double* of = blob<double>(tr, "dir" + std::to_string(k) + ".o", rows * E);
+            // summed in the reference's order: per sample, scan step t, channel
+            // (s6_scan returns o in scan order, quant.cpp:566-570); o is stored here at
+            // canonical rows
             double acc = 0.0;
-            for (size_t i = 0; i < rows * E; ++i) {
-                const double e = of[i] - oh[i];
-                acc += e * e;
-            }
+            for (int s = 0; s < B; ++s)
+                for (int t = 0; t < L; ++t) {
+                    const size_t r = (static_cast<size_t>(s) * L + row_at(order, t, L, d.grid())) * E;
+                    for (int e = 0; e < E; ++e) {
+                        const double df = of[r + e] - oh[r + e];
+                        acc += df * df;
+                    }
+                }
             out.layer_mse.emplace_back("block" + std::to_string(blk) + ".dir" + std::to_string(k),
                                        g17(acc / static_cast<double>(rows * E)));
         }

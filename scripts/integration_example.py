@@ -22,7 +22,9 @@ logits = m.forward(images_cuda, cal, ob.MODE_DYNAMIC)
 logits_h = m.forward_host(images_np, cal, ob.MODE_DYNAMIC)
 torch.cuda.synchronize()
 assert np.array_equal(logits.cpu().numpy(), logits_h)
-res = m.quant_eval(images_np, cal, ob.MODE_DYNAMIC, d1=False, d2=False, spikes=ob.SpikeSettings(rate=0.05, gain=100.0))
+# the reference's own quantized_forward (no D1/D2) needs a calibration recorded the same way
+cal_ref = m.calibrate(calib_images_cuda, ob.QuantSpec(wbits=4, abits=4, obits=8, n_refresh=10, rho=0.01, d1=False, d2=False))
+res = m.quant_eval(images_np, cal_ref, ob.MODE_DYNAMIC, d1=False, d2=False, spikes=ob.SpikeSettings(rate=0.05, gain=100.0))
 sweep = ctx.refresh_sweep((1, 5, 10, 20, 0), steps=50, trials=1)
 bench = ctx.gemm_bench((64, 128, 256), trials=1)
 m.set_option("split_parts", 2)
