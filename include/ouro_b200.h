@@ -192,7 +192,8 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
 
 /* Engine options: "scan_variant" = 0 auto (fast K3 path wherever the
  * channel-local detector is exact), 1 per-direction reference scan kernel,
- * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid);
+ * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid),
+ * 3 / 4 fast path on the two- / one-thread-per-channel kernel (A/B aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
  * detector kernel everywhere; "split_parts" in [1, 4] (default 2) runs a batch of
  * >= 32 * parts samples as that many independent sub-batches on their own

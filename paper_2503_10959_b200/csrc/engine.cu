@@ -717,7 +717,7 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
             sps[dd].spike.sample0 = spikes.sample0 + sample0;
         }
         if (fast_ok && !any_literal && scan_variant != 1 && !(spikes.rate > 0.0)) {
-            cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant == 2 ? 1 : (scan_variant == 3 ? 2 : 0)), "scan");
+            cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant >= 2 ? scan_variant - 1 : 0), "scan");
         } else {
             for (int dd = 0; dd < nd; ++dd) {
                 bool l = false;

@@ -180,7 +180,7 @@ class Model {
     int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
     SpikeCfg spikes;       // SpikeHook settings (rate 0 = off); block/dir set per scan
     int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only,
-                           // 3 the round-1 fast kernel (A/B)
+                           // 3 fast path on the two-threads-per-channel kernel, 4 on the one-thread-per-channel kernel
 
     // workspace
     struct Work {

@@ -502,22 +502,38 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
     }
 }
 
-// Round-1 form of the kernel below (output sum at the end of each step), kept
-// as scan variant 3 for A/B runs.
-template <bool EXACT, int ABITS>
-__global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const StepShared* __restrict__ steps) {
-    extern __shared__ __align__(16) uint8_t scan_smem_raw[];
-    const int warp = threadIdx.x >> 5;
-    WarpSmem& sh = reinterpret_cast<WarpSmem*>(scan_smem_raw)[warp];
+// ---- one thread per channel ---------------------------------------------------
+// Same arithmetic as k3_scan_fast (every certification bound above holds
+// unchanged), with lane = channel and all N = 16 states in one thread: the
+// per-step work that does not scale with the states (step-record loads,
+// detection, votes, branches, the output store) is paid once per 32 channels
+// instead of once per 16, and the output sum 0 + C_0 h_0 + ... + C_15 h_15 is
+// one in-order chain in one thread (no half-duplicated additions, no shuffles).
+// A chunk pre-pass evaluates, per (step, channel) with the chunk's steps as
+// independent streams, the f32 delta, the inlier certification margins, the
+// detector's "near or above theta" flag and the clamp flag; the step loop reads
+// them with one 16-byte shared load.
+template <int KC>
+struct C1Smem {
+    StepShared st[2][KC];
+    double dp[2][KC][32];  // x_proj delta pre-activations (raw), lane = channel
+    double u[2][KC][32];
+    float4 pre[KC][32];    // df, inlier halfA, inlier halfB, flags (bit 0 detect, bit 1 clamp)
+    uint64_t bar[2];
+};
+
+template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB>
+__global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const StepShared* __restrict__ steps) {
+    extern __shared__ __align__(16) uint8_t c1_smem_raw[];
+    using Sm = C1Smem<KC>;
+    Sm& sh = *reinterpret_cast<Sm*>(c1_smem_raw);
     const ScanParams& p = P.d[blockIdx.z];
     const unsigned lane = threadIdx.x & 31;
-    const int s = blockIdx.y, c = lane >> 1, half = lane & 1;
-    const int cw = blockIdx.x * kCh + warp * kWarpCh;  // first channel of this warp
-    if (cw >= p.E) return;  // no CTA-wide barriers below
-    const int i = cw + c;
+    const int s = blockIdx.y;
+    const int cw = blockIdx.x * 32;  // first channel of this warp (CTA = one warp)
+    const int i = cw + static_cast<int>(lane);
     const bool active = i < p.E;
-    const int E = p.E, T = p.T, P2 = E + 32, m0 = half * 8;
-    const unsigned pair = 3u << (lane & ~1u);
+    const int E = p.E, T = p.T, P2 = E + 32;
     const bool dyn = p.mode == MODE_DYNAMIC;
     constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;  // outlier_bits = 8
     constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
@@ -525,25 +541,22 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
     const double* __restrict__ uin = p.u;
     double* __restrict__ obase = p.o + static_cast<size_t>(s) * T * E + (active ? i : 0);
     const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
-    float2 A2f[4];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
+    float2 A2f[8];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
     double Amax = -1e300;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const double a0 = active ? arow[m0 + 2 * k] : -1.0, a1 = active ? arow[m0 + 2 * k + 1] : -1.0;
+    for (int k = 0; k < 8; ++k) {
+        const double a0 = active ? arow[2 * k] : -1.0, a1 = active ? arow[2 * k + 1] : -1.0;
         A2f[k] = make_float2(__double2float_rn(a0 * 1.4426950408889634), __double2float_rn(a1 * 1.4426950408889634));
         Amax = fmax(Amax, fmax(a0, a1));
     }
-    Amax = fmax(Amax, __shfl_xor_sync(0xffffffffu, Amax, 1));
     const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
-    double h[8];
+    double h[16];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) h[m] = 0.0;
+    for (int m = 0; m < 16; ++m) h[m] = 0.0;
     unsigned fl = 0;  // channel in O: bit 0 a_bar, bit 1 b_bar, bit 2 h
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
-    // chunk staging: lane -> (step, channel) = (lane >> 4 + 2k, lane & 15)
-    const int sc = lane & 15, sic = cw + sc;
-    const double bd = sic < E ? p.b_delta[sic] : 0.0;
+    const double bd = active ? p.b_delta[i] : 0.0;
     const StepShared* wsteps = steps + (static_cast<size_t>(blockIdx.z) * p.S + s) * T;
     if (lane == 0) {
         ptx::mbar_init(&sh.bar[0], 1);
@@ -551,79 +564,108 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
         ptx::fence_barrier_init();
     }
     __syncwarp();
-    auto issue = [&](int t0, int buf) {  // async copies of chunk t0 into buffer buf
-        const int nt = min(kChunk, T - t0);
-#pragma unroll
-        for (int k = 0; k < kChunk / 2; ++k) {
-            const int tt = (lane >> 4) + 2 * k, t = min(t0 + tt, T - 1);
-            const bool ok = tt < nt && sic < E;
+    const uint32_t rowbytes = static_cast<uint32_t>(min(32, E - cw)) * 8u;  // E even: a multiple of 16
+    // chunk t0 into buffer buf: lane tt < nt bulk-copies step t0 + tt's x_proj delta row
+    // and its scan input row (canonical position) for the warp's 32 channels; lane 0 the
+    // step records; all complete on the buffer's mbarrier
+    auto issue = [&](int t0, int buf) {
+        const int nt = min(KC, T - t0);
+        if (lane == 0)
+            ptx::mbar_arrive_expect_tx(&sh.bar[buf], static_cast<uint32_t>(nt) * (sizeof(StepShared) + 2u * rowbytes));
+        __syncwarp();
+        if (static_cast<int>(lane) < nt) {
+            const int t = t0 + static_cast<int>(lane);
             const int cr = row_at(p.order, t, T, p.grid);
-            cp_async8(&sh.dp[buf][tt][sc], proj + (static_cast<size_t>(s) * T + t) * P2 + (ok ? sic : 0), ok);
-            cp_async8(&sh.u[buf][tt][sc], uin + (static_cast<size_t>(s) * T + cr) * E + (ok ? sic : 0), ok);
+            ptx::bulk_g2s(&sh.dp[buf][lane][0], proj + (static_cast<size_t>(s) * T + t) * P2 + cw, rowbytes, &sh.bar[buf]);
+            ptx::bulk_g2s(&sh.u[buf][lane][0], uin + (static_cast<size_t>(s) * T + cr) * E + cw, rowbytes, &sh.bar[buf]);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        if (lane == 0) {
-            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
-            ptx::mbar_arrive_expect_tx(&sh.bar[buf], bytes);
-            ptx::bulk_g2s(&sh.st[buf][0], wsteps + t0, bytes, &sh.bar[buf]);
-        }
+        if (lane == 0) ptx::bulk_g2s(&sh.st[buf][0], wsteps + t0, static_cast<uint32_t>(nt * sizeof(StepShared)), &sh.bar[buf]);
     };
     issue(0, 0);
+    constexpr bool kDefer = ABITS == 4;
+    const float hBc = 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f);
 
-    for (int t0 = 0, ci = 0; t0 < T; t0 += kChunk, ++ci) {
-        const int nt = min(kChunk, T - t0), cur = ci & 1;
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();  // chunk ci's per-channel inputs landed; chunk ci-1 consumed
-#pragma unroll
-        for (int k = 0; k < kChunk / 2; ++k) {
-            const int tt = (lane >> 4) + 2 * k;
-            const double x = dadd(sh.dp[cur][tt][sc], bd);  // softplus argument, ssm.cpp:150-151
-            float eps;
-            sh.x[tt][sc] = x;
-            sh.deltaf[tt][sc] = softplus_f32(__double2float_rn(x), eps);
-            sh.epsd[tt][sc] = eps;
-        }
-        if (t0 + kChunk < T) issue(t0 + kChunk, cur ^ 1);
-        __syncwarp();
+    for (int t0 = 0, ci = 0; t0 < T; t0 += KC, ++ci) {
+        const int nt = min(KC, T - t0), cur = ci & 1;
+        __syncwarp();  // chunk ci-1 consumed
         ptx::mbar_wait(&sh.bar[cur], (ci >> 1) & 1);
-
-        for (int tt = 0; tt < nt; ++tt) {
-            const int t = t0 + tt;
+        // pre-pass: per step of the chunk, this channel's f32 delta (softplus with its
+        // bound), the certified a_bar peak, the detector flag and the inlier margins
+#pragma unroll
+        for (int tt = 0; tt < KC; ++tt) {
             const StepShared& ss = sh.st[cur][tt];
-            const float df = sh.deltaf[tt][c];
-            const float ed = sh.epsd[tt][c];
-            const double uv = sh.u[cur][tt][c];
-            // exact delta and peaks, computed on demand (decisions near theta, outlier
-            // scales, fallbacks)
+            const double x = dadd(sh.dp[cur][tt][lane], bd);  // softplus argument, ssm.cpp:150-151
+            float ed;
+            const float df = softplus_f32(__double2float_rn(x), ed);
+            const float x2m = df * Amax2f;
+            const float paf = ex2_approx(x2m);
+            const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
+            const float pbf = df * ss.Bmaxf;
+            const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
+            const bool det = (paf >= thAf * (1.0f - ea)) | (pbf >= thBf * (1.0f - eb));
+            const bool clip = !(df * ss.BSmaxf <= qaf + 0.25f && paf * ss.invSaf * 1.000001f <= qaf + 0.25f);
+            sh.pre[tt][lane] = make_float4(df, fmaf(-ss.hA1, ed, ss.hA0), fmaf(-(qaf + 1.0f), ed, hBc),
+                                           __uint_as_float((det ? 1u : 0u) | (clip ? 2u : 0u)));
+        }
+        if (t0 + KC < T) issue(t0 + KC, cur ^ 1);
+
+        // output of step te from the carried state (see k3_scan_fast's emit); A4 issues it
+        // from inside pass 1 of step te+1 so its DADD chain overlaps independent f32 work
+        auto emit = [&](int te, unsigned fl_e) {
+            const StepShared& se = sh.st[cur][te];
+            const double2* C2 = reinterpret_cast<const double2*>(se.C);
+            double o = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double2 c = C2[k];
+                o = dadd(o, dmul(c.x, h[2 * k]));
+                o = dadd(o, dmul(c.y, h[2 * k + 1]));
+            }
+            if (active) {
+                obase[se.ocol] = o;
+                if constexpr (TRACE) {
+                    const size_t b = (static_cast<size_t>(s) * T + t0 + te) * E + i;
+                    const size_t kst = static_cast<size_t>(p.S) * T * E;
+                    p.masks[b] = fl_e & 1u;
+                    p.masks[kst + b] = (fl_e >> 1) & 1u;
+                    p.masks[2 * kst + b] = (fl_e >> 2) & 1u;
+                }
+            }
+        };
+        unsigned fl_prev = fl;
+#pragma unroll 1
+        for (int tt = 0; tt < nt; ++tt) {
+            const StepShared& ss = sh.st[cur][tt];
+            const float4 pr = sh.pre[tt][lane];
+            const float df = pr.x;
+            const unsigned pf = __float_as_uint(pr.w);
+            const double uv = sh.u[cur][tt][lane];
             bool have = false;
             double delta, pa, pb;
             auto exact = [&]() {
                 if (!have) {
-                    delta = softplus_call(sh.x[tt][c]);
+                    delta = softplus_call(dadd(sh.dp[cur][tt][lane], bd));
                     pa = exp_call(dmul(delta, Amax));
                     pb = dmul(delta, ss.Bmax);
                     have = true;
                 }
             };
-            // inlier scales (static mode; dynamic steps where neither tensor is an outlier)
             double sA = ss.Sa, sB = ss.Sb;
             float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
-            // Certification margins (in units of q) where rounding matters (|q| <= qmax+1):
-            // a_bar: |dq| <= q (ln2 |x2| (ed + 2^-23) + 2^-21), ln2 |x2| <= LA there;
-            // b_bar: |dq| <= |q| (ed + 8 2^-24). Inlier forms folded to h0 - h1*ed.
-            float halfA = fmaf(-ss.hA1, ed, ss.hA0);
-            float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
-            // f32 a_bar peak: the detector's certified estimate and the clipping bound below
-            const float x2m = df * Amax2f;
-            const float paf = ex2_approx(x2m);
+            float halfA = pr.y, halfB = pr.z;
+            bool clip = pf & 2u;
             if (dyn) {
                 fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh, quant.cpp:303-311
-                // detect_outliers, channel-local form, on certified f32 peaks
-                const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
-                const float pbf = df * ss.Bmaxf;
-                const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
-                // one branch off the inlier path: outlier channels and decisions within the bound
-                if ((fl & 3u) | (paf >= thAf * (1.0f - ea)) | (pbf >= thBf * (1.0f - eb))) {
+                // detect_outliers, channel-local form: only outlier channels and certified-peak
+                // decisions within the bound of theta leave the inlier path
+                if ((fl & 3u) | (pf & 1u)) {
+                    float ed;
+                    softplus_f32(__double2float_rn(dadd(sh.dp[cur][tt][lane], bd)), ed);
+                    const float x2m = df * Amax2f;
+                    const float paf = ex2_approx(x2m);
+                    const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
+                    const float pbf = df * ss.Bmaxf;
+                    const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
                     if (!(fl & 1u)) {
                         if (paf > thAf * (1.0f + ea)) {
                             fl |= 1u;
@@ -640,36 +682,38 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
                             if (pb > thB) fl |= 2u;
                         }
                     }
-                    if (fl & 3u) exact();
-                    if (fl & 1u) {
-                        sA = scale_call(pa, qo);
-                        invA = __double2float_rn(recip_call(sA));
-                        qAf = qof;
-                        const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
-                        halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
-                    }
-                    if (fl & 2u) {
-                        sB = scale_call(pb, qo);
-                        kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
-                        qBf = qof;
-                        halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                    if (fl & 3u) {
+                        exact();
+                        if (fl & 1u) {
+                            sA = scale_call(pa, qo);
+                            invA = __double2float_rn(recip_call(sA));
+                            qAf = qof;
+                            const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                            halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+                        }
+                        if (fl & 2u) {
+                            sB = scale_call(pb, qo);
+                            kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
+                            qBf = qof;
+                            halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                        }
+                        clip = !(df * kB * ss.BSmaxf <= qBf + 0.25f && paf * invA * 1.000001f <= qAf + 0.25f);
                     }
                 }
             }
             const float dfb = df * kB;
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
-            // pass 1: codes from the f32 quotients (round-to-nearest via 1.5*2^23), clamped
-            // before rounding so the integer is the reference's clipped code. Two elements
-            // per packed f32x2 instruction; codes are kept as magic bit patterns.
-            unsigned ca[8];  // a_bar codes (>= 0) as integers, b_bar codes as exact f32 integers
-            float cb[8];
+            unsigned ca[16];  // a_bar codes (>= 0) as integers, b_bar codes as exact f32 integers
+            float cb[16];
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
-            const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
+            const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf);
             auto pass1 = [&](auto clamp) {
                 constexpr bool CL = decltype(clamp)::value;
-                float mda = 0.0f, mdb = 0.0f;  // largest distance to the rounded code (3-input max)
+                if constexpr (kDefer)
+                    if (tt > 0) emit(tt - 1, fl_prev);  // previous step's output
+                float mda = 0.0f, mdb = 0.0f;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 8; ++k) {
                     const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
                     float2 qa2 = __fmul2_rn(make_float2(ex2_approx(x2.x), ex2_approx(x2.y)), f2(invA));
                     if constexpr (CL) {
@@ -696,49 +740,38 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
                 }
                 redo |= (mda > halfA) | (mdb > halfB);
             };
-            // The clamps can bind only if the largest quotient exceeds the cap: q_b <=
-            // dfb*max|BSf| and q_a <= paf*invA (monotone rounding; the factor covers
-            // ex2.approx's relative error). Warp-uniform choice, both forms are exact.
-            const bool noclip = dfb * ss.BSmaxf <= capB && paf * invA * 1.000001f <= capA;
-            if (__all_sync(0xffffffffu, noclip)) pass1(std::false_type{});
-            else pass1(std::true_type{});
+            if (__any_sync(0xffffffffu, clip)) pass1(std::true_type{});
+            else pass1(std::false_type{});
             if (redo) {  // exact f64 codes where the f32 quotient is not certified
                 exact();
 #pragma unroll
-                for (int m = 0; m < 8; ++m) {
+                for (int m = 0; m < 16; ++m) {
                     const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
                     if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
                         ca[m] = static_cast<unsigned>(static_cast<int>(
-                            qdiv_call(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
-                    const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
+                            qdiv_call(exp_call(dmul(delta, arow[m])), sA, static_cast<double>(qAf))));
+                    const float qb_f = fminf(fmaxf(dfb * ss.BSf[m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
-                        cb[m] = static_cast<float>(
-                            qdiv_call(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
+                        cb[m] = static_cast<float>(qdiv_call(dmul(delta, ss.B[m]), sB, static_cast<double>(qBf)));
                 }
             }
-            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update.
-            // a_bar codes are >= 0: fma(2^52 + c, sA, -2^52 sA) = c sA before its one rounding,
-            // i.e. exactly dmul(c, sA).
+            // pass 2: dequantized values (code * s) and the exact f64 update, ssm.cpp:165-167
             const double nKA = dmul(sA, -4503599627370496.0);
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < 16; ++m) {
                 const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
                 const double b_q = dmul(static_cast<double>(cb[m]), sB);
-                h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
+                h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));
             }
-            // h detection + codes. Rounding to f32 is monotone, so the f32 peak
-            // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
-            // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
-            // needs the exact f64 peak. Outlier channels take the exact peak for their scale.
-            float2 hfv[4];
+            // h detection + codes (see k3_scan_fast): f32 peak = fl32 of the exact peak
+            float2 hfv[8];
             float phf = 0.0f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 8; ++k) {
                 hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
                 phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
             }
-            phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
             double sH = ss.Sh, qH = qa;
             float invHf = ss.invShf;
             if (dyn && ((fl & 4u) | (phf >= thHf))) {
@@ -748,16 +781,14 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
                     } else {  // phf == fl32(theta): the exact peak decides
                         double ph = 0.0;
 #pragma unroll
-                        for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
-                        ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                        for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(h[m]));
                         if (ph > thH) fl |= 4u;
                     }
                 }
                 if (fl & 4u) {
                     double ph = 0.0;
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
-                    ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                    for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(h[m]));
                     sH = scale_call(ph, qo);
                     invHf = __double2float_rn(recip_call(sH));
                     qH = qo;
@@ -766,13 +797,13 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
             {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
                 const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
                 const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
-                float chd[8];  // h codes as exact f32 integers (F2F.F64 balances the XU and FP64 pipes)
+                float chd[16];
                 bool hredo = EXACT;
                 auto hcodes = [&](auto clamp) {
                     constexpr bool CL = decltype(clamp)::value;
                     float mdh = 0.0f;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < 8; ++k) {
                         float2 q = __fmul2_rn(hfv[k], f2(invHf));
                         if constexpr (CL) {
                             q.x = fminf(fmaxf(q.x, -capH), capH);
@@ -787,47 +818,43 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_r1(const ScanDirs P, const St
                     }
                     hredo |= mdh > halfH;
                 };
-                if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});  // |q| <= phf*invHf
+                if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});
                 else hcodes(std::true_type{});
                 if (hredo) {
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) {
+                    for (int m = 0; m < 16; ++m) {
                         const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
                         const float q = fminf(fmaxf(hv * invHf, -capH), capH);
-                        if (EXACT || fabsf(q - rintf(q)) > halfH)
-                            chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
+                        if (EXACT || fabsf(q - rintf(q)) > halfH) chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 8; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
-            }
-            // o = 0 + C_0 h_0 + ... + C_15 h_15 in order: both halves form their products,
-            // the first half sums from 0, the second continues the same chain
-            double pr[8];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) pr[m] = dmul(ss.C[m0 + m], h[m]);
-            double o = 0.0;
-            if (half == 0) {
-#pragma unroll
-                for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
+                for (int m = 0; m < 16; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
             }
-            o = __shfl_sync(0xffffffffu, o, lane & ~1u);
-            if (half == 1) {
-#pragma unroll
-                for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
-                if (active) {
-                    obase[ss.ocol] = o;
-                    if (p.masks) {
-                        const size_t b = (static_cast<size_t>(s) * T + t) * E + i;
-                        const size_t kst = static_cast<size_t>(p.S) * T * E;
-                        p.masks[b] = fl & 1u;
-                        p.masks[kst + b] = (fl >> 1) & 1u;
-                        p.masks[2 * kst + b] = (fl >> 2) & 1u;
-                    }
-                }
-            }
+            if constexpr (!kDefer) emit(tt, fl);
+            fl_prev = fl;
         }
+        if constexpr (kDefer) emit(nt - 1, fl_prev);
     }
+}
+
+// Shapes measured at Vim-B batch 256 (ms per launch, both directions): one warp
+// per CTA, 4-step chunks, 12 CTAs per SM (<= 168 registers) 2.225; two or four
+// warps per CTA 2.306 / 2.375; 8-step chunks 2.376; 128 registers (16 warps per SM)
+// spills and runs 3.01; per-lane cp.async staging instead of bulk rows 2.306.
+constexpr int kC1Chunk = 4, kC1MinBlocks = 12;
+
+template <bool EXACT, int ABITS, bool TRACE>
+static cudaError_t launch_c1(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
+    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, kC1MinBlocks>;
+    const int smem = static_cast<int>(sizeof(C1Smem<kC1Chunk>));
+    cudaError_t e = ensure_smem_attr<kern>(smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((P.d[0].E + 31) / 32, P.d[0].S, ndirs);
+    kern<<<grid, 32, smem, st>>>(P, steps);
+    ++kernel_launch_counter();
+    return cudaGetLastError();
 }
 
 template <bool EXACT, int ABITS, bool TRACE>
@@ -841,27 +868,17 @@ static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* s
     return cudaGetLastError();
 }
 
+// kernel: 0 the one-thread-per-channel kernel (needs an even E: 16-byte rows), 1 the
+// two-threads-per-channel kernel
 template <int ABITS>
-static cudaError_t launch_r1(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
-    const int smem = static_cast<int>(sizeof(WarpSmem)) * (kThr / 32);
-    cudaError_t e = ensure_smem_attr<k3_scan_r1<false, ABITS>>(smem);
-    if (e != cudaSuccess) return e;
-    dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
-    k3_scan_r1<false, ABITS><<<grid, kThr, smem, st>>>(P, steps);
-    ++kernel_launch_counter();
-    return cudaGetLastError();
-}
-
-template <int ABITS>
-static cudaError_t launch_variant(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st,
-                                  int variant, bool trace) {
-    switch (variant) {
-        case 0: return trace ? launch_fast<false, ABITS, true>(P, ndirs, steps, st)
-                             : launch_fast<false, ABITS, false>(P, ndirs, steps, st);
-        case 1: return trace ? launch_fast<true, ABITS, true>(P, ndirs, steps, st)
-                             : launch_fast<true, ABITS, false>(P, ndirs, steps, st);
-        default: return launch_r1<ABITS>(P, ndirs, steps, st);
+static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st,
+                                 int kernel, bool exact, bool trace) {
+    if (kernel == 0) {
+        if (exact) return trace ? launch_c1<true, ABITS, true>(P, ndirs, steps, st) : launch_c1<true, ABITS, false>(P, ndirs, steps, st);
+        return trace ? launch_c1<false, ABITS, true>(P, ndirs, steps, st) : launch_c1<false, ABITS, false>(P, ndirs, steps, st);
     }
+    if (exact) return trace ? launch_fast<true, ABITS, true>(P, ndirs, steps, st) : launch_fast<true, ABITS, false>(P, ndirs, steps, st);
+    return trace ? launch_fast<false, ABITS, true>(P, ndirs, steps, st) : launch_fast<false, ABITS, false>(P, ndirs, steps, st);
 }
 
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs) {
@@ -890,9 +907,19 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const bool trace = dirs[0].masks != nullptr;
+    const bool even = (dirs[0].E & 1) == 0;
+    // auto: one thread per channel for A4 (measured 2.225 vs 2.43 ms at Vim-B, 0.358 vs
+    // 0.415 at Vim-S), two per channel for A8 (1.17 vs 1.63 ms at Vim-T batch 256)
+    int kernel = (dirs[0].abits == 4 && even) ? 0 : 1;
+    if (variant == 2) kernel = 1;
+    if (variant == 3) {
+        if (!even) return cudaErrorNotSupported;
+        kernel = 0;
+    }
+    const bool exact = variant == 1;
     switch (dirs[0].abits) {
-        case 4: return launch_variant<4>(P, ndirs, steps, st, variant, trace);
-        default: return launch_variant<8>(P, ndirs, steps, st, variant, trace);
+        case 4: return launch_kernel<4>(P, ndirs, steps, st, kernel, exact, trace);
+        default: return launch_kernel<8>(P, ndirs, steps, st, kernel, exact, trace);
     }
 }
 

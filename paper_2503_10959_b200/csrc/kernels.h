@@ -172,9 +172,10 @@ struct ScanParams {
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
 // Fast path (dynamic/static, channel-local detector): both directions in one
 // launch (plus a step-table prep launch); work = scan_fast_workspace_bytes(S, T,
-// ndirs) bytes, 16-aligned. variant 0: the shipped kernel (k3_scan_v2); 1: the
-// same with the certified f32 codes disabled (every element exact f64); 2: the
-// round-1 kernel (k3_scan_fast), kept for A/B runs. Non-null `masks` selects the
+// ndirs) bytes, 16-aligned. variant 0: auto (one thread per channel for A4 and
+// even E, two per channel otherwise); 1: the same with the certified f32 codes
+// disabled (every element exact f64); 2: the two-threads-per-channel kernel; 3:
+// the one-thread-per-channel kernel (even E). Non-null `masks` selects the
 // parity-trace instantiation.
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,

@@ -1,0 +1,36 @@
+"""Per-CUDA-source-line instruction counts and stall samples of the first kernel in an
+ncu report (source page, cuda+sass view), sorted by samples.
+
+usage: ncu_srclines.py REPORT [normaliser] [top]
+"""
+import csv, subprocess, sys
+
+rep = sys.argv[1]
+norm = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 60
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+fname, hdr, rows = None, None, []
+for r in csv.reader(out.splitlines()):
+    if not r:
+        continue
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
+        hdr = r
+        continue
+    if hdr is None or not r[0] or r[0] in ("Function Name",):
+        continue
+    try:
+        ie = int(r[hdr.index("Instructions Executed")])
+        sm = int(r[hdr.index("# Samples")])
+    except (ValueError, IndexError):
+        continue
+    if ie or sm:
+        rows.append((sm, ie, f"{fname}:{r[0]}", r[1].strip()[:90]))
+ts = sum(r[0] for r in rows) or 1
+ti = sum(r[1] for r in rows) or 1
+print(f"total instructions {ti} ({ti / norm:.1f} per unit), samples {ts}")
+for sm, ie, loc, src in sorted(rows, reverse=True)[:top]:
+    print(f"{sm / ts * 100:5.1f}% smp {ie / norm:7.1f} inst  {loc:24s} {src}")

@@ -2,7 +2,7 @@
 
     python scripts/scan_ab.py E B blocks abits [variants...]
 
-variant 0 = shipped fast kernel, 3 = round-1 fast kernel, 2 = exact codes, 1 = reference kernel.
+variant 0 = auto, 1 = reference kernel, 2 = exact codes, 3 = two threads per channel, 4 = one thread per channel.
 """
 import os
 import sys
@@ -13,7 +13,7 @@ import torch
 import paper_2503_10959_b200 as ob
 
 E, B, blocks, abits = (int(a) for a in sys.argv[1:5])
-variants = [int(v) for v in sys.argv[5:]] or [0, 3, 2]
+variants = [int(v) for v in sys.argv[5:]] or [0, 3, 4, 2]
 ctx = ob.Context(0)
 m = ob.Model(ctx, ob.Dims(embed=E, blocks=blocks), 1234)
 g = torch.Generator(device="cuda").manual_seed(0)

@@ -208,17 +208,17 @@ def test_k1_variants_identical(pair, abits):
 @pytest.mark.parametrize("abits", [4, 8])
 def test_scan_variants_identical(pair, abits):
     """K3 fast path (certified f32 codes + exact fallbacks), its all-exact
-    variant, the round-1 fast kernel and the per-direction reference kernel
-    agree bit-for-bit."""
+    variant, the per-direction reference kernel and both fast kernels (one and
+    two threads per channel) agree bit-for-bit."""
     om, gm, imgs, cimgs = pair
     spec = _spec(abits, rho=0.05)
     gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
     outs = []
-    for v in (0, 1, 2, 3):
+    for v in (0, 1, 2, 3, 4):
         gm.set_option("scan_variant", v)
         outs.append(gm.forward_host(imgs, gcal, 1))
     gm.set_option("scan_variant", 0)
-    for v in (1, 2, 3):
+    for v in (1, 2, 3, 4):
         assert np.array_equal(outs[0], outs[v]), v
 
 
