@@ -90,6 +90,17 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
                                       int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
                                       uint8_t* scanned, double* rs_work);
 
+/* K1 with the A4 inlier codes nibble-packed (pack_int4's layout, gemm.cpp:60-73 / PackedInt4,
+ * gemm.hpp:40-49, with the channels as its columns: byte [m][ch/2], low nibble = even channel),
+ * act_bits = 4, E even: codes4 dev uint8 [S*T][E/2]. Every other argument as
+ * ouro_b200_detect_quantize. */
+ouro_status ouro_b200_detect_quantize_packed(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
+                                             size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
+                                             const double* s_in, const double* s_full, size_t n_refresh,
+                                             unsigned outlier_bits, int mode, int literal, uint8_t* codes4,
+                                             double* s_row, int32_t* ocnt, uint32_t* omask, int8_t* ocode,
+                                             double* oscale, uint8_t* scanned);
+
 /* K2: hybrid quant-linear on tcgen05 kind::i8 (hybrid_gemm, gemm.hpp:78-87,
  * gemm.cpp:181-225): out[m][r] = ws[r]*(s_row[m]*acc_in[m][r]
  *   + sum_{ch in O(m), ascending} (oscale[m][ch]*w[r][ch])*ocode[m][ch]),
@@ -104,6 +115,17 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
                                    const int8_t* ocode, const double* oscale, const int8_t* w, const int8_t* wt,
                                    const double* ws, int post, double* out, size_t ld_out, double* out2, size_t split,
                                    const double* bias, int32_t* acc_in, int32_t* acc_out);
+
+/* K2 on the nibble-packed A4 operand of ouro_b200_detect_quantize_packed (codes4 dev uint8
+ * [M][K/2], K a multiple of 32): the packed tiles are loaded by TMA and expanded to int8
+ * in shared memory before the tcgen05 MMA (gemm_i4 unpacks per call, gemm.cpp:142-143).
+ * Every other argument and every output as ouro_b200_quant_linear. */
+ouro_status ouro_b200_quant_linear_packed(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const uint8_t* codes4,
+                                          const double* s_row, const int32_t* ocnt, const uint32_t* omask,
+                                          const int8_t* ocode, const double* oscale, const int8_t* w,
+                                          const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
+                                          double* out2, size_t split, const double* bias, int32_t* acc_in,
+                                          int32_t* acc_out);
 
 /* K3: selective scan of one direction with the QuantHook policy (s6_scan,
  * ssm.hpp:131-132, ssm.cpp:124-186; QuantHook quant.cpp:456-501), N = 16.
@@ -195,7 +217,8 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid),
  * 3 / 4 fast path on the two- / one-thread-per-channel kernel (A/B aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
- * detector kernel everywhere; "split_parts" in [1, 4] (default 2) runs a batch of
+ * detector kernel everywhere; "pack_a4" = 1: A4 activation codes travel
+ * nibble-packed from K1 to K2, 0 (default) one int8 byte per code; "split_parts" in [1, 4] (default 2) runs a batch of
  * >= 32 * parts samples as that many independent sub-batches on their own
  * streams (results identical), 1 one stream; "feed_chunks" (default 8) = H2D
  * chunks of forward_host for batches >= 64. */

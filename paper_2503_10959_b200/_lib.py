@@ -35,6 +35,10 @@ _SIGS = {
                                    _P, _P, _P, _P, _P, _P, _P], _I),
     "ouro_b200_quant_linear": ([_P, _SZ, _SZ, _SZ, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P, _SZ, _P,
                                 _P, _P], _I),
+    "ouro_b200_detect_quantize_packed": ([_P, _P, _P, _P, _SZ, _SZ, _SZ, _I, _I, _I, _D, _P, _P, _SZ, _U, _I, _I,
+                                          _P, _P, _P, _P, _P, _P, _P], _I),
+    "ouro_b200_quant_linear_packed": ([_P, _SZ, _SZ, _SZ, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P, _SZ,
+                                       _P, _P, _P], _I),
     "ouro_b200_quant_scan": ([_P, _SZ, _SZ, _SZ, _SZ, _I, _I, _P, _P, _P, _P, _P, _I, _SZ, _U, _U, _P, _P, _P, _P,
                               _I, _P], _I),
     "ouro_b200_dgemm": ([_P, _SZ, _SZ, _SZ, _P, _SZ, _P, _I, _P, _SZ, _P, _SZ, _P], _I),

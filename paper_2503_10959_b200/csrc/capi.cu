@@ -175,14 +175,17 @@ ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out) {
     });
 }
 
-ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
-                                      size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
-                                      const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
-                                      unsigned outlier_bits, int mode, int literal, int8_t* codes, double* s_row,
-                                      int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
-                                      uint8_t* scanned, double* rs_work) {
+static ouro_status detect_quantize_impl(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
+                                        size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
+                                        const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
+                                        unsigned outlier_bits, int mode, int literal, int8_t* codes, uint8_t* codes4,
+                                        double* s_row, int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
+                                        uint8_t* scanned) {
     return guarded([&] {
-        require(ctx && x && codes && s_row && ocnt && omask && ocode && oscale, "detect_quantize: NULL argument");
+        require(ctx && x && (codes || codes4) && s_row && ocnt && omask && ocode && oscale,
+                "detect_quantize: NULL argument");
+        require(!codes4 || (act_bits == 4 && E % 2 == 0),
+                "detect_quantize_packed: packed codes need act_bits = 4 and an even channel count");
         require(mode == ob::MODE_DYNAMIC || mode == ob::MODE_STATIC, "detect_quantize: mode must be dynamic or static");
         require(mode == ob::MODE_STATIC ? s_full != nullptr : s_in != nullptr, "detect_quantize: missing scales");
         require(act_bits >= 2 && act_bits <= 8 && outlier_bits >= act_bits && outlier_bits <= 8,
@@ -210,9 +213,9 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
         k.cal.theta = theta;
         k.cal.s_in = s_in;
         k.cal.s_full = s_full;
-        (void)rs_work;
         k.force_literal = literal;
         k.codes = codes;
+        k.codes4 = codes4;
         k.s_row = s_row;
         k.ocnt = ocnt;
         k.omask = omask;
@@ -223,15 +226,40 @@ ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const
     });
 }
 
-ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
-                                   const double* s_row, const int32_t* ocnt, const uint32_t* omask,
-                                   const int8_t* ocode, const double* oscale, const int8_t* w, const int8_t* wt,
-                                   const double* ws, int post, double* out, size_t ld_out, double* out2, size_t split,
-                                   const double* bias, int32_t* acc_in, int32_t* acc_out) {
+ouro_status ouro_b200_detect_quantize(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
+                                      size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
+                                      const double* s_in, const double* s_full, size_t n_refresh, unsigned act_bits,
+                                      unsigned outlier_bits, int mode, int literal, int8_t* codes, double* s_row,
+                                      int32_t* ocnt, uint32_t* omask, int8_t* ocode, double* oscale,
+                                      uint8_t* scanned, double* rs_work) {
+    (void)rs_work;  // kept for ABI stability (round-1 signature); the row factor is computed in-kernel
+    if (!codes) return guarded([] { throw ob::ValidationError("detect_quantize: NULL argument"); });
+    return detect_quantize_impl(ctx, x, x2, gate, S, T, E, src, order, grid, theta, s_in, s_full, n_refresh, act_bits,
+                                outlier_bits, mode, literal, codes, nullptr, s_row, ocnt, omask, ocode, oscale, scanned);
+}
+
+ouro_status ouro_b200_detect_quantize_packed(ouro_b200_ctx* ctx, const double* x, const double* x2, const double* gate,
+                                             size_t S, size_t T, size_t E, int src, int order, int grid, double theta,
+                                             const double* s_in, const double* s_full, size_t n_refresh,
+                                             unsigned outlier_bits, int mode, int literal, uint8_t* codes4,
+                                             double* s_row, int32_t* ocnt, uint32_t* omask, int8_t* ocode,
+                                             double* oscale, uint8_t* scanned) {
+    if (!codes4) return guarded([] { throw ob::ValidationError("detect_quantize_packed: NULL argument"); });
+    return detect_quantize_impl(ctx, x, x2, gate, S, T, E, src, order, grid, theta, s_in, s_full, n_refresh, 4u,
+                                outlier_bits, mode, literal, nullptr, codes4, s_row, ocnt, omask, ocode, oscale, scanned);
+}
+
+static ouro_status quant_linear_impl(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
+                                     const uint8_t* codes4, const double* s_row, const int32_t* ocnt,
+                                     const uint32_t* omask, const int8_t* ocode, const double* oscale, const int8_t* w,
+                                     const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
+                                     double* out2, size_t split, const double* bias, int32_t* acc_in,
+                                     int32_t* acc_out) {
     return guarded([&] {
-        require(ctx && codes && s_row && ocnt && omask && ocode && oscale && w && wt && ws && out,
+        require(ctx && (codes || codes4) && s_row && ocnt && omask && ocode && oscale && w && wt && ws && out,
                 "quant_linear: NULL argument");
         require(K % 16 == 0 && R % 32 == 0, "quant_linear: K must be a multiple of 16 and R of 32");
+        require(!codes4 || K % 32 == 0, "quant_linear_packed: K must be a multiple of 32");
         require((acc_in == nullptr) == (acc_out == nullptr), "quant_linear: acc_in and acc_out go together");
         require(post != ob::POST_INPROJ || (out2 != nullptr && split % 32 == 0 && split < R),
                 "quant_linear: in_proj post-op needs out2 and a split that is a multiple of 32");
@@ -242,6 +270,7 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
         q.R = static_cast<int>(R);
         q.K = static_cast<int>(K);
         q.a.codes = const_cast<int8_t*>(codes);
+        q.a.codes4 = const_cast<uint8_t*>(codes4);
         q.a.s_row = const_cast<double*>(s_row);
         q.a.ocnt = const_cast<int*>(ocnt);
         q.a.omask = const_cast<uint32_t*>(omask);
@@ -261,6 +290,27 @@ ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_
         q.epi.acc_out = acc_out;
         ob::cuda_check(ob::launch_qlinear(q, ctx->c->stream, ctx->c->num_sms), "quant_linear");
     });
+}
+
+ouro_status ouro_b200_quant_linear(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const int8_t* codes,
+                                   const double* s_row, const int32_t* ocnt, const uint32_t* omask,
+                                   const int8_t* ocode, const double* oscale, const int8_t* w, const int8_t* wt,
+                                   const double* ws, int post, double* out, size_t ld_out, double* out2, size_t split,
+                                   const double* bias, int32_t* acc_in, int32_t* acc_out) {
+    if (!codes) return guarded([] { throw ob::ValidationError("quant_linear: NULL argument"); });
+    return quant_linear_impl(ctx, M, R, K, codes, nullptr, s_row, ocnt, omask, ocode, oscale, w, wt, ws, post, out,
+                             ld_out, out2, split, bias, acc_in, acc_out);
+}
+
+ouro_status ouro_b200_quant_linear_packed(ouro_b200_ctx* ctx, size_t M, size_t R, size_t K, const uint8_t* codes4,
+                                          const double* s_row, const int32_t* ocnt, const uint32_t* omask,
+                                          const int8_t* ocode, const double* oscale, const int8_t* w,
+                                          const int8_t* wt, const double* ws, int post, double* out, size_t ld_out,
+                                          double* out2, size_t split, const double* bias, int32_t* acc_in,
+                                          int32_t* acc_out) {
+    if (!codes4) return guarded([] { throw ob::ValidationError("quant_linear_packed: NULL argument"); });
+    return quant_linear_impl(ctx, M, R, K, nullptr, codes4, s_row, ocnt, omask, ocode, oscale, w, wt, ws, post, out,
+                             ld_out, out2, split, bias, acc_in, acc_out);
 }
 
 static void quant_scan_impl(ouro_b200_ctx* ctx, size_t S, size_t T, size_t E, size_t N, int order, int grid,
@@ -631,6 +681,9 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         } else if (k == "split_parts") {
             require(value >= 1 && value <= 4, "model_set_option: split_parts must be in [1, 4]");
             m->m->split_parts = static_cast<int>(value);
+        } else if (k == "pack_a4") {
+            require(value == 0 || value == 1, "model_set_option: pack_a4 must be 0 or 1");
+            m->m->pack_a4 = static_cast<int>(value);
         } else if (k == "k1_variant") {
             require(value >= 0 && value <= 1, "model_set_option: k1_variant must be 0 or 1");
             m->m->k1_variant = static_cast<int>(value);
@@ -738,7 +791,7 @@ ouro_status ouro_b200_detect_quantize_planes(ouro_b200_ctx* ctx, const double* x
         p.n_refresh = static_cast<int>(n_refresh);
         p.abits = static_cast<int>(act_bits);
         p.obits = static_cast<int>(outlier_bits);
-        p.a = ob::QAct{codes, s_row, ocnt, omask, ocode, oscale, static_cast<int>((Kp + 31) / 32)};
+        p.a = ob::QAct{codes, nullptr, s_row, ocnt, omask, ocode, oscale, static_cast<int>((Kp + 31) / 32)};
         p.scanned = scanned;
         void* work = nullptr;
         cudaStream_t st = ctx->c->stream;

@@ -312,6 +312,7 @@ void Model::ensure_work(Work& w, int S, bool trace) {
     // both directions runs as one launch); slot 0 also serves in_proj / out_proj
     const size_t slots = std::max<size_t>(1, nd);
     w.codes.ensure(slots * rows * E);
+    w.codes4.ensure(slots * rows * E / 2);
     w.ocode.ensure(slots * rows * E);
     w.oscale.ensure(slots * rows * E);
     w.omask.ensure(slots * rows * ((E + 31) / 32));
@@ -511,6 +512,7 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
 
     int qslot = 0;  // QAct slot the K1 / K2 / trace lambdas address
     const size_t J = (E + 31) / 32;
+    const bool pk = qlin && pack_a4 && cal->spec.abits == 4;  // nibble-packed A4 operand
     auto k1_base = [&](int src, const double* x, int order, int b, int site, bool record) {
         K1Params k;
         k.S = S;
@@ -532,7 +534,8 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
             k.cal.s_full = cal->s_full_dev(true, li);
             k.inv_in = cal->inv_in_dev(true, li);
             k.inv_full = cal->inv_full_dev(true, li);
-            k.codes = w.codes.p + qslot * rows * E;
+            if (pk) k.codes4 = w.codes4.p + qslot * rows * E / 2;
+            else k.codes = w.codes.p + qslot * rows * E;
             k.s_row = w.s_row.p + qslot * rows;
             k.ocnt = w.ocnt.p + qslot * rows;
             k.omask = w.omask.p + qslot * rows * J;
@@ -552,7 +555,8 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
     };
     auto qact = [&]() {
         QAct a;
-        a.codes = w.codes.p + qslot * rows * E;
+        if (pk) a.codes4 = w.codes4.p + qslot * rows * E / 2;
+        else a.codes = w.codes.p + qslot * rows * E;
         a.s_row = w.s_row.p + qslot * rows;
         a.ocnt = w.ocnt.p + qslot * rows;
         a.omask = w.omask.p + qslot * rows * J;
@@ -564,7 +568,15 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
     auto trace_lin = [&](int b, int site, int R) {
         if (!tb(b) || !qlin) return;
         std::string p = "lin" + std::to_string(site) + ".";
-        grab(trace, p + "codes", w.codes.p + qslot * rows * E, rows * E, st);
+        if (pk) {  // the packed operand, and its codes unpacked (one int8 per code) for the parity checks
+            grab(trace, p + "codes4", w.codes4.p + qslot * rows * E / 2, rows * E / 2, st);
+            const std::vector<char>& b4 = trace->blobs[p + "codes4"];
+            std::vector<char> c(rows * E);
+            unpack_nibbles(reinterpret_cast<const uint8_t*>(b4.data()), rows * E, reinterpret_cast<int8_t*>(c.data()));
+            trace->blobs[p + "codes"] = std::move(c);
+        } else {
+            grab(trace, p + "codes", w.codes.p + qslot * rows * E, rows * E, st);
+        }
         grab(trace, p + "s_row", w.s_row.p + qslot * rows, rows, st);
         grab(trace, p + "ocnt", w.ocnt.p + qslot * rows, rows, st);
         grab(trace, p + "ocode", w.ocode.p + qslot * rows * E, rows * E, st);

@@ -178,6 +178,12 @@ class Model {
     void quantize(unsigned bits);
     bool fp_dirty = true;
     int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
+    int pack_a4 = 0;       // 1: A4 inlier codes travel nibble-packed from K1 to K2, which unpacks them in
+                           // shared memory (QAct::codes4); 0 (default): one int8 byte per code. Measured at
+                           // Vim-B batch 256: packed K2 176 / 107 / 127 us vs 157 / 93 / 119 (in_proj / x_proj /
+                           // out_proj), forward +1.5 ms: the f64 outputs (260-560 MB per launch) bound K2, the
+                           // packed operand saves 19 MB per launch and its unpack warpgroup adds ~4.5K
+                           // warp-instructions per 128x128 tile
     SpikeCfg spikes;       // SpikeHook settings (rate 0 = off); block/dir set per scan
     int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only,
                            // 3 fast path on the two-threads-per-channel kernel, 4 on the one-thread-per-channel kernel
@@ -191,7 +197,7 @@ class Model {
         DevBuf<double> s_row, oscale;
         DevBuf<int> ocnt;
         DevBuf<uint32_t> omask;
-        DevBuf<uint8_t> scanned, masks, scan_steps;
+        DevBuf<uint8_t> scanned, masks, scan_steps, codes4;
         DevBuf<unsigned long long> peaks;
         DevBuf<int32_t> acc_in, acc_out;
         std::vector<cudaEvent_t> feed_events;  // host-feed chunk events, created on first use

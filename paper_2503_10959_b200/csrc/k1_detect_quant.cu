@@ -46,6 +46,12 @@ namespace ob {
 
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 
+// four consecutive codes in [-7, 7] as two pack_int4 bytes (gemm.cpp:60-73: low nibble
+// = even column), one 16-bit store
+__device__ __forceinline__ uint16_t pack4(int c0, int c1, int c2, int c3) {
+    return static_cast<uint16_t>((c0 & 0xF) | ((c1 & 0xF) << 4) | ((c2 & 0xF) << 8) | ((c3 & 0xF) << 12));
+}
+
 
 // exact merged value y = merged * silu(gate) (ssm.cpp:231): the rare path, kept out of line
 __device__ __noinline__ double merge_exact(double m, double g) { return dmul(m, silu_d(g)); }
@@ -155,9 +161,12 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
                     c[k] = quant_code_int(v[k], S, inv, qa, qai);
                 }
             }
-            *reinterpret_cast<char4*>(p.codes + row * E + ch) =
-                make_char4(static_cast<signed char>(c[0]), static_cast<signed char>(c[1]),
-                           static_cast<signed char>(c[2]), static_cast<signed char>(c[3]));
+            if (p.codes4)
+                *reinterpret_cast<uint16_t*>(p.codes4 + row * (E >> 1) + (ch >> 1)) = pack4(c[0], c[1], c[2], c[3]);
+            else
+                *reinterpret_cast<char4*>(p.codes + row * E + ch) =
+                    make_char4(static_cast<signed char>(c[0]), static_cast<signed char>(c[1]),
+                               static_cast<signed char>(c[2]), static_cast<signed char>(c[3]));
         }
         // mask word of channels 32w..32w+31 from 8 lanes x 4 bits (all zero in the common case)
         unsigned bits = active ? in << ((lane & 7) * 4) : 0u;
@@ -242,6 +251,7 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
     const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
     int8_t* __restrict__ const codes = p.codes;
+    uint8_t* __restrict__ const codes4 = p.codes4;
     int8_t* __restrict__ const ocode = p.ocode;
     double* __restrict__ const oscale = p.oscale;
     uint32_t* __restrict__ const omask = p.omask;
@@ -270,8 +280,9 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
         const double* xr = sb + ch;
         const size_t row0 = static_cast<size_t>(s) * T + ts;
         int8_t* cp = codes + row0 * E + ch;
+        uint16_t* cp4 = reinterpret_cast<uint16_t*>(codes4 + row0 * (E >> 1) + (ch >> 1));
         uint32_t* mp = omask + row0 * J + (ch >> 5);
-        for (int t = ts; t < te; ++t, xr += E, cp += E, mp += J) {
+        for (int t = ts; t < te; ++t, xr += E, cp += E, cp4 += E >> 2, mp += J) {
             const int slot = t - ts;
             const size_t row = row0 + slot;
             const double S = s_tab[t];
@@ -319,9 +330,12 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
             if (active) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) cc[k] = ((in >> k) & 1u) ? 0 : min(max(cc[k], -qai), qai);
-                *reinterpret_cast<char4*>(cp) =
-                    make_char4(static_cast<signed char>(cc[0]), static_cast<signed char>(cc[1]),
-                               static_cast<signed char>(cc[2]), static_cast<signed char>(cc[3]));
+                if (codes4)
+                    *cp4 = pack4(cc[0], cc[1], cc[2], cc[3]);
+                else
+                    *reinterpret_cast<char4*>(cp) =
+                        make_char4(static_cast<signed char>(cc[0]), static_cast<signed char>(cc[1]),
+                                   static_cast<signed char>(cc[2]), static_cast<signed char>(cc[3]));
                 if (in) {  // outlier channels: own scale |x|/q_o, code at o_bits
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -443,6 +457,7 @@ __global__ void __launch_bounds__(256) k1_literal(const K1Params p) {
             const int ch = j * 32 + lane;
             const bool valid = j < J && ch < E;
             const bool isout = valid && ((inmask >> j) & 1u);
+            int ci = 0;
             if (valid) {
                 double c = 0.0;
                 if (isout) {
@@ -452,7 +467,13 @@ __global__ void __launch_bounds__(256) k1_literal(const K1Params p) {
                 } else {
                     c = quant_code_inv(v[j], S, inv, qa);
                 }
-                p.codes[row * E + ch] = static_cast<int8_t>(static_cast<int>(c));
+                ci = static_cast<int>(c);
+                if (!p.codes4) p.codes[row * E + ch] = static_cast<int8_t>(ci);
+            }
+            if (p.codes4) {  // lanes 2i, 2i+1 hold channels 32j + 2i, 32j + 2i + 1: one packed byte
+                const unsigned nib = static_cast<unsigned>(ci) & 0xFu;
+                const unsigned hi = __shfl_down_sync(0xffffffffu, nib, 1);
+                if (valid && !(lane & 1)) p.codes4[row * (E >> 1) + (ch >> 1)] = static_cast<uint8_t>(nib | (hi << 4));
             }
             if (j < J) {
                 const unsigned mb = __ballot_sync(0xffffffffu, isout);
@@ -528,6 +549,8 @@ static bool k1_fast(const K1Params& p) {
 
 cudaError_t launch_k1(const K1Params& p, cudaStream_t st) {
     if (p.E < 1 || p.E > 1024 || p.T < 1 || p.S < 1 || p.window < 1) return cudaErrorInvalidValue;
+    if (p.codes4 && (p.abits != 4 || (p.E & 1))) return cudaErrorInvalidValue;  // nibbles hold [-7, 7]
+    if (!p.codes4 && !p.codes && p.mode != MODE_FP) return cudaErrorInvalidValue;
     const bool fast = k1_fast(p);
     switch (p.src) {
         case K1_SRC_PLAIN: return fast ? launch_staged<K1_SRC_PLAIN>(k1_dirs(&p, 1), st) : launch_literal<K1_SRC_PLAIN>(p, st);

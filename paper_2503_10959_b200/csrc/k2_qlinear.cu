@@ -21,6 +21,11 @@
 //   warp 3      row metadata (S_m, |O(t)|, mask words) of upcoming tiles, bulk-copied
 //   warps 4..   epilogue: tcgen05.ld 32x32b, f64 dequant + outlier terms per row, then
 //               ws[r] * y, the post-op and TMA stores of 32x16 f64 boxes from swizzled staging
+//   last 4      (A4 nibble-packed activations, PK) unpack warpgroup: the producer's TMA puts
+//               the stage's packed 128 x 64-byte A box into the upper half of the stage's A
+//               region; these warps expand it in place to the 128B-swizzled int8 tile
+//               (pack_int4's layout, gemm.cpp:60-73: low nibble = even channel), fence it to
+//               the async proxy and arrive on the stage's full barrier next to the TMA bytes
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,10 +43,11 @@ constexpr int kStgBufs = 1;  // epilogue staging buffers per warp
 //    warpgroup 0 to the epilogue: epilogue-heavy calls (residual post-op,
 //    outlier terms; the f64 epilogue, not the int8 main loop, bounds those —
 //    main loop alone 0.039 ms of 0.135 for the Vim-B out_proj).
-template <int EW>
+template <int EW, bool PK = false>
 struct K2Cfg {
     static constexpr int kEpiWarps = EW;
-    static constexpr int kThreads = 128 + 32 * EW;
+    static constexpr int kUnpackWarps = PK ? 4 : 0;
+    static constexpr int kThreads = 128 + 32 * EW + 32 * kUnpackWarps;
     static constexpr int kStages = EW >= 16 ? 2 : 4;
     static constexpr int kMaskWords = 24;  // mask words per row staged in shared memory (K <= 768; else global)
 };
@@ -62,14 +68,38 @@ struct K2Smem {
     static constexpr int kTotal = kBarOff + 512 + 1024;  // barriers + tmem slot + alignment slack
 };
 
+// Eight pack_int4 codes (one 32-bit word, low nibble = even channel) -> eight int8
+// codes in channel order: each nibble sign-extended into its byte ((n & 8) * 0x1E puts
+// 0xF0 over a negative nibble; no carries cross bytes), then the even / odd bytes
+// interleaved.
+__device__ __forceinline__ void unpack_nibbles8(uint32_t x, uint32_t& o0, uint32_t& o1) {
+    const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;
+    const uint32_t rlo = (lo & 0x08080808u) * 0x1Eu + lo, rhi = (hi & 0x08080808u) * 0x1Eu + hi;
+    o0 = __byte_perm(rlo, rhi, 0x5140);
+    o1 = __byte_perm(rlo, rhi, 0x7362);
+}
+
+// 32 packed codes (16 bytes) of row r, channel quarter kq of the K-block -> the two
+// 16-byte chunks 2kq, 2kq+1 of the 128B-swizzled int8 row
+__device__ __forceinline__ void unpack_chunk(uint8_t* sa, int r, int kq, uint4 x) {
+    uint4 a, b;
+    unpack_nibbles8(x.x, a.x, a.y);
+    unpack_nibbles8(x.y, a.z, a.w);
+    unpack_nibbles8(x.z, b.x, b.y);
+    unpack_nibbles8(x.w, b.z, b.w);
+    uint8_t* row = sa + r * 128;
+    *reinterpret_cast<uint4*>(row + (((2 * kq) ^ (r & 7)) << 4)) = a;
+    *reinterpret_cast<uint4*>(row + (((2 * kq + 1) ^ (r & 7)) << 4)) = b;
+}
+
 // int32 -> f64, exact, without the conversion pipe (I2F.F64 is slow on sm_100):
 // 2^52 + (v + 2^31) assembled from words, minus 2^52 + 2^31.
 __device__ __forceinline__ double i32_to_f64(uint32_t v) {
     return __hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)) - 4503601774854144.0;
 }
 
-template <int BN, int EW, int POST, bool PLANES>
-__global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
+template <int BN, int EW, int POST, bool PLANES, bool PK>
+__global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
     k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, const QLinParams p) {
     using L = K2Smem<BN, EW>;
@@ -83,7 +113,8 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
     uint64_t* res_bar = acc_empty + 2;  // per epilogue warp and staging buffer: residual tile loads
     uint64_t* meta_full = res_bar + 2 * kEpiWarps;
     uint64_t* meta_empty = meta_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(meta_empty + 2);
+    uint64_t* pk_full = meta_empty + 2;  // PK: the stage's packed A box landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pk_full + kStages);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.R + BN - 1) / BN;
@@ -94,8 +125,9 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         for (int s = 0; s < kStages; ++s) {
-            ptx::mbar_init(full + s, 1);
+            ptx::mbar_init(full + s, PK ? 1 + 4 : 1);  // PK: + one arrive per unpack warp
             ptx::mbar_init(empty + s, 1);
+            ptx::mbar_init(pk_full + s, 1);
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(acc_full + s, 1);
@@ -116,8 +148,10 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
 
     // warpgroup 0 (TMA, MMA, TMEM allocator, row metadata) needs few registers: it hands
     // them to the four epilogue warpgroups (register budgets per role region)
+    // (PK adds a warpgroup: the 8-epilogue-warp shape then moves registers too)
+    constexpr bool kRegMove = EW >= 16 || PK;
     if (warp < 4) {
-    if constexpr (EW >= 16) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if constexpr (kRegMove) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
             int stage = 0;
@@ -127,8 +161,14 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
                 for (int kb = 0; kb < kblocks; ++kb) {
                     ptx::mbar_wait(empty + stage, phase ^ 1);
                     uint8_t* sa = smem + stage * L::kStageBytes;
-                    ptx::mbar_arrive_expect_tx(full + stage, L::kStageBytes);
-                    ptx::tma_load_2d(sa, &tmA, full + stage, kb * kBK, m0);
+                    if constexpr (PK) {  // packed A box (128 rows x 64 bytes) into the A region's upper half
+                        ptx::mbar_arrive_expect_tx(pk_full + stage, L::kABytes / 2);
+                        ptx::tma_load_2d(sa + L::kABytes / 2, &tmA, pk_full + stage, kb * (kBK / 2), m0);
+                        ptx::mbar_arrive_expect_tx(full + stage, L::kBBytes);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(full + stage, L::kStageBytes);
+                        ptx::tma_load_2d(sa, &tmA, full + stage, kb * kBK, m0);
+                    }
                     ptx::tma_load_2d(sa + L::kABytes, &tmB, full + stage, kb * kBK, n0);
                     if (++stage == kStages) {
                         stage = 0;
@@ -207,8 +247,42 @@ __global__ void __launch_bounds__(K2Cfg<EW>::kThreads, 1)
             if (lane == 0) ptx::mbar_arrive(meta_full + slot);
         }
     }
+    } else if (PK && warp >= 4 + EW) {  // ---- unpack warpgroup (PK)
+        static_assert(!PK || EW == 8, "the unpack warpgroup's register budget is laid out for 8 epilogue warps");
+        if constexpr (kRegMove) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;\n" ::: "memory");
+        const int u = threadIdx.x - 32 * (4 + EW);  // 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+                uint8_t* sa = smem + stage * L::kStageBytes;
+                const uint8_t* pk = sa + L::kABytes / 2;  // packed row r at pk + 64 r
+                ptx::mbar_wait(pk_full + stage, phase);
+                // in place: rows 0..63 expand into [0, 8 KB), below the packed box; rows
+                // 64..127 expand over it, so their packed bytes are read first and every
+                // read of the group precedes the second half's writes (named barrier)
+                const uint4 h0 = *reinterpret_cast<const uint4*>(pk + 4096 + u * 16);
+                const uint4 h1 = *reinterpret_cast<const uint4*>(pk + 4096 + (u + 128) * 16);
+#pragma unroll
+                for (int i = u; i < 256; i += 128) unpack_chunk(sa, i >> 2, i & 3, *reinterpret_cast<const uint4*>(pk + i * 16));
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                unpack_chunk(sa, 64 + (u >> 2), u & 3, h0);
+                unpack_chunk(sa, 64 + ((u + 128) >> 2), u & 3, h1);
+                ptx::fence_async_smem();  // generic-proxy writes -> the tensor core's async proxy
+                __syncwarp();
+                if ((u & 31) == 0) ptx::mbar_arrive(full + stage);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
     } else {  // ---- epilogue: 16 warps = 4 TMEM lane quarters x 4 column groups
+        // register budgets within the CTA's pool (threads x launch registers): 128 x 40 (+ 128 x 48
+        // unpack) + 32 EW x epilogue, i.e. 640 x 96 >= 128 x 40 + 512 x 104 and 512 x 128 >=
+        // 128 x 40 + 128 x 48 + 256 x 200
         if constexpr (EW >= 16) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        else if constexpr (PK) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
         const int ew = warp - 4;
         const int q = warp & 3;       // TMEM lanes 32q..32q+31 (a warp may only touch its quarter)
         const int cgrp = ew >> 2;     // which quarter of the BN columns
@@ -470,10 +544,26 @@ static bool make_map_f64(CUtensorMap* m, const double* base, int rows, int cols,
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int EW, int POST, bool PLANES>
+// 2-D packed A4 codes [rows][cols/2 bytes]: 128-row x 64-byte boxes, no swizzle (the
+// unpack warps read them row-linear).
+static bool make_map_packed(CUtensorMap* m, const void* base, int rows, int cols) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols / 2), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols / 2)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK / 2), static_cast<cuuint32_t>(kBM)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, int EW, int POST, bool PLANES, bool PK>
 static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) {
     CUtensorMap ta, tb, to, to2;
-    if (!make_map(&ta, p.a.codes, p.M, p.K, kBM) || !make_map(&tb, p.w, p.R, p.K, BN)) return cudaErrorInvalidValue;
+    const bool amap = PK ? make_map_packed(&ta, p.a.codes4, p.M, p.K) : make_map(&ta, p.a.codes, p.M, p.K, kBM);
+    if (!amap || !make_map(&tb, p.w, p.R, p.K, BN)) return cudaErrorInvalidValue;
     const bool inproj = p.epi.post == POST_INPROJ;
     const int ocols = inproj ? p.epi.split : p.R;
     if (!make_map_f64(&to, p.epi.out, p.M, ocols, p.epi.ld_out)) return cudaErrorInvalidValue;
@@ -481,11 +571,11 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
                       inproj ? p.epi.split : p.epi.ld_out))
         return cudaErrorInvalidValue;
     const int smem = K2Smem<BN, EW>::kTotal;
-    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, EW, POST, PLANES>>(smem);
+    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, EW, POST, PLANES, PK>>(smem);
     if (e != cudaSuccess) return e;
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
-    k2_qlinear<BN, EW, POST, PLANES><<<grid, K2Cfg<EW>::kThreads, smem, st>>>(ta, tb, to, to2, p);
+    k2_qlinear<BN, EW, POST, PLANES, PK><<<grid, K2Cfg<EW, PK>::kThreads, smem, st>>>(ta, tb, to, to2, p);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }
@@ -495,17 +585,27 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (p.epi.post == POST_INPROJ && (p.epi.split % 32) != 0) return cudaErrorInvalidValue;
     if ((p.epi.ld_out % 2) != 0 || (p.R % 32) != 0) return cudaErrorInvalidValue;  // TMA pitch, whole chunks
     if (p.a.J < (p.K + 31) / 32) return cudaErrorInvalidValue;
+    const bool pk = p.a.codes4 != nullptr;
+    if (pk ? (p.K % 32) != 0 : p.a.codes == nullptr) return cudaErrorInvalidValue;  // packed rows: 16-byte pitch
     const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
     if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
     // main-loop-heavy calls (wide outputs, no residual) take the 8-warp / 4-stage shape
     // (x_proj, R = 800: measured 0.25 ms per forward faster than 16 epilogue warps; 4 stages
     // 0.33 ms per forward faster than 3)
-    const bool wide = p.epi.post != POST_RESID && (p.R > 512 || p.K > 1024);
+    // The packed-A4 operand adds an unpack warpgroup; it runs on the 8-epilogue-warp shape only
+    // (16 epilogue warps + 4 unpack warps: 768 threads leave a per-CTA register pool of 80 x 768,
+    // too small for the 104-register epilogue after setmaxnreg)
+    const bool wide = pk || (p.epi.post != POST_RESID && (p.R > 512 || p.K > 1024));
 #define K2_CASE(P)                                                                                       \
     case P:                                                                                              \
+        if (pk)                                                                                          \
+            return planes ? launch_bn<128, 8, P, true, true>(p, st, num_sms)                             \
+                          : launch_bn<128, 8, P, false, true>(p, st, num_sms);                           \
         if (wide)                                                                                        \
-            return planes ? launch_bn<128, 8, P, true>(p, st, num_sms) : launch_bn<128, 8, P, false>(p, st, num_sms); \
-        return planes ? launch_bn<128, 16, P, true>(p, st, num_sms) : launch_bn<128, 16, P, false>(p, st, num_sms);
+            return planes ? launch_bn<128, 8, P, true, false>(p, st, num_sms)                            \
+                          : launch_bn<128, 8, P, false, false>(p, st, num_sms);                          \
+        return planes ? launch_bn<128, 16, P, true, false>(p, st, num_sms)                               \
+                      : launch_bn<128, 16, P, false, false>(p, st, num_sms);
     switch (p.epi.post) {
         K2_CASE(POST_STORE)
         K2_CASE(POST_INPROJ)

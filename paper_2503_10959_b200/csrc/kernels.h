@@ -53,6 +53,8 @@ struct SiteCal {
 // Quantized activation operand of one quant-linear call: row m = (sample, step).
 struct QAct {
     int8_t* codes = nullptr;      // [M][E] inlier codes, 0 at outlier positions
+    uint8_t* codes4 = nullptr;    // or the same codes nibble-packed (A4): [M][E/2], low nibble = even channel
+                                  // (pack_int4's layout, gemm.cpp:60-73, with the channels as its columns)
     double* s_row = nullptr;      // [M] inlier scale of the row's plane (S^I(t) or S_full(t))
     int* ocnt = nullptr;          // [M] |O(t)|
     uint32_t* omask = nullptr;    // [M][J] bit ch%32 of word ch/32: channel in O(t)
@@ -75,6 +77,7 @@ struct K1Params {
     int force_literal = 0;             // run the literal detector kernel
     // quantized outputs (rows in step order, row = s*T + t): the QAct operand
     int8_t* codes = nullptr;
+    uint8_t* codes4 = nullptr;    // A4: the inlier codes nibble-packed instead (QAct::codes4), codes unused
     double* s_row = nullptr;
     int* ocnt = nullptr;
     uint32_t* omask = nullptr;    // [S*T][ceil(E/32)]

@@ -277,7 +277,7 @@ std::vector<SweepRecord> refresh_sweep(const SweepSettings& s, cudaStream_t st, 
     pp.s_in = dsin.p;
     pp.abits = 4;
     pp.obits = 8;
-    pp.a = QAct{codes.p, s_row.p, ocnt.p, omask.p, ocode.p, oscale.p, static_cast<int>(J)};
+    pp.a = QAct{codes.p, nullptr, s_row.p, ocnt.p, omask.p, ocode.p, oscale.p, static_cast<int>(J)};
     pp.scanned = scanned.p;
     pp.work = work.p;
     pp.count_out = count.p;
@@ -401,7 +401,7 @@ std::vector<BenchRecord> gemm_bench(const BenchSettings& s, cudaStream_t st, int
         q.M = static_cast<int>(Mp);
         q.R = static_cast<int>(Rp);
         q.K = static_cast<int>(Kp);
-        q.a = QAct{dcodes.p, dsrow.p, docnt.p, domask.p, doc.p, dos.p, static_cast<int>(J)};
+        q.a = QAct{dcodes.p, nullptr, dsrow.p, docnt.p, domask.p, doc.p, dos.p, static_cast<int>(J)};
         q.w = dw.p;
         q.wt = dwt.p;
         q.ws = dws.p;

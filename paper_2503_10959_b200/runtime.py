@@ -196,40 +196,51 @@ class Context:
     # ---- operators (device tensors) --------------------------------------------
     def detect_quantize(self, x, *, S, T, E, theta, s_in, s_full, n_refresh, act_bits, outlier_bits,
                         mode=L.MODE_DYNAMIC, src=L.SRC_PLAIN, x2=None, gate=None, order=-1, grid=0, literal=False,
-                        scanned=None):
+                        scanned=None, packed=False):
         """K1 over S x T planes. Returns the QAct operand as a dict of device
-        tensors: codes, s_row, ocnt, omask (uint32 words), ocode/oscale (dense,
-        valid at outlier positions)."""
+        tensors: codes (or, packed=True with act_bits 4, codes4: the nibble-packed
+        codes [rows][E/2] in pack_int4's layout), s_row, ocnt, omask (uint32 words),
+        ocode/oscale (dense, valid at outlier positions)."""
         import torch
         dev = x.device
         rows = S * T
         J = (E + 31) // 32
-        codes = torch.empty(rows, E, dtype=torch.int8, device=dev)
         s_row = torch.empty(rows, dtype=torch.float64, device=dev)
         ocnt = torch.empty(rows, dtype=torch.int32, device=dev)
         omask = torch.zeros(rows, J, dtype=torch.int32, device=dev)
         ocode = torch.zeros(rows, E, dtype=torch.int8, device=dev)
         oscale = torch.zeros(rows, E, dtype=torch.float64, device=dev)
-        rs = torch.empty(rows, dtype=torch.float64, device=dev) if src == L.SRC_RMSNORM else None
+        if packed:
+            if act_bits != 4:
+                raise L.ValidationError(2, "detect_quantize: packed codes are 4-bit (act_bits must be 4)")
+            codes4 = torch.empty(rows, (E + 1) // 2, dtype=torch.uint8, device=dev)
+            L.check(self.lib.ouro_b200_detect_quantize_packed(
+                self.h, _ptr(x), _ptr(x2), _ptr(gate), S, T, E, src, order, grid, float(theta), _ptr(s_in),
+                _ptr(s_full), n_refresh, outlier_bits, mode, int(literal), _ptr(codes4), _ptr(s_row), _ptr(ocnt),
+                _ptr(omask), _ptr(ocode), _ptr(oscale), _ptr(scanned)))
+            return dict(codes4=codes4, s_row=s_row, ocnt=ocnt, omask=omask, ocode=ocode, oscale=oscale)
+        codes = torch.empty(rows, E, dtype=torch.int8, device=dev)
         L.check(self.lib.ouro_b200_detect_quantize(
             self.h, _ptr(x), _ptr(x2), _ptr(gate), S, T, E, src, order, grid, float(theta), _ptr(s_in), _ptr(s_full),
             n_refresh, act_bits, outlier_bits, mode, int(literal), _ptr(codes), _ptr(s_row), _ptr(ocnt), _ptr(omask),
-            _ptr(ocode), _ptr(oscale), _ptr(scanned), _ptr(rs)))
+            _ptr(ocode), _ptr(oscale), _ptr(scanned), None))
         return dict(codes=codes, s_row=s_row, ocnt=ocnt, omask=omask, ocode=ocode, oscale=oscale)
 
     def quant_linear(self, act: dict, w, wt, ws, *, post=L.POST_STORE, out=None, out2=None, split=0, acc_in=None,
                      acc_out=None):
-        """K2: hybrid quant-linear over K1's operand dict; returns `out`."""
+        """K2: hybrid quant-linear over K1's operand dict (int8 `codes` or nibble-packed
+        `codes4`); returns `out`."""
         import torch
-        M, K = act["codes"].shape
+        packed = "codes4" in act
+        M, K = (act["codes4"].shape[0], 2 * act["codes4"].shape[1]) if packed else act["codes"].shape
         R = w.shape[0]
         if out is None:
             out = torch.empty(M, R, dtype=torch.float64, device=w.device)
         ld = out.shape[1]
-        L.check(self.lib.ouro_b200_quant_linear(
-            self.h, M, R, K, _ptr(act["codes"]), _ptr(act["s_row"]), _ptr(act["ocnt"]), _ptr(act["omask"]),
-            _ptr(act["ocode"]), _ptr(act["oscale"]), _ptr(w), _ptr(wt), _ptr(ws), post,
-            _ptr(out), ld, _ptr(out2), split, None, _ptr(acc_in), _ptr(acc_out)))
+        fn = self.lib.ouro_b200_quant_linear_packed if packed else self.lib.ouro_b200_quant_linear
+        L.check(fn(self.h, M, R, K, _ptr(act["codes4"] if packed else act["codes"]), _ptr(act["s_row"]),
+                   _ptr(act["ocnt"]), _ptr(act["omask"]), _ptr(act["ocode"]), _ptr(act["oscale"]), _ptr(w), _ptr(wt),
+                   _ptr(ws), post, _ptr(out), ld, _ptr(out2), split, None, _ptr(acc_in), _ptr(acc_out)))
         return out
 
     def quant_scan(self, *, S, T, E, order, grid, u, proj, a, b_delta, o, mode, n_refresh=10, act_bits=8,
