@@ -203,7 +203,7 @@ __device__ __forceinline__ int k1_row_of(const K1Params& p, int t) {
     return row_at(p.order, t, p.T, p.grid);
 }
 
-template <int SRC>
+template <int SRC, bool PK>
 __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs dirs) {
     extern __shared__ __align__(128) unsigned char k1_smem[];
     double* stage = reinterpret_cast<double*>(k1_smem);  // [kK1Stages][rc][E]
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
     const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
     int8_t* __restrict__ const codes = p.codes;
-    uint8_t* __restrict__ const codes4 = p.codes4;
+    uint8_t* __restrict__ const codes4 = p.codes4;  // PK (a template flag: the int8 form keeps its 76 registers)
     int8_t* __restrict__ const ocode = p.ocode;
     double* __restrict__ const oscale = p.oscale;
     uint32_t* __restrict__ const omask = p.omask;
@@ -279,10 +279,10 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
         // running pointers (row = s*T + t; the staged row `slot` of this chunk)
         const double* xr = sb + ch;
         const size_t row0 = static_cast<size_t>(s) * T + ts;
-        int8_t* cp = codes + row0 * E + ch;
-        uint16_t* cp4 = reinterpret_cast<uint16_t*>(codes4 + row0 * (E >> 1) + (ch >> 1));
+        int8_t* cp = PK ? nullptr : codes + row0 * E + ch;
+        uint16_t* cp4 = PK ? reinterpret_cast<uint16_t*>(codes4 + row0 * (E >> 1) + (ch >> 1)) : nullptr;
         uint32_t* mp = omask + row0 * J + (ch >> 5);
-        for (int t = ts; t < te; ++t, xr += E, cp += E, cp4 += E >> 2, mp += J) {
+        for (int t = ts; t < te; ++t, xr += E, mp += J, cp += (PK ? 0 : E), cp4 += (PK ? (E >> 2) : 0)) {
             const int slot = t - ts;
             const size_t row = row0 + slot;
             const double S = s_tab[t];
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
             if (active) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) cc[k] = ((in >> k) & 1u) ? 0 : min(max(cc[k], -qai), qai);
-                if (codes4)
+                if constexpr (PK)
                     *cp4 = pack4(cc[0], cc[1], cc[2], cc[3]);
                 else
                     *reinterpret_cast<char4*>(cp) =
@@ -517,17 +517,23 @@ static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int SRC>
-static cudaError_t launch_staged(const K1Dirs& dirs, cudaStream_t st) {
+template <int SRC, bool PK>
+static cudaError_t launch_staged_pk(const K1Dirs& dirs, cudaStream_t st) {
     const K1Params& p = dirs.p[0];
     const int nwin = (p.T + p.window - 1) / p.window;
     const int threads = ((p.E / 4 + 31) / 32) * 32;  // E <= 1024: one CTA covers every channel
     const size_t smem = static_cast<size_t>(kK1Stages) * dirs.rc * p.E * sizeof(double);
-    cudaError_t e = ensure_smem_attr<k1_staged<SRC>>(static_cast<int>(smem));
+    cudaError_t e = ensure_smem_attr<k1_staged<SRC, PK>>(static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k1_staged<SRC><<<dim3(1, p.S * nwin * dirs.n), threads, smem, st>>>(dirs);
+    k1_staged<SRC, PK><<<dim3(1, p.S * nwin * dirs.n), threads, smem, st>>>(dirs);
     ++kernel_launch_counter();
     return cudaGetLastError();
+}
+
+template <int SRC>
+static cudaError_t launch_staged(const K1Dirs& dirs, cudaStream_t st) {
+    if ((dirs.p[0].codes4 != nullptr) != (dirs.p[1].codes4 != nullptr)) return cudaErrorInvalidValue;
+    return dirs.p[0].codes4 ? launch_staged_pk<SRC, true>(dirs, st) : launch_staged_pk<SRC, false>(dirs, st);
 }
 
 static K1Dirs k1_dirs(const K1Params* ps, int n) {
