@@ -61,6 +61,8 @@ struct __align__(16) StepShared {
     int keep;        // outlier flags kept at this step: 0 at a maybe_refresh point (quant.cpp:303-311), else ~0
     int ocol;        // crow * E: canonical token of this scan step (ssm.cpp:30-46), as an output offset
     int pad[2];
+    float Saf, Sbf, Shf;  // f32(S_a), f32(S_b), f32(S_h): the f32 state update of k3_scan_c1<FS>
+    float pad2;
 };
 
 static_assert(sizeof(StepShared) % 16 == 0, "bulk-copied step tables");
@@ -156,6 +158,10 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         ss.hA1 = qa1 * ss.LA;
         ss.hA0 = 0.5f - fmaf(qa1, fmaf(ss.LA, 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
         ss.pad[0] = ss.pad[1] = 0;
+        ss.Saf = __double2float_rn(Sa);
+        ss.Sbf = __double2float_rn(Sb);
+        ss.Shf = __double2float_rn(Sh);
+        ss.pad2 = 0.0f;
     }
     __syncwarp();
     constexpr int kChunks16 = static_cast<int>(sizeof(StepShared) / 16);
@@ -513,6 +519,26 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
 // independent streams, the f32 delta, the inlier certification margins, the
 // detector's "near or above theta" flag and the clamp flag; the step loop reads
 // them with one 16-byte shared load.
+//
+// FS (f32 state update). The carried state is h' = rh' * S_h' (codes rh', exact f32
+// integers, and the previous step's scale), so no f64 state is kept. The update
+// h = fl64(fl64(a_q h') + fl64(b_q u)) (ssm.cpp:165-167) is evaluated in f32 as
+//   P1 = fl32(fl32(ra * rh') * fl32(f32(S_a) f32(S_h'))),  P2 = fl32(rb * fl32(f32(S_b) f32(u))),
+//   hf = fl32(P1 + P2)
+// (ra, rb: the a_bar / b_bar codes; ra * rh' <= 127^2 is exact). Each of P1, P2 is
+// within 4.0002 u of its f64 counterpart (u = 2^-24: four / three roundings of
+// exact inputs, against 2^-53 ones), the sum and the f64 roundings add u |P1 + P2|
+// and 2^-53 (|A| + |B|), so |hf - h| <= (|P1| + |P2|) 5.01 u <= D = (max|P1| +
+// max|P2|) 5.2 u + 1e-37 (the absolute term covers f32 underflow). Then:
+//  * code: q = fl32(hf * invH) is within |q| 2.001 u + D invH 1.0001 of h / S_h, so
+//    round(q) is the reference's code when |q - round(q)| <= 0.5 - that (clamped
+//    quotients as in the f64-state form);
+//  * detector (dynamic): max|h| < theta is certain when max|hf| + D < theta (rounded
+//    down); h-outlier channels, peaks not certainly below theta, non-finite values
+//    and uncertified codes take the exact path: the f64 update from the codes and
+//    scales, then the f64-state form's detection and codes.
+// The output o = sum C_m (rh_m * S_h) is the reference's f64 sum of the dequantized
+// state.
 template <int KC>
 struct C1Smem {
     StepShared st[2][KC];
@@ -522,7 +548,7 @@ struct C1Smem {
     uint64_t bar[2];
 };
 
-template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB>
+template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB, bool FS>
 __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t c1_smem_raw[];
     using Sm = C1Smem<KC>;
@@ -556,6 +582,13 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
     unsigned fl = 0;  // channel in O: bit 0 a_bar, bit 1 b_bar, bit 2 h
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
+    // FS: the previous step's h codes (exact f32 integers) and f32 h scale; thHlo <= theta
+    float2 rhp[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) rhp[k] = make_float2(0.0f, 0.0f);
+    float sHf_prev = 0.0f;
+    double sHp = 0.0;  // FS: the previous step's h scale; the state is rhp * sHp, exact (no f64 state kept)
+    const float thHlo = thHf * (1.0f - 4.0f * 5.9604645e-8f);
     const double bd = active ? p.b_delta[i] : 0.0;
     const StepShared* wsteps = steps + (static_cast<size_t>(blockIdx.z) * p.S + s) * T;
     if (lane == 0) {
@@ -618,8 +651,13 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const double2 c = C2[k];
-                o = dadd(o, dmul(c.x, h[2 * k]));
-                o = dadd(o, dmul(c.y, h[2 * k + 1]));
+                if constexpr (FS) {  // h = code * s (fake_quant_step's dequantized state), then C h
+                    o = dadd(o, dmul(c.x, dmul(static_cast<double>(rhp[k].x), sHp)));
+                    o = dadd(o, dmul(c.y, dmul(static_cast<double>(rhp[k].y), sHp)));
+                } else {
+                    o = dadd(o, dmul(c.x, h[2 * k]));
+                    o = dadd(o, dmul(c.y, h[2 * k + 1]));
+                }
             }
             if (active) {
                 obase[se.ocol] = o;
@@ -705,6 +743,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
             unsigned ca[16];  // a_bar codes (>= 0) as integers, b_bar codes as exact f32 integers
             float cb[16];
+            float raf[16];    // FS: a_bar codes as exact f32 integers
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
             const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf);
             auto pass1 = [&](auto clamp) {
@@ -723,8 +762,13 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                     const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
                     const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
                     const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
-                    ca[2 * k] = __float_as_uint(ta.x) - kMagicBits;
-                    ca[2 * k + 1] = __float_as_uint(ta.y) - kMagicBits;
+                    if constexpr (FS) {
+                        raf[2 * k] = ra.x;
+                        raf[2 * k + 1] = ra.y;
+                    } else {
+                        ca[2 * k] = __float_as_uint(ta.x) - kMagicBits;
+                        ca[2 * k + 1] = __float_as_uint(ta.y) - kMagicBits;
+                    }
                     float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
                     if constexpr (CL) {
                         qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
@@ -748,63 +792,51 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                 for (int m = 0; m < 16; ++m) {
                     const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
-                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
-                        ca[m] = static_cast<unsigned>(static_cast<int>(
-                            qdiv_call(exp_call(dmul(delta, arow[m])), sA, static_cast<double>(qAf))));
+                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA) {
+                        const double cq = qdiv_call(exp_call(dmul(delta, arow[m])), sA, static_cast<double>(qAf));
+                        ca[m] = static_cast<unsigned>(static_cast<int>(cq));
+                        raf[m] = static_cast<float>(cq);
+                    }
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
                         cb[m] = static_cast<float>(qdiv_call(dmul(delta, ss.B[m]), sB, static_cast<double>(qBf)));
                 }
             }
-            // pass 2: dequantized values (code * s) and the exact f64 update, ssm.cpp:165-167
-            const double nKA = dmul(sA, -4503599627370496.0);
+            if constexpr (FS) {
+                // f32 state update with a rigorous bound (header comment of k3_scan_c1<FS>):
+                // P1 = (ra * rh_prev) * f32(S_a S_h'), P2 = rb * f32(S_b u), hf = P1 + P2 stands for
+                // h = fl64(fl64(a_q h') + fl64(b_q u)) within D = (max|P1| + max|P2|) 5.2 2^-24
+                const float sAf = (fl & 1u) ? __double2float_rn(sA) : ss.Saf;
+                const float sBf = (fl & 2u) ? __double2float_rn(sB) : ss.Sbf;
+                const float sAsH = sAf * sHf_prev, sBu = sBf * __double2float_rn(uv);
+                float2 hf2[8];
+                float mp1 = 0.0f, mp2 = 0.0f, phf = 0.0f;
 #pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
-                const double b_q = dmul(static_cast<double>(cb[m]), sB);
-                h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));
-            }
-            // h detection + codes (see k3_scan_fast): f32 peak = fl32 of the exact peak
-            float2 hfv[8];
-            float phf = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
-                phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
-            }
-            double sH = ss.Sh, qH = qa;
-            float invHf = ss.invShf;
-            if (dyn && ((fl & 4u) | (phf >= thHf))) {
-                if (!(fl & 4u)) {
-                    if (phf > thHf) {
-                        fl |= 4u;
-                    } else {  // phf == fl32(theta): the exact peak decides
-                        double ph = 0.0;
-#pragma unroll
-                        for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(h[m]));
-                        if (ph > thH) fl |= 4u;
-                    }
+                for (int k = 0; k < 8; ++k) {
+                    const float2 p1 = __fmul2_rn(__fmul2_rn(make_float2(raf[2 * k], raf[2 * k + 1]), rhp[k]), f2(sAsH));
+                    const float2 p2 = __fmul2_rn(make_float2(cb[2 * k], cb[2 * k + 1]), f2(sBu));
+                    const float2 hv = __fadd2_rn(p1, p2);
+                    mp1 = fmaxf(mp1, fmaxf(fabsf(p1.x), fabsf(p1.y)));
+                    mp2 = fmaxf(mp2, fmaxf(fabsf(p2.x), fabsf(p2.y)));
+                    phf = fmaxf(phf, fmaxf(fabsf(hv.x), fabsf(hv.y)));
+                    hf2[k] = hv;
                 }
-                if (fl & 4u) {
-                    double ph = 0.0;
-#pragma unroll
-                    for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(h[m]));
-                    sH = scale_call(ph, qo);
-                    invHf = __double2float_rn(recip_call(sH));
-                    qH = qo;
-                }
-            }
-            {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
-                const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
-                const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+                const float maxD = fmaf(mp1 + mp2, 5.2f * 5.9604645e-8f, 1e-37f);
+                double sH = ss.Sh, qH = qa;
+                float invHf = ss.invShf;
+                // exact state path: h-outlier channels (their scale needs the exact peak), peaks
+                // not certainly below theta, non-finite values, uncertified codes
+                bool hexact = EXACT || !(maxD < 1e30f);
+                if (dyn) hexact |= (fl & 4u) || !(fmaf(maxD, 1.0000003f, phf) < thHlo);
+                const float capH = qaf + 0.25f;
+                const float halfH = 0.5f - fmaf(maxD, invHf * 1.0001f, fmaf(qaf + 1.0f, 1.25e-7f, 1e-6f));
                 float chd[16];
-                bool hredo = EXACT;
+                float mdh = 0.0f;
                 auto hcodes = [&](auto clamp) {
                     constexpr bool CL = decltype(clamp)::value;
-                    float mdh = 0.0f;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                        float2 q = __fmul2_rn(hf2[k], f2(invHf));
                         if constexpr (CL) {
                             q.x = fminf(fmaxf(q.x, -capH), capH);
                             q.y = fminf(fmaxf(q.y, -capH), capH);
@@ -816,21 +848,120 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                         chd[2 * k + 1] = rh.y;
                         mdh = fmaxf(mdh, fmaxf(fabsf(dh.x), fabsf(dh.y)));
                     }
-                    hredo |= mdh > halfH;
                 };
                 if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});
                 else hcodes(std::true_type{});
-                if (hredo) {
+                hexact |= !(mdh <= halfH);
+                if (hexact) {  // the exact f64 update (ssm.cpp:165-167) and the c1 h logic on it
+                    double hn[16];
 #pragma unroll
                     for (int m = 0; m < 16; ++m) {
-                        const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
-                        const float q = fminf(fmaxf(hv * invHf, -capH), capH);
-                        if (EXACT || fabsf(q - rintf(q)) > halfH) chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
+                        const double a_q = dmul(static_cast<double>(raf[m]), sA);
+                        const double b_q = dmul(static_cast<double>(cb[m]), sB);
+                        const double hp = dmul(static_cast<double>((m & 1) ? rhp[m >> 1].y : rhp[m >> 1].x), sHp);
+                        hn[m] = dadd(dmul(a_q, hp), dmul(b_q, uv));
+                    }
+                    if (dyn) {
+                        double ph = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(hn[m]));
+                        if (ph > thH) fl |= 4u;
+                        if (fl & 4u) {
+                            sH = scale_call(ph, qo);
+                            invHf = __double2float_rn(recip_call(sH));
+                            qH = qo;
+                        }
+                    }
+                    const float qHf = static_cast<float>(qH), capHx = qHf + 0.25f;
+                    const float halfHx = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) {  // |dq| <= |q| 4 2^-24 from the exact value
+                        const float q = fminf(fmaxf(__double2float_rn(hn[m]) * invHf, -capHx), capHx);
+                        const float r = rintf(q);
+                        chd[m] = (EXACT || !(fabsf(q - r) <= halfHx)) ? static_cast<float>(qdiv_call(hn[m], sH, qH)) : r;
                     }
                 }
 #pragma unroll
-#pragma unroll
-                for (int m = 0; m < 16; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
+                for (int k = 0; k < 8; ++k) rhp[k] = make_float2(chd[2 * k], chd[2 * k + 1]);  // carried state
+                sHp = sH;
+                sHf_prev = (fl & 4u) ? __double2float_rn(sH) : ss.Shf;
+            } else {
+            // pass 2: dequantized values (code * s) and the exact f64 update, ssm.cpp:165-167
+                const double nKA = dmul(sA, -4503599627370496.0);
+    #pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
+                    const double b_q = dmul(static_cast<double>(cb[m]), sB);
+                    h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));
+                }
+                // h detection + codes (see k3_scan_fast): f32 peak = fl32 of the exact peak
+                float2 hfv[8];
+                float phf = 0.0f;
+    #pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
+                    phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
+                }
+                double sH = ss.Sh, qH = qa;
+                float invHf = ss.invShf;
+                if (dyn && ((fl & 4u) | (phf >= thHf))) {
+                    if (!(fl & 4u)) {
+                        if (phf > thHf) {
+                            fl |= 4u;
+                        } else {  // phf == fl32(theta): the exact peak decides
+                            double ph = 0.0;
+    #pragma unroll
+                            for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(h[m]));
+                            if (ph > thH) fl |= 4u;
+                        }
+                    }
+                    if (fl & 4u) {
+                        double ph = 0.0;
+    #pragma unroll
+                        for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(h[m]));
+                        sH = scale_call(ph, qo);
+                        invHf = __double2float_rn(recip_call(sH));
+                        qH = qo;
+                    }
+                }
+                {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
+                    const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
+                    const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+                    float chd[16];
+                    bool hredo = EXACT;
+                    auto hcodes = [&](auto clamp) {
+                        constexpr bool CL = decltype(clamp)::value;
+                        float mdh = 0.0f;
+    #pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                            if constexpr (CL) {
+                                q.x = fminf(fmaxf(q.x, -capH), capH);
+                                q.y = fminf(fmaxf(q.y, -capH), capH);
+                            }
+                            const float2 th = __fadd2_rn(q, f2(12582912.0f));
+                            const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
+                            const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
+                            chd[2 * k] = rh.x;
+                            chd[2 * k + 1] = rh.y;
+                            mdh = fmaxf(mdh, fmaxf(fabsf(dh.x), fabsf(dh.y)));
+                        }
+                        hredo |= mdh > halfH;
+                    };
+                    if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});
+                    else hcodes(std::true_type{});
+                    if (hredo) {
+    #pragma unroll
+                        for (int m = 0; m < 16; ++m) {
+                            const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
+                            const float q = fminf(fmaxf(hv * invHf, -capH), capH);
+                            if (EXACT || fabsf(q - rintf(q)) > halfH) chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
+                        }
+                    }
+    #pragma unroll
+    #pragma unroll
+                    for (int m = 0; m < 16; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
+                }
             }
             if constexpr (!kDefer) emit(tt, fl);
             fl_prev = fl;
@@ -845,9 +976,9 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
 // spills and runs 3.01; per-lane cp.async staging instead of bulk rows 2.306.
 constexpr int kC1Chunk = 4, kC1MinBlocks = 12;
 
-template <bool EXACT, int ABITS, bool TRACE>
+template <bool EXACT, int ABITS, bool TRACE, bool FS>
 static cudaError_t launch_c1(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
-    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, kC1MinBlocks>;
+    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, kC1MinBlocks, FS>;
     const int smem = static_cast<int>(sizeof(C1Smem<kC1Chunk>));
     cudaError_t e = ensure_smem_attr<kern>(smem);
     if (e != cudaSuccess) return e;
@@ -869,14 +1000,19 @@ static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* s
 }
 
 // kernel: 0 the one-thread-per-channel kernel (needs an even E: 16-byte rows), 1 the
-// two-threads-per-channel kernel
+// two-threads-per-channel kernel, 2 the one-thread-per-channel kernel with the f32 state update
+template <int ABITS, bool FS>
+static cudaError_t launch_c1_any(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st, bool exact,
+                                 bool trace) {
+    if (exact) return trace ? launch_c1<true, ABITS, true, FS>(P, ndirs, steps, st) : launch_c1<true, ABITS, false, FS>(P, ndirs, steps, st);
+    return trace ? launch_c1<false, ABITS, true, FS>(P, ndirs, steps, st) : launch_c1<false, ABITS, false, FS>(P, ndirs, steps, st);
+}
+
 template <int ABITS>
 static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st,
                                  int kernel, bool exact, bool trace) {
-    if (kernel == 0) {
-        if (exact) return trace ? launch_c1<true, ABITS, true>(P, ndirs, steps, st) : launch_c1<true, ABITS, false>(P, ndirs, steps, st);
-        return trace ? launch_c1<false, ABITS, true>(P, ndirs, steps, st) : launch_c1<false, ABITS, false>(P, ndirs, steps, st);
-    }
+    if (kernel == 0) return launch_c1_any<ABITS, false>(P, ndirs, steps, st, exact, trace);
+    if (kernel == 2) return launch_c1_any<ABITS, true>(P, ndirs, steps, st, exact, trace);
     if (exact) return trace ? launch_fast<true, ABITS, true>(P, ndirs, steps, st) : launch_fast<true, ABITS, false>(P, ndirs, steps, st);
     return trace ? launch_fast<false, ABITS, true>(P, ndirs, steps, st) : launch_fast<false, ABITS, false>(P, ndirs, steps, st);
 }
@@ -908,13 +1044,15 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     if (e != cudaSuccess) return e;
     const bool trace = dirs[0].masks != nullptr;
     const bool even = (dirs[0].E & 1) == 0;
-    // auto: one thread per channel for A4 (measured 2.225 vs 2.43 ms at Vim-B, 0.358 vs
-    // 0.415 at Vim-S), two per channel for A8 (1.17 vs 1.63 ms at Vim-T batch 256)
-    int kernel = (dirs[0].abits == 4 && even) ? 0 : 1;
+    // auto: one thread per channel with the f32 state update for A4 (ms per Vim-B launch at
+    // batch 256: 1.79, vs 2.23 with the f64 state update and 2.43 with two threads per
+    // channel; Vim-S batch 64: 0.297 / 0.360 / 0.415), two threads per channel for A8 (Vim-T
+    // batch 256: 1.17 vs 1.41 / 1.63)
+    int kernel = (dirs[0].abits == 4 && even) ? 2 : 1;
     if (variant == 2) kernel = 1;
-    if (variant == 3) {
+    if (variant >= 3) {
         if (!even) return cudaErrorNotSupported;
-        kernel = 0;
+        kernel = variant == 3 ? 0 : 2;
     }
     const bool exact = variant == 1;
     switch (dirs[0].abits) {

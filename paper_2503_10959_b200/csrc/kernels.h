@@ -175,11 +175,12 @@ struct ScanParams {
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
 // Fast path (dynamic/static, channel-local detector): both directions in one
 // launch (plus a step-table prep launch); work = scan_fast_workspace_bytes(S, T,
-// ndirs) bytes, 16-aligned. variant 0: auto (one thread per channel for A4 and
-// even E, two per channel otherwise); 1: the same with the certified f32 codes
-// disabled (every element exact f64); 2: the two-threads-per-channel kernel; 3:
-// the one-thread-per-channel kernel (even E). Non-null `masks` selects the
-// parity-trace instantiation.
+// ndirs) bytes, 16-aligned. variant 0: auto (one thread per channel with the f32
+// state update for A4 and even E, two per channel otherwise); 1: the same with the
+// certified f32 codes disabled (every element exact f64); 2: the
+// two-threads-per-channel kernel; 3 / 4: the one-thread-per-channel kernel with the
+// f64 / f32 state update (even E). Non-null `masks` selects the parity-trace
+// instantiation.
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
                              int variant);

@@ -2,7 +2,8 @@
 
     python scripts/scan_ab.py E B blocks abits [variants...]
 
-variant 0 = auto, 1 = reference kernel, 2 = exact codes, 3 = two threads per channel, 4 = one thread per channel.
+variant 0 = auto, 1 = reference kernel, 2 = exact codes, 3 = two threads per channel, 4 / 5 = one thread per
+channel with the f64 / f32 state update.
 """
 import os
 import sys
@@ -13,13 +14,14 @@ import torch
 import paper_2503_10959_b200 as ob
 
 E, B, blocks, abits = (int(a) for a in sys.argv[1:5])
-variants = [int(v) for v in sys.argv[5:]] or [0, 3, 4, 2]
+rho = float(os.environ.get("RHO", "0.01"))
+variants = [int(v) for v in sys.argv[5:]] or [0, 3, 4, 5, 2]
 ctx = ob.Context(0)
 m = ob.Model(ctx, ob.Dims(embed=E, blocks=blocks), 1234)
 g = torch.Generator(device="cuda").manual_seed(0)
 cal_imgs = torch.randn(8, 224, 224, 3, dtype=torch.float64, device="cuda", generator=g)
 imgs = torch.randn(B, 224, 224, 3, dtype=torch.float64, device="cuda", generator=g)
-cal = m.calibrate(cal_imgs, ob.QuantSpec(wbits=4, abits=abits, obits=8, n_refresh=10, rho=0.01), chunk=8)
+cal = m.calibrate(cal_imgs, ob.QuantSpec(wbits=4, abits=abits, obits=8, n_refresh=10, rho=rho), chunk=8)
 res = {}
 for v in variants:
     m.set_option("scan_variant", v)
