@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
     float2 rhp[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) rhp[k] = make_float2(0.0f, 0.0f);
-    float sHf_prev = 0.0f;
+    float sHf_prev = 0.0f, qHp = 0.0f;  // FS: f32 of the previous step's h scale, its code bound
     double sHp = 0.0;  // FS: the previous step's h scale; the state is rhp * sHp, exact (no f64 state kept)
     const float thHlo = thHf * (1.0f - 4.0f * 5.9604645e-8f);
     const double bd = active ? p.b_delta[i] : 0.0;
@@ -692,6 +692,17 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
             float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
             float halfA = pr.y, halfB = pr.z;
             bool clip = pf & 2u;
+            // FS: an outlier channel's scale (scale_for of its row, quant.cpp:37-42) as a
+            // certified f32 estimate sXf with relative error epsX; the exact f64 scale is
+            // computed only where an exact value is needed (sXexact false until then)
+            float sAfo = 0.0f, sBfo = 0.0f, epsA = 0.0f, epsB = 0.0f;
+            bool sAexact = true, sBexact = true;
+            auto exact_scales = [&]() {
+                if (!sAexact || !sBexact) exact();
+                if (!sAexact) sA = scale_call(pa, qo);
+                if (!sBexact) sB = scale_call(pb, qo);
+                sAexact = sBexact = true;
+            };
             if (dyn) {
                 fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh, quant.cpp:303-311
                 // detect_outliers, channel-local form: only outlier channels and certified-peak
@@ -721,19 +732,43 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                         }
                     }
                     if (fl & 3u) {
-                        exact();
-                        if (fl & 1u) {
-                            sA = scale_call(pa, qo);
-                            invA = __double2float_rn(recip_call(sA));
-                            qAf = qof;
-                            const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
-                            halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
-                        }
-                        if (fl & 2u) {
-                            sB = scale_call(pb, qo);
-                            kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
-                            qBf = qof;
-                            halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                        if constexpr (FS) {
+                            // sA = max a_bar / 127 = paf / 127 within eta_a (paf's bound) + 2.2 u; sB =
+                            // delta max|B| / 127 = pbf / 127 within ed + 5.2 u. The quotient margins
+                            // grow by these; codes stay certified against the exact scales
+                            if (fl & 1u) {
+                                epsA = fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1.32e-7f;
+                                sAfo = paf * (1.0f / 127.0f);
+                                sAexact = false;
+                                invA = __frcp_rn(sAfo);
+                                qAf = qof;
+                                const float LA = 0.6931472f * (1.001f + fmaxf(0.0f, -__log2f(sAfo)));
+                                halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f) + epsA + 1.8e-7f,
+                                                    1e-6f);
+                            }
+                            if (fl & 2u) {
+                                epsB = ed + 3.1e-7f;
+                                sBfo = pbf * (1.0f / 127.0f);
+                                sBexact = false;
+                                kB = __frcp_rn(sBfo) / ss.invSbf;
+                                qBf = qof;
+                                halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f + epsB + 1.2e-7f, 1e-6f);
+                            }
+                        } else {
+                            exact();
+                            if (fl & 1u) {
+                                sA = scale_call(pa, qo);
+                                invA = __double2float_rn(recip_call(sA));
+                                qAf = qof;
+                                const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                                halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+                            }
+                            if (fl & 2u) {
+                                sB = scale_call(pb, qo);
+                                kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
+                                qBf = qof;
+                                halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                            }
                         }
                         clip = !(df * kB * ss.BSmaxf <= qBf + 0.25f && paf * invA * 1.000001f <= qAf + 0.25f);
                     }
@@ -788,6 +823,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
             else pass1(std::false_type{});
             if (redo) {  // exact f64 codes where the f32 quotient is not certified
                 exact();
+                if constexpr (FS) exact_scales();
 #pragma unroll
                 for (int m = 0; m < 16; ++m) {
                     const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
@@ -806,22 +842,24 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                 // f32 state update with a rigorous bound (header comment of k3_scan_c1<FS>):
                 // P1 = (ra * rh_prev) * f32(S_a S_h'), P2 = rb * f32(S_b u), hf = P1 + P2 stands for
                 // h = fl64(fl64(a_q h') + fl64(b_q u)) within D = (max|P1| + max|P2|) 5.2 2^-24
-                const float sAf = (fl & 1u) ? __double2float_rn(sA) : ss.Saf;
-                const float sBf = (fl & 2u) ? __double2float_rn(sB) : ss.Sbf;
+                const float sAf = (fl & 1u) ? sAfo : ss.Saf;
+                const float sBf = (fl & 2u) ? sBfo : ss.Sbf;
                 const float sAsH = sAf * sHf_prev, sBu = sBf * __double2float_rn(uv);
                 float2 hf2[8];
-                float mp1 = 0.0f, mp2 = 0.0f, phf = 0.0f;
+                float phf = 0.0f;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const float2 p1 = __fmul2_rn(__fmul2_rn(make_float2(raf[2 * k], raf[2 * k + 1]), rhp[k]), f2(sAsH));
                     const float2 p2 = __fmul2_rn(make_float2(cb[2 * k], cb[2 * k + 1]), f2(sBu));
                     const float2 hv = __fadd2_rn(p1, p2);
-                    mp1 = fmaxf(mp1, fmaxf(fabsf(p1.x), fabsf(p1.y)));
-                    mp2 = fmaxf(mp2, fmaxf(fabsf(p2.x), fabsf(p2.y)));
                     phf = fmaxf(phf, fmaxf(fabsf(hv.x), fabsf(hv.y)));
                     hf2[k] = hv;
                 }
-                const float maxD = fmaf(mp1 + mp2, 5.2f * 5.9604645e-8f, 1e-37f);
+                // |P1| <= qA qH' |f32(S_a) f32(S_h')| and |P2| <= qB |f32(S_b) f32(u)| (codes are clipped
+                // to their q): D from the step's scalars, with 5.3 u for the rounding of these products
+                // (outlier a / b scales: + their relative bound epsA / epsB)
+                const float maxD =
+                    fmaf(qAf * qHp * sAsH, 5.3f * 5.9604645e-8f + epsA, fmaf(qBf * fabsf(sBu), 5.3f * 5.9604645e-8f + epsB, 1e-37f));
                 double sH = ss.Sh, qH = qa;
                 float invHf = ss.invShf;
                 // exact state path: h-outlier channels (their scale needs the exact peak), peaks
@@ -853,6 +891,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                 else hcodes(std::true_type{});
                 hexact |= !(mdh <= halfH);
                 if (hexact) {  // the exact f64 update (ssm.cpp:165-167) and the c1 h logic on it
+                    exact_scales();
                     double hn[16];
 #pragma unroll
                     for (int m = 0; m < 16; ++m) {
@@ -885,6 +924,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                 for (int k = 0; k < 8; ++k) rhp[k] = make_float2(chd[2 * k], chd[2 * k + 1]);  // carried state
                 sHp = sH;
                 sHf_prev = (fl & 4u) ? __double2float_rn(sH) : ss.Shf;
+                qHp = static_cast<float>(qH);
             } else {
             // pass 2: dequantized values (code * s) and the exact f64 update, ssm.cpp:165-167
                 const double nKA = dmul(sA, -4503599627370496.0);
