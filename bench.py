@@ -499,7 +499,8 @@ def run_ours(args):
         if kern:
             k3 = kern["k3.scan"]
             nc = ncu_summary()
-            line["roofline"] = {"kernel": "k3_scan_fast (both directions + step tables)", "bound": k3["bound"],
+            line["roofline"] = {"kernel": "k3 scan: k3_scan_c1<FS> (one thread per channel, f32 state update, "
+                                          "both directions) + k3_step_tables", "bound": k3["bound"],
                                 "achieved": k3["achieved"], "peak": k3["peak"], "unit": k3["unit"],
                                 "frac": k3["frac"], "model": k3["model"],
                                 "traffic": nc.get("dram_bytes_per_launch") if nc else None,
