@@ -261,11 +261,6 @@ def kernel_rooflines(launches, *, B, L, E, N, blocks, abits, peaks, i8_tops, fp6
                            f"(SURVEY §8d); peak = {FP32_LANES_PER_CLK_SM} lanes/clk/SM x {sms} SMs x "
                            f"{peaks['sm_max_mhz']:.0f} MHz",
                      hbm_gbs=f["bytes"] / t / 1e9, hbm_frac=f["bytes"] / t / 1e9 / hbm)
-            if fp64_tflops:
-                dfma_lane_ops = fp64_tflops / 2.0
-                e["secondary_f64"] = {"achieved": work / t / 1e12, "peak": dfma_lane_ops,
-                                      "frac": work / t / 1e12 / dfma_lane_ops,
-                                      "unit": "T f64 lane-op/s (same 28-op count vs the in-process DFMA probe)"}
         else:
             e.update(bound="hbm", unit="GB/s", achieved=f["bytes"] / t / 1e9, peak=hbm,
                      frac=f["bytes"] / t / 1e9 / hbm, bytes_per_launch=f["bytes"])
@@ -506,7 +501,6 @@ def run_ours(args):
                                 "traffic": nc.get("dram_bytes_per_launch") if nc else None,
                                 "traffic_source": nc["file"] if nc else None,
                                 "ncu": {k: v for k, v in (nc or {}).items() if k not in ("file",)},
-                                "secondary_f64": k3.get("secondary_f64"),
                                 "peaks": peaks["source"]}
             line["kernels"] = kern
         line["kernels_ms_per_step"] = {k: v[0] for k, v in fam.items()}

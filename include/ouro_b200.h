@@ -342,8 +342,8 @@ enum { OURO_B200_DTYPE_F64 = 0, OURO_B200_DTYPE_I8 = 1, OURO_B200_DTYPE_U4 = 2 }
 /* write_tensor_f64 / _i8 / _u4 (tensor_io.cpp): data = f64[numel], int8[numel],
  * or for U4 either int8 codes in [-8, 7] (data_packed = 0: packed here, element
  * i in the low nibble of byte i/2 when i is even) or the packed payload itself
- * (data_packed = 1, ceil(numel/2) bytes, e.g. a K1 operand produced with
- * OURO_B200_CODES_PACKED_I4 and copied from the device). Written atomically
+ * (data_packed = 1, ceil(numel/2) bytes, e.g. the codes4 operand of
+ * ouro_b200_detect_quantize_packed copied from the device). Written atomically
  * (temporary file + rename). A code outside [-8, 7] is a validation error. */
 ouro_status ouro_b200_tensor_save(const char* path, int dtype, const uint64_t* shape, size_t rank, const void* data,
                                   int data_packed);
