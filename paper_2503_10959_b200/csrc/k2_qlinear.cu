@@ -330,21 +330,26 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
                     }
                 }
             }
+            constexpr int kChunksPerWarp = BN / 32 / (EW / 4);
+            // column scales ws[r] of the warp's first chunk, loaded before the accumulator wait;
+            // each chunk prefetches the next one's (an L2 round trip per chunk otherwise)
+            const int rfirst = n0 + cgrp * kChunksPerWarp * 32;
+            double wsn = rfirst < p.R ? __ldg(p.ws + rfirst + lane) : 0.0;
             ptx::mbar_wait(acc_full + buf, aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            constexpr int kChunksPerWarp = BN / 32 / (EW / 4);
             for (int cc = 0; cc < kChunksPerWarp; ++cc, ++cs) {
                 const int c = cgrp * kChunksPerWarp + cc;
                 const int r0 = n0 + c * 32;
                 if (r0 >= p.R) break;  // uniform across the warp
+                const double wsl = wsn;  // R % 32 == 0: in range
+                if (cc + 1 < kChunksPerWarp && r0 + 32 < p.R) wsn = __ldg(p.ws + r0 + 32 + lane);
                 const bool to2 = POST == POST_INPROJ && r0 >= p.epi.split;
                 const CUtensorMap* om = to2 ? &tmO2 : &tmO;
                 const int oc0 = to2 ? r0 - p.epi.split : r0;
                 const int sb = kStgBufs == 2 ? (cs & 1) : 0;
                 uint8_t* stg = stg0 + sb * 8192;
                 uint64_t* rbar = res_bar + 2 * ew + sb;
-                const double wsl = __ldg(p.ws + r0 + lane);  // R % 32 == 0: in range
                 if (lane == 0) {
                     if (kStgBufs == 2) ptx::bulk_wait_read1();  // this buffer's store (two chunks ago) has left it
                     else ptx::bulk_wait_read0();
