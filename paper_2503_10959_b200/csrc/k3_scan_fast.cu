@@ -105,38 +105,27 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
 }
 
 // Per (direction, sample, scan step) tables the scan consumes: B, C, the
-// calibrated scales and their f32 inverses, the b_bar quotients per unit delta
-// and max_m |B_m|. One warp per step; lane j holds column E + j of the x_proj row.
+// calibrated scales and their f32 inverses / copies, the b_bar quotients per unit
+// delta and max_m |B_m|. One warp per (direction, step, group of kTabSamples
+// samples): the step's calibration fields (global loads of the scale tables, a
+// log2) are computed once and kept in the warp's shared record, then each sample
+// overwrites its B / C fields (lane j holds column E + j of the x_proj row; the
+// next sample's row is loaded before this one is written) and the record leaves as
+// 16-byte coalesced chunks.
+constexpr int kTabSamples = 8;
 __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndirs, StepShared* __restrict__ out) {
-    // each warp assembles its record in shared memory, then writes it as 16-byte
-    // coalesced chunks (the fields are scattered scalars)
     __shared__ StepShared rec[8];
     const int wi = threadIdx.x >> 5, gw = blockIdx.x * 8 + wi, lane = threadIdx.x & 31;
     const ScanParams& p0 = P.d[0];
-    const int S = p0.S, T = p0.T;
-    if (gw >= ndirs * S * T) return;
-    const int dd = gw / (S * T), st_idx = gw - dd * S * T, t = st_idx % T;
+    const int S = p0.S, T = p0.T, groups = (S + kTabSamples - 1) / kTabSamples;
+    if (gw >= ndirs * T * groups) return;
+    const int dd = gw / (T * groups), rem = gw - dd * T * groups, t = rem / groups, s0 = (rem % groups) * kTabSamples;
     const ScanParams& p = P.d[dd];
     const bool dyn = p.mode == MODE_DYNAMIC;
-    const double v = p.proj[static_cast<size_t>(st_idx) * (p.E + 32) + p.E + lane];
     StepShared& ss = rec[wi];
     const double Sb = dyn ? p.cal[1].s_in[t] : p.cal[1].s_full[t];
     const double* ib = dyn ? p.cal[1].inv_in : p.cal[1].inv_full;
     const float invSbf = __double2float_rn(ib ? ib[t] : __ddiv_rn(1.0, Sb));
-    double bm = fabs(v);
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-    float bs = 0.0f;
-    if (lane < 16) {
-        bs = __double2float_rn(v) * invSbf;
-        ss.B[lane] = v;
-        ss.BSf[lane] = bs;
-    } else {
-        ss.C[lane - 16] = v;
-    }
-    bs = fabsf(bs);
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) bs = fmaxf(bs, __shfl_xor_sync(0xffffffffu, bs, o));
     if (lane == 0) {
         const double Sa = dyn ? p.cal[0].s_in[t] : p.cal[0].s_full[t];
         const double Sh = dyn ? p.cal[2].s_in[t] : p.cal[2].s_full[t];
@@ -145,9 +134,6 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         ss.Sa = Sa;
         ss.Sb = Sb;
         ss.Sh = Sh;
-        ss.Bmax = bm;
-        ss.Bmaxf = __double2float_rn(bm);
-        ss.BSmaxf = bs;
         ss.invSaf = __double2float_rn(ia ? ia[t] : __ddiv_rn(1.0, Sa));
         ss.invSbf = invSbf;
         ss.invShf = __double2float_rn(ih ? ih[t] : __ddiv_rn(1.0, Sh));
@@ -163,11 +149,39 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         ss.Shf = __double2float_rn(Sh);
         ss.pad2 = 0.0f;
     }
-    __syncwarp();
     constexpr int kChunks16 = static_cast<int>(sizeof(StepShared) / 16);
-    const uint4* src = reinterpret_cast<const uint4*>(&rec[wi]);
-    uint4* dst = reinterpret_cast<uint4*>(out + gw);
-    for (int k = lane; k < kChunks16; k += 32) dst[k] = src[k];
+    const uint4* src = reinterpret_cast<const uint4*>(&ss);
+    const int s1 = min(S, s0 + kTabSamples);
+    const size_t P2 = static_cast<size_t>(p.E) + 32;
+    const double* col = p.proj + static_cast<size_t>(t) * P2 + p.E + lane;  // + s*T*P2 per sample
+    double v = col[static_cast<size_t>(s0) * T * P2];
+    for (int s = s0; s < s1; ++s) {
+        const double vn = s + 1 < s1 ? col[static_cast<size_t>(s + 1) * T * P2] : 0.0;
+        double bm = fabs(v);
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        float bs = 0.0f;
+        __syncwarp();  // the previous sample's record has been copied out
+        if (lane < 16) {
+            bs = __double2float_rn(v) * invSbf;
+            ss.B[lane] = v;
+            ss.BSf[lane] = bs;
+        } else {
+            ss.C[lane - 16] = v;
+        }
+        bs = fabsf(bs);
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) bs = fmaxf(bs, __shfl_xor_sync(0xffffffffu, bs, o));
+        if (lane == 0) {
+            ss.Bmax = bm;
+            ss.Bmaxf = __double2float_rn(bm);
+            ss.BSmaxf = bs;
+        }
+        __syncwarp();
+        uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<size_t>(dd) * S + s) * T + t);
+        for (int k = lane; k < kChunks16; k += 32) dst[k] = src[k];
+        v = vn;
+    }
 }
 
 template <bool EXACT, int ABITS, bool TRACE>
@@ -1077,7 +1091,7 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     if (!work || work_bytes < scan_fast_workspace_bytes(S, T, ndirs) || (reinterpret_cast<uintptr_t>(work) & 15))
         return cudaErrorInvalidValue;
     StepShared* steps = static_cast<StepShared*>(work);
-    const int warps = ndirs * S * T;
+    const int warps = ndirs * T * ((S + kTabSamples - 1) / kTabSamples);
     k3_step_tables<<<(warps + 7) / 8, 256, 0, st>>>(P, ndirs, steps);
     ++kernel_launch_counter();
     cudaError_t e = cudaGetLastError();
