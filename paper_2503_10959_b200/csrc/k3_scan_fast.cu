@@ -559,10 +559,11 @@ struct C1Smem {
     double dp[2][KC][32];  // x_proj delta pre-activations (raw), lane = channel
     double u[2][KC][32];
     float4 pre[KC][32];    // df, inlier halfA, inlier halfB, flags (bit 0 detect, bit 1 clamp)
+    float4 a2[4][32];      // SMA2: f32(A_m log2 e) of the lane's channel (frees 16 registers)
     uint64_t bar[2];
 };
 
-template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB, bool FS>
+template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB, bool FS, bool SMA2 = false>
 __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t c1_smem_raw[];
     using Sm = C1Smem<KC>;
@@ -581,14 +582,20 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
     const double* __restrict__ uin = p.u;
     double* __restrict__ obase = p.o + static_cast<size_t>(s) * T * E + (active ? i : 0);
     const double* __restrict__ arow = p.a + static_cast<size_t>(active ? i : 0) * 16;
-    float2 A2f[8];  // f32(A_m log2 e), pairs for the packed f32x2 pipe
+    float2 A2r[SMA2 ? 1 : 8];  // f32(A_m log2 e), pairs for the packed f32x2 pipe (registers or shared)
     double Amax = -1e300;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const double a0 = active ? arow[2 * k] : -1.0, a1 = active ? arow[2 * k + 1] : -1.0;
-        A2f[k] = make_float2(__double2float_rn(a0 * 1.4426950408889634), __double2float_rn(a1 * 1.4426950408889634));
+        const float2 v = make_float2(__double2float_rn(a0 * 1.4426950408889634), __double2float_rn(a1 * 1.4426950408889634));
+        if constexpr (SMA2) reinterpret_cast<float2*>(&sh.a2[k >> 1][lane])[k & 1] = v;
+        else A2r[k] = v;
         Amax = fmax(Amax, fmax(a0, a1));
     }
+    auto A2f_at = [&](int k) -> float2 {
+        if constexpr (SMA2) return reinterpret_cast<const float2*>(&sh.a2[k >> 1][lane])[k & 1];
+        else return A2r[k];
+    };
     const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
     double h[16];
 #pragma unroll
@@ -802,7 +809,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                 float mda = 0.0f, mdb = 0.0f;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const float2 x2 = __fmul2_rn(f2(df), A2f[k]);
+                    const float2 x2 = __fmul2_rn(f2(df), A2f_at(k));
                     float2 qa2 = __fmul2_rn(make_float2(ex2_approx(x2.x), ex2_approx(x2.y)), f2(invA));
                     if constexpr (CL) {
                         qa2.x = fminf(qa2.x, capA);
@@ -840,7 +847,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
                 if constexpr (FS) exact_scales();
 #pragma unroll
                 for (int m = 0; m < 16; ++m) {
-                    const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
+                    const float a2 = (m & 1) ? A2f_at(m >> 1).y : A2f_at(m >> 1).x;
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
                     if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA) {
                         const double cq = qdiv_call(exp_call(dmul(delta, arow[m])), sA, static_cast<double>(qAf));
@@ -1030,9 +1037,9 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
 // spills and runs 3.01; per-lane cp.async staging instead of bulk rows 2.306.
 constexpr int kC1Chunk = 4, kC1MinBlocks = 12;
 
-template <bool EXACT, int ABITS, bool TRACE, bool FS>
+template <bool EXACT, int ABITS, bool TRACE, bool FS, int MB = kC1MinBlocks, bool SMA2 = false>
 static cudaError_t launch_c1(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
-    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, kC1MinBlocks, FS>;
+    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, MB, FS, SMA2>;
     const int smem = static_cast<int>(sizeof(C1Smem<kC1Chunk>));
     cudaError_t e = ensure_smem_attr<kern>(smem);
     if (e != cudaSuccess) return e;
@@ -1059,7 +1066,13 @@ template <int ABITS, bool FS>
 static cudaError_t launch_c1_any(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st, bool exact,
                                  bool trace) {
     if (exact) return trace ? launch_c1<true, ABITS, true, FS>(P, ndirs, steps, st) : launch_c1<true, ABITS, false, FS>(P, ndirs, steps, st);
-    return trace ? launch_c1<false, ABITS, true, FS>(P, ndirs, steps, st) : launch_c1<false, ABITS, false, FS>(P, ndirs, steps, st);
+    if (trace) return launch_c1<false, ABITS, true, FS>(P, ndirs, steps, st);
+    // FS on large grids (>= 2 waves of 16 CTAs per SM): A stays in shared memory and the
+    // kernel fits 128 registers, 16 warps per SM (Vim-B batch 256: 1.705 vs 1.741 ms); small
+    // grids keep 168 registers (Vim-S batch 64: 0.286 vs 0.296)
+    const long ctas = static_cast<long>((P.d[0].E + 31) / 32) * P.d[0].S * ndirs;
+    if (FS && ctas >= 2L * 148 * 16) return launch_c1<false, ABITS, false, FS, 13, true>(P, ndirs, steps, st);
+    return launch_c1<false, ABITS, false, FS>(P, ndirs, steps, st);
 }
 
 template <int ABITS>
