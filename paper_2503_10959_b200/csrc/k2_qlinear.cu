@@ -335,6 +335,15 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
             // each chunk prefetches the next one's (an L2 round trip per chunk otherwise)
             const int rfirst = n0 + cgrp * kChunksPerWarp * 32;
             double wsn = rfirst < p.R ? __ldg(p.ws + rfirst + lane) : 0.0;
+            // the first outlier channel's 32 weights of the warp's first chunk, loaded before the
+            // accumulator wait; each chunk prefetches the next chunk's (8-warp shape)
+            int4 pw0 = make_int4(0, 0, 0, 0), pw1 = make_int4(0, 0, 0, 0);
+            const bool pre0 = EW < 16 && hoisted && cnt > 0;
+            if (pre0 && rfirst < p.R) {
+                const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(hch[0]) * p.R + rfirst);
+                pw0 = __ldg(wp);
+                pw1 = __ldg(wp + 1);
+            }
             ptx::mbar_wait(acc_full + buf, aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -372,24 +381,34 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) aout[j] = 0;
                 // outlier terms in ascending channel order (gemm.cpp:208-216)
-                auto outlier_term = [&](int ch, int xo_i, double osc) {
+                auto outlier_term_w = [&](int xo_i, double osc, int4 w01, int4 w23) {
                     const double xo = i32_to_f64(static_cast<uint32_t>(xo_i));
-                    const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(ch) * p.R + r0);
-                    int4 w01 = __ldg(wp), w23 = __ldg(wp + 1);
-                    const int8_t* wv = reinterpret_cast<const int8_t*>(&w01);
-                    const int8_t* wv2 = reinterpret_cast<const int8_t*>(&w23);
+                    const int wd[8] = {w01.x, w01.y, w01.z, w01.w, w23.x, w23.y, w23.z, w23.w};
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const int wq = j < 16 ? wv[j] : wv2[j - 16];
+                        const int wq = static_cast<int8_t>(static_cast<uint32_t>(wd[j >> 2]) >> (8 * (j & 3)));  // register byte
                         const double coeff = dmul(osc, i32_to_f64(static_cast<uint32_t>(wq)));
                         y[j] = dadd(y[j], dmul(coeff, xo));
                         if (PLANES) aout[j] += wq * xo_i;
                     }
                 };
+                auto outlier_term = [&](int ch, int xo_i, double osc) {
+                    const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(ch) * p.R + r0);
+                    outlier_term_w(xo_i, osc, __ldg(wp), __ldg(wp + 1));
+                };
                 if (hoisted) {
+                    if (pre0) {  // the prefetched weights of channel hch[0]; the next chunk's in flight
+                        const int4 w01 = pw0, w23 = pw1;
+                        if (cc + 1 < kChunksPerWarp && r0 + 32 < p.R) {
+                            const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(hch[0]) * p.R + r0 + 32);
+                            pw0 = __ldg(wp);
+                            pw1 = __ldg(wp + 1);
+                        }
+                        outlier_term_w(hxo[0], hosc[0], w01, w23);
+                    }
 #pragma unroll
                     for (int o = 0; o < kHoist; ++o)
-                        if (o < cnt) outlier_term(hch[o], hxo[o], hosc[o]);
+                        if (o < cnt && !(o == 0 && pre0)) outlier_term(hch[o], hxo[o], hosc[o]);
                 } else {  // more than kHoist: mask word by word, bit by bit
                     int word = -1;
                     unsigned bits = 0;
