@@ -219,7 +219,9 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * channel with the f64 state update / with the f32 state update (A/B aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
  * detector kernel everywhere; "pack_a4" = 1: A4 activation codes travel
- * nibble-packed from K1 to K2, 0 (default) one int8 byte per code; "split_parts" in [1, 4] (default 2) runs a batch of
+ * nibble-packed from K1 to K2, 0 (default) one int8 byte per code; "merge_fuse" = 1:
+ * the out_proj input K1 runs as the f32-state scan's tail, 0 (default) its own
+ * launch; "split_parts" in [1, 4] (default 2) runs a batch of
  * >= 32 * parts samples as that many independent sub-batches on their own
  * streams (results identical), 1 one stream; "feed_chunks" (default 8) = H2D
  * chunks of forward_host for batches >= 64. */

@@ -681,6 +681,9 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         } else if (k == "split_parts") {
             require(value >= 1 && value <= 4, "model_set_option: split_parts must be in [1, 4]");
             m->m->split_parts = static_cast<int>(value);
+        } else if (k == "merge_fuse") {
+            require(value == 0 || value == 1, "model_set_option: merge_fuse must be 0 or 1");
+            m->m->merge_fuse = static_cast<int>(value);
         } else if (k == "pack_a4") {
             require(value == 0 || value == 1, "model_set_option: pack_a4 must be 0 or 1");
             m->m->pack_a4 = static_cast<int>(value);

@@ -320,6 +320,10 @@ void Model::ensure_work(Work& w, int S, bool trace) {
     w.ocnt.ensure(slots * rows);
     w.scanned.ensure(slots * rows);
     w.scan_steps.ensure(scan_fast_workspace_bytes(S, static_cast<int>(L), static_cast<int>(nd)));
+    if (w.merge_cnt.n < static_cast<size_t>(S) * ((E + 31) / 32)) {
+        w.merge_cnt.ensure(static_cast<size_t>(S) * ((E + 31) / 32));
+        cuda_check(cudaMemset(w.merge_cnt.p, 0, w.merge_cnt.n * sizeof(int)), "merge counters");
+    }
     if (trace) {
         w.masks.ensure(2 * 3 * rows * E);
         w.acc_in.ensure(rows * std::max(2 * E, E + 2 * N));
@@ -728,8 +732,19 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
             sps[dd].spike.dir = dd;
             sps[dd].spike.sample0 = spikes.sample0 + sample0;
         }
+        // the out_proj input K1 (merge source) rides on the fast scan's tail where that
+        // kernel runs it (qslot 0, its |O(t)| zeroed first); else it runs after the scan
+        qslot = 0;
+        K1Params km = k1_base(K1_SRC_MERGE, w.o.p, -1, b, nsites - 1, true);
+        km.x2 = nd > 1 ? w.o.p + rows * E : nullptr;
+        km.gate = w.gate.p;
+        bool merged = false;
         if (fast_ok && !any_literal && scan_variant != 1 && !(spikes.rate > 0.0)) {
-            cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant >= 2 ? scan_variant - 1 : 0), "scan");
+            const bool fuse = qlin && merge_fuse && !km.force_literal && !km.scanned;
+            if (fuse) cuda_check(cudaMemsetAsync(km.ocnt, 0, rows * sizeof(int), st), "merge ocnt");
+            cuda_check(launch_scan_fast(sps, nd, w.scan_steps.p, w.scan_steps.n, st, scan_variant >= 2 ? scan_variant - 1 : 0,
+                                        fuse ? &km : nullptr, fuse ? w.merge_cnt.p : nullptr, &merged),
+                       "scan");
         } else {
             for (int dd = 0; dd < nd; ++dd) {
                 bool l = false;
@@ -746,13 +761,11 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
                 if (quant && mode == MODE_DYNAMIC) grab(trace, p + "masks", sps[dd].masks, 3 * rows * E, st);
                 trace->blobs[p + "literal"] = std::vector<char>(1, static_cast<char>(lit ? 1 : 0));
             }
-        qslot = 0;
-        K1Params km = k1_base(K1_SRC_MERGE, w.o.p, -1, b, nsites - 1, true);
-        km.x2 = nd > 1 ? w.o.p + rows * E : nullptr;
-        km.gate = w.gate.p;
-        tick_begin(FAM_K1);
-        cuda_check(launch_k1(km, st), "K1 out_proj");
-        tick_end(FAM_K1);
+        if (!merged) {
+            tick_begin(FAM_K1);
+            cuda_check(launch_k1(km, st), "K1 out_proj");
+            tick_end(FAM_K1);
+        }
         if (tb(b) && !qlin) grab(trace, "y", w.xin.p, rows * E, st);
         {
             GemmEpi e;

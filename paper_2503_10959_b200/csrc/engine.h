@@ -178,6 +178,10 @@ class Model {
     void quantize(unsigned bits);
     bool fp_dirty = true;
     int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
+    int merge_fuse = 0;    // 1: the out_proj input K1 runs as the f32-state scan's tail (last direction of each
+                           // (sample, channel group) to finish quantizes it); 0 (default): separate k1_channel
+                           // launch. Measured at Vim-B batch 256: 3.36 ms scan per block fused vs 1.71 + 0.216
+                           // separate (the tails walk 196 tokens per warp)
     int pack_a4 = 0;       // 1: A4 inlier codes travel nibble-packed from K1 to K2, which unpacks them in
                            // shared memory (QAct::codes4); 0 (default): one int8 byte per code. Measured at
                            // Vim-B batch 256: packed K2 176 / 107 / 127 us vs 157 / 93 / 119 (in_proj / x_proj /
@@ -199,6 +203,7 @@ class Model {
         DevBuf<int> ocnt;
         DevBuf<uint32_t> omask;
         DevBuf<uint8_t> scanned, masks, scan_steps, codes4;
+        DevBuf<int> merge_cnt;  // [S][E/32] finish counters of the scan's fused merge K1 (zero between launches)
         DevBuf<unsigned long long> peaks;
         DevBuf<int32_t> acc_in, acc_out;
         std::vector<cudaEvent_t> feed_events;  // host-feed chunk events, created on first use

@@ -35,6 +35,7 @@
 //    the output sum in the reference's order.
 #include "common.cuh"
 #include "kernels.h"
+#include "merge_f32.cuh"
 #include "scan_f32.cuh"
 #include "sm100_ptx.cuh"
 
@@ -48,6 +49,11 @@ constexpr int kChunk = 8;      // steps staged per chunk
 
 struct ScanDirs {
     ScanParams d[2];
+    int n = 1;              // directions in this launch
+    // the out_proj input K1 fused into the one-thread-per-channel kernel (merge_tail):
+    // the last of the n directions to finish a (sample, 32-channel group) quantizes it
+    K1Params merge;
+    int* merge_cnt = nullptr;  // [S][E/32] finish counters (zero between launches)
 };
 
 struct __align__(16) StepShared {
@@ -522,6 +528,107 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
     }
 }
 
+// ---- the out_proj input K1 fused into the scan ----------------
+// k1_channel's merge source (k1_detect_quant.cu) for one (sample, 32-channel group)
+// with lane = channel walking the T tokens in canonical order: merged = (0 + o_0) +
+// o_1 (ssm.cpp:214-229), v = merged * silu(gate) certified in f32 (merge_f32.cuh),
+// maybe_refresh / detect_outliers in the channel-local form, split_quantize's codes;
+// the group's 32 channels are one mask word (a ballot) and |O(t)| is accumulated
+// across the E/32 groups with one atomic per row. The scan outputs o_d come from L2
+// (the other direction's CTA of the same group ran alongside: dir is the grid's
+// fastest index); the next tokens' operands are in flight while one is quantized.
+__device__ __noinline__ double merge_exact_call(double m, double g) { return dmul(m, silu_d(g)); }
+
+__device__ void merge_tail(const K1Params& p, int s, int grp, unsigned lane) {
+    const int E = p.E, T = p.T, J = E >> 5, i = grp * 32 + static_cast<int>(lane);
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
+    const int qai = static_cast<int>(qa);
+    const double theta = p.cal.theta;
+    const float thetaf = __double2float_rn(theta), capf = static_cast<float>(qa) + 1.0f;
+    const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
+    const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
+    const size_t base = static_cast<size_t>(s) * T;
+    constexpr int kG = 4;  // tokens per group; the next group's loads are issued before this one is used
+    double o0[2][kG], o1[2][kG], gt[2][kG];
+    auto load = [&](int b, int t0) {
+#pragma unroll
+        for (int k = 0; k < kG; ++k) {
+            const int t = min(t0 + k, T - 1);
+            const size_t idx = (base + t) * E + i;
+            o0[b][k] = __ldcg(p.x + idx);
+            o1[b][k] = p.x2 ? __ldcg(p.x2 + idx) : 0.0;
+            gt[b][k] = __ldg(p.gate + idx);
+        }
+    };
+    load(0, 0);
+    bool in = false;
+    for (int t0 = 0, b = 0; t0 < T; t0 += kG, b ^= 1) {
+        if (t0 + kG < T) {
+            if (b) load(0, t0 + kG);
+            else load(1, t0 + kG);
+        }
+#pragma unroll
+        for (int k = 0; k < kG; ++k) {
+            const int t = t0 + k;
+            if (t >= T) break;
+            const size_t row = base + t;
+            const double a0 = b ? o0[1][k] : o0[0][k], a1 = b ? o1[1][k] : o1[0][k];
+            const double g = b ? gt[1][k] : gt[0][k];
+            double mg = dadd(0.0, a0);  // (0 + o_0) + o_1
+            if (p.x2) mg = dadd(mg, a1);
+            const MergeApprox ap = merge_approx(mg, g);
+            bool have = false;
+            double v = 0.0;
+            if (dyn) {
+                if (refresh_at(t, p.n_refresh)) in = false;  // maybe_refresh
+                if (!in) {                                   // detect_outliers, channel-local form
+                    const float av = fabsf(ap.v);
+                    if (av * (1.0f - ap.eps) > thetaf * 1.0000003f) {
+                        in = true;
+                    } else if (av * (1.0f + ap.eps) >= thetaf * 0.9999997f) {
+                        v = merge_exact_call(mg, g);
+                        have = true;
+                        in = fabs(v) > theta;
+                    }
+                }
+            }
+            const double S = s_tab[t];
+            const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
+            int c = 0;
+            if (in) {
+                if (!have) v = merge_exact_call(mg, g);
+                const double os = scale_from_peak(fabs(v), qo);  // scale_for over the 1-value row
+                p.ocode[row * E + i] = static_cast<int8_t>(static_cast<int>(quant_code_div(v, os, qo)));
+                p.oscale[row * E + i] = os;
+            } else {
+                // certified f32 quotient: |dq| <= (|q| + 1) (eps + 3 2^-24)
+                const float q = fminf(fmaxf(ap.v * __double2float_rn(inv), -capf), capf);
+                const float r = rintf(q);
+                if (!have && fabsf(q - r) < 0.5f - fmaf(fabsf(q) + 1.0f, ap.eps + 1.8e-7f, 1e-6f)) {
+                    c = min(max(static_cast<int>(r), -qai), qai);
+                } else {
+                    if (!have) v = merge_exact_call(mg, g);
+                    c = quant_code_int(v, S, inv, qa, qai);
+                }
+            }
+            if (p.codes4) {  // lanes 2j, 2j+1: one pack_int4 byte
+                const unsigned nib = static_cast<unsigned>(c) & 0xFu;
+                const unsigned hi = __shfl_down_sync(0xffffffffu, nib, 1);
+                if (!(lane & 1)) p.codes4[row * (E >> 1) + (i >> 1)] = static_cast<uint8_t>(nib | (hi << 4));
+            } else {
+                p.codes[row * E + i] = static_cast<int8_t>(c);
+            }
+            const unsigned bits = __ballot_sync(0xffffffffu, in);
+            if (lane == 0) {
+                p.omask[row * J + grp] = bits;
+                if (bits) atomicAdd(p.ocnt + row, __popc(bits));
+                if (grp == 0) p.s_row[row] = S;
+            }
+        }
+    }
+}
+
 // ---- one thread per channel ---------------------------------------------------
 // Same arithmetic as k3_scan_fast (every certification bound above holds
 // unchanged), with lane = channel and all N = 16 states in one thread: the
@@ -563,15 +670,19 @@ struct C1Smem {
     uint64_t bar[2];
 };
 
-template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB, bool FS, bool SMA2 = false>
+template <bool EXACT, int ABITS, bool TRACE, int KC, int MINB, bool FS, bool SMA2 = false, bool MT = false>
 __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t c1_smem_raw[];
     using Sm = C1Smem<KC>;
     Sm& sh = *reinterpret_cast<Sm*>(c1_smem_raw);
-    const ScanParams& p = P.d[blockIdx.z];
+    // grid x = channel group * n + direction: the directions of a (sample, group) run side by
+    // side (the fused merge tail reads both outputs from L2)
+    const int dir = P.n == 2 ? static_cast<int>(blockIdx.x & 1) : 0;
+    const int grp = P.n == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const ScanParams& p = P.d[dir];
     const unsigned lane = threadIdx.x & 31;
     const int s = blockIdx.y;
-    const int cw = blockIdx.x * 32;  // first channel of this warp (CTA = one warp)
+    const int cw = grp * 32;  // first channel of this warp (CTA = one warp)
     const int i = cw + static_cast<int>(lane);
     const bool active = i < p.E;
     const int E = p.E, T = p.T, P2 = E + 32;
@@ -611,7 +722,7 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
     double sHp = 0.0;  // FS: the previous step's h scale; the state is rhp * sHp, exact (no f64 state kept)
     const float thHlo = thHf * (1.0f - 4.0f * 5.9604645e-8f);
     const double bd = active ? p.b_delta[i] : 0.0;
-    const StepShared* wsteps = steps + (static_cast<size_t>(blockIdx.z) * p.S + s) * T;
+    const StepShared* wsteps = steps + (static_cast<size_t>(dir) * p.S + s) * T;
     if (lane == 0) {
         ptx::mbar_init(&sh.bar[0], 1);
         ptx::mbar_init(&sh.bar[1], 1);
@@ -1029,6 +1140,18 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
         }
         if constexpr (kDefer) emit(nt - 1, fl_prev);
     }
+    if constexpr (MT) {
+        // the last of the directions to finish this (sample, group) quantizes its merged output
+        const size_t ci = static_cast<size_t>(s) * (gridDim.x / P.n) + grp;
+        __threadfence();  // this warp's o stores are visible before its arrival
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(P.merge_cnt + ci, 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev != P.n - 1) return;
+        if (lane == 0) P.merge_cnt[ci] = 0;  // ready for the next launch
+        __threadfence();
+        merge_tail(P.merge, s, grp, lane);
+    }
 }
 
 // Shapes measured at Vim-B batch 256 (ms per launch, both directions): one warp
@@ -1037,13 +1160,13 @@ __global__ void __launch_bounds__(32, MINB) k3_scan_c1(const ScanDirs P, const S
 // spills and runs 3.01; per-lane cp.async staging instead of bulk rows 2.306.
 constexpr int kC1Chunk = 4, kC1MinBlocks = 12;
 
-template <bool EXACT, int ABITS, bool TRACE, bool FS, int MB = kC1MinBlocks, bool SMA2 = false>
+template <bool EXACT, int ABITS, bool TRACE, bool FS, int MB = kC1MinBlocks, bool SMA2 = false, bool MT = false>
 static cudaError_t launch_c1(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
-    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, MB, FS, SMA2>;
+    constexpr auto kern = k3_scan_c1<EXACT, ABITS, TRACE, kC1Chunk, MB, FS, SMA2, MT>;
     const int smem = static_cast<int>(sizeof(C1Smem<kC1Chunk>));
     cudaError_t e = ensure_smem_attr<kern>(smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((P.d[0].E + 31) / 32, P.d[0].S, ndirs);
+    dim3 grid(((P.d[0].E + 31) / 32) * ndirs, P.d[0].S, 1);
     kern<<<grid, 32, smem, st>>>(P, steps);
     ++kernel_launch_counter();
     return cudaGetLastError();
@@ -1071,7 +1194,12 @@ static cudaError_t launch_c1_any(const ScanDirs& P, int ndirs, const StepShared*
     // kernel fits 128 registers, 16 warps per SM (Vim-B batch 256: 1.705 vs 1.741 ms); small
     // grids keep 168 registers (Vim-S batch 64: 0.286 vs 0.296)
     const long ctas = static_cast<long>((P.d[0].E + 31) / 32) * P.d[0].S * ndirs;
-    if (FS && ctas >= 2L * 148 * 16) return launch_c1<false, ABITS, false, FS, 13, true>(P, ndirs, steps, st);
+    const bool big = ctas >= 2L * 148 * 16;
+    if (FS && P.merge_cnt) {
+        if (big) return launch_c1<false, ABITS, false, FS, 13, true, true>(P, ndirs, steps, st);
+        return launch_c1<false, ABITS, false, FS, kC1MinBlocks, false, true>(P, ndirs, steps, st);
+    }
+    if (FS && big) return launch_c1<false, ABITS, false, FS, 13, true>(P, ndirs, steps, st);
     return launch_c1<false, ABITS, false, FS>(P, ndirs, steps, st);
 }
 
@@ -1089,9 +1217,11 @@ size_t scan_fast_workspace_bytes(int S, int T, int ndirs) {
 }
 
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
-                             int variant) {
+                             int variant, const K1Params* merge, int* merge_cnt, bool* merged) {
+    if (merged) *merged = false;
     if (ndirs < 1 || ndirs > 2) return cudaErrorInvalidValue;
     ScanDirs P;
+    P.n = ndirs;
     for (int k = 0; k < ndirs; ++k) {
         P.d[k] = dirs[k];
         if (dirs[k].N != 16 || dirs[k].E != dirs[0].E || dirs[k].S != dirs[0].S || dirs[k].T != dirs[0].T)
@@ -1122,6 +1252,15 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
         kernel = variant == 3 ? 0 : 2;
     }
     const bool exact = variant == 1;
+    // the out_proj input K1 rides on the f32-state kernel's tail (plain, non-trace launches;
+    // the caller zeroes ocnt and keeps merge_cnt zero between launches)
+    if (merge && merge_cnt && kernel == 2 && !exact && !trace && merge->mode != MODE_FP && merge->src == K1_SRC_MERGE &&
+        !merge->force_literal && !merge->scanned && merge->E == dirs[0].E && merge->T == T && merge->S == S &&
+        (merge->E % 32) == 0 && (!merge->codes4 || merge->abits == 4)) {
+        P.merge = *merge;
+        P.merge_cnt = merge_cnt;
+        if (merged) *merged = true;
+    }
     switch (dirs[0].abits) {
         case 4: return launch_kernel<4>(P, ndirs, steps, st, kernel, exact, trace);
         default: return launch_kernel<8>(P, ndirs, steps, st, kernel, exact, trace);

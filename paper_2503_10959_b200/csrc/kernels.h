@@ -182,8 +182,13 @@ cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal
 // f64 / f32 state update (even E). Non-null `masks` selects the parity-trace
 // instantiation.
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
+// merge (may be null): the out_proj input K1 (merge source), fused into the
+// one-thread-per-channel f32-state kernel when that kernel runs (*merged = true;
+// the caller has zeroed merge->ocnt; merge_cnt = [S][E/32] ints, zero between
+// launches, left zero); otherwise the caller launches it.
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
-                             int variant);
+                             int variant, const K1Params* merge = nullptr, int* merge_cnt = nullptr,
+                             bool* merged = nullptr);
 
 // K4 auxiliaries.
 cudaError_t launch_patch_gather(const double* img, double* patches, int S, int image, int channels, int patch,

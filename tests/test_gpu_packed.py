@@ -151,3 +151,31 @@ def test_trace_packed_codes(oracle_checker, gpu_ctx):
         for k in ("acc_in", "acc_out"):
             assert np.array_equal(tp.get(p + k, np.int32), ti.get(p + k, np.int32)), (site, k)
     assert np.array_equal(tp.get("logits", np.float64), ti.get("logits", np.float64))
+
+
+@pytest.mark.parametrize("pack", [0, 1])
+def test_merge_fused_into_scan_identical(oracle_checker, gpu_ctx, pack):
+    """The out_proj input K1 fused into the f32-state scan's tail (merge_fuse 1)
+    == the separate k1_channel launch == the oracle, int8 and packed operands."""
+    import paper_2503_10959_b200 as ob
+    from oracle import oracle as O
+    dims = dict(image=32, channels=3, patch=8, embed=128, state=16, blocks=2, classes=10, conv_width=4)
+    od = O.Dims(**dims)
+    om = oracle_checker.model(od, 8)
+    gm = ob.Model(gpu_ctx, ob.Dims(**dims), 8)
+    imgs = oracle_checker.normal(81, 5 * od.pix).reshape(5, 32, 32, 3)
+    spec = O.Spec(wbits=4, abits=4, obits=8, n_refresh=3, rho=0.05)
+    ocal = om.calibrate(oracle_checker.normal(82, 3 * od.pix).reshape(3, 32, 32, 3), spec).export()
+    conv = lambda t: ob.TensorCal(t.theta, t.s_in, t.s_full, t.excluded)
+    gcal = gm.calibration_from([conv(t) for t in ocal.scan], [conv(t) for t in ocal.lin],
+                               ob.QuantSpec(4, 4, 8, 3, 0.05, True, True))
+    gm.set_option("pack_a4", pack)
+    for mode in (ob.MODE_DYNAMIC, ob.MODE_STATIC):
+        outs = []
+        for f in (1, 0):
+            gm.set_option("merge_fuse", f)
+            outs.append(gm.forward_host(imgs, gcal, mode))
+        gm.set_option("merge_fuse", 0)
+        assert np.array_equal(outs[0], outs[1]), mode
+        assert np.array_equal(outs[0], om.forward(imgs, om.calib_from(ocal), mode)), mode
+    gm.set_option("pack_a4", 0)
