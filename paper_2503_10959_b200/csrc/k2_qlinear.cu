@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
 #pragma unroll
                     for (int o = 0; o < kHoist; ++o)
                         if (o < cnt && !(o == 0 && pre0)) outlier_term(hch[o], hxo[o], hosc[o]);
-                } else {  // more than kHoist: mask word by word, bit by bit
+                } else if (EW >= 16) {  // more than kHoist (16-warp shape: its register budget): word by word
                     int word = -1;
                     unsigned bits = 0;
                     for (int o = 0; o < cnt; ++o) {
@@ -418,6 +418,54 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
                         bits &= bits - 1;
                         const size_t oi = static_cast<size_t>(row) * p.K + ch;
                         outlier_term(ch, p.a.ocode[oi], p.a.oscale[oi]);
+                    }
+                } else {  // more than kHoist: the mask walked 4 words per load (J % 4 == 0), the next
+                          // outlier's code, scale and weights in flight while this one's terms run
+                    const uint32_t* mrow = msk + lane * p.a.J;
+                    const bool vec = (p.a.J & 3) == 0;
+                    int word = 0, gi = 4, wbase = 0;
+                    uint4 grp = make_uint4(0u, 0u, 0u, 0u);
+                    unsigned bits = 0;
+                    auto next_ch = [&]() {
+                        while (bits == 0) {
+                            if (vec) {
+                                if (gi == 4) {
+                                    grp = *reinterpret_cast<const uint4*>(mrow + word);
+                                    word += 4;
+                                    gi = 0;
+                                }
+                                bits = gi == 0 ? grp.x : (gi == 1 ? grp.y : (gi == 2 ? grp.z : grp.w));
+                                wbase = (word - 4 + gi) * 32;
+                                ++gi;
+                            } else {
+                                bits = mrow[word];
+                                wbase = word * 32;
+                                ++word;
+                            }
+                        }
+                        const int ch = wbase + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        return ch;
+                    };
+                    int xo = 0;
+                    double osc = 0.0;
+                    int4 wa = make_int4(0, 0, 0, 0), wb = make_int4(0, 0, 0, 0);
+                    auto fetch = [&]() {
+                        const int ch = next_ch();
+                        const size_t oi = static_cast<size_t>(row) * p.K + ch;
+                        xo = p.a.ocode[oi];
+                        osc = p.a.oscale[oi];
+                        const int4* wp = reinterpret_cast<const int4*>(p.wt + static_cast<size_t>(ch) * p.R + r0);
+                        wa = __ldg(wp);
+                        wb = __ldg(wp + 1);
+                    };
+                    if (cnt > 0) fetch();
+                    for (int o = 0; o < cnt; ++o) {
+                        const int xo_c = xo;
+                        const double osc_c = osc;
+                        const int4 wa_c = wa, wb_c = wb;
+                        if (o + 1 < cnt) fetch();
+                        outlier_term_w(xo_c, osc_c, wa_c, wb_c);
                     }
                 }
                 if (PLANES && rv) {  // the reference's integer planes (parity path)

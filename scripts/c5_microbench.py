@@ -12,7 +12,11 @@ each. Bound time = max(ops / int8 peak, bytes / HBM peak, 3 M N |O| / FP64
 lane-op peak), all three measured on the device. Prints one JSON line per shape
 and a summary table; `frac` = bound time / measured time.
 
-usage: c5_microbench.py [out.json]
+With PACKED=1 the activation operand is the nibble-packed A4 form (K1's codes4,
+pack_int4's layout) through ouro_b200_quant_linear_packed, and the byte model
+counts M K / 2 for it.
+
+usage: [PACKED=1] c5_microbench.py [out.json]
 """
 import json
 import os
@@ -32,6 +36,14 @@ with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 print(f"# measured int8 tensor peak {i8_peak:.0f} TOP/s, FP64 {f64_lane:.1f} T lane-ops/s, "
       f"HBM copy peak {hbm:.0f} GB/s", flush=True)
 g = torch.Generator(device="cuda").manual_seed(0)
+packed = os.environ.get("PACKED", "0") == "1"
+
+
+def pack_int4(c):  # pack_int4's layout (gemm.cpp:60-73): low nibble = even column
+    u = (c.to(torch.int16) & 0xF).to(torch.uint8)
+    return (u[:, 0::2] | (u[:, 1::2] << 4)).contiguous()
+
+
 rows = []
 for M in (4096, 16384, 65536):
     for K in (192, 384, 768, 1536, 3072):
@@ -49,7 +61,8 @@ for M in (4096, 16384, 65536):
                 words = np.zeros((K + 31) // 32, np.uint32)
                 for ch in chans:
                     words[ch // 32] |= np.uint32(1) << np.uint32(ch % 32)
-                act = dict(codes=codes, s_row=torch.full((M,), 0.01, dtype=torch.float64, device="cuda"),
+                cf = dict(codes4=pack_int4(codes)) if packed else dict(codes=codes)
+                act = dict(**cf, s_row=torch.full((M,), 0.01, dtype=torch.float64, device="cuda"),
                            ocnt=torch.full((M,), n_o, dtype=torch.int32, device="cuda"),
                            omask=torch.from_numpy(np.tile(words.view(np.int32), (M, 1))).cuda(),
                            ocode=ocode, oscale=oscale)
@@ -65,13 +78,13 @@ for M in (4096, 16384, 65536):
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) / n * 1e3
                 ops = 2.0 * M * N * (K + n_o)
-                byts = M * K + N * K + 8.0 * M * N + 9.0 * M * n_o
+                byts = M * K * (0.5 if packed else 1.0) + N * K + 8.0 * M * N + 9.0 * M * n_o
                 tops = ops / us / 1e6
                 gbs = byts / us / 1e3
                 t_b = {"tensor": ops / i8_peak / 1e6, "hbm": byts / hbm / 1e3,
                        "fp64": 3.0 * M * N * n_o / f64_lane / 1e6}  # us
                 bound = max(t_b, key=t_b.get)
-                r = dict(M=M, K=K, N=N, f=f, n_outlier_channels=n_o, us=us, tops=tops, gbs=gbs, bound=bound,
+                r = dict(M=M, K=K, N=N, f=f, packed=packed, n_outlier_channels=n_o, us=us, tops=tops, gbs=gbs, bound=bound,
                          frac=t_b[bound] / us)
                 rows.append(r)
                 print(json.dumps(r), flush=True)
