@@ -215,8 +215,9 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
 /* Engine options: "scan_variant" = 0 auto (fast K3 path wherever the
  * channel-local detector is exact), 1 per-direction reference scan kernel,
  * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid),
- * 3 / 4 / 5 fast path on the two-threads-per-channel kernel / one thread per
- * channel with the f64 state update / with the f32 state update (A/B aid);
+ * 3 / 4 / 5 / 6 fast path on two threads per channel (f32 state) / one thread
+ * per channel (f64 state) / one thread per channel (f32 state) / two threads per
+ * channel (f64 state) (A/B aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
  * detector kernel everywhere; "pack_a4" = 1: A4 activation codes travel
  * nibble-packed from K1 to K2, 0 (default) one int8 byte per code; "merge_fuse" = 1:

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
     }
 }
 
-template <bool EXACT, int ABITS, bool TRACE>
+template <bool EXACT, int ABITS, bool TRACE, bool FS = false>
 __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const StepShared* __restrict__ steps) {
     extern __shared__ __align__(16) uint8_t scan_smem_raw[];
     const int warp = threadIdx.x >> 5;
@@ -227,6 +227,13 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
     unsigned fl = 0;  // channel in O: bit 0 a_bar, bit 1 b_bar, bit 2 h
     const double thA = p.cal[0].theta, thB = p.cal[1].theta, thH = p.cal[2].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB), thHf = __double2float_rn(thH);
+    // FS (k3_scan_c1's f32 state update, 8 states per thread): previous h codes and scale
+    float2 rhp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rhp[k] = make_float2(0.0f, 0.0f);
+    float sHf_prev = 0.0f, qHp = 0.0f;
+    double sHp = 0.0;
+    const float thHlo = thHf * (1.0f - 4.0f * 5.9604645e-8f);
     // chunk staging: lane -> (step, channel) = (lane >> 4 + 2k, lane & 15)
     const int sc = lane & 15, sic = cw + sc;
     const double bd = sic < E ? p.b_delta[sic] : 0.0;
@@ -285,7 +292,12 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
             const StepShared& se = sh.st[cur][te];
             double pr[8];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) pr[m] = dmul(se.C[m0 + m], h[m]);
+            for (int m = 0; m < 8; ++m) {
+                if constexpr (FS)  // the state is code * scale (fake_quant_step's dequantized value)
+                    pr[m] = dmul(se.C[m0 + m], dmul(static_cast<double>((m & 1) ? rhp[m >> 1].y : rhp[m >> 1].x), sHp));
+                else
+                    pr[m] = dmul(se.C[m0 + m], h[m]);
+            }
             double o = 0.0;
 #pragma unroll
             for (int m = 0; m < 8; ++m) o = dadd(o, pr[m]);
@@ -381,6 +393,7 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
             // per packed f32x2 instruction; codes are kept as magic bit patterns.
             unsigned ca[8];  // a_bar codes (>= 0) as integers, b_bar codes as exact f32 integers
             float cb[8];
+            float raf[8];  // FS: a_bar codes as exact f32 integers
             bool redo = EXACT || sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
             const float2* BS2 = reinterpret_cast<const float2*>(ss.BSf + m0);
             auto pass1 = [&](auto clamp) {
@@ -399,8 +412,13 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                     const float2 ta = __fadd2_rn(qa2, f2(12582912.0f));
                     const float2 ra = __fadd2_rn(ta, f2(-12582912.0f));
                     const float2 da = __fadd2_rn(qa2, make_float2(-ra.x, -ra.y));
-                    ca[2 * k] = __float_as_uint(ta.x) - kMagicBits;
-                    ca[2 * k + 1] = __float_as_uint(ta.y) - kMagicBits;
+                    if constexpr (FS) {
+                        raf[2 * k] = ra.x;
+                        raf[2 * k + 1] = ra.y;
+                    } else {
+                        ca[2 * k] = __float_as_uint(ta.x) - kMagicBits;
+                        ca[2 * k + 1] = __float_as_uint(ta.y) - kMagicBits;
+                    }
                     float2 qb2 = __fmul2_rn(f2(dfb), BS2[k]);
                     if constexpr (CL) {
                         qb2.x = fminf(fmaxf(qb2.x, -capB), capB);
@@ -428,72 +446,48 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                 for (int m = 0; m < 8; ++m) {
                     const float a2 = (m & 1) ? A2f[m >> 1].y : A2f[m >> 1].x;
                     const float qa_f = fminf(ex2_approx(df * a2) * invA, capA);
-                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA)
-                        ca[m] = static_cast<unsigned>(static_cast<int>(
-                            qdiv_call(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf))));
+                    if (EXACT || sA < 1e-30 || fabsf(qa_f - rintf(qa_f)) > halfA) {
+                        const double cq = qdiv_call(exp_call(dmul(delta, arow[m0 + m])), sA, static_cast<double>(qAf));
+                        ca[m] = static_cast<unsigned>(static_cast<int>(cq));
+                        raf[m] = static_cast<float>(cq);
+                    }
                     const float qb_f = fminf(fmaxf(dfb * ss.BSf[m0 + m], -capB), capB);
                     if (EXACT || fabsf(qb_f - rintf(qb_f)) > halfB)
                         cb[m] = static_cast<float>(
                             qdiv_call(dmul(delta, ss.B[m0 + m]), sB, static_cast<double>(qBf)));
                 }
             }
-            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update.
-            // a_bar codes are >= 0: fma(2^52 + c, sA, -2^52 sA) = c sA before its one rounding,
-            // i.e. exactly dmul(c, sA).
-            const double nKA = dmul(sA, -4503599627370496.0);
+            if constexpr (FS) {
+                // f32 state update with its bound (k3_scan_c1<FS>'s header comment), 8 states per
+                // thread; the pair shares the channel's peak, detector decision and exact path
+                const float sAf = (fl & 1u) ? __double2float_rn(sA) : ss.Saf;
+                const float sBf = (fl & 2u) ? __double2float_rn(sB) : ss.Sbf;
+                const float sAsH = sAf * sHf_prev, sBu = sBf * __double2float_rn(uv);
+                float2 hf2[4];
+                float phf = 0.0f;
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
-                const double b_q = dmul(static_cast<double>(cb[m]), sB);
-                h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
-            }
-            // h detection + codes. Rounding to f32 is monotone, so the f32 peak
-            // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
-            // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
-            // needs the exact f64 peak. Outlier channels take the exact peak for their scale.
-            float2 hfv[4];
-            float phf = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
-                phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
-            }
-            phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
-            double sH = ss.Sh, qH = qa;
-            float invHf = ss.invShf;
-            if (dyn && ((fl & 4u) | (phf >= thHf))) {
-                if (!(fl & 4u)) {
-                    if (phf > thHf) {
-                        fl |= 4u;
-                    } else {  // phf == fl32(theta): the exact peak decides
-                        double ph = 0.0;
-#pragma unroll
-                        for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
-                        ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
-                        if (ph > thH) fl |= 4u;
-                    }
+                for (int k = 0; k < 4; ++k) {
+                    const float2 p1 = __fmul2_rn(__fmul2_rn(make_float2(raf[2 * k], raf[2 * k + 1]), rhp[k]), f2(sAsH));
+                    const float2 p2 = __fmul2_rn(make_float2(cb[2 * k], cb[2 * k + 1]), f2(sBu));
+                    const float2 hv = __fadd2_rn(p1, p2);
+                    phf = fmaxf(phf, fmaxf(fabsf(hv.x), fabsf(hv.y)));
+                    hf2[k] = hv;
                 }
-                if (fl & 4u) {
-                    double ph = 0.0;
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
-                    ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
-                    sH = scale_call(ph, qo);
-                    invHf = __double2float_rn(recip_call(sH));
-                    qH = qo;
-                }
-            }
-            {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
-                const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
-                const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
-                float chd[8];  // h codes as exact f32 integers (F2F.F64 balances the XU and FP64 pipes)
-                bool hredo = EXACT;
+                phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
+                const float maxD = fmaf(fmaf(qAf * qHp, sAsH, qBf * fabsf(sBu)), 5.3f * 5.9604645e-8f, 1e-37f);
+                double sH = ss.Sh, qH = qa;
+                float invHf = ss.invShf;
+                bool hexact = EXACT || !(maxD < 1e30f);
+                if (dyn) hexact |= (fl & 4u) || !(fmaf(maxD, 1.0000003f, phf) < thHlo);
+                const float capH = qaf + 0.25f;
+                const float halfH = 0.5f - fmaf(maxD, invHf * 1.0001f, fmaf(qaf + 1.0f, 1.25e-7f, 1e-6f));
+                float chd[8];
+                float mdh = 0.0f;
                 auto hcodes = [&](auto clamp) {
                     constexpr bool CL = decltype(clamp)::value;
-                    float mdh = 0.0f;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                        float2 q = __fmul2_rn(hf2[k], f2(invHf));
                         if constexpr (CL) {
                             q.x = fminf(fmaxf(q.x, -capH), capH);
                             q.y = fminf(fmaxf(q.y, -capH), capH);
@@ -505,21 +499,131 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
                         chd[2 * k + 1] = rh.y;
                         mdh = fmaxf(mdh, fmaxf(fabsf(dh.x), fabsf(dh.y)));
                     }
-                    hredo |= mdh > halfH;
                 };
-                if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});  // |q| <= phf*invHf
+                if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});
                 else hcodes(std::true_type{});
-                if (hredo) {
+                hexact |= !(mdh <= halfH);
+                hexact |= __shfl_xor_sync(0xffffffffu, hexact ? 1 : 0, 1) != 0;  // the pair decides together
+                if (hexact) {  // the exact f64 update (ssm.cpp:165-167) and the f64-state h logic on it
+                    double hn[8];
 #pragma unroll
                     for (int m = 0; m < 8; ++m) {
-                        const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
-                        const float q = fminf(fmaxf(hv * invHf, -capH), capH);
-                        if (EXACT || fabsf(q - rintf(q)) > halfH)
-                            chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
+                        const double a_q = dmul(static_cast<double>(raf[m]), sA);
+                        const double b_q = dmul(static_cast<double>(cb[m]), sB);
+                        const double hp = dmul(static_cast<double>((m & 1) ? rhp[m >> 1].y : rhp[m >> 1].x), sHp);
+                        hn[m] = dadd(dmul(a_q, hp), dmul(b_q, uv));
+                    }
+                    if (dyn) {
+                        double ph = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(hn[m]));
+                        ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                        if (ph > thH) fl |= 4u;
+                        if (fl & 4u) {
+                            sH = scale_call(ph, qo);
+                            invHf = __double2float_rn(recip_call(sH));
+                            qH = qo;
+                        }
+                    }
+                    const float qHf = static_cast<float>(qH), capHx = qHf + 0.25f;
+                    const float halfHx = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {  // |dq| <= |q| 4 2^-24 from the exact value
+                        const float q = fminf(fmaxf(__double2float_rn(hn[m]) * invHf, -capHx), capHx);
+                        const float r = rintf(q);
+                        chd[m] = (EXACT || !(fabsf(q - r) <= halfHx)) ? static_cast<float>(qdiv_call(hn[m], sH, qH)) : r;
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 8; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
+                for (int k = 0; k < 4; ++k) rhp[k] = make_float2(chd[2 * k], chd[2 * k + 1]);  // carried state
+                sHp = sH;
+                sHf_prev = (fl & 4u) ? __double2float_rn(sH) : ss.Shf;
+                qHp = static_cast<float>(qH);
+            } else {
+            // pass 2: dequantized values (code * s, fake_quant_step) and the exact f64 update.
+                // a_bar codes are >= 0: fma(2^52 + c, sA, -2^52 sA) = c sA before its one rounding,
+                // i.e. exactly dmul(c, sA).
+                const double nKA = dmul(sA, -4503599627370496.0);
+    #pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const double a_q = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(ca[m])), sA, nKA);
+                    const double b_q = dmul(static_cast<double>(cb[m]), sB);
+                    h[m] = dadd(dmul(a_q, h[m]), dmul(b_q, uv));  // ssm.cpp:165-167
+                }
+                // h detection + codes. Rounding to f32 is monotone, so the f32 peak
+                // max_m fl32|h_m| equals fl32(max_m |h_m|): phf > fl32(theta) implies
+                // peak > theta, phf < fl32(theta) implies peak <= theta; only equality
+                // needs the exact f64 peak. Outlier channels take the exact peak for their scale.
+                float2 hfv[4];
+                float phf = 0.0f;
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    hfv[k] = make_float2(__double2float_rn(h[2 * k]), __double2float_rn(h[2 * k + 1]));
+                    phf = fmaxf(phf, fmaxf(fabsf(hfv[k].x), fabsf(hfv[k].y)));
+                }
+                phf = fmaxf(phf, __shfl_xor_sync(0xffffffffu, phf, 1));
+                double sH = ss.Sh, qH = qa;
+                float invHf = ss.invShf;
+                if (dyn && ((fl & 4u) | (phf >= thHf))) {
+                    if (!(fl & 4u)) {
+                        if (phf > thHf) {
+                            fl |= 4u;
+                        } else {  // phf == fl32(theta): the exact peak decides
+                            double ph = 0.0;
+    #pragma unroll
+                            for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                            ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                            if (ph > thH) fl |= 4u;
+                        }
+                    }
+                    if (fl & 4u) {
+                        double ph = 0.0;
+    #pragma unroll
+                        for (int m = 0; m < 8; ++m) ph = fmax(ph, fabs(h[m]));
+                        ph = fmax(ph, __shfl_xor_sync(pair, ph, 1));
+                        sH = scale_call(ph, qo);
+                        invHf = __double2float_rn(recip_call(sH));
+                        qH = qo;
+                    }
+                }
+                {  // |dq| <= |q| 4 2^-24 (h and 1/s rounded to f32, one product)
+                    const float qHf = static_cast<float>(qH), capH = qHf + 0.25f;
+                    const float halfH = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+                    float chd[8];  // h codes as exact f32 integers (F2F.F64 balances the XU and FP64 pipes)
+                    bool hredo = EXACT;
+                    auto hcodes = [&](auto clamp) {
+                        constexpr bool CL = decltype(clamp)::value;
+                        float mdh = 0.0f;
+    #pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            float2 q = __fmul2_rn(hfv[k], f2(invHf));
+                            if constexpr (CL) {
+                                q.x = fminf(fmaxf(q.x, -capH), capH);
+                                q.y = fminf(fmaxf(q.y, -capH), capH);
+                            }
+                            const float2 th = __fadd2_rn(q, f2(12582912.0f));
+                            const float2 rh = __fadd2_rn(th, f2(-12582912.0f));
+                            const float2 dh = __fadd2_rn(q, make_float2(-rh.x, -rh.y));
+                            chd[2 * k] = rh.x;
+                            chd[2 * k + 1] = rh.y;
+                            mdh = fmaxf(mdh, fmaxf(fabsf(dh.x), fabsf(dh.y)));
+                        }
+                        hredo |= mdh > halfH;
+                    };
+                    if (__all_sync(0xffffffffu, phf * invHf <= capH)) hcodes(std::false_type{});  // |q| <= phf*invHf
+                    else hcodes(std::true_type{});
+                    if (hredo) {
+    #pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const float hv = (m & 1) ? hfv[m >> 1].y : hfv[m >> 1].x;
+                            const float q = fminf(fmaxf(hv * invHf, -capH), capH);
+                            if (EXACT || fabsf(q - rintf(q)) > halfH)
+                                chd[m] = static_cast<float>(qdiv_call(h[m], sH, qH));
+                        }
+                    }
+    #pragma unroll
+                    for (int m = 0; m < 8; ++m) h[m] = dmul(static_cast<double>(chd[m]), sH);  // carried state
+                }
             }
             if constexpr (!kDefer) emit(tt, fl, true);
             fl_prev = fl;
@@ -1172,13 +1276,13 @@ static cudaError_t launch_c1(const ScanDirs& P, int ndirs, const StepShared* ste
     return cudaGetLastError();
 }
 
-template <bool EXACT, int ABITS, bool TRACE>
+template <bool EXACT, int ABITS, bool TRACE, bool FS = false>
 static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st) {
     const int smem = static_cast<int>(sizeof(WarpSmem)) * (kThr / 32);
-    cudaError_t e = ensure_smem_attr<k3_scan_fast<EXACT, ABITS, TRACE>>(smem);
+    cudaError_t e = ensure_smem_attr<k3_scan_fast<EXACT, ABITS, TRACE, FS>>(smem);
     if (e != cudaSuccess) return e;
     dim3 grid((P.d[0].E + kCh - 1) / kCh, P.d[0].S, ndirs);
-    k3_scan_fast<EXACT, ABITS, TRACE><<<grid, kThr, smem, st>>>(P, steps);
+    k3_scan_fast<EXACT, ABITS, TRACE, FS><<<grid, kThr, smem, st>>>(P, steps);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }
@@ -1208,6 +1312,10 @@ static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared*
                                  int kernel, bool exact, bool trace) {
     if (kernel == 0) return launch_c1_any<ABITS, false>(P, ndirs, steps, st, exact, trace);
     if (kernel == 2) return launch_c1_any<ABITS, true>(P, ndirs, steps, st, exact, trace);
+    if (kernel == 3) {  // two threads per channel, f32 state update
+        if (exact) return trace ? launch_fast<true, ABITS, true, true>(P, ndirs, steps, st) : launch_fast<true, ABITS, false, true>(P, ndirs, steps, st);
+        return trace ? launch_fast<false, ABITS, true, true>(P, ndirs, steps, st) : launch_fast<false, ABITS, false, true>(P, ndirs, steps, st);
+    }
     if (exact) return trace ? launch_fast<true, ABITS, true>(P, ndirs, steps, st) : launch_fast<true, ABITS, false>(P, ndirs, steps, st);
     return trace ? launch_fast<false, ABITS, true>(P, ndirs, steps, st) : launch_fast<false, ABITS, false>(P, ndirs, steps, st);
 }
@@ -1242,15 +1350,17 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     const bool trace = dirs[0].masks != nullptr;
     const bool even = (dirs[0].E & 1) == 0;
     // auto: one thread per channel with the f32 state update for A4 (ms per Vim-B launch at
-    // batch 256: 1.79, vs 2.23 with the f64 state update and 2.43 with two threads per
-    // channel; Vim-S batch 64: 0.297 / 0.360 / 0.415), two threads per channel for A8 (Vim-T
-    // batch 256: 1.17 vs 1.41 / 1.63)
-    int kernel = (dirs[0].abits == 4 && even) ? 2 : 1;
+    // batch 256: 1.70, vs 2.23 with the f64 state update and 2.43 with two threads per
+    // channel; Vim-S batch 64: 0.286 / 0.360 / 0.415), two threads per channel with the f32
+    // state update for A8 (Vim-T batch 256: 1.100 vs 1.154 with the f64 state, 1.41 / 1.63
+    // one thread per channel; batch 1: 7.22 vs 7.38 ms per forward's 24 scans)
+    int kernel = (dirs[0].abits == 4 && even) ? 2 : 3;
     if (variant == 2) kernel = 1;
-    if (variant >= 3) {
+    if (variant == 3 || variant == 4) {
         if (!even) return cudaErrorNotSupported;
         kernel = variant == 3 ? 0 : 2;
     }
+    if (variant == 5) kernel = 1;
     const bool exact = variant == 1;
     // the out_proj input K1 rides on the f32-state kernel's tail (plain, non-trace launches;
     // the caller zeroes ocnt and keeps merge_cnt zero between launches)

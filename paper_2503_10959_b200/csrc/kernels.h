@@ -175,12 +175,12 @@ struct ScanParams {
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal);
 // Fast path (dynamic/static, channel-local detector): both directions in one
 // launch (plus a step-table prep launch); work = scan_fast_workspace_bytes(S, T,
-// ndirs) bytes, 16-aligned. variant 0: auto (one thread per channel with the f32
-// state update for A4 and even E, two per channel otherwise); 1: the same with the
-// certified f32 codes disabled (every element exact f64); 2: the
-// two-threads-per-channel kernel; 3 / 4: the one-thread-per-channel kernel with the
-// f64 / f32 state update (even E). Non-null `masks` selects the parity-trace
-// instantiation.
+// ndirs) bytes, 16-aligned. variant 0: auto (the f32 state update on one thread
+// per channel for A4 and even E, on two per channel otherwise); 1: the same with the
+// certified f32 codes disabled (every element exact f64); 2: two threads per
+// channel, f32 state; 3 / 4: one thread per channel with the f64 / f32 state update
+// (even E); 5: two threads per channel, f64 state. Non-null `masks` selects the
+// parity-trace instantiation.
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
 // merge (may be null): the out_proj input K1 (merge source), fused into the
 // one-thread-per-channel f32-state kernel when that kernel runs (*merged = true;

@@ -14,7 +14,7 @@ cal = m.calibrate(torch.randn(8, 224, 224, 3, dtype=torch.float64, device="cuda"
 x = torch.randn(B, 224, 224, 3, dtype=torch.float64, device="cuda", generator=g)
 out = torch.empty(B, 1000, dtype=torch.float64, device="cuda")
 res = {}
-for v in (0, 3, 4, 5):
+for v in (0, 3, 4, 5, 6):
     m.set_option("scan_variant", v)
     m.use_graphs(True)
     for _ in range(3):

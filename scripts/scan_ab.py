@@ -2,8 +2,8 @@
 
     python scripts/scan_ab.py E B blocks abits [variants...]
 
-variant 0 = auto, 1 = reference kernel, 2 = exact codes, 3 = two threads per channel, 4 / 5 = one thread per
-channel with the f64 / f32 state update.
+variant 0 = auto, 1 = reference kernel, 2 = exact codes, 3 / 6 = two threads per channel with the f32 / f64
+state update, 4 / 5 = one thread per channel with the f64 / f32 state update.
 """
 import os
 import sys

@@ -214,11 +214,11 @@ def test_scan_variants_identical(pair, abits):
     spec = _spec(abits, rho=0.05)
     gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
     outs = []
-    for v in (0, 1, 2, 3, 4, 5):
+    for v in (0, 1, 2, 3, 4, 5, 6):
         gm.set_option("scan_variant", v)
         outs.append(gm.forward_host(imgs, gcal, 1))
     gm.set_option("scan_variant", 0)
-    for v in (1, 2, 3, 4, 5):
+    for v in (1, 2, 3, 4, 5, 6):
         assert np.array_equal(outs[0], outs[v]), v
 
 
