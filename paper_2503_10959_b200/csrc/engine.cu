@@ -319,7 +319,7 @@ void Model::ensure_work(Work& w, int S, bool trace) {
     w.s_row.ensure(slots * rows);
     w.ocnt.ensure(slots * rows);
     w.scanned.ensure(slots * rows);
-    w.scan_steps.ensure(scan_fast_workspace_bytes(S, static_cast<int>(L), static_cast<int>(nd)));
+    w.scan_steps.ensure(scan_fast_workspace_bytes(S, static_cast<int>(L), static_cast<int>(nd), static_cast<int>(E)));
     if (w.merge_cnt.n < static_cast<size_t>(S) * ((E + 31) / 32)) {
         w.merge_cnt.ensure(static_cast<size_t>(S) * ((E + 31) / 32));
         cuda_check(cudaMemset(w.merge_cnt.p, 0, w.merge_cnt.n * sizeof(int)), "merge counters");

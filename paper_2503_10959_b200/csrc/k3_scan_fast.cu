@@ -1320,8 +1320,417 @@ static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared*
     return trace ? launch_fast<false, ABITS, true>(P, ndirs, steps, st) : launch_fast<false, ABITS, false>(P, ndirs, steps, st);
 }
 
-size_t scan_fast_workspace_bytes(int S, int T, int ndirs) {
-    return static_cast<size_t>(ndirs) * S * T * sizeof(StepShared);
+// ---- small batches: the scan split into three phases -----------------------------
+// At batch 1 (BASELINE C1) a launch has a few warps on the whole GPU, so each step
+// costs its full instruction latency. Only the h update is sequential in t; the
+// a_bar / b_bar codes (their detector state runs per refresh window) and the output
+// sum are not. So: (A) codes for every (step, channel), one thread per (channel,
+// refresh window); (B) the f32 state update (k3_scan_c1<FS>) walking the steps with
+// the next step's codes in flight; (C) the outputs of every (step, channel) in
+// parallel. Same arithmetic as k3_scan_c1<FS>; the intermediates (73 B per
+// direction, sample, step and channel) stay in L2 at these sizes.
+// phase A's record per (direction, sample, step, channel): a_bar codes (0..q) | b_bar codes |
+// the exact scales of the step (outlier channels: their own) | outlier flags after detection
+struct __align__(16) SmallRec {
+    uint4 ca, cb;
+    double sA, sB;
+    unsigned fab;
+    unsigned pad[3];
+};
+static_assert(sizeof(SmallRec) == 64, "four 16-byte copies per record");
+struct SmallWork {
+    SmallRec* rec;  // [dir][s][t][E]
+    int8_t* rh;     // [dir][s][t][E][16] h codes
+    double* sh;     // [dir][s][t][E] h scale
+};
+constexpr size_t kSmallPerElem = sizeof(SmallRec) + 16 + 8;
+constexpr long kSmallMaxChannels = 148L * 32;  // below one warp per SM: the split path
+
+static bool small_path(int S, int E, int ndirs) {
+    return static_cast<long>(S) * E * ndirs <= kSmallMaxChannels && (E % 32) == 0;
+}
+
+static SmallWork small_work(void* base, int S, int T, int E, int ndirs) {
+    const size_t n = static_cast<size_t>(ndirs) * S * T * E;
+    uint8_t* q = static_cast<uint8_t*>(base);
+    SmallWork w;
+    w.rec = reinterpret_cast<SmallRec*>(q);
+    q += n * sizeof(SmallRec);
+    w.rh = reinterpret_cast<int8_t*>(q);
+    q += n * 16;
+    w.sh = reinterpret_cast<double*>(q);
+    return w;
+}
+
+// (A) one thread per (direction, sample, channel, refresh window): k3_scan_c1's detector
+// and certified code pass per step (outlier channels take their exact scales)
+constexpr int kSA = 16;  // steps staged per pass of phase A
+struct SmallASmem {
+    StepShared st[kSA];
+    double dp[kSA][32];
+    uint64_t bar;
+};
+
+template <int ABITS>
+__global__ void __launch_bounds__(32) k3s_codes(const ScanDirs P, const StepShared* __restrict__ steps, SmallWork w,
+                                                int win) {
+    extern __shared__ __align__(16) uint8_t sa_smem_raw[];
+    SmallASmem& sm = *reinterpret_cast<SmallASmem*>(sa_smem_raw);
+    const int ndirs = P.n, groups = P.d[0].E / 32;
+    const int dir = static_cast<int>(blockIdx.x) % ndirs, grp = static_cast<int>(blockIdx.x) / ndirs;
+    const ScanParams& p = P.d[dir];
+    const unsigned lane = threadIdx.x;
+    const int E = p.E, T = p.T, P2 = E + 32, i = grp * 32 + static_cast<int>(lane);
+    const int nwin = (T + win - 1) / win, s = static_cast<int>(blockIdx.y) / nwin;
+    const int t0 = (static_cast<int>(blockIdx.y) % nwin) * win, t1 = min(T, t0 + win);
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;
+    constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
+    const double* __restrict__ arow = p.a + static_cast<size_t>(i) * 16;
+    float A2[16];
+    double Amax = -1e300;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        A2[m] = __double2float_rn(arow[m] * 1.4426950408889634);
+        Amax = fmax(Amax, arow[m]);
+    }
+    const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
+    const double thA = p.cal[0].theta, thB = p.cal[1].theta;
+    const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB);
+    const double bd = p.b_delta[i];
+    const size_t rowbase = static_cast<size_t>(dir) * p.S * T + static_cast<size_t>(s) * T;
+    if (lane == 0) {
+        ptx::mbar_init(&sm.bar, 1);
+        ptx::fence_barrier_init();
+    }
+    __syncwarp();
+    unsigned fl = 0;
+    for (int tb = t0, pass = 0; tb < t1; tb += kSA, ++pass) {  // the pass's step records and delta inputs, staged
+        const int nt = min(kSA, t1 - tb);
+        __syncwarp();
+        for (int tt = 0; tt < nt; ++tt)
+            cp_async8(&sm.dp[tt][lane], p.proj + (static_cast<size_t>(s) * T + tb + tt) * P2 + i, true);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (lane == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
+            ptx::mbar_arrive_expect_tx(&sm.bar, bytes);
+            ptx::bulk_g2s(&sm.st[0], steps + rowbase + tb, bytes, &sm.bar);
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        ptx::mbar_wait(&sm.bar, pass & 1);
+    for (int t = tb; t < tb + nt; ++t) {
+        const StepShared& ss = sm.st[t - tb];
+        const double x = dadd(sm.dp[t - tb][lane], bd);  // ssm.cpp:150-151
+        float ed;
+        const float df = softplus_f32(__double2float_rn(x), ed);
+        bool have = false;
+        double delta, pa, pb;
+        auto exact = [&]() {
+            if (!have) {
+                delta = softplus_call(x);
+                pa = exp_call(dmul(delta, Amax));
+                pb = dmul(delta, ss.Bmax);
+                have = true;
+            }
+        };
+        double sA = ss.Sa, sB = ss.Sb;
+        float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
+        float halfA = fmaf(-ss.hA1, ed, ss.hA0);
+        float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
+        if (dyn) {
+            fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh
+            const float x2m = df * Amax2f;
+            const float paf = ex2_approx(x2m);
+            const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
+            const float pbf = df * ss.Bmaxf;
+            const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
+            if (!(fl & 1u)) {
+                if (paf > thAf * (1.0f + ea)) {
+                    fl |= 1u;
+                } else if (paf >= thAf * (1.0f - ea)) {
+                    exact();
+                    if (pa > thA) fl |= 1u;
+                }
+            }
+            if (!(fl & 2u)) {
+                if (pbf > thBf * (1.0f + eb)) {
+                    fl |= 2u;
+                } else if (pbf >= thBf * (1.0f - eb)) {
+                    exact();
+                    if (pb > thB) fl |= 2u;
+                }
+            }
+            if (fl & 3u) {
+                exact();
+                if (fl & 1u) {
+                    sA = scale_call(pa, qo);
+                    invA = __double2float_rn(recip_call(sA));
+                    qAf = qof;
+                    const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                    halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+                }
+                if (fl & 2u) {
+                    sB = scale_call(pb, qo);
+                    kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
+                    qBf = qof;
+                    halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                }
+            }
+        }
+        const float dfb = df * kB;
+        const float capA = qAf + 0.25f, capB = qBf + 0.25f;
+        int cq[32];
+        const bool tiny = sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {  // clamped quotients (k3_scan_c1's clamp form), exact where uncertified
+            const float qaq = fminf(ex2_approx(df * A2[m]) * invA, capA);
+            const float ra = rintf(qaq);
+            if (tiny || !(fabsf(qaq - ra) <= halfA)) {
+                exact();
+                cq[m] = static_cast<int>(qdiv_call(exp_call(dmul(delta, arow[m])), sA, static_cast<double>(qAf)));
+            } else {
+                cq[m] = static_cast<int>(ra);
+            }
+            const float qbq = fminf(fmaxf(dfb * ss.BSf[m], -capB), capB);
+            const float rb = rintf(qbq);
+            if (!(fabsf(qbq - rb) <= halfB)) {
+                exact();
+                cq[16 + m] = static_cast<int>(qdiv_call(dmul(delta, ss.B[m]), sB, static_cast<double>(qBf)));
+            } else {
+                cq[16 + m] = static_cast<int>(rb);
+            }
+        }
+        const size_t e = (rowbase + t) * E + i;
+        uint4 cv[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            uint32_t* vw = reinterpret_cast<uint32_t*>(&cv[k]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                vw[j] = (static_cast<uint32_t>(cq[16 * k + 4 * j] & 0xFF)) | (static_cast<uint32_t>(cq[16 * k + 4 * j + 1] & 0xFF) << 8) |
+                        (static_cast<uint32_t>(cq[16 * k + 4 * j + 2] & 0xFF) << 16) |
+                        (static_cast<uint32_t>(cq[16 * k + 4 * j + 3] & 0xFF) << 24);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(w.rec + e);
+        dst[0] = cv[0];
+        dst[1] = cv[1];
+        dst[2] = make_uint4(__double2loint(sA), __double2hiint(sA), __double2loint(sB), __double2hiint(sB));
+        dst[3] = make_uint4(fl, 0u, 0u, 0u);
+    }
+    }
+}
+
+__device__ __forceinline__ void unpack_codes16(uint4 v, float (&c)[16]) {
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int m = 0; m < 16; ++m) c[m] = static_cast<float>(static_cast<int8_t>(wd[m >> 2] >> (8 * (m & 3))));
+}
+
+// (B) one thread per (direction, sample, channel): k3_scan_c1<FS>'s h update over the
+// steps; chunks of kSB steps (phase A's records, the scan input, the step records) are
+// staged in shared memory by cp.async / a bulk copy one chunk ahead
+constexpr int kSB = 8;
+struct SmallBSmem {
+    SmallRec rec[2][kSB][32];
+    double u[2][kSB][32];
+    StepShared st[2][kSB];
+    uint64_t bar[2];
+};
+
+template <int ABITS>
+__global__ void __launch_bounds__(32) k3s_state(const ScanDirs P, const StepShared* __restrict__ steps, SmallWork w) {
+    extern __shared__ __align__(16) uint8_t sb_smem_raw[];
+    SmallBSmem& sh = *reinterpret_cast<SmallBSmem*>(sb_smem_raw);
+    const int ndirs = P.n;
+    const int dir = static_cast<int>(blockIdx.x) % ndirs, grp = static_cast<int>(blockIdx.x) / ndirs;
+    const ScanParams& p = P.d[dir];
+    const unsigned lane = threadIdx.x;
+    const int E = p.E, T = p.T, i = grp * 32 + static_cast<int>(lane), s = static_cast<int>(blockIdx.y);
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;
+    constexpr float qaf = static_cast<float>(qa);
+    const double thH = p.cal[2].theta;
+    const float thHlo = __double2float_rn(thH) * (1.0f - 4.0f * 5.9604645e-8f);
+    const size_t rowbase = static_cast<size_t>(dir) * p.S * T + static_cast<size_t>(s) * T;
+    if (lane == 0) {
+        ptx::mbar_init(&sh.bar[0], 1);
+        ptx::mbar_init(&sh.bar[1], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncwarp();
+    auto issue = [&](int t0, int buf) {
+        const int nt = min(kSB, T - t0);
+#pragma unroll
+        for (int tt = 0; tt < kSB; ++tt) {
+            const int t = min(t0 + tt, T - 1);
+            const uint4* src = reinterpret_cast<const uint4*>(w.rec + (rowbase + t) * E + i);
+            uint4* dst = reinterpret_cast<uint4*>(&sh.rec[buf][tt][lane]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(dst + k)), "l"(src + k) : "memory");
+            cp_async8(&sh.u[buf][tt][lane], p.u + (static_cast<size_t>(s) * T + row_at(p.order, t, T, p.grid)) * E + i, true);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (lane == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
+            ptx::mbar_arrive_expect_tx(&sh.bar[buf], bytes);
+            ptx::bulk_g2s(&sh.st[buf][0], steps + rowbase + t0, bytes, &sh.bar[buf]);
+        }
+    };
+    float rhp[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) rhp[m] = 0.0f;
+    double sHp = 0.0;
+    float sHf_prev = 0.0f, qHp = 0.0f;
+    unsigned flh = 0;
+    issue(0, 0);
+    for (int t0 = 0, ci = 0; t0 < T; t0 += kSB, ++ci) {
+        const int nt = min(kSB, T - t0), cur = ci & 1;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        ptx::mbar_wait(&sh.bar[cur], (ci >> 1) & 1);
+        if (t0 + kSB < T) issue(t0 + kSB, cur ^ 1);
+        for (int tt = 0; tt < nt; ++tt) {
+            const int t = t0 + tt;
+            const StepShared& ss = sh.st[cur][tt];
+            const SmallRec& r = sh.rec[cur][tt][lane];
+            const double uv = sh.u[cur][tt][lane];
+            float raf[16], cb[16];
+            unpack_codes16(r.ca, raf);
+            unpack_codes16(r.cb, cb);
+            const double sA = r.sA, sB = r.sB;
+            const unsigned fab = r.fab;
+            const float qAf = (fab & 1u) ? 127.0f : qaf, qBf = (fab & 2u) ? 127.0f : qaf;
+            if (dyn) flh &= static_cast<unsigned>(ss.keep) & 4u;
+            const float sAf = (fab & 1u) ? __double2float_rn(sA) : ss.Saf;
+            const float sBf = (fab & 2u) ? __double2float_rn(sB) : ss.Sbf;
+            const float sAsH = sAf * sHf_prev, sBu = sBf * __double2float_rn(uv);
+            float hf[16];
+            float phf = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // packed f32x2, as k3_scan_c1<FS>
+                const float2 p1 = __fmul2_rn(__fmul2_rn(make_float2(raf[2 * k], raf[2 * k + 1]),
+                                                        make_float2(rhp[2 * k], rhp[2 * k + 1])), f2(sAsH));
+                const float2 p2 = __fmul2_rn(make_float2(cb[2 * k], cb[2 * k + 1]), f2(sBu));
+                const float2 hv = __fadd2_rn(p1, p2);
+                hf[2 * k] = hv.x;
+                hf[2 * k + 1] = hv.y;
+                phf = fmaxf(phf, fmaxf(fabsf(hv.x), fabsf(hv.y)));
+            }
+            const float maxD = fmaf(fmaf(qAf * qHp, sAsH, qBf * fabsf(sBu)), 5.3f * 5.9604645e-8f, 1e-37f);
+            double sH = ss.Sh, qH = qa;
+            float invHf = ss.invShf;
+            bool hexact = !(maxD < 1e30f);
+            if (dyn) hexact |= (flh & 4u) || !(fmaf(maxD, 1.0000003f, phf) < thHlo);
+            const float capH = qaf + 0.25f;
+            const float halfH = 0.5f - fmaf(maxD, invHf * 1.0001f, fmaf(qaf + 1.0f, 1.25e-7f, 1e-6f));
+            float chd[16];
+            float mdh = 0.0f;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const float q = fminf(fmaxf(__fmul_rn(hf[m], invHf), -capH), capH);
+                chd[m] = rintf(q);
+                mdh = fmaxf(mdh, fabsf(q - chd[m]));
+            }
+            hexact |= !(mdh <= halfH);
+            if (hexact) {  // the exact f64 update and k3_scan_c1's f64-state h logic
+                double hn[16];
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    const double a_q = dmul(static_cast<double>(raf[m]), sA);
+                    const double b_q = dmul(static_cast<double>(cb[m]), sB);
+                    hn[m] = dadd(dmul(a_q, dmul(static_cast<double>(rhp[m]), sHp)), dmul(b_q, uv));
+                }
+                if (dyn) {
+                    double ph = 0.0;
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(hn[m]));
+                    if (ph > thH) flh |= 4u;
+                    if (flh & 4u) {
+                        sH = scale_call(ph, qo);
+                        invHf = __double2float_rn(recip_call(sH));
+                        qH = qo;
+                    }
+                }
+                const float qHf = static_cast<float>(qH), capHx = qHf + 0.25f;
+                const float halfHx = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    const float q = fminf(fmaxf(__double2float_rn(hn[m]) * invHf, -capHx), capHx);
+                    const float rr = rintf(q);
+                    chd[m] = !(fabsf(q - rr) <= halfHx) ? static_cast<float>(qdiv_call(hn[m], sH, qH)) : rr;
+                }
+            }
+            const size_t e = (rowbase + t) * E + i;
+            uint4 v;
+            uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                vw[j] = (static_cast<uint32_t>(static_cast<int>(chd[4 * j]) & 0xFF)) |
+                        (static_cast<uint32_t>(static_cast<int>(chd[4 * j + 1]) & 0xFF) << 8) |
+                        (static_cast<uint32_t>(static_cast<int>(chd[4 * j + 2]) & 0xFF) << 16) |
+                        (static_cast<uint32_t>(static_cast<int>(chd[4 * j + 3]) & 0xFF) << 24);
+            reinterpret_cast<uint4*>(w.rh)[e] = v;
+            w.sh[e] = sH;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) rhp[m] = chd[m];
+            sHp = sH;
+            sHf_prev = (flh & 4u) ? __double2float_rn(sH) : ss.Shf;
+            qHp = static_cast<float>(qH);
+        }
+    }
+}
+
+// (C) one thread per (direction, sample, step, channel): o = 0 + C_0 h_0 + ... + C_15 h_15
+// with h = code * scale (ssm.cpp:170-174), stored at the canonical row
+__global__ void __launch_bounds__(256) k3s_out(const ScanDirs P, const StepShared* __restrict__ steps, SmallWork w) {
+    const ScanParams& p0 = P.d[0];
+    const int E = p0.E, T = p0.T, S = p0.S;
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t n = static_cast<size_t>(P.n) * S * T * E;
+    if (idx >= n) return;
+    const int i = static_cast<int>(idx % E);
+    const size_t row = idx / E;  // (dir * S + s) * T + t
+    const int dir = static_cast<int>(row / (static_cast<size_t>(S) * T));
+    const int s = static_cast<int>((row / T) % S);
+    const StepShared& ss = steps[row];
+    float rc[16];
+    unpack_codes16(reinterpret_cast<const uint4*>(w.rh)[idx], rc);
+    const double sH = w.sh[idx];
+    double o = 0.0;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) o = dadd(o, dmul(ss.C[m], dmul(static_cast<double>(rc[m]), sH)));
+    P.d[dir].o[static_cast<size_t>(s) * T * E + ss.ocol + i] = o;
+}
+
+template <int ABITS>
+static cudaError_t launch_small(const ScanDirs& P, int ndirs, const StepShared* steps, void* small_base,
+                                cudaStream_t st) {
+    const ScanParams& p = P.d[0];
+    const SmallWork w = small_work(small_base, p.S, p.T, p.E, ndirs);
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    // refresh windows carry the a_bar / b_bar detector state; without refreshes it runs
+    // through the whole sequence (static mode has none: any window)
+    const int win = dyn ? (p.n_refresh > 0 ? p.n_refresh : p.T) : 8;
+    const int groups = p.E / 32, nwin = (p.T + win - 1) / win;
+    cudaError_t ea = ensure_smem_attr<k3s_codes<ABITS>>(static_cast<int>(sizeof(SmallASmem)));
+    if (ea != cudaSuccess) return ea;
+    k3s_codes<ABITS><<<dim3(groups * ndirs, p.S * nwin), 32, sizeof(SmallASmem), st>>>(P, steps, w, win);
+    ++kernel_launch_counter();
+    cudaError_t e = ensure_smem_attr<k3s_state<ABITS>>(static_cast<int>(sizeof(SmallBSmem)));
+    if (e != cudaSuccess) return e;
+    k3s_state<ABITS><<<dim3(groups * ndirs, p.S), 32, sizeof(SmallBSmem), st>>>(P, steps, w);
+    ++kernel_launch_counter();
+    const size_t n = static_cast<size_t>(ndirs) * p.S * p.T * p.E;
+    k3s_out<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(P, steps, w);
+    ++kernel_launch_counter();
+    return cudaGetLastError();
+}
+
+size_t scan_fast_workspace_bytes(int S, int T, int ndirs, int E) {
+    const size_t steps = static_cast<size_t>(ndirs) * S * T * sizeof(StepShared);
+    return steps + ((E > 0 && small_path(S, E, ndirs)) ? static_cast<size_t>(ndirs) * S * T * E * kSmallPerElem : 0);
 }
 
 cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size_t work_bytes, cudaStream_t st,
@@ -1339,7 +1748,7 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
     if (dirs[0].obits != 8) return cudaErrorNotSupported;  // fast path is built for 8-bit outliers
     if (dirs[0].abits != 4 && dirs[0].abits != 8) return cudaErrorNotSupported;
     const int S = dirs[0].S, T = dirs[0].T;
-    if (!work || work_bytes < scan_fast_workspace_bytes(S, T, ndirs) || (reinterpret_cast<uintptr_t>(work) & 15))
+    if (!work || work_bytes < scan_fast_workspace_bytes(S, T, ndirs, 0) || (reinterpret_cast<uintptr_t>(work) & 15))
         return cudaErrorInvalidValue;
     StepShared* steps = static_cast<StepShared*>(work);
     const int warps = ndirs * T * ((S + kTabSamples - 1) / kTabSamples);
@@ -1370,6 +1779,15 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
         P.merge = *merge;
         P.merge_cnt = merge_cnt;
         if (merged) *merged = true;
+    }
+    // small batches (< one warp per SM): the split-phase scan (auto only; it needs the
+    // workspace's second part)
+    const int E = dirs[0].E;
+    if (variant == 0 && !trace && !P.merge_cnt && small_path(S, E, ndirs) &&
+        work_bytes >= scan_fast_workspace_bytes(S, T, ndirs, E)) {
+        void* small_base = static_cast<uint8_t*>(work) + scan_fast_workspace_bytes(S, T, ndirs, 0);
+        return dirs[0].abits == 4 ? launch_small<4>(P, ndirs, steps, small_base, st)
+                                  : launch_small<8>(P, ndirs, steps, small_base, st);
     }
     switch (dirs[0].abits) {
         case 4: return launch_kernel<4>(P, ndirs, steps, st, kernel, exact, trace);

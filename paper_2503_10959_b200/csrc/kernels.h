@@ -181,7 +181,9 @@ cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal
 // channel, f32 state; 3 / 4: one thread per channel with the f64 / f32 state update
 // (even E); 5: two threads per channel, f64 state. Non-null `masks` selects the
 // parity-trace instantiation.
-size_t scan_fast_workspace_bytes(int S, int T, int ndirs);
+// E > 0: also the small-batch split-phase scan's intermediates when S * E * ndirs
+// is below one warp per SM (launch_scan_fast then uses that path in auto mode)
+size_t scan_fast_workspace_bytes(int S, int T, int ndirs, int E = 0);
 // merge (may be null): the out_proj input K1 (merge source), fused into the
 // one-thread-per-channel f32-state kernel when that kernel runs (*merged = true;
 // the caller has zeroed merge->ocnt; merge_cnt = [S][E/32] ints, zero between
