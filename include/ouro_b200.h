@@ -75,7 +75,9 @@ ouro_status ouro_b200_ctx_num_sms(ouro_b200_ctx* ctx, int* out);
  *   literal  1 = run the verbatim detector (cross-channel max per plane); 0 =
  *          channel-parallel kernel, exact when fl(nextafter(theta)/q_a) > s_in[t]
  *          for every t (the caller checks), unless `scanned`
- *          is requested
+ *          is requested; 2 = the channel-parallel path on the register window
+ *          kernel for SRC_PLAIN / SRC_RMSNORM where E % 64 == 0 and E <= 768
+ *          (A/B aid; 0 runs the bulk-copy staged kernel)
  * Outputs (row = s*T + t, dev): codes int8 [S*T][E] (0 at outliers), s_row
  * f64 [S*T], ocnt int32 [S*T] = |O(t)|, omask uint32 [S*T][ceil(E/32)]
  * (bit ch%32 of word ch/32 = channel in O(t)), ocode int8 / oscale f64
@@ -219,7 +221,8 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * per channel (f64 state) / one thread per channel (f32 state) / two threads per
  * channel (f64 state) (A/B aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
- * detector kernel everywhere; "pack_a4" = 1: A4 activation codes travel
+ * detector kernel everywhere, 2 auto with the register window plain / RMSNorm
+ * kernel (A/B aid); "pack_a4" = 1: A4 activation codes travel
  * nibble-packed from K1 to K2, 0 (default) one int8 byte per code; "merge_fuse" = 1:
  * the out_proj input K1 runs as the f32-state scan's tail, 0 (default) its own
  * launch; "split_parts" in [1, 4] (default 2) runs a batch of

@@ -192,6 +192,7 @@ static ouro_status detect_quantize_impl(ouro_b200_ctx* ctx, const double* x, con
                 "detect_quantize: bit widths must satisfy 2 <= act <= outlier <= 8");
         require(src != ob::K1_SRC_MERGE || gate != nullptr, "detect_quantize: merge source needs the gate");
         require(src >= 0 && src <= 2, "detect_quantize: unknown source");
+        require(literal >= 0 && literal <= 2, "detect_quantize: literal must be 0, 1 or 2");
         require(order >= -1 && order <= 3, "detect_quantize: order must be -1 (identity) or a scan order 0-3");
         require(order < 2 || (grid >= 1 && static_cast<size_t>(grid) * grid == T),
                 "detect_quantize: column scan orders need T = grid^2");
@@ -213,7 +214,8 @@ static ouro_status detect_quantize_impl(ouro_b200_ctx* ctx, const double* x, con
         k.cal.theta = theta;
         k.cal.s_in = s_in;
         k.cal.s_full = s_full;
-        k.force_literal = literal;
+        k.force_literal = literal == 1;
+        k.window_kernel = literal == 2;
         k.codes = codes;
         k.codes4 = codes4;
         k.s_row = s_row;
@@ -688,7 +690,7 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
             require(value == 0 || value == 1, "model_set_option: pack_a4 must be 0 or 1");
             m->m->pack_a4 = static_cast<int>(value);
         } else if (k == "k1_variant") {
-            require(value >= 0 && value <= 1, "model_set_option: k1_variant must be 0 or 1");
+            require(value >= 0 && value <= 2, "model_set_option: k1_variant must be 0, 1 or 2");
             m->m->k1_variant = static_cast<int>(value);
         } else {
             throw ob::ValidationError("model_set_option: unknown option '" + k + "'");

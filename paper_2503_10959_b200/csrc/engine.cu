@@ -548,6 +548,7 @@ void Model::forward_impl(const Calibration* cal, int mode, bool d1, bool d2, con
             // literal detector where the channel-local form is not exact, on request,
             // and in trace mode (it also reports DetectResult::scanned)
             k.force_literal = (mode == MODE_DYNAMIC && cal->lin_literal[li]) || k1_variant == 1 || tb(b);
+            k.window_kernel = k1_variant == 2;
             if (tb(b)) k.scanned = w.scanned.p + qslot * rows;
         } else {
             k.mode = MODE_FP;

@@ -177,7 +177,8 @@ class Model {
     void upload_fp();
     void quantize(unsigned bits);
     bool fp_dirty = true;
-    int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel
+    int k1_variant = 0;    // 0 auto (channel-parallel K1 wherever exact), 1 literal detector kernel,
+                           // 2 auto with the register window kernel for plain / RMSNorm sources (A/B aid)
     int merge_fuse = 0;    // 1: the out_proj input K1 runs as the f32-state scan's tail (last direction of each
                            // (sample, channel group) to finish quantizes it); 0 (default): separate k1_channel
                            // launch. Measured at Vim-B batch 256: 3.36 ms scan per block fused vs 1.71 + 0.216

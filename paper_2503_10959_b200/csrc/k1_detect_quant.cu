@@ -36,6 +36,7 @@
 //    warp reduction, so the reference is followed verbatim (also provides
 //    DetectResult::scanned).
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -52,6 +53,19 @@ __device__ __forceinline__ uint16_t pack4(int c0, int c1, int c2, int c3) {
     return static_cast<uint16_t>((c0 & 0xF) | ((c1 & 0xF) << 4) | ((c2 & 0xF) << 8) | ((c3 & 0xF) << 12));
 }
 
+
+// |a|, |b|, |c| or |d| > th as one predicate chain (setp.gt.or)
+__device__ __forceinline__ bool any_abs_gt4(double a, double b, double c, double d, double th) {
+    unsigned r;
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 x;\n\t"
+        "abs.f64 x, %1;\n\tsetp.gt.f64 p, x, %5;\n\t"
+        "abs.f64 x, %2;\n\tsetp.gt.or.f64 p, x, %5, p;\n\t"
+        "abs.f64 x, %3;\n\tsetp.gt.or.f64 p, x, %5, p;\n\t"
+        "abs.f64 x, %4;\n\tsetp.gt.or.f64 p, x, %5, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r) : "d"(a), "d"(b), "d"(c), "d"(d), "d"(th));
+    return r != 0u;
+}
 
 // exact merged value y = merged * silu(gate) (ssm.cpp:231): the rare path, kept out of line
 __device__ __noinline__ double merge_exact(double m, double g) { return dmul(m, silu_d(g)); }
@@ -192,6 +206,7 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
 constexpr int kK1StageBytes = 24 * 1024;
 constexpr int kK1Stages = 2;  // 3 stages (fewer CTAs per SM) measured 165 / 117 us vs 155 / 113
 constexpr int kK1MaxRc = 16;
+constexpr int kK1MaxWin = 64;  // windows up to 64 steps keep their scales in shared memory
 struct K1Dirs {
     K1Params p[2];
     int n = 1;       // directions in this launch
@@ -203,6 +218,20 @@ __device__ __forceinline__ int k1_row_of(const K1Params& p, int t) {
     return row_at(p.order, t, p.T, p.grid);
 }
 
+// the outlier channels of a quad: own scale |x|/q_o, code at o_bits (out of line: rare)
+__device__ __noinline__ void outliers4(unsigned in, double v0, double v1, double v2, double v3, double qo,
+                                       int8_t* ocode, double* oscale) {
+    const double v[4] = {v0, v1, v2, v3};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if ((in >> k) & 1u) {
+            const double os = scale_from_peak(fabs(v[k]), qo);  // scale_for over the 1-value row
+            ocode[k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[k], os, qo)));
+            oscale[k] = os;
+        }
+    }
+}
+
 template <int SRC, bool PK>
 __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs dirs) {
     extern __shared__ __align__(128) unsigned char k1_smem[];
@@ -210,6 +239,7 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     __shared__ uint64_t bar[kK1Stages];
     __shared__ int cnt[kK1Stages][kK1MaxRc];     // |O(t)| of the chunk's rows
     __shared__ double rsv[kK1Stages][kK1MaxRc];  // D1 row factors of the chunk's rows
+    __shared__ double2 si_win[kK1MaxWin];         // {S^I(t), 1/S^I(t)} of the window's steps
     const int d = dirs.n == 2 ? static_cast<int>(blockIdx.y & 1) : 0;
     const K1Params& p = dirs.p[d];
     const int yy = dirs.n == 2 ? static_cast<int>(blockIdx.y >> 1) : static_cast<int>(blockIdx.y);
@@ -225,12 +255,6 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     const bool active = ch < E;
     const uint32_t row_bytes = static_cast<uint32_t>(E) * 8u;
 
-    if (tid == 0) {
-        for (int b = 0; b < kK1Stages; ++b) ptx::mbar_init(&bar[b], 1);
-        ptx::fence_barrier_init();
-    }
-    for (int i = tid; i < kK1Stages * kK1MaxRc; i += blockDim.x) cnt[i / kK1MaxRc][i % kK1MaxRc] = 0;
-    __syncthreads();
     auto issue = [&](int c) {  // thread 0
         const int buf = c % kK1Stages, ts = t0 + c * rc, te = min(t1, ts + rc);
         ptx::mbar_arrive_expect_tx(&bar[buf], static_cast<uint32_t>(te - ts) * row_bytes);
@@ -238,8 +262,22 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
             ptx::bulk_g2s(stage + (static_cast<size_t>(buf) * rc + (t - ts)) * E,
                      p.x + (static_cast<size_t>(s) * T + k1_row_of(p, t)) * E, row_bytes, &bar[buf]);
     };
-    if (tid == 0)
+    if (tid == 0) {  // the first chunks are in flight before the CTA barrier
+        for (int b = 0; b < kK1Stages; ++b) ptx::mbar_init(&bar[b], 1);
+        ptx::fence_barrier_init();
         for (int c = 0; c < kK1Stages && c < nchunks; ++c) issue(c);
+    }
+    for (int i = tid; i < kK1Stages * kK1MaxRc; i += blockDim.x) cnt[i / kK1MaxRc][i % kK1MaxRc] = 0;
+    {
+        const bool dyn0 = p.mode == MODE_DYNAMIC;
+        const double* st = dyn0 ? p.cal.s_in : p.cal.s_full;
+        const double* it = dyn0 ? p.inv_in : p.inv_full;
+        for (int i = tid; i < t1 - t0 && i < kK1MaxWin; i += blockDim.x) {
+            const double S = st[t0 + i];
+            si_win[i] = make_double2(S, it ? it[t0 + i] : __ddiv_rn(1.0, S));
+        }
+    }
+    __syncthreads();
 
     // every field the loop needs, read once (the direction's parameter block is
     // selected at run time)
@@ -257,6 +295,8 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
     uint32_t* __restrict__ const omask = p.omask;
     double* __restrict__ const s_row = p.s_row;
     int* __restrict__ const ocnt = p.ocnt;
+    const unsigned qq = (static_cast<unsigned>(qai) << 16) | static_cast<unsigned>(qai);
+    const unsigned nq = (static_cast<unsigned>(-qai) << 16) | (static_cast<unsigned>(-qai) & 0xFFFFu);
     int next_ref = (dyn && n_refresh > 0) ? t0 + n_refresh : 0x7fffffff;
     unsigned in = 0;  // bit k: channel ch+k is in O
     for (int c = 0; c < nchunks; ++c) {
@@ -285,8 +325,15 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
         for (int t = ts; t < te; ++t, xr += E, mp += J, cp += (PK ? 0 : E), cp4 += (PK ? (E >> 2) : 0)) {
             const int slot = t - ts;
             const size_t row = row0 + slot;
-            const double S = s_tab[t];
-            const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
+            double S, inv;
+            if (t - t0 < kK1MaxWin) {
+                const double2 si = si_win[t - t0];
+                S = si.x;
+                inv = si.y;
+            } else {
+                S = s_tab[t];
+                inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
+            }
             double v[4] = {0.0, 0.0, 0.0, 0.0};
             if (active) {
                 const double2 lo = *reinterpret_cast<const double2*>(xr);
@@ -306,45 +353,55 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
                     in = 0;
                     next_ref += n_refresh;
                 }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)  // detect_outliers, channel-local form
-                    in |= (fabs(v[k]) > theta ? 1u : 0u) << k;
+                // detect_outliers, channel-local form (one predicate chain; the bits only
+                // when a channel crosses theta)
+                if (any_abs_gt4(v[0], v[1], v[2], v[3], theta))
+                    in |= (fabs(v[0]) > theta ? 1u : 0u) | (fabs(v[1]) > theta ? 2u : 0u) |
+                          (fabs(v[2]) > theta ? 4u : 0u) | (fabs(v[3]) > theta ? 8u : 0u);
             }
-            // inlier codes for all four channels: quant_code_int's rounding without its
-            // f64 clamp (round, then clamp the integer: same code for |q| < 2^50); a
-            // quotient near a half-integer or beyond 2^50 is decided exactly below
+            // inlier codes for all four channels: tq = fl(v * inv + 1.5 * 2^52) holds
+            // RNE(v * inv) in its low word while |v * inv| < 2^31 and d = fl(v * inv - that)
+            // is its distance, so quant_code_int's test reads |d| <= 0.4999999999990 (a NaN
+            // fails it); the integer clamp replaces its f64 clamp. In dynamic mode inliers
+            // have |v| <= theta, so theta / S < 2^14 bounds every inlier quotient of the row
+            // (outlier channels' codes are zeroed); otherwise each quotient is range-checked
+            // (|q| < 2^14 also keeps the s16x2 clamp exact). A failed test decides the four
+            // exactly (quant_code_int).
             constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
             int cc[4];
             bool tie = false;
+            auto codes_of = [&](auto ranged) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double q2 = dmul(v[k], inv);
-                const double tq = dadd(q2, kMagic);
-                cc[k] = __double2loint(tq);
-                tie |= (fabs(dadd(q2, -dadd(tq, -kMagic))) > 0.4999999999990) | !(fabs(q2) < 0x1p50);
-            }
+                for (int k = 0; k < 4; ++k) {
+                    const double tq = __fma_rn(v[k], inv, kMagic);
+                    const double r = dadd(tq, -kMagic);
+                    cc[k] = __double2loint(tq);
+                    tie |= !(fabs(__fma_rn(v[k], inv, -r)) <= 0.4999999999990);
+                    if constexpr (decltype(ranged)::value) tie |= !(fabs(r) < 16384.0);
+                }
+            };
+            if (dyn && theta * inv < 16384.0)
+                codes_of(std::false_type{});
+            else
+                codes_of(std::true_type{});
             if (tie) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) cc[k] = quant_code_int(v[k], S, inv, qa, qai);
             }
             if (active) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) cc[k] = ((in >> k) & 1u) ? 0 : min(max(cc[k], -qai), qai);
-                if constexpr (PK)
-                    *cp4 = pack4(cc[0], cc[1], cc[2], cc[3]);
-                else
-                    *reinterpret_cast<char4*>(cp) =
-                        make_char4(static_cast<signed char>(cc[0]), static_cast<signed char>(cc[1]),
-                                   static_cast<signed char>(cc[2]), static_cast<signed char>(cc[3]));
-                if (in) {  // outlier channels: own scale |x|/q_o, code at o_bits
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if ((in >> k) & 1u) {
-                            const double os = scale_from_peak(fabs(v[k]), qo);  // scale_for over the 1-value row
-                            ocode[row * E + ch + k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[k], os, qo)));
-                            oscale[row * E + ch + k] = os;
-                        }
-                    }
+                // clamp as two s16x2 pairs, bytes c0..c3
+                const unsigned p01 = __vmaxs2(__vmins2(__byte_perm(cc[0], cc[1], 0x5410), qq), nq);
+                const unsigned p23 = __vmaxs2(__vmins2(__byte_perm(cc[2], cc[3], 0x5410), qq), nq);
+                unsigned w = __byte_perm(p01, p23, 0x6420);
+                if (in) {
+                    w &= ~(((in * 0x00204081u) & 0x01010101u) * 0xFFu);  // outlier channels: code 0
+                    outliers4(in, v[0], v[1], v[2], v[3], qo, ocode + row * E + ch, oscale + row * E + ch);
+                }
+                if constexpr (PK) {
+                    const unsigned n = w & 0x0F0F0F0Fu;  // pack_int4: low nibble = even column
+                    *cp4 = static_cast<uint16_t>(__byte_perm(n | (n >> 4), 0u, 0x0020));
+                } else {
+                    *reinterpret_cast<unsigned*>(cp) = w;
                 }
             }
             // mask word of channels 32w..32w+31 from 8 lanes x 4 bits (all zero in the common case)
@@ -365,6 +422,168 @@ __global__ void __launch_bounds__(256) k1_staged(const __grid_constant__ K1Dirs 
         if (tid == 0 && c + kK1Stages < nchunks) {
             ptx::fence_async_smem();  // generic-proxy reads of the stage before the async refill
             issue(c + kK1Stages);
+        }
+    }
+}
+
+// Register-resident window path (plain / RMSNorm sources, E % 64 == 0): a CTA owns
+// one (sample, refresh window) of one direction with blockDim = E/2, one thread
+// per channel pair; a chunk of R rows of the window (R >= the window in the usual
+// case) is loaded into registers at once (R x 16 B per thread in flight, like the
+// conv's), and the channel-local detector runs down the rows with the channel
+// state in a register. Each thread's two codes are independent of every other
+// thread's, so the only CTA-wide work is D1's row factor (squares through shared
+// memory, one warp per row in the k%32 partial order of rmsnorm_row) and |O(t)|.
+__device__ __forceinline__ bool any_abs_gt2(double a, double b, double th) {
+    unsigned r;
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 x;\n\t"
+        "abs.f64 x, %1;\n\tsetp.gt.f64 p, x, %3;\n\t"
+        "abs.f64 x, %2;\n\tsetp.gt.or.f64 p, x, %3, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r) : "d"(a), "d"(b), "d"(th));
+    return r != 0u;
+}
+
+// the rare paths out of line, so the unrolled rows stay compact in the icache
+__device__ __noinline__ int2 codes_exact2(double v0, double v1, double S, double inv, double qa, int qai) {
+    return make_int2(quant_code_int(v0, S, inv, qa, qai), quant_code_int(v1, S, inv, qa, qai));
+}
+__device__ __noinline__ void outliers2(unsigned in, double v0, double v1, double qo, int8_t* ocode, double* oscale) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if ((in >> k) & 1u) {
+            const double v = k ? v1 : v0;
+            const double os = scale_from_peak(fabs(v), qo);  // scale_for over the 1-value row
+            ocode[k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v, os, qo)));
+            oscale[k] = os;
+        }
+    }
+}
+
+template <int SRC, bool PK, int R>
+__global__ void __launch_bounds__(384, 2) k1_window(const __grid_constant__ K1Dirs dirs) {
+    extern __shared__ __align__(16) double k1w_sq[];  // RMSNorm: [R][E] squares
+    __shared__ int cnt[R];
+    __shared__ double rsv[R], s_s[R], s_i[R];
+    const int d = dirs.n == 2 ? static_cast<int>(blockIdx.x & 1) : 0;
+    const K1Params& p = dirs.p[d];
+    const int yy = dirs.n == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int E = p.E, T = p.T, J = E >> 5;
+    const int win = p.window, nwin = (T + win - 1) / win;
+    const int s = yy / nwin;
+    int wi = yy % nwin;
+    if (d == 1 && dirs.mirror) wi = nwin - 1 - wi;
+    const int t0 = wi * win, t1 = min(T, t0 + win);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int ch = tid * 2;
+    const bool dyn = p.mode == MODE_DYNAMIC;
+    const int n_refresh = p.n_refresh;
+    const double qa = qmax_for(p.abits), qo = qmax_for(p.obits);
+    const int qai = static_cast<int>(qa);
+    const double theta = p.cal.theta;
+    const double* __restrict__ s_tab = dyn ? p.cal.s_in : p.cal.s_full;
+    const double* __restrict__ i_tab = dyn ? p.inv_in : p.inv_full;
+    const double* __restrict__ xs = p.x + static_cast<size_t>(s) * T * E + ch;
+    const unsigned qq = (static_cast<unsigned>(qai) << 16) | static_cast<unsigned>(qai);
+    const unsigned nq = (static_cast<unsigned>(-qai) << 16) | (static_cast<unsigned>(-qai) & 0xFFFFu);
+    int next_ref = (dyn && n_refresh > 0) ? t0 + n_refresh : 0x7fffffff;
+    unsigned in = 0;  // bit k: channel ch+k is in O
+    if (tid < R) cnt[tid] = 0;
+    for (int c0 = t0; c0 < t1; c0 += R) {
+        const int n = min(R, t1 - c0);
+        double2 xv[R];
+        if (p.order <= 1) {  // identity / reversed order: rows at a fixed stride
+            const long long step = p.order == 1 ? -static_cast<long long>(E) : static_cast<long long>(E);
+            const double* b = xs + static_cast<size_t>(p.order == 1 ? T - 1 - c0 : c0) * E;
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                if (j < n) xv[j] = ldg2(b + j * step);
+        } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                if (j < n) xv[j] = ldg2(xs + static_cast<size_t>(k1_row_of(p, c0 + j)) * E);
+        }
+        if (tid < n) {
+            const double S = s_tab[c0 + tid];
+            s_s[tid] = S;
+            s_i[tid] = i_tab ? i_tab[c0 + tid] : __ddiv_rn(1.0, S);
+        }
+        if (SRC == K1_SRC_RMSNORM) {
+            // 1/sqrt(mean(x^2) + 1e-6): 32 lane-strided partials (channel k -> partial
+            // k%32, k ascending) combined by an xor butterfly (oracle/driver.hpp rmsnorm_row)
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                if (j < n)
+                    *reinterpret_cast<double2*>(k1w_sq + static_cast<size_t>(j) * E + ch) =
+                        make_double2(dmul(xv[j].x, xv[j].x), dmul(xv[j].y, xv[j].y));
+            __syncthreads();
+            for (int r = warp; r < n; r += nwarps) {
+                const double* q = k1w_sq + static_cast<size_t>(r) * E;
+                double ps = 0.0;
+                for (int k = lane; k < E; k += 32) ps = dadd(ps, q[k]);
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) ps = dadd(ps, __shfl_xor_sync(0xffffffffu, ps, o));
+                if (lane == 0) rsv[r] = __ddiv_rn(1.0, __dsqrt_rn(dadd(__ddiv_rn(ps, static_cast<double>(E)), 1e-6)));
+            }
+        }
+        __syncthreads();  // row scales, D1 factors, zeroed counts
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            if (j >= n) break;
+            const int t = c0 + j;
+            const size_t row = static_cast<size_t>(s) * T + t;
+            const double S = s_s[j], inv = s_i[j];
+            double v0 = xv[j].x, v1 = xv[j].y;
+            if (SRC == K1_SRC_RMSNORM) {
+                const double r = rsv[j];
+                v0 = dmul(v0, r);
+                v1 = dmul(v1, r);
+            }
+            if (dyn) {
+                if (t == next_ref) {  // maybe_refresh
+                    in = 0;
+                    next_ref += n_refresh;
+                }
+                if (any_abs_gt2(v0, v1, theta))  // detect_outliers, channel-local form
+                    in |= (fabs(v0) > theta ? 1u : 0u) | (fabs(v1) > theta ? 2u : 0u);
+            }
+            // k1_staged's code test on two channels (tq = fl(v * inv + 1.5 * 2^52), d the
+            // remainder; quotients bounded by theta / S in dynamic mode, else range-checked)
+            constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+            const double tq0 = __fma_rn(v0, inv, kMagic), tq1 = __fma_rn(v1, inv, kMagic);
+            const double r0 = dadd(tq0, -kMagic), r1 = dadd(tq1, -kMagic);
+            int c0i = __double2loint(tq0), c1i = __double2loint(tq1);
+            bool tie = !(fabs(__fma_rn(v0, inv, -r0)) <= 0.4999999999990) |
+                       !(fabs(__fma_rn(v1, inv, -r1)) <= 0.4999999999990);
+            if (!(dyn && theta * inv < 16384.0)) tie |= !(fabs(r0) < 16384.0) | !(fabs(r1) < 16384.0);
+            if (tie) {
+                const int2 c = codes_exact2(v0, v1, S, inv, qa, qai);
+                c0i = c.x;
+                c1i = c.y;
+            }
+            unsigned pr = __vmaxs2(__vmins2(__byte_perm(c0i, c1i, 0x5410), qq), nq);  // s16 x2
+            if (in) {
+                pr &= ~(((in & 1u) ? 0x0000FFFFu : 0u) | ((in & 2u) ? 0xFFFF0000u : 0u));  // outliers: code 0
+                outliers2(in, v0, v1, qo, p.ocode + row * E + ch, p.oscale + row * E + ch);
+            }
+            if constexpr (PK)  // pack_int4: low nibble = even column
+                p.codes4[row * (E >> 1) + tid] = static_cast<uint8_t>((pr & 0xFu) | ((pr >> 12) & 0xF0u));
+            else
+                *reinterpret_cast<uint16_t*>(p.codes + row * E + ch) = static_cast<uint16_t>(__byte_perm(pr, 0u, 0x0020));
+            // mask word of channels 32w..32w+31 from 16 lanes x 2 bits (all zero in the common case)
+            unsigned bits = in << ((lane & 15) * 2);
+            if (__any_sync(0xffffffffu, bits != 0u)) {
+#pragma unroll
+                for (int o = 8; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+                if ((lane & 15) == 0 && bits) atomicAdd(&cnt[j], __popc(bits));
+            }
+            if ((lane & 15) == 0) p.omask[row * J + (ch >> 5)] = bits;
+            if (tid == 0) p.s_row[row] = S;
+        }
+        __syncthreads();  // counts complete, s_s / s_i / rsv / squares consumed
+        if (tid < n) {
+            p.ocnt[static_cast<size_t>(s) * T + c0 + tid] = cnt[tid];
+            cnt[tid] = 0;
         }
     }
 }
@@ -530,9 +749,32 @@ static cudaError_t launch_staged_pk(const K1Dirs& dirs, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int SRC, bool PK, int R>
+static cudaError_t launch_window_r(const K1Dirs& dirs, cudaStream_t st) {
+    const K1Params& p = dirs.p[0];
+    const int nwin = (p.T + p.window - 1) / p.window;
+    const size_t smem = SRC == K1_SRC_RMSNORM ? static_cast<size_t>(R) * p.E * sizeof(double) : 0;
+    cudaError_t e = ensure_smem_attr<k1_window<SRC, PK, R>>(static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    k1_window<SRC, PK, R><<<p.S * nwin * dirs.n, p.E / 2, smem, st>>>(dirs);
+    ++kernel_launch_counter();
+    return cudaGetLastError();
+}
+
+template <int SRC, bool PK>
+static cudaError_t launch_window(const K1Dirs& dirs, cudaStream_t st) {
+    // rows per register chunk: the whole window when it has <= 12 rows, else 12
+    const int w = dirs.p[0].window;
+    if (w <= 8) return launch_window_r<SRC, PK, 8>(dirs, st);
+    if (w <= 10) return launch_window_r<SRC, PK, 10>(dirs, st);
+    return launch_window_r<SRC, PK, 12>(dirs, st);
+}
+
 template <int SRC>
 static cudaError_t launch_staged(const K1Dirs& dirs, cudaStream_t st) {
     if ((dirs.p[0].codes4 != nullptr) != (dirs.p[1].codes4 != nullptr)) return cudaErrorInvalidValue;
+    if (dirs.p[0].window_kernel && dirs.p[0].E % 64 == 0 && dirs.p[0].E <= 768)
+        return dirs.p[0].codes4 ? launch_window<SRC, true>(dirs, st) : launch_window<SRC, false>(dirs, st);
     return dirs.p[0].codes4 ? launch_staged_pk<SRC, true>(dirs, st) : launch_staged_pk<SRC, false>(dirs, st);
 }
 

@@ -75,6 +75,8 @@ struct K1Params {
     const double* inv_in = nullptr;    // optional [T] 1/s_in (host-computed); else divided in-kernel
     const double* inv_full = nullptr;  // optional [T] 1/s_full
     int force_literal = 0;             // run the literal detector kernel
+    int window_kernel = 0;             // plain / RMSNorm channel-parallel path: 1 = the register window
+                                       // kernel where E % 64 == 0, E <= 768 (A/B aid), 0 = the staged kernel
     // quantized outputs (rows in step order, row = s*T + t): the QAct operand
     int8_t* codes = nullptr;
     uint8_t* codes4 = nullptr;    // A4: the inlier codes nibble-packed instead (QAct::codes4), codes unused

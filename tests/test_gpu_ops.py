@@ -215,3 +215,46 @@ def test_scan_order_geometry_validated(gpu_ctx):
         gpu_ctx.detect_quantize(x, order=5, grid=0, **kw)
     gpu_ctx.detect_quantize(x, order=1, grid=0, **kw)  # row orders need no grid
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("E", [64, 192, 768])
+@pytest.mark.parametrize("src", [0, 1])
+def test_detect_quantize_window_staged_literal_identical(gpu_ctx, E, src):
+    """Plain / RMSNorm sources: the bulk-copy staged kernel (literal=0), the
+    register window kernel (literal=2, E % 64 == 0) and the literal detector
+    (literal=1) give identical operands — dynamic (refresh windows of 8, 10 and
+    12+ rows, quotient bound theta/S below and above 2^14) and static (quotients
+    up to 1e12, beyond the low-word range), every scan order, int8 and packed."""
+    import torch
+    S, T = 3, 36  # T = 6^2 for the column orders
+    rng = np.random.default_rng(E + src)
+    x = rng.normal(size=(S, T, E)) * 2.0
+    x[rng.random((S, T, E)) < 0.02] *= 40.0
+    x[0, 5, 3] = 1e12  # static mode: |q| >= 2^31
+    x[1, 7, 10] = -3e11
+    xd = _dev(x)
+    # theta / q_a = 0.44 > every S(t) <= 0.3 * 1.3: the channel-local form is exact
+    cases = [(1, 4, 0.3, 3.1), (1, 10, 0.3, 3.1), (1, 13, 0.3, 3.1), (1, 10, 1e-5, 3.1), (2, 10, 0.3, 3.1)]
+    for mode, n_refresh, sc, theta in cases:
+        s_in = _dev(np.full(T, sc) * np.linspace(1.0, 1.3, T))
+        for order, grid in ((-1, 0), (1, 0), (2, 6), (3, 6)):
+            for packed in (False, True):
+                outs = []
+                for lit in (0, 2, 1):
+                    r = gpu_ctx.detect_quantize(xd, S=S, T=T, E=E, theta=theta, s_in=s_in, s_full=s_in,
+                                                n_refresh=n_refresh, act_bits=4, outlier_bits=8, mode=mode, src=src,
+                                                order=order, grid=grid, literal=lit, packed=packed)
+                    torch.cuda.synchronize()
+                    outs.append({k: v.cpu().numpy() for k, v in r.items()})
+                tag = (mode, n_refresh, sc, order, packed)
+                for b in outs[1:]:
+                    for k in ("codes4" if packed else "codes", "s_row", "ocnt", "omask"):
+                        assert np.array_equal(outs[0][k], b[k]), (tag, k)
+                    m = _unpack(outs[0]["omask"], E).astype(bool)
+                    assert np.array_equal(outs[0]["ocode"][m], b["ocode"][m]), tag
+                    assert np.array_equal(outs[0]["oscale"][m], b["oscale"][m]), tag
+                if mode == 1:
+                    assert _unpack(outs[0]["omask"], E).any(), tag
+                elif not packed and order == -1:
+                    c = outs[0]["codes"].reshape(S, T, E)
+                    assert c[0, 5, 3] == 7 and c[1, 7, 10] == -7, tag  # saturated, not wrapped
