@@ -33,6 +33,8 @@
 //  * h update (f64, reference order), h codes certified the same way from the
 //    f32 rounding of the exact h (the f32 peak equals fl32 of the exact peak),
 //    the output sum in the reference's order.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "merge_f32.cuh"
@@ -318,7 +320,6 @@ __global__ void __launch_bounds__(kThr, 8) k3_scan_fast(const ScanDirs P, const 
         constexpr bool kDefer = ABITS == 4;
         unsigned fl_prev = fl;
         for (int tt = 0; tt < nt; ++tt) {
-            const int t = t0 + tt;
             const StepShared& ss = sh.st[cur][tt];
             const float df = sh.deltaf[tt][c];
             const float ed = sh.epsd[tt][c];
@@ -1331,11 +1332,13 @@ static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared*
 // direction, sample, step and channel) stay in L2 at these sizes.
 // phase A's record per (direction, sample, step, channel): a_bar codes (0..q) | b_bar codes |
 // the exact scales of the step (outlier channels: their own) | outlier flags after detection
+// plus the f32 scalars phase B's common path needs: f32 of the a scale, f32(S_b) f32(u)
+// and q_b |that| (k3_scan_c1<FS>'s sAf, sBu and the b term of its bound D)
 struct __align__(16) SmallRec {
     uint4 ca, cb;
     double sA, sB;
     unsigned fab;
-    unsigned pad[3];
+    float sAf, sBu, qBsBu;
 };
 static_assert(sizeof(SmallRec) == 64, "four 16-byte copies per record");
 struct SmallWork {
@@ -1362,162 +1365,157 @@ static SmallWork small_work(void* base, int S, int T, int E, int ndirs) {
     return w;
 }
 
-// (A) one thread per (direction, sample, channel, refresh window): k3_scan_c1's detector
-// and certified code pass per step (outlier channels take their exact scales)
 constexpr int kSA = 16;  // steps staged per pass of phase A
-struct SmallASmem {
+// (A') sixteen lanes per (channel, refresh window), lane m computing state m's a_bar /
+// b_bar codes; the channel's detector runs redundantly on its 16 lanes (same values, no
+// communication). CTA = 8 channels of one window; the window's step records and delta
+// inputs are staged in shared memory per pass of kSA steps.
+constexpr int kCh16 = 8;  // channels per CTA of the sixteen-lane phases (128 threads)
+struct SmallA16Smem {
     StepShared st[kSA];
-    double dp[kSA][32];
-    uint64_t bar;
+    double dp[kSA][kCh16];
+    double u[kSA][kCh16];
 };
 
 template <int ABITS>
-__global__ void __launch_bounds__(32) k3s_codes(const ScanDirs P, const StepShared* __restrict__ steps, SmallWork w,
-                                                int win) {
-    extern __shared__ __align__(16) uint8_t sa_smem_raw[];
-    SmallASmem& sm = *reinterpret_cast<SmallASmem*>(sa_smem_raw);
-    const int ndirs = P.n, groups = P.d[0].E / 32;
-    const int dir = static_cast<int>(blockIdx.x) % ndirs, grp = static_cast<int>(blockIdx.x) / ndirs;
+__global__ void __launch_bounds__(128) k3s_codes16(const ScanDirs P, const StepShared* __restrict__ steps, SmallWork w,
+                                                   int win) {
+    extern __shared__ __align__(16) uint8_t sa16_smem_raw[];
+    SmallA16Smem& sm = *reinterpret_cast<SmallA16Smem*>(sa16_smem_raw);
+    const int ndirs = P.n;
+    const int nwin = (P.d[0].T + win - 1) / win;
+    const int dir = static_cast<int>(blockIdx.y) % ndirs, sw = static_cast<int>(blockIdx.y) / ndirs;
     const ScanParams& p = P.d[dir];
-    const unsigned lane = threadIdx.x;
-    const int E = p.E, T = p.T, P2 = E + 32, i = grp * 32 + static_cast<int>(lane);
-    const int nwin = (T + win - 1) / win, s = static_cast<int>(blockIdx.y) / nwin;
-    const int t0 = (static_cast<int>(blockIdx.y) % nwin) * win, t1 = min(T, t0 + win);
+    const int tid = threadIdx.x, cl = tid >> 4, m = tid & 15;
+    const int E = p.E, T = p.T, P2 = E + 32, ch0 = static_cast<int>(blockIdx.x) * kCh16, i = ch0 + cl;
+    const int s = sw / nwin;
+    const int t0 = (sw % nwin) * win, t1 = min(T, t0 + win);
     const bool dyn = p.mode == MODE_DYNAMIC;
     constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;
     constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
     const double* __restrict__ arow = p.a + static_cast<size_t>(i) * 16;
-    float A2[16];
+    const double am = arow[m];
+    const float A2m = __double2float_rn(am * 1.4426950408889634);
     double Amax = -1e300;
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-        A2[m] = __double2float_rn(arow[m] * 1.4426950408889634);
-        Amax = fmax(Amax, arow[m]);
-    }
+    for (int k = 0; k < 16; ++k) Amax = fmax(Amax, arow[k]);
     const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
     const double thA = p.cal[0].theta, thB = p.cal[1].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB);
     const double bd = p.b_delta[i];
     const size_t rowbase = static_cast<size_t>(dir) * p.S * T + static_cast<size_t>(s) * T;
-    if (lane == 0) {
-        ptx::mbar_init(&sm.bar, 1);
-        ptx::fence_barrier_init();
-    }
-    __syncwarp();
+    constexpr int kStPieces = static_cast<int>(sizeof(StepShared) / 16);
     unsigned fl = 0;
-    for (int tb = t0, pass = 0; tb < t1; tb += kSA, ++pass) {  // the pass's step records and delta inputs, staged
+    for (int tb = t0; tb < t1; tb += kSA) {  // the pass's step records and delta inputs, staged
         const int nt = min(kSA, t1 - tb);
-        __syncwarp();
-        for (int tt = 0; tt < nt; ++tt)
-            cp_async8(&sm.dp[tt][lane], p.proj + (static_cast<size_t>(s) * T + tb + tt) * P2 + i, true);
+        __syncthreads();  // the previous pass is consumed
+        for (int q = tid; q < nt * kStPieces; q += 128) {
+            const int tt = q / kStPieces, k = q % kStPieces;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(
+                             reinterpret_cast<uint4*>(&sm.st[tt]) + k)),
+                         "l"(reinterpret_cast<const uint4*>(steps + rowbase + tb + tt) + k) : "memory");
+        }
+        for (int q = tid; q < nt * kCh16; q += 128) {
+            const int tt = q / kCh16, c = q % kCh16;
+            cp_async8(&sm.dp[tt][c], p.proj + (static_cast<size_t>(s) * T + tb + tt) * P2 + ch0 + c, true);
+            cp_async8(&sm.u[tt][c], p.u + (static_cast<size_t>(s) * T + row_at(p.order, tb + tt, T, p.grid)) * E + ch0 + c,
+                      true);
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
-        if (lane == 0) {
-            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
-            ptx::mbar_arrive_expect_tx(&sm.bar, bytes);
-            ptx::bulk_g2s(&sm.st[0], steps + rowbase + tb, bytes, &sm.bar);
-        }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        ptx::mbar_wait(&sm.bar, pass & 1);
-    for (int t = tb; t < tb + nt; ++t) {
-        const StepShared& ss = sm.st[t - tb];
-        const double x = dadd(sm.dp[t - tb][lane], bd);  // ssm.cpp:150-151
-        float ed;
-        const float df = softplus_f32(__double2float_rn(x), ed);
-        bool have = false;
-        double delta, pa, pb;
-        auto exact = [&]() {
-            if (!have) {
-                delta = softplus_call(x);
-                pa = exp_call(dmul(delta, Amax));
-                pb = dmul(delta, ss.Bmax);
-                have = true;
-            }
-        };
-        double sA = ss.Sa, sB = ss.Sb;
-        float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
-        float halfA = fmaf(-ss.hA1, ed, ss.hA0);
-        float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
-        if (dyn) {
-            fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh
-            const float x2m = df * Amax2f;
-            const float paf = ex2_approx(x2m);
-            const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
-            const float pbf = df * ss.Bmaxf;
-            const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
-            if (!(fl & 1u)) {
-                if (paf > thAf * (1.0f + ea)) {
-                    fl |= 1u;
-                } else if (paf >= thAf * (1.0f - ea)) {
+        __syncthreads();
+        for (int t = tb; t < tb + nt; ++t) {
+            const StepShared& ss = sm.st[t - tb];
+            const double x = dadd(sm.dp[t - tb][cl], bd);  // ssm.cpp:150-151
+            float ed;
+            const float df = softplus_f32(__double2float_rn(x), ed);
+            bool have = false;
+            double delta, pa, pb;
+            auto exact = [&]() {
+                if (!have) {
+                    delta = softplus_call(x);
+                    pa = exp_call(dmul(delta, Amax));
+                    pb = dmul(delta, ss.Bmax);
+                    have = true;
+                }
+            };
+            double sA = ss.Sa, sB = ss.Sb;
+            float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
+            float halfA = fmaf(-ss.hA1, ed, ss.hA0);
+            float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
+            if (dyn) {
+                fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh
+                const float x2m = df * Amax2f;
+                const float paf = ex2_approx(x2m);
+                const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
+                const float pbf = df * ss.Bmaxf;
+                const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
+                if (!(fl & 1u)) {
+                    if (paf > thAf * (1.0f + ea)) {
+                        fl |= 1u;
+                    } else if (paf >= thAf * (1.0f - ea)) {
+                        exact();
+                        if (pa > thA) fl |= 1u;
+                    }
+                }
+                if (!(fl & 2u)) {
+                    if (pbf > thBf * (1.0f + eb)) {
+                        fl |= 2u;
+                    } else if (pbf >= thBf * (1.0f - eb)) {
+                        exact();
+                        if (pb > thB) fl |= 2u;
+                    }
+                }
+                if (fl & 3u) {
                     exact();
-                    if (pa > thA) fl |= 1u;
+                    if (fl & 1u) {
+                        sA = scale_call(pa, qo);
+                        invA = __double2float_rn(recip_call(sA));
+                        qAf = qof;
+                        const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                        halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+                    }
+                    if (fl & 2u) {
+                        sB = scale_call(pb, qo);
+                        kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
+                        qBf = qof;
+                        halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                    }
                 }
             }
-            if (!(fl & 2u)) {
-                if (pbf > thBf * (1.0f + eb)) {
-                    fl |= 2u;
-                } else if (pbf >= thBf * (1.0f - eb)) {
-                    exact();
-                    if (pb > thB) fl |= 2u;
-                }
-            }
-            if (fl & 3u) {
-                exact();
-                if (fl & 1u) {
-                    sA = scale_call(pa, qo);
-                    invA = __double2float_rn(recip_call(sA));
-                    qAf = qof;
-                    const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
-                    halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
-                }
-                if (fl & 2u) {
-                    sB = scale_call(pb, qo);
-                    kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
-                    qBf = qof;
-                    halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
-                }
-            }
-        }
-        const float dfb = df * kB;
-        const float capA = qAf + 0.25f, capB = qBf + 0.25f;
-        int cq[32];
-        const bool tiny = sA < 1e-30;  // ex2.approx.ftz flushes below 2^-126
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {  // clamped quotients (k3_scan_c1's clamp form), exact where uncertified
-            const float qaq = fminf(ex2_approx(df * A2[m]) * invA, capA);
+            const float dfb = df * kB;
+            const float capA = qAf + 0.25f, capB = qBf + 0.25f;
+            // clamped quotients (k3_scan_c1's clamp form), exact where uncertified
+            int ca, cb;
+            const float qaq = fminf(ex2_approx(df * A2m) * invA, capA);
             const float ra = rintf(qaq);
-            if (tiny || !(fabsf(qaq - ra) <= halfA)) {
+            if (sA < 1e-30 || !(fabsf(qaq - ra) <= halfA)) {  // ex2.approx.ftz flushes below 2^-126
                 exact();
-                cq[m] = static_cast<int>(qdiv_call(exp_call(dmul(delta, arow[m])), sA, static_cast<double>(qAf)));
+                ca = static_cast<int>(qdiv_call(exp_call(dmul(delta, am)), sA, static_cast<double>(qAf)));
             } else {
-                cq[m] = static_cast<int>(ra);
+                ca = static_cast<int>(ra);
             }
             const float qbq = fminf(fmaxf(dfb * ss.BSf[m], -capB), capB);
             const float rb = rintf(qbq);
             if (!(fabsf(qbq - rb) <= halfB)) {
                 exact();
-                cq[16 + m] = static_cast<int>(qdiv_call(dmul(delta, ss.B[m]), sB, static_cast<double>(qBf)));
+                cb = static_cast<int>(qdiv_call(dmul(delta, ss.B[m]), sB, static_cast<double>(qBf)));
             } else {
-                cq[16 + m] = static_cast<int>(rb);
+                cb = static_cast<int>(rb);
+            }
+            SmallRec& rec = w.rec[(rowbase + t) * E + i];
+            reinterpret_cast<int8_t*>(&rec.ca)[m] = static_cast<int8_t>(ca);
+            reinterpret_cast<int8_t*>(&rec.cb)[m] = static_cast<int8_t>(cb);
+            if (m == 0) {
+                rec.sA = sA;
+                rec.sB = sB;
+                rec.fab = fl;
+                const float sBu = ((fl & 2u) ? __double2float_rn(sB) : ss.Sbf) * __double2float_rn(sm.u[t - tb][cl]);
+                rec.sAf = (fl & 1u) ? __double2float_rn(sA) : ss.Saf;
+                rec.sBu = sBu;
+                rec.qBsBu = ((fl & 2u) ? 127.0f : qaf) * fabsf(sBu);
             }
         }
-        const size_t e = (rowbase + t) * E + i;
-        uint4 cv[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            uint32_t* vw = reinterpret_cast<uint32_t*>(&cv[k]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                vw[j] = (static_cast<uint32_t>(cq[16 * k + 4 * j] & 0xFF)) | (static_cast<uint32_t>(cq[16 * k + 4 * j + 1] & 0xFF) << 8) |
-                        (static_cast<uint32_t>(cq[16 * k + 4 * j + 2] & 0xFF) << 16) |
-                        (static_cast<uint32_t>(cq[16 * k + 4 * j + 3] & 0xFF) << 24);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(w.rec + e);
-        dst[0] = cv[0];
-        dst[1] = cv[1];
-        dst[2] = make_uint4(__double2loint(sA), __double2hiint(sA), __double2loint(sB), __double2hiint(sB));
-        dst[3] = make_uint4(fl, 0u, 0u, 0u);
-    }
     }
 }
 
@@ -1527,125 +1525,125 @@ __device__ __forceinline__ void unpack_codes16(uint4 v, float (&c)[16]) {
     for (int m = 0; m < 16; ++m) c[m] = static_cast<float>(static_cast<int8_t>(wd[m >> 2] >> (8 * (m & 3))));
 }
 
-// (B) one thread per (direction, sample, channel): k3_scan_c1<FS>'s h update over the
-// steps; chunks of kSB steps (phase A's records, the scan input, the step records) are
-// staged in shared memory by cp.async / a bulk copy one chunk ahead
-constexpr int kSB = 8;
-struct SmallBSmem {
-    SmallRec rec[2][kSB][32];
-    double u[2][kSB][32];
-    StepShared st[2][kSB];
-    uint64_t bar[2];
+// (B') sixteen lanes per channel, lane m owning state m: the same update with the
+// per-channel decisions as group votes. phf <= theta' and max|d| <= half hold iff they
+// hold on every lane (fl32(x + a) is monotone in x; fmaxf(0, .) keeps the NaN rule of
+// the max chain), so the group's ballot decides the exact path exactly as (B) does; the
+// exact path's peak is a 16-lane max (shuffles within the group). A step's critical path
+// is then a handful of dependent f32 ops and one vote instead of 16 states in series.
+constexpr int kSB16 = 8;   // steps per staged chunk
+struct SmallB16Smem {
+    SmallRec rec[2][kSB16][kCh16];
+    double u[2][kSB16][kCh16];
+    StepShared st[2][kSB16];
 };
 
 template <int ABITS>
-__global__ void __launch_bounds__(32) k3s_state(const ScanDirs P, const StepShared* __restrict__ steps, SmallWork w) {
-    extern __shared__ __align__(16) uint8_t sb_smem_raw[];
-    SmallBSmem& sh = *reinterpret_cast<SmallBSmem*>(sb_smem_raw);
+__global__ void __launch_bounds__(128) k3s_state16(const ScanDirs P, const StepShared* __restrict__ steps,
+                                                   SmallWork w) {
+    extern __shared__ __align__(16) uint8_t sb16_smem_raw[];
+    SmallB16Smem& sh = *reinterpret_cast<SmallB16Smem*>(sb16_smem_raw);
     const int ndirs = P.n;
-    const int dir = static_cast<int>(blockIdx.x) % ndirs, grp = static_cast<int>(blockIdx.x) / ndirs;
+    const int dir = static_cast<int>(blockIdx.y) % ndirs, s = static_cast<int>(blockIdx.y) / ndirs;
     const ScanParams& p = P.d[dir];
-    const unsigned lane = threadIdx.x;
-    const int E = p.E, T = p.T, i = grp * 32 + static_cast<int>(lane), s = static_cast<int>(blockIdx.y);
+    const int tid = threadIdx.x, lane = tid & 31, cl = tid >> 4, m = tid & 15;
+    const int E = p.E, T = p.T, ch0 = static_cast<int>(blockIdx.x) * kCh16, i = ch0 + cl;
+    const unsigned gmask = 0xFFFFu << (lane & 16);
     const bool dyn = p.mode == MODE_DYNAMIC;
     constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;
     constexpr float qaf = static_cast<float>(qa);
     const double thH = p.cal[2].theta;
     const float thHlo = __double2float_rn(thH) * (1.0f - 4.0f * 5.9604645e-8f);
     const size_t rowbase = static_cast<size_t>(dir) * p.S * T + static_cast<size_t>(s) * T;
-    if (lane == 0) {
-        ptx::mbar_init(&sh.bar[0], 1);
-        ptx::mbar_init(&sh.bar[1], 1);
-        ptx::fence_barrier_init();
-    }
-    __syncwarp();
-    auto issue = [&](int t0, int buf) {
-        const int nt = min(kSB, T - t0);
-#pragma unroll
-        for (int tt = 0; tt < kSB; ++tt) {
+    constexpr int kStPieces = static_cast<int>(sizeof(StepShared) / 16);
+    auto issue = [&](int t0, int buf) {  // records, scan inputs and step records of chunk t0 (16-byte copies)
+        for (int q = tid; q < kSB16 * kCh16 * 4; q += 128) {
+            const int tt = q / (kCh16 * 4), c = (q / 4) % kCh16, k = q % 4;
             const int t = min(t0 + tt, T - 1);
-            const uint4* src = reinterpret_cast<const uint4*>(w.rec + (rowbase + t) * E + i);
-            uint4* dst = reinterpret_cast<uint4*>(&sh.rec[buf][tt][lane]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(dst + k)), "l"(src + k) : "memory");
-            cp_async8(&sh.u[buf][tt][lane], p.u + (static_cast<size_t>(s) * T + row_at(p.order, t, T, p.grid)) * E + i, true);
+            const uint4* src = reinterpret_cast<const uint4*>(w.rec + (rowbase + t) * E + ch0 + c) + k;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(
+                             reinterpret_cast<uint4*>(&sh.rec[buf][tt][c]) + k)), "l"(src) : "memory");
+        }
+        for (int q = tid; q < kSB16 * kCh16; q += 128) {
+            const int tt = q / kCh16, c = q % kCh16;
+            const int t = min(t0 + tt, T - 1);
+            cp_async8(&sh.u[buf][tt][c], p.u + (static_cast<size_t>(s) * T + row_at(p.order, t, T, p.grid)) * E + ch0 + c,
+                      true);
+        }
+        for (int q = tid; q < kSB16 * kStPieces; q += 128) {
+            const int tt = q / kStPieces, k = q % kStPieces;
+            const int t = min(t0 + tt, T - 1);
+            const uint4* src = reinterpret_cast<const uint4*>(steps + rowbase + t) + k;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(
+                             reinterpret_cast<uint4*>(&sh.st[buf][tt]) + k)), "l"(src) : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
-        if (lane == 0) {
-            const uint32_t bytes = static_cast<uint32_t>(nt * sizeof(StepShared));
-            ptx::mbar_arrive_expect_tx(&sh.bar[buf], bytes);
-            ptx::bulk_g2s(&sh.st[buf][0], steps + rowbase + t0, bytes, &sh.bar[buf]);
-        }
     };
-    float rhp[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) rhp[m] = 0.0f;
+    float rhp = 0.0f;  // this state's previous code (exact f32 integer)
     double sHp = 0.0;
     float sHf_prev = 0.0f, qHp = 0.0f;
     unsigned flh = 0;
     issue(0, 0);
-    for (int t0 = 0, ci = 0; t0 < T; t0 += kSB, ++ci) {
-        const int nt = min(kSB, T - t0), cur = ci & 1;
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        ptx::mbar_wait(&sh.bar[cur], (ci >> 1) & 1);
-        if (t0 + kSB < T) issue(t0 + kSB, cur ^ 1);
-        for (int tt = 0; tt < nt; ++tt) {
-            const int t = t0 + tt;
+    for (int t0 = 0, ci = 0; t0 < T; t0 += kSB16, ++ci) {
+        const int nt = min(kSB16, T - t0), cur = ci & 1;
+        if (t0 + kSB16 < T) {
+            issue(t0 + kSB16, cur ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        // the step's inputs that do not depend on the carried state, loaded (and the next
+        // step's prefetched) ahead of the carried chain so the in-order issue overlaps them
+        struct In {
+            float raf, cbf, sAf, sBu, qBsBu, qAf, invHf, Shf;
+            double Sh;
+            unsigned keep;
+        };
+        auto load = [&](int tt) {
+            In v;
             const StepShared& ss = sh.st[cur][tt];
-            const SmallRec& r = sh.rec[cur][tt][lane];
-            const double uv = sh.u[cur][tt][lane];
-            float raf[16], cb[16];
-            unpack_codes16(r.ca, raf);
-            unpack_codes16(r.cb, cb);
-            const double sA = r.sA, sB = r.sB;
-            const unsigned fab = r.fab;
-            const float qAf = (fab & 1u) ? 127.0f : qaf, qBf = (fab & 2u) ? 127.0f : qaf;
-            if (dyn) flh &= static_cast<unsigned>(ss.keep) & 4u;
-            const float sAf = (fab & 1u) ? __double2float_rn(sA) : ss.Saf;
-            const float sBf = (fab & 2u) ? __double2float_rn(sB) : ss.Sbf;
-            const float sAsH = sAf * sHf_prev, sBu = sBf * __double2float_rn(uv);
-            float hf[16];
-            float phf = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {  // packed f32x2, as k3_scan_c1<FS>
-                const float2 p1 = __fmul2_rn(__fmul2_rn(make_float2(raf[2 * k], raf[2 * k + 1]),
-                                                        make_float2(rhp[2 * k], rhp[2 * k + 1])), f2(sAsH));
-                const float2 p2 = __fmul2_rn(make_float2(cb[2 * k], cb[2 * k + 1]), f2(sBu));
-                const float2 hv = __fadd2_rn(p1, p2);
-                hf[2 * k] = hv.x;
-                hf[2 * k + 1] = hv.y;
-                phf = fmaxf(phf, fmaxf(fabsf(hv.x), fabsf(hv.y)));
-            }
-            const float maxD = fmaf(fmaf(qAf * qHp, sAsH, qBf * fabsf(sBu)), 5.3f * 5.9604645e-8f, 1e-37f);
-            double sH = ss.Sh, qH = qa;
-            float invHf = ss.invShf;
-            bool hexact = !(maxD < 1e30f);
-            if (dyn) hexact |= (flh & 4u) || !(fmaf(maxD, 1.0000003f, phf) < thHlo);
+            const SmallRec& r = sh.rec[cur][tt][cl];
+            v.raf = static_cast<float>(reinterpret_cast<const int8_t*>(&r.ca)[m]);
+            v.cbf = static_cast<float>(reinterpret_cast<const int8_t*>(&r.cb)[m]);
+            const float4 f = *reinterpret_cast<const float4*>(&r.fab);  // fab | sAf | sBu | qBsBu
+            v.qAf = (__float_as_uint(f.x) & 1u) ? 127.0f : qaf;
+            v.sAf = f.y;
+            v.sBu = f.z;
+            v.qBsBu = f.w;
+            v.keep = static_cast<unsigned>(ss.keep);
+            v.Sh = ss.Sh;
+            v.invHf = ss.invShf;
+            v.Shf = ss.Shf;
+            return v;
+        };
+        int8_t* rh_out = w.rh + ((rowbase + t0) * E + i) * 16 + m;
+        double* sh_out = w.sh + (rowbase + t0) * E + i;
+        In cu = load(0);
+#pragma unroll 1
+        for (int tt = 0; tt < nt; ++tt, rh_out += static_cast<size_t>(E) * 16, sh_out += E) {
+            if (dyn) flh &= cu.keep & 4u;
+            const float sAsH = cu.sAf * sHf_prev;
+            const float hv = __fadd_rn(__fmul_rn(__fmul_rn(cu.raf, rhp), sAsH), __fmul_rn(cu.cbf, cu.sBu));
+            const float maxD = fmaf(fmaf(cu.qAf * qHp, sAsH, cu.qBsBu), 5.3f * 5.9604645e-8f, 1e-37f);
+            double sH = cu.Sh, qH = qa;
+            float invHf = cu.invHf;
             const float capH = qaf + 0.25f;
             const float halfH = 0.5f - fmaf(maxD, invHf * 1.0001f, fmaf(qaf + 1.0f, 1.25e-7f, 1e-6f));
-            float chd[16];
-            float mdh = 0.0f;
-#pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const float q = fminf(fmaxf(__fmul_rn(hf[m], invHf), -capH), capH);
-                chd[m] = rintf(q);
-                mdh = fmaxf(mdh, fabsf(q - chd[m]));
-            }
-            hexact |= !(mdh <= halfH);
-            if (hexact) {  // the exact f64 update and k3_scan_c1's f64-state h logic
-                double hn[16];
-#pragma unroll
-                for (int m = 0; m < 16; ++m) {
-                    const double a_q = dmul(static_cast<double>(raf[m]), sA);
-                    const double b_q = dmul(static_cast<double>(cb[m]), sB);
-                    hn[m] = dadd(dmul(a_q, dmul(static_cast<double>(rhp[m]), sHp)), dmul(b_q, uv));
-                }
+            const float q = fminf(fmaxf(__fmul_rn(hv, invHf), -capH), capH);
+            float chd = rintf(q);
+            bool bad = !(fabsf(q - chd) <= halfH) || !(maxD < 1e30f);
+            if (dyn) bad |= (flh & 4u) || !(fmaf(maxD, 1.0000003f, fmaxf(0.0f, fabsf(hv))) < thHlo);
+            const In nx = load(tt + 1 < nt ? tt + 1 : tt);
+            if (__ballot_sync(0xffffffffu, bad) & gmask) {  // the channel's exact f64 update
+                const SmallRec& r = sh.rec[cur][tt][cl];
+                const double a_q = dmul(static_cast<double>(cu.raf), r.sA);
+                const double b_q = dmul(static_cast<double>(cu.cbf), r.sB);
+                const double hn = dadd(dmul(a_q, dmul(static_cast<double>(rhp), sHp)), dmul(b_q, sh.u[cur][tt][cl]));
                 if (dyn) {
-                    double ph = 0.0;
+                    double ph = fabs(hn);
 #pragma unroll
-                    for (int m = 0; m < 16; ++m) ph = fmax(ph, fabs(hn[m]));
+                    for (int o = 8; o >= 1; o >>= 1) ph = fmax(ph, __shfl_xor_sync(gmask, ph, o));
                     if (ph > thH) flh |= 4u;
                     if (flh & 4u) {
                         sH = scale_call(ph, qo);
@@ -1655,30 +1653,19 @@ __global__ void __launch_bounds__(32) k3s_state(const ScanDirs P, const StepShar
                 }
                 const float qHf = static_cast<float>(qH), capHx = qHf + 0.25f;
                 const float halfHx = 0.5f - fmaf(qHf + 1.0f, 2.3841858e-7f, 1e-6f);
-#pragma unroll
-                for (int m = 0; m < 16; ++m) {
-                    const float q = fminf(fmaxf(__double2float_rn(hn[m]) * invHf, -capHx), capHx);
-                    const float rr = rintf(q);
-                    chd[m] = !(fabsf(q - rr) <= halfHx) ? static_cast<float>(qdiv_call(hn[m], sH, qH)) : rr;
-                }
+                const float qx = fminf(fmaxf(__double2float_rn(hn) * invHf, -capHx), capHx);
+                const float rr = rintf(qx);
+                chd = !(fabsf(qx - rr) <= halfHx) ? static_cast<float>(qdiv_call(hn, sH, qH)) : rr;
             }
-            const size_t e = (rowbase + t) * E + i;
-            uint4 v;
-            uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                vw[j] = (static_cast<uint32_t>(static_cast<int>(chd[4 * j]) & 0xFF)) |
-                        (static_cast<uint32_t>(static_cast<int>(chd[4 * j + 1]) & 0xFF) << 8) |
-                        (static_cast<uint32_t>(static_cast<int>(chd[4 * j + 2]) & 0xFF) << 16) |
-                        (static_cast<uint32_t>(static_cast<int>(chd[4 * j + 3]) & 0xFF) << 24);
-            reinterpret_cast<uint4*>(w.rh)[e] = v;
-            w.sh[e] = sH;
-#pragma unroll
-            for (int m = 0; m < 16; ++m) rhp[m] = chd[m];
+            *rh_out = static_cast<int8_t>(static_cast<int>(chd));
+            if (m == 0) *sh_out = sH;
+            rhp = chd;
             sHp = sH;
-            sHf_prev = (flh & 4u) ? __double2float_rn(sH) : ss.Shf;
+            sHf_prev = (flh & 4u) ? __double2float_rn(sH) : cu.Shf;
             qHp = static_cast<float>(qH);
+            cu = nx;
         }
+        __syncthreads();  // chunk consumed before its buffer is refilled
     }
 }
 
@@ -1713,14 +1700,14 @@ static cudaError_t launch_small(const ScanDirs& P, int ndirs, const StepShared* 
     // refresh windows carry the a_bar / b_bar detector state; without refreshes it runs
     // through the whole sequence (static mode has none: any window)
     const int win = dyn ? (p.n_refresh > 0 ? p.n_refresh : p.T) : 8;
-    const int groups = p.E / 32, nwin = (p.T + win - 1) / win;
-    cudaError_t ea = ensure_smem_attr<k3s_codes<ABITS>>(static_cast<int>(sizeof(SmallASmem)));
+    const int nwin = (p.T + win - 1) / win;
+    cudaError_t ea = ensure_smem_attr<k3s_codes16<ABITS>>(static_cast<int>(sizeof(SmallA16Smem)));
     if (ea != cudaSuccess) return ea;
-    k3s_codes<ABITS><<<dim3(groups * ndirs, p.S * nwin), 32, sizeof(SmallASmem), st>>>(P, steps, w, win);
+    k3s_codes16<ABITS><<<dim3(p.E / kCh16, p.S * nwin * ndirs), 128, sizeof(SmallA16Smem), st>>>(P, steps, w, win);
     ++kernel_launch_counter();
-    cudaError_t e = ensure_smem_attr<k3s_state<ABITS>>(static_cast<int>(sizeof(SmallBSmem)));
+    cudaError_t e = ensure_smem_attr<k3s_state16<ABITS>>(static_cast<int>(sizeof(SmallB16Smem)));
     if (e != cudaSuccess) return e;
-    k3s_state<ABITS><<<dim3(groups * ndirs, p.S), 32, sizeof(SmallBSmem), st>>>(P, steps, w);
+    k3s_state16<ABITS><<<dim3(p.E / kCh16, p.S * ndirs), 128, sizeof(SmallB16Smem), st>>>(P, steps, w);
     ++kernel_launch_counter();
     const size_t n = static_cast<size_t>(ndirs) * p.S * p.T * p.E;
     k3s_out<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(P, steps, w);
