@@ -1366,15 +1366,28 @@ static SmallWork small_work(void* base, int S, int T, int E, int ndirs) {
 }
 
 constexpr int kSA = 16;  // steps staged per pass of phase A
-// (A') sixteen lanes per (channel, refresh window), lane m computing state m's a_bar /
-// b_bar codes; the channel's detector runs redundantly on its 16 lanes (same values, no
-// communication). CTA = 8 channels of one window; the window's step records and delta
-// inputs are staged in shared memory per pass of kSA steps.
+// (A') one CTA per (8 channels, refresh window). The channel's detector is split into
+// its independent parts: per (step, channel) the certified delta / peaks and the
+// detection of that step (exact where the f32 peak is within its bound of theta); the
+// sticky O state is a prefix OR along the window (maybe_refresh clears it), one thread
+// per channel; then per (step, channel) the step's scales and margins (outlier
+// channels' exact scales); then sixteen lanes per channel, lane m computing state m's
+// a_bar / b_bar codes from those. Same values as k3_scan_c1's per-step detector (the
+// OR of the per-step detections equals its sticky update, which skips the test once a
+// bit is set). The window's step records and inputs are staged per pass of kSA steps.
+struct SmallStepScal {  // per (step, channel)
+    float df, invA, dfb, halfA, halfB;
+    unsigned fl;
+    double sA, sB;
+};
 constexpr int kCh16 = 8;  // channels per CTA of the sixteen-lane phases (128 threads)
 struct SmallA16Smem {
     StepShared st[kSA];
     double dp[kSA][kCh16];
     double u[kSA][kCh16];
+    SmallStepScal sc[kSA][kCh16];
+    unsigned char det[kSA][kCh16];
+    double amax[kCh16], bd[kCh16];
 };
 
 template <int ABITS>
@@ -1393,20 +1406,22 @@ __global__ void __launch_bounds__(128) k3s_codes16(const ScanDirs P, const StepS
     const bool dyn = p.mode == MODE_DYNAMIC;
     constexpr double qa = static_cast<double>((1 << (ABITS - 1)) - 1), qo = 127.0;
     constexpr float qaf = static_cast<float>(qa), qof = 127.0f;
-    const double* __restrict__ arow = p.a + static_cast<size_t>(i) * 16;
-    const double am = arow[m];
+    const double am = p.a[static_cast<size_t>(i) * 16 + m];
     const float A2m = __double2float_rn(am * 1.4426950408889634);
-    double Amax = -1e300;
+    if (tid < kCh16) {
+        const double* arow = p.a + static_cast<size_t>(ch0 + tid) * 16;
+        double Amax = -1e300;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) Amax = fmax(Amax, arow[k]);
-    const float Amax2f = __double2float_rn(Amax * 1.4426950408889634);
+        for (int k = 0; k < 16; ++k) Amax = fmax(Amax, arow[k]);
+        sm.amax[tid] = Amax;
+        sm.bd[tid] = p.b_delta[ch0 + tid];
+    }
     const double thA = p.cal[0].theta, thB = p.cal[1].theta;
     const float thAf = __double2float_rn(thA), thBf = __double2float_rn(thB);
-    const double bd = p.b_delta[i];
     const size_t rowbase = static_cast<size_t>(dir) * p.S * T + static_cast<size_t>(s) * T;
     constexpr int kStPieces = static_cast<int>(sizeof(StepShared) / 16);
-    unsigned fl = 0;
-    for (int tb = t0; tb < t1; tb += kSA) {  // the pass's step records and delta inputs, staged
+    unsigned flc = 0;  // threads < kCh16: channel tid's O state along the window
+    for (int tb = t0; tb < t1; tb += kSA) {
         const int nt = min(kSA, t1 - tb);
         __syncthreads();  // the previous pass is consumed
         for (int q = tid; q < nt * kStPieces; q += 128) {
@@ -1424,97 +1439,129 @@ __global__ void __launch_bounds__(128) k3s_codes16(const ScanDirs P, const StepS
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
-        for (int t = tb; t < tb + nt; ++t) {
-            const StepShared& ss = sm.st[t - tb];
-            const double x = dadd(sm.dp[t - tb][cl], bd);  // ssm.cpp:150-151
-            float ed;
-            const float df = softplus_f32(__double2float_rn(x), ed);
-            bool have = false;
-            double delta, pa, pb;
-            auto exact = [&]() {
-                if (!have) {
-                    delta = softplus_call(x);
-                    pa = exp_call(dmul(delta, Amax));
-                    pb = dmul(delta, ss.Bmax);
-                    have = true;
-                }
-            };
-            double sA = ss.Sa, sB = ss.Sb;
-            float invA = ss.invSaf, kB = 1.0f, qAf = qaf, qBf = qaf;
-            float halfA = fmaf(-ss.hA1, ed, ss.hA0);
-            float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
-            if (dyn) {
-                fl &= static_cast<unsigned>(ss.keep);  // maybe_refresh
-                const float x2m = df * Amax2f;
+        // (1) per (step, channel): this step's detection (detect_outliers, channel-local form)
+        if (dyn) {
+            for (int q = tid; q < nt * kCh16; q += 128) {
+                const int tt = q / kCh16, c = q % kCh16;
+                const StepShared& ss = sm.st[tt];
+                const double x = dadd(sm.dp[tt][c], sm.bd[c]);  // ssm.cpp:150-151
+                float ed;
+                const float df = softplus_f32(__double2float_rn(x), ed);
+                const float x2m = df * __double2float_rn(sm.amax[c] * 1.4426950408889634);
                 const float paf = ex2_approx(x2m);
                 const float ea = 2.0f * fmaf(0.6931472f * fabsf(x2m), ed + 1.1920929e-7f, 4.7683716e-7f) + 1e-6f;
                 const float pbf = df * ss.Bmaxf;
                 const float eb = 2.0f * (ed + 2.3841858e-7f) + 1e-6f;
-                if (!(fl & 1u)) {
-                    if (paf > thAf * (1.0f + ea)) {
-                        fl |= 1u;
-                    } else if (paf >= thAf * (1.0f - ea)) {
-                        exact();
-                        if (pa > thA) fl |= 1u;
+                unsigned d = 0;
+                bool have = false;
+                double pa = 0.0, pb = 0.0;
+                auto exact = [&]() {
+                    if (!have) {
+                        const double delta = softplus_call(x);
+                        pa = exp_call(dmul(delta, sm.amax[c]));
+                        pb = dmul(delta, ss.Bmax);
+                        have = true;
                     }
-                }
-                if (!(fl & 2u)) {
-                    if (pbf > thBf * (1.0f + eb)) {
-                        fl |= 2u;
-                    } else if (pbf >= thBf * (1.0f - eb)) {
-                        exact();
-                        if (pb > thB) fl |= 2u;
-                    }
-                }
-                if (fl & 3u) {
+                };
+                if (paf > thAf * (1.0f + ea)) {
+                    d |= 1u;
+                } else if (paf >= thAf * (1.0f - ea)) {
                     exact();
-                    if (fl & 1u) {
-                        sA = scale_call(pa, qo);
-                        invA = __double2float_rn(recip_call(sA));
-                        qAf = qof;
-                        const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
-                        halfA = 0.5f - fmaf(qAf + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
-                    }
-                    if (fl & 2u) {
-                        sB = scale_call(pb, qo);
-                        kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
-                        qBf = qof;
-                        halfB = 0.5f - fmaf(qBf + 1.0f, ed + 4.7683716e-7f, 1e-6f);
-                    }
+                    if (pa > thA) d |= 1u;
+                }
+                if (pbf > thBf * (1.0f + eb)) {
+                    d |= 2u;
+                } else if (pbf >= thBf * (1.0f - eb)) {
+                    exact();
+                    if (pb > thB) d |= 2u;
+                }
+                sm.det[tt][c] = static_cast<unsigned char>(d);
+            }
+            __syncthreads();
+            // (2) the sticky O state: maybe_refresh, then the step's detection
+            if (tid < kCh16) {
+                for (int tt = 0; tt < nt; ++tt) {
+                    flc = (flc & static_cast<unsigned>(sm.st[tt].keep)) | sm.det[tt][tid];
+                    sm.sc[tt][tid].fl = flc;
                 }
             }
-            const float dfb = df * kB;
+        } else {
+            for (int q = tid; q < nt * kCh16; q += 128) sm.sc[q / kCh16][q % kCh16].fl = 0u;
+        }
+        __syncthreads();
+        // (3) per (step, channel): scales and margins of the step (outlier channels: their
+        // exact scales), and the record's scalars
+        for (int q = tid; q < nt * kCh16; q += 128) {
+            const int tt = q / kCh16, c = q % kCh16;
+            const StepShared& ss = sm.st[tt];
+            SmallStepScal& sc = sm.sc[tt][c];
+            const unsigned fl = sc.fl;
+            const double x = dadd(sm.dp[tt][c], sm.bd[c]);
+            float ed;
+            const float df = softplus_f32(__double2float_rn(x), ed);
+            double sA = ss.Sa, sB = ss.Sb;
+            float invA = ss.invSaf, kB = 1.0f;
+            float halfA = fmaf(-ss.hA1, ed, ss.hA0);
+            float halfB = fmaf(-(qaf + 1.0f), ed, 0.5f - fmaf(qaf + 1.0f, 4.7683716e-7f, 1e-6f));
+            if (fl & 3u) {
+                const double delta = softplus_call(x);
+                if (fl & 1u) {
+                    sA = scale_call(exp_call(dmul(delta, sm.amax[c])), qo);
+                    invA = __double2float_rn(recip_call(sA));
+                    const float LA = 0.6931472f * (1.0f + fmaxf(0.0f, -__log2f(__double2float_rn(sA))));
+                    halfA = 0.5f - fmaf(qof + 1.0f, fmaf(LA, ed + 1.1920929e-7f, 4.7683716e-7f), 1e-6f);
+                }
+                if (fl & 2u) {
+                    sB = scale_call(dmul(delta, ss.Bmax), qo);
+                    kB = __double2float_rn(recip_call(sB)) / ss.invSbf;
+                    halfB = 0.5f - fmaf(qof + 1.0f, ed + 4.7683716e-7f, 1e-6f);
+                }
+            }
+            sc.df = df;
+            sc.invA = invA;
+            sc.dfb = df * kB;
+            sc.halfA = halfA;
+            sc.halfB = halfB;
+            sc.sA = sA;
+            sc.sB = sB;
+            SmallRec& rec = w.rec[(rowbase + tb + tt) * E + ch0 + c];
+            rec.sA = sA;
+            rec.sB = sB;
+            rec.fab = fl;
+            const float sBu = ((fl & 2u) ? __double2float_rn(sB) : ss.Sbf) * __double2float_rn(sm.u[tt][c]);
+            rec.sAf = (fl & 1u) ? __double2float_rn(sA) : ss.Saf;
+            rec.sBu = sBu;
+            rec.qBsBu = ((fl & 2u) ? qof : qaf) * fabsf(sBu);
+        }
+        __syncthreads();
+        // (4) sixteen lanes per channel: state m's clamped quotients (k3_scan_c1's clamp
+        // form), exact where uncertified
+        for (int tt = 0; tt < nt; ++tt) {
+            const StepShared& ss = sm.st[tt];
+            const SmallStepScal& sc = sm.sc[tt][cl];
+            const unsigned fl = sc.fl;
+            const float qAf = (fl & 1u) ? qof : qaf, qBf = (fl & 2u) ? qof : qaf;
             const float capA = qAf + 0.25f, capB = qBf + 0.25f;
-            // clamped quotients (k3_scan_c1's clamp form), exact where uncertified
             int ca, cb;
-            const float qaq = fminf(ex2_approx(df * A2m) * invA, capA);
+            const float qaq = fminf(ex2_approx(sc.df * A2m) * sc.invA, capA);
             const float ra = rintf(qaq);
-            if (sA < 1e-30 || !(fabsf(qaq - ra) <= halfA)) {  // ex2.approx.ftz flushes below 2^-126
-                exact();
-                ca = static_cast<int>(qdiv_call(exp_call(dmul(delta, am)), sA, static_cast<double>(qAf)));
+            if (sc.sA < 1e-30 || !(fabsf(qaq - ra) <= sc.halfA)) {  // ex2.approx.ftz flushes below 2^-126
+                const double delta = softplus_call(dadd(sm.dp[tt][cl], sm.bd[cl]));
+                ca = static_cast<int>(qdiv_call(exp_call(dmul(delta, am)), sc.sA, static_cast<double>(qAf)));
             } else {
                 ca = static_cast<int>(ra);
             }
-            const float qbq = fminf(fmaxf(dfb * ss.BSf[m], -capB), capB);
+            const float qbq = fminf(fmaxf(sc.dfb * ss.BSf[m], -capB), capB);
             const float rb = rintf(qbq);
-            if (!(fabsf(qbq - rb) <= halfB)) {
-                exact();
-                cb = static_cast<int>(qdiv_call(dmul(delta, ss.B[m]), sB, static_cast<double>(qBf)));
+            if (!(fabsf(qbq - rb) <= sc.halfB)) {
+                const double delta = softplus_call(dadd(sm.dp[tt][cl], sm.bd[cl]));
+                cb = static_cast<int>(qdiv_call(dmul(delta, ss.B[m]), sc.sB, static_cast<double>(qBf)));
             } else {
                 cb = static_cast<int>(rb);
             }
-            SmallRec& rec = w.rec[(rowbase + t) * E + i];
+            SmallRec& rec = w.rec[(rowbase + tb + tt) * E + i];
             reinterpret_cast<int8_t*>(&rec.ca)[m] = static_cast<int8_t>(ca);
             reinterpret_cast<int8_t*>(&rec.cb)[m] = static_cast<int8_t>(cb);
-            if (m == 0) {
-                rec.sA = sA;
-                rec.sB = sB;
-                rec.fab = fl;
-                const float sBu = ((fl & 2u) ? __double2float_rn(sB) : ss.Sbf) * __double2float_rn(sm.u[t - tb][cl]);
-                rec.sAf = (fl & 1u) ? __double2float_rn(sA) : ss.Saf;
-                rec.sBu = sBu;
-                rec.qBsBu = ((fl & 2u) ? 127.0f : qaf) * fabsf(sBu);
-            }
         }
     }
 }
