@@ -127,11 +127,14 @@ def test_detect_quantize_matches_oracle(oracle_checker, gpu_ctx, abits, n_refres
         assert n_outliers > 0
 
 
+@pytest.mark.parametrize("S,E", [(2, 64), (8, 768)])
 @pytest.mark.parametrize("src", [1, 2])
-def test_detect_quantize_sources(oracle_checker, gpu_ctx, src):
-    """RMSNorm (D1) and merge-gate sources: channel-parallel == literal kernel."""
+def test_detect_quantize_sources(oracle_checker, gpu_ctx, src, S, E):
+    """RMSNorm (D1) and merge-gate sources: channel-parallel == literal kernel
+    (merge: the lane-per-channel kernel of small batches, S x E <= 148 x 32, and
+    the four-channel kernel above that)."""
     import torch
-    S, T, E = 2, 25, 64
+    T = 25
     rng = np.random.default_rng(src)
     x = _dev(rng.normal(size=(S, T, E)) * 3)
     x2 = _dev(rng.normal(size=(S, T, E)))
@@ -217,16 +220,18 @@ def test_scan_order_geometry_validated(gpu_ctx):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("E", [64, 192, 768])
+@pytest.mark.parametrize("S,E", [(3, 64), (3, 192), (3, 768), (8, 768)])
 @pytest.mark.parametrize("src", [0, 1])
-def test_detect_quantize_window_staged_literal_identical(gpu_ctx, E, src):
-    """Plain / RMSNorm sources: the bulk-copy staged kernel (literal=0), the
-    register window kernel (literal=2, E % 64 == 0) and the literal detector
-    (literal=1) give identical operands — dynamic (refresh windows of 8, 10 and
-    12+ rows, quotient bound theta/S below and above 2^14) and static (quotients
-    up to 1e12, beyond the low-word range), every scan order, int8 and packed."""
+def test_detect_quantize_window_staged_literal_identical(gpu_ctx, S, E, src):
+    """Plain / RMSNorm sources: the default channel-parallel kernel (literal=0:
+    the register window kernel for small batches, S x E <= 148 x 32, else the
+    bulk-copy staged kernel), the register window kernel (literal=2) and the
+    literal detector (literal=1) give identical operands — dynamic (refresh
+    windows of 8, 10 and 12+ rows, quotient bound theta/S below and above 2^14)
+    and static (quotients up to 1e12, beyond the low-word range), every scan
+    order, int8 and packed."""
     import torch
-    S, T = 3, 36  # T = 6^2 for the column orders
+    T = 36  # T = 6^2 for the column orders
     rng = np.random.default_rng(E + src)
     x = rng.normal(size=(S, T, E)) * 2.0
     x[rng.random((S, T, E)) < 0.02] *= 40.0
