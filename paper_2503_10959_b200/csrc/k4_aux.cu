@@ -16,18 +16,23 @@ namespace ob {
 // while the current one is multiplied. Every output keeps its own sequential
 // k order, so tiling does not change a bit of the result. FP64-bound: a MAC is a
 // separately rounded DMUL + DADD (the reference builds with -ffp-contract=off).
-constexpr int DG_BM = 128, DG_BN = 64, DG_BK = 16, DG_TM = 8;
+// Small problems (fewer 128x64 tiles than SMs, e.g. the batch-1 patch embedding:
+// 6 CTAs of 256 threads for 196 x 192 outputs, 104 us) take 16x16 tiles, one output
+// per thread (TM = TN = 1): the same per-output k order, 156 CTAs.
+constexpr int DG_BK = 16;
 
+template <int TM, int TN>
 __global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
+    constexpr int DG_BM = 16 * TM, DG_BN = 16 * TN, DG_TM = TM;
     __shared__ double sa[DG_BK][DG_BM + 1];
     __shared__ double sw[DG_BK][DG_BN + 1];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int m0 = blockIdx.y * DG_BM, r0 = blockIdx.x * DG_BN;
-    double acc[DG_TM][4];
+    double acc[DG_TM][TN];
 #pragma unroll
     for (int i = 0; i < DG_TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
     // k-tile element idx = threadIdx.x + 256 * u: row idx / 16, k idx % 16 (128 B runs)
     double ra[DG_BM * DG_BK / 256], rw[DG_BN * DG_BK / 256];
     auto fetch = [&](int k0) {
@@ -58,15 +63,15 @@ __global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
         if (k0 + DG_BK < p.K) fetch(k0 + DG_BK);  // in flight during this tile's products
         const int kk = min(DG_BK, p.K - k0);
         for (int k = 0; k < kk; ++k) {
-            double av[DG_TM], wv[4];
+            double av[DG_TM], wv[TN];
 #pragma unroll
             for (int i = 0; i < DG_TM; ++i) av[i] = sa[k][ty + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) wv[j] = sw[k][tx + 16 * j];
+            for (int j = 0; j < TN; ++j) wv[j] = sw[k][tx + 16 * j];
 #pragma unroll
             for (int i = 0; i < DG_TM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = dadd(acc[i][j], dmul(av[i], wv[j]));
+                for (int j = 0; j < TN; ++j) acc[i][j] = dadd(acc[i][j], dmul(av[i], wv[j]));
         }
         __syncthreads();
     }
@@ -75,7 +80,7 @@ __global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
         const int m = m0 + ty + 16 * i;
         if (m >= p.M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < TN; ++j) {
             const int r = r0 + tx + 16 * j;
             if (r >= p.R) continue;
             double y = dadd(0.0, acc[i][j]);
@@ -101,8 +106,12 @@ __global__ void __launch_bounds__(256) k4_dgemm(const DGemmParams p) {
 
 cudaError_t launch_dgemm(const DGemmParams& p, cudaStream_t st) {
     if (p.M < 1 || p.R < 1 || p.K < 1) return cudaErrorInvalidValue;
-    dim3 grid((p.R + DG_BN - 1) / DG_BN, (p.M + DG_BM - 1) / DG_BM);
-    k4_dgemm<<<grid, 256, 0, st>>>(p);
+    const long big_tiles = static_cast<long>((p.R + 63) / 64) * ((p.M + 127) / 128);
+    if (big_tiles >= 148) {
+        k4_dgemm<8, 4><<<dim3((p.R + 63) / 64, (p.M + 127) / 128), 256, 0, st>>>(p);
+    } else {
+        k4_dgemm<1, 1><<<dim3((p.R + 15) / 16, (p.M + 15) / 16), 256, 0, st>>>(p);
+    }
     ++kernel_launch_counter();
     return cudaGetLastError();
 }

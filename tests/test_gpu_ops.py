@@ -263,3 +263,27 @@ def test_detect_quantize_window_staged_literal_identical(gpu_ctx, S, E, src):
                 elif not packed and order == -1:
                     c = outs[0]["codes"].reshape(S, T, E)
                     assert c[0, 5, 3] == 7 and c[1, 7, 10] == -7, tag  # saturated, not wrapped
+
+
+@pytest.mark.parametrize("M,R,K", [(196, 192, 48), (200, 1000, 32), (1280, 960, 32)])
+def test_dgemm_tiles_sequential_k(gpu_ctx, M, R, K):
+    """The f64 projection GEMM (detail::mm, tensor.cpp:373-382): every output is
+    0.0 + a[m][0] w[r][0] + a[m][1] w[r][1] + ... with separately rounded
+    products and sums in ascending k, for both tile shapes (16x16 for problems
+    with fewer 128x64 tiles than SMs, 128x64 above), store / bias / residual."""
+    import paper_2503_10959_b200 as ob
+    import torch
+    rng = np.random.default_rng(M + R + K)
+    a = rng.normal(size=(M, K))
+    w = rng.normal(size=(R, K))
+    bias = rng.normal(size=R)
+    prev = rng.normal(size=(M, R))
+    acc = np.zeros((M, R))
+    for k in range(K):
+        acc = acc + a[:, k:k + 1] * w[:, k][None, :]
+    acc = 0.0 + acc
+    for post, want in ((ob.POST_STORE, acc), (ob.POST_BIAS, acc + bias[None, :]), (ob.POST_RESID, prev + acc)):
+        out = _dev(prev.copy()) if post == ob.POST_RESID else None
+        got = gpu_ctx.dgemm(_dev(a), _dev(w), post=post, out=out, bias=_dev(bias) if post == ob.POST_BIAS else None)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), want), post
