@@ -224,7 +224,16 @@ __global__ void k4_meanpool(const double* __restrict__ x, double* __restrict__ p
     const int s = blockIdx.y;
     if (i >= E) return;
     double acc = 0.0;
-    for (int t = 0; t < T; ++t) acc = dadd(acc, x[(static_cast<size_t>(s) * T + t) * E + i]);
+    const double* xs = x + static_cast<size_t>(s) * T * E + i;
+    int t = 0;
+    for (; t + 8 <= T; t += 8) {  // eight rows' loads in flight, then the sums in ascending t
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = xs[static_cast<size_t>(t + j) * E];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = dadd(acc, v[j]);
+    }
+    for (; t < T; ++t) acc = dadd(acc, xs[static_cast<size_t>(t) * E]);
     pooled[static_cast<size_t>(s) * E + i] = dmul(acc, __ddiv_rn(1.0, static_cast<double>(T)));
 }
 
