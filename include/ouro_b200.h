@@ -219,7 +219,8 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * 2 fast path with every a_bar/b_bar code computed in exact f64 (test aid),
  * 3 / 4 / 5 / 6 fast path on two threads per channel (f32 state) / one thread
  * per channel (f64 state) / one thread per channel (f32 state) / two threads per
- * channel (f64 state) (A/B aid);
+ * channel (f64 state) (A/B aid); 7 the one-thread f32-state kernel in its
+ * large-grid shape (A in shared memory) at any size (test aid);
  * "k1_variant" = 0 auto (channel-parallel K1 wherever exact), 1 literal
  * detector kernel everywhere, 2 auto with the register window plain / RMSNorm
  * kernel (A/B aid); "pack_a4" = 1: A4 activation codes travel

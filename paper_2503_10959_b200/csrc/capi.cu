@@ -675,7 +675,7 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         require(m && key, "model_set_option: NULL argument");
         const std::string k(key);
         if (k == "scan_variant") {
-            require(value >= 0 && value <= 6, "model_set_option: scan_variant must be 0..6");
+            require(value >= 0 && value <= 7, "model_set_option: scan_variant must be 0..7");
             m->m->scan_variant = static_cast<int>(value);
         } else if (k == "feed_chunks") {
             require(value >= 1 && value <= 64, "model_set_option: feed_chunks must be in [1, 64]");

@@ -193,7 +193,8 @@ class Model {
     int scan_variant = 0;  // 0 auto (fast path when exact), 1 per-direction reference kernel, 2 fast path, exact codes only,
                            // 3 fast path on the two-threads-per-channel kernel, 4 on the one-thread-per-channel kernel
                            // (f64 state update), 5 the one-thread-per-channel kernel with the f32 state update,
-                           // 6 the two-threads-per-channel kernel with the f64 state update
+                           // 6 the two-threads-per-channel kernel with the f64 state update, 7 the
+                           // one-thread f32-state kernel in its large-grid shape (A in shared memory)
 
     // workspace
     struct Work {

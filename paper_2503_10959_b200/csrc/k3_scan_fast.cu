@@ -1292,14 +1292,14 @@ static cudaError_t launch_fast(const ScanDirs& P, int ndirs, const StepShared* s
 // two-threads-per-channel kernel, 2 the one-thread-per-channel kernel with the f32 state update
 template <int ABITS, bool FS>
 static cudaError_t launch_c1_any(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st, bool exact,
-                                 bool trace) {
+                                 bool trace, bool force_big = false) {
     if (exact) return trace ? launch_c1<true, ABITS, true, FS>(P, ndirs, steps, st) : launch_c1<true, ABITS, false, FS>(P, ndirs, steps, st);
     if (trace) return launch_c1<false, ABITS, true, FS>(P, ndirs, steps, st);
     // FS on large grids (>= 2 waves of 16 CTAs per SM): A stays in shared memory and the
     // kernel fits 128 registers, 16 warps per SM (Vim-B batch 256: 1.705 vs 1.741 ms); small
     // grids keep 168 registers (Vim-S batch 64: 0.286 vs 0.296)
     const long ctas = static_cast<long>((P.d[0].E + 31) / 32) * P.d[0].S * ndirs;
-    const bool big = ctas >= 2L * 148 * 16;
+    const bool big = force_big || ctas >= 2L * 148 * 16;
     if (FS && P.merge_cnt) {
         if (big) return launch_c1<false, ABITS, false, FS, 13, true, true>(P, ndirs, steps, st);
         return launch_c1<false, ABITS, false, FS, kC1MinBlocks, false, true>(P, ndirs, steps, st);
@@ -1310,9 +1310,9 @@ static cudaError_t launch_c1_any(const ScanDirs& P, int ndirs, const StepShared*
 
 template <int ABITS>
 static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared* steps, cudaStream_t st,
-                                 int kernel, bool exact, bool trace) {
+                                 int kernel, bool exact, bool trace, bool force_big = false) {
     if (kernel == 0) return launch_c1_any<ABITS, false>(P, ndirs, steps, st, exact, trace);
-    if (kernel == 2) return launch_c1_any<ABITS, true>(P, ndirs, steps, st, exact, trace);
+    if (kernel == 2) return launch_c1_any<ABITS, true>(P, ndirs, steps, st, exact, trace, force_big);
     if (kernel == 3) {  // two threads per channel, f32 state update
         if (exact) return trace ? launch_fast<true, ABITS, true, true>(P, ndirs, steps, st) : launch_fast<true, ABITS, false, true>(P, ndirs, steps, st);
         return trace ? launch_fast<false, ABITS, true, true>(P, ndirs, steps, st) : launch_fast<false, ABITS, false, true>(P, ndirs, steps, st);
@@ -1804,6 +1804,10 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
         kernel = variant == 3 ? 0 : 2;
     }
     if (variant == 5) kernel = 1;
+    if (variant == 6) {  // the large-grid shape of the f32-state kernel (A in shared memory) at any size
+        if (!even) return cudaErrorNotSupported;
+        kernel = 2;
+    }
     const bool exact = variant == 1;
     // the out_proj input K1 rides on the f32-state kernel's tail (plain, non-trace launches;
     // the caller zeroes ocnt and keeps merge_cnt zero between launches)
@@ -1824,8 +1828,8 @@ cudaError_t launch_scan_fast(const ScanParams* dirs, int ndirs, void* work, size
                                   : launch_small<8>(P, ndirs, steps, small_base, st);
     }
     switch (dirs[0].abits) {
-        case 4: return launch_kernel<4>(P, ndirs, steps, st, kernel, exact, trace);
-        default: return launch_kernel<8>(P, ndirs, steps, st, kernel, exact, trace);
+        case 4: return launch_kernel<4>(P, ndirs, steps, st, kernel, exact, trace, variant == 6);
+        default: return launch_kernel<8>(P, ndirs, steps, st, kernel, exact, trace, variant == 6);
     }
 }
 

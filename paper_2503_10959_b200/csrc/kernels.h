@@ -181,8 +181,9 @@ cudaError_t launch_scan(const ScanParams& p, cudaStream_t st, bool* used_literal
 // per channel for A4 and even E, on two per channel otherwise); 1: the same with the
 // certified f32 codes disabled (every element exact f64); 2: two threads per
 // channel, f32 state; 3 / 4: one thread per channel with the f64 / f32 state update
-// (even E); 5: two threads per channel, f64 state. Non-null `masks` selects the
-// parity-trace instantiation.
+// (even E); 5: two threads per channel, f64 state; 6: one thread per channel, f32
+// state, in its large-grid shape (A in shared memory, 128 registers) at any size.
+// Non-null `masks` selects the parity-trace instantiation.
 // E > 0: also the small-batch split-phase scan's intermediates when S * E * ndirs
 // is below one warp per SM (launch_scan_fast then uses that path in auto mode)
 size_t scan_fast_workspace_bytes(int S, int T, int ndirs, int E = 0);

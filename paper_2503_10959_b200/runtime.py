@@ -423,7 +423,8 @@ class Model:
 
     def set_option(self, key: str, value: int) -> None:
         """Engine option, e.g. scan_variant (0 auto, 1 reference kernel, 2 exact codes, 3 / 6 two threads per
-        channel with the f32 / f64 state update, 4 / 5 one thread per channel with the f64 / f32 state update)."""
+        channel with the f32 / f64 state update, 4 / 5 one thread per channel with the f64 / f32 state update, 7 the
+        one-thread f32-state kernel in its large-grid shape)."""
         L.check(self.lib.ouro_b200_model_set_option(self.h, key.encode(), int(value)))
 
     def use_graphs(self, on: bool = True) -> None:

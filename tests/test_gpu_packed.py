@@ -170,12 +170,15 @@ def test_merge_fused_into_scan_identical(oracle_checker, gpu_ctx, pack):
     gcal = gm.calibration_from([conv(t) for t in ocal.scan], [conv(t) for t in ocal.lin],
                                ob.QuantSpec(4, 4, 8, 3, 0.05, True, True))
     gm.set_option("pack_a4", pack)
-    for mode in (ob.MODE_DYNAMIC, ob.MODE_STATIC):
-        outs = []
-        for f in (1, 0):
-            gm.set_option("merge_fuse", f)
-            outs.append(gm.forward_host(imgs, gcal, mode))
-        gm.set_option("merge_fuse", 0)
-        assert np.array_equal(outs[0], outs[1]), mode
-        assert np.array_equal(outs[0], om.forward(imgs, om.calib_from(ocal), mode)), mode
+    for sv in (0, 7):  # 7: the scan kernel's large-grid shape (A in shared memory), as at batch 256
+        gm.set_option("scan_variant", sv)
+        for mode in (ob.MODE_DYNAMIC, ob.MODE_STATIC):
+            outs = []
+            for f in (1, 0):
+                gm.set_option("merge_fuse", f)
+                outs.append(gm.forward_host(imgs, gcal, mode))
+            gm.set_option("merge_fuse", 0)
+            assert np.array_equal(outs[0], outs[1]), (sv, mode)
+            assert np.array_equal(outs[0], om.forward(imgs, om.calib_from(ocal), mode)), (sv, mode)
+    gm.set_option("scan_variant", 0)
     gm.set_option("pack_a4", 0)

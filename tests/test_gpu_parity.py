@@ -207,18 +207,20 @@ def test_k1_variants_identical(pair, abits):
 
 @pytest.mark.parametrize("abits", [4, 8])
 def test_scan_variants_identical(pair, abits):
-    """K3 fast path (certified f32 codes + exact fallbacks), its all-exact
-    variant, the per-direction reference kernel and both fast kernels (one and
-    two threads per channel) agree bit-for-bit."""
+    """K3 fast path (certified f32 codes + exact fallbacks; at this batch the
+    small-batch split-phase scan), its all-exact variant, the per-direction
+    reference kernel and every fast kernel (one and two threads per channel,
+    f32 / f64 state, the large-grid shape with A in shared memory that the
+    benchmark batch runs) agree bit-for-bit."""
     om, gm, imgs, cimgs = pair
     spec = _spec(abits, rho=0.05)
     gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
     outs = []
-    for v in (0, 1, 2, 3, 4, 5, 6):
+    for v in (0, 1, 2, 3, 4, 5, 6, 7):
         gm.set_option("scan_variant", v)
         outs.append(gm.forward_host(imgs, gcal, 1))
     gm.set_option("scan_variant", 0)
-    for v in (1, 2, 3, 4, 5, 6):
+    for v in (1, 2, 3, 4, 5, 6, 7):
         assert np.array_equal(outs[0], outs[v]), v
 
 
