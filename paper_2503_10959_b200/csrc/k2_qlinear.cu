@@ -37,12 +37,18 @@ namespace ob {
 
 constexpr int kBM = 128, kBK = 128;
 constexpr int kStgBufs = 1;  // epilogue staging buffers per warp
-// Two shapes of the same kernel, chosen per call (launch_qlinear):
-//  * EW = 8 epilogue warps, 4 operand stages: main-loop-heavy calls (wide R);
-//  * EW = 16 epilogue warps, 2 operand stages, setmaxnreg moving registers from
-//    warpgroup 0 to the epilogue: epilogue-heavy calls (residual post-op,
-//    outlier terms; the f64 epilogue, not the int8 main loop, bounds those —
-//    main loop alone 0.039 ms of 0.135 for the Vim-B out_proj).
+// Shapes of the same kernel, chosen per call (launch_qlinear). The f64 epilogue, not the
+// int8 main loop, bounds K2 (Vim-B in_proj: main loop alone 61 of 159 us; each epilogue
+// warp's chunks are a serial chain of TMEM load, f64 dequant / outlier terms, staging and
+// the TMA store's smem read), so more epilogue warps pay where the grid is full:
+//  * ONEBOX: 16 epilogue warps (setmaxnreg moving registers from warpgroup 0), one 4 KB
+//    staging box per warp reused by the chunk's two boxes, 4 operand stages — calls of at
+//    least a wave of tiles, K <= 1024, no residual (in_proj 141 vs 159 us, x_proj 87 vs
+//    95 us with the 8-warp shape);
+//  * 16 epilogue warps, two boxes per warp, 2 stages: the residual post-op (its tile is
+//    loaded into the boxes) and narrow calls below a wave;
+//  * 8 epilogue warps, 4 stages: wide calls below a wave or with K > 1024 (its hoisted,
+//    vectorised outlier walk); with the unpack warpgroup for the packed A4 operand (PK).
 template <int EW, bool PK = false>
 struct K2Cfg {
     static constexpr int kEpiWarps = EW;
@@ -52,14 +58,18 @@ struct K2Cfg {
     static constexpr int kMaskWords = 24;  // mask words per row staged in shared memory (K <= 768; else global)
 };
 
-template <int BN, int EW>
+// ONEBOX (16 epilogue warps, no residual): one 4 KB staging box per warp, reused by the
+// chunk's two boxes, pays for four operand stages instead of two (16 x 4 KB + 4 x 32 KB +
+// metadata = 225 KB)
+template <int BN, int EW, bool ONEBOX = false>
 struct K2Smem {
-    static constexpr int kStages = K2Cfg<EW>::kStages, kEpiWarps = EW, kMaskWords = K2Cfg<EW>::kMaskWords;
+    static constexpr int kStages = ONEBOX ? 4 : K2Cfg<EW>::kStages, kEpiWarps = EW, kMaskWords = K2Cfg<EW>::kMaskWords;
+    static constexpr int kStgBytes = ONEBOX ? 4096 : 8192;
     static constexpr int kABytes = kBM * kBK;
     static constexpr int kBBytes = BN * kBK;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kEpiOff = kStages * kStageBytes;  // per warp: 2 x (32 x 32 f64 output tile = 2 TMA boxes)
-    static constexpr int kWsOff = kEpiOff + kEpiWarps * kStgBufs * 8192;  // per warp: the chunk's 32 column scales
+    static constexpr int kWsOff = kEpiOff + kEpiWarps * kStgBufs * kStgBytes;  // per warp: the chunk's 32 column scales
     // row metadata ring (2 tiles ahead, filled by warp 3): S_m, |O|, mask words (J <= 32)
     static constexpr int kMetaS = 0, kMetaCnt = kBM * 8, kMetaMask = kMetaCnt + kBM * 4;
     static constexpr int kMetaBytes = kMetaMask + kBM * kMaskWords * 4;
@@ -98,11 +108,12 @@ __device__ __forceinline__ double i32_to_f64(uint32_t v) {
     return __hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)) - 4503601774854144.0;
 }
 
-template <int BN, int EW, int POST, bool PLANES, bool PK>
+template <int BN, int EW, int POST, bool PLANES, bool PK, bool ONEBOX>
 __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
     k2_qlinear(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, const QLinParams p) {
-    using L = K2Smem<BN, EW>;
+    static_assert(!ONEBOX || (EW >= 16 && POST != POST_RESID && !PK), "one-box staging: 16 warps, no residual");
+    using L = K2Smem<BN, EW, ONEBOX>;
     constexpr int kStages = L::kStages, kEpiWarps = EW, kMaskWords = L::kMaskWords;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -287,7 +298,8 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
         const int q = warp & 3;       // TMEM lanes 32q..32q+31 (a warp may only touch its quarter)
         const int cgrp = ew >> 2;     // which quarter of the BN columns
         // per-warp output tiles (double-buffered): two 32-row x 16-double boxes each, 128B-swizzled
-        uint8_t* stg0 = smem + L::kEpiOff + ew * kStgBufs * 8192;
+        uint8_t* stg0 = smem + L::kEpiOff + ew * kStgBufs * L::kStgBytes;
+        constexpr bool kOneBox = L::kStgBytes == 4096;  // the chunk's two boxes pass through one buffer
         double* wss = reinterpret_cast<double*>(smem + L::kWsOff + ew * 256);
 
         constexpr bool resid = POST == POST_RESID;
@@ -357,7 +369,7 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
                 const CUtensorMap* om = to2 ? &tmO2 : &tmO;
                 const int oc0 = to2 ? r0 - p.epi.split : r0;
                 const int sb = kStgBufs == 2 ? (cs & 1) : 0;
-                uint8_t* stg = stg0 + sb * 8192;
+                uint8_t* stg = stg0 + sb * L::kStgBytes;
                 uint64_t* rbar = res_bar + 2 * ew + sb;
                 if (lane == 0) {
                     if (kStgBufs == 2) ptx::bulk_wait_read1();  // this buffer's store (two chunks ago) has left it
@@ -480,7 +492,17 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
                 if (resid) ptx::mbar_wait(rbar, (kStgBufs == 2 ? cs >> 1 : cs) & 1);
 #pragma unroll
                 for (int j2 = 0; j2 < 16; ++j2) {  // 16-byte chunk j2 = columns 2*j2, 2*j2+1
-                    double2* cell = reinterpret_cast<double2*>(stg + (j2 >> 3) * 4096 + lane * 128 +
+                    if (kOneBox && j2 == 8) {  // box 0 leaves, then box 1 reuses the buffer
+                        ptx::fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_2d(om, stg, oc0, rbase);
+                            ptx::bulk_commit();
+                            ptx::bulk_wait_read0();
+                        }
+                        __syncwarp();
+                    }
+                    double2* cell = reinterpret_cast<double2*>(stg + (kOneBox ? 0 : (j2 >> 3) * 4096) + lane * 128 +
                                                                (((j2 & 7) ^ (lane & 7)) << 4));
                     double v0 = y[2 * j2], v1 = y[2 * j2 + 1];
                     const int ca = r0 + 2 * j2;
@@ -501,8 +523,12 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
                 ptx::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(om, stg, oc0, rbase);
-                    ptx::tma_store_2d(om, stg + 4096, oc0 + 16, rbase);
+                    if constexpr (kOneBox) {
+                        ptx::tma_store_2d(om, stg, oc0 + 16, rbase);
+                    } else {
+                        ptx::tma_store_2d(om, stg, oc0, rbase);
+                        ptx::tma_store_2d(om, stg + 4096, oc0 + 16, rbase);
+                    }
                     ptx::bulk_commit();
                 }
             }
@@ -631,7 +657,7 @@ static bool make_map_packed(CUtensorMap* m, const void* base, int rows, int cols
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int EW, int POST, bool PLANES, bool PK>
+template <int BN, int EW, int POST, bool PLANES, bool PK, bool ONEBOX = false>
 static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) {
     CUtensorMap ta, tb, to, to2;
     const bool amap = PK ? make_map_packed(&ta, p.a.codes4, p.M, p.K) : make_map(&ta, p.a.codes, p.M, p.K, kBM);
@@ -642,12 +668,12 @@ static cudaError_t launch_bn(const QLinParams& p, cudaStream_t st, int num_sms) 
     if (!make_map_f64(&to2, inproj ? p.epi.out2 : p.epi.out, p.M, inproj ? p.R - p.epi.split : ocols,
                       inproj ? p.epi.split : p.epi.ld_out))
         return cudaErrorInvalidValue;
-    const int smem = K2Smem<BN, EW>::kTotal;
-    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, EW, POST, PLANES, PK>>(smem);
+    const int smem = K2Smem<BN, EW, ONEBOX>::kTotal;
+    cudaError_t e = ensure_smem_attr<k2_qlinear<BN, EW, POST, PLANES, PK, ONEBOX>>(smem);
     if (e != cudaSuccess) return e;
     const int tiles = ((p.M + kBM - 1) / kBM) * ((p.R + BN - 1) / BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
-    k2_qlinear<BN, EW, POST, PLANES, PK><<<grid, K2Cfg<EW, PK>::kThreads, smem, st>>>(ta, tb, to, to2, p);
+    k2_qlinear<BN, EW, POST, PLANES, PK, ONEBOX><<<grid, K2Cfg<EW, PK>::kThreads, smem, st>>>(ta, tb, to, to2, p);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }
@@ -752,13 +778,17 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
     if (pk ? (p.K % 32) != 0 : p.a.codes == nullptr) return cudaErrorInvalidValue;  // packed rows: 16-byte pitch
     const bool planes = p.epi.acc_in != nullptr && p.epi.acc_out != nullptr;
     if (planes != (p.epi.acc_in != nullptr || p.epi.acc_out != nullptr)) return cudaErrorInvalidValue;
-    // main-loop-heavy calls (wide outputs, no residual) take the 8-warp / 4-stage shape
-    // (x_proj, R = 800: measured 0.25 ms per forward faster than 16 epilogue warps; 4 stages
-    // 0.33 ms per forward faster than 3)
     // The packed-A4 operand adds an unpack warpgroup; it runs on the 8-epilogue-warp shape only
     // (16 epilogue warps + 4 unpack warps: 768 threads leave a per-CTA register pool of 80 x 768,
     // too small for the 104-register epilogue after setmaxnreg)
-    const bool wide = pk || (p.epi.post != POST_RESID && (p.R > 512 || p.K > 1024));
+    // 16 epilogue warps with one staging box and 4 stages for calls of at least a wave of tiles
+    // with K <= 1024 and no residual; below a wave (the box reuse's serialisation shows) and
+    // for K > 1024 (the 8-warp shape's hoisted / vectorised outlier walk) the earlier rule:
+    // 8 epilogue warps and 4 stages for wide R, else 16 epilogue warps and 2 stages
+    // (profiles/r02/c5_quant_linear_r02q.txt)
+    const long tiles = static_cast<long>((p.M + kBM - 1) / kBM) * ((p.R + 127) / 128);
+    const bool onebox = p.epi.post != POST_RESID && p.K <= 1024 && tiles >= num_sms;
+    const bool wide = p.epi.post != POST_RESID && (p.R > 512 || p.K > 1024);
     // at most two 128-row tiles: the dp4a kernel (M = 196 at batch 1: 5.8 vs 9.3 us per launch)
     const bool small = p.M <= 2 * kBM;
 #define K2_CASE(P)                                                                                       \
@@ -769,6 +799,9 @@ cudaError_t launch_qlinear(const QLinParams& p, cudaStream_t st, int num_sms) {
         if (pk)                                                                                          \
             return planes ? launch_bn<128, 8, P, true, true>(p, st, num_sms)                             \
                           : launch_bn<128, 8, P, false, true>(p, st, num_sms);                           \
+        if (onebox)                                                                                      \
+            return planes ? launch_bn<128, 16, P, true, false, P != POST_RESID>(p, st, num_sms)          \
+                          : launch_bn<128, 16, P, false, false, P != POST_RESID>(p, st, num_sms);        \
         if (wide)                                                                                        \
             return planes ? launch_bn<128, 8, P, true, false>(p, st, num_sms)                            \
                           : launch_bn<128, 8, P, false, false>(p, st, num_sms);                          \
