@@ -45,6 +45,12 @@
 
 namespace ob {
 
+// channels per thread of the merge K1 (k1_channel): 4 (Vim-B batch 256: 217 us per launch;
+// 2 channels per thread, 60 registers and a third more warps, measured 267 us)
+#ifndef K1_MERGE_CPT
+#define K1_MERGE_CPT 4
+#endif
+
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 
 // four consecutive codes in [-7, 7] as two pack_int4 bytes (gemm.cpp:60-73: low nibble
@@ -72,11 +78,13 @@ __device__ __noinline__ double merge_exact(double m, double g) { return dmul(m, 
 
 // One thread owns four channels of one (sample, refresh window) and walks the
 // window's tokens; a warp covers 128 channels = 4 mask words (8 lanes x 4 bits).
-template <int SRC>
+template <int SRC, int CPT>
 __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
     static_assert(SRC == K1_SRC_MERGE, "plain and RMSNorm sources run on k1_staged");
+    static_assert(CPT == 2 || CPT == 4, "two or four channels per thread");
+    constexpr int kLanesPerWord = 32 / CPT;
     const int E = p.E, T = p.T, J = E >> 5;
-    const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * 4;  // channels ch .. ch+3
+    const int ch = (blockIdx.x * blockDim.x + threadIdx.x) * CPT;  // channels ch .. ch+CPT-1
     const int lane = threadIdx.x & 31;
     const int win = p.window, nwin = (T + win - 1) / win;
     const int s = blockIdx.y / nwin;
@@ -97,52 +105,43 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
         const int crow = row_at(p.order, t, T, p.grid);
         const size_t cg = static_cast<size_t>(s) * T + crow;
         const size_t row = static_cast<size_t>(s) * T + t;
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        double mg[4], gg[4];  // merge source: merged scan output and gate pre-activation
-        MergeApprox ap[4];
-        if (active) {
-            if (SRC == K1_SRC_MERGE) {
-                const size_t src = cg * E + ch;
-                const double2 a0 = ldg2(p.x + src), a1 = ldg2(p.x + src + 2);
-                const double2 g0 = ldg2(p.gate + src), g1 = ldg2(p.gate + src + 2);
-                mg[0] = dadd(0.0, a0.x);  // (0 + o_0) + o_1, ssm.cpp:214-229
-                mg[1] = dadd(0.0, a0.y);
-                mg[2] = dadd(0.0, a1.x);
-                mg[3] = dadd(0.0, a1.y);
-                if (p.x2) {
-                    const double2 b0 = ldg2(p.x2 + src), b1 = ldg2(p.x2 + src + 2);
-                    mg[0] = dadd(mg[0], b0.x);
-                    mg[1] = dadd(mg[1], b0.y);
-                    mg[2] = dadd(mg[2], b1.x);
-                    mg[3] = dadd(mg[3], b1.y);
-                }
-                gg[0] = g0.x;
-                gg[1] = g0.y;
-                gg[2] = g1.x;
-                gg[3] = g1.y;
+        double v[CPT], mg[CPT], gg[CPT];  // merge source: merged scan output and gate pre-activation
+        MergeApprox ap[CPT];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) ap[k] = merge_approx(mg[k], gg[k]);
+        for (int k = 0; k < CPT; ++k) v[k] = 0.0;
+        if (active) {
+            const size_t src = cg * E + ch;
+#pragma unroll
+            for (int h = 0; h < CPT / 2; ++h) {
+                const double2 a = ldg2(p.x + src + 2 * h), g = ldg2(p.gate + src + 2 * h);
+                mg[2 * h] = dadd(0.0, a.x);  // (0 + o_0) + o_1, ssm.cpp:214-229
+                mg[2 * h + 1] = dadd(0.0, a.y);
+                if (p.x2) {
+                    const double2 b2 = ldg2(p.x2 + src + 2 * h);
+                    mg[2 * h] = dadd(mg[2 * h], b2.x);
+                    mg[2 * h + 1] = dadd(mg[2 * h + 1], b2.y);
+                }
+                gg[2 * h] = g.x;
+                gg[2 * h + 1] = g.y;
             }
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) ap[k] = merge_approx(mg[k], gg[k]);
         }
-        unsigned have = 0;  // merge: bit k = v[k] holds the exact value
+        unsigned have = 0;  // bit k = v[k] holds the exact value
         if (dyn) {
             if (t == next_ref) {  // maybe_refresh
                 in = 0;
                 next_ref += p.n_refresh;
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // detect_outliers, channel-local form
-                if (SRC == K1_SRC_MERGE) {
-                    if (!active || ((in >> k) & 1u)) continue;
-                    const float av = fabsf(ap[k].v);
-                    if (av * (1.0f - ap[k].eps) > thetaf * 1.0000003f) {
-                        in |= 1u << k;
-                    } else if (av * (1.0f + ap[k].eps) >= thetaf * 0.9999997f) {
-                        v[k] = merge_exact(mg[k], gg[k]);
-                        have |= 1u << k;
-                        if (fabs(v[k]) > theta) in |= 1u << k;
-                    }
-                } else {
+            for (int k = 0; k < CPT; ++k) {  // detect_outliers, channel-local form
+                if (!active || ((in >> k) & 1u)) continue;
+                const float av = fabsf(ap[k].v);
+                if (av * (1.0f - ap[k].eps) > thetaf * 1.0000003f) {
+                    in |= 1u << k;
+                } else if (av * (1.0f + ap[k].eps) >= thetaf * 0.9999997f) {
+                    v[k] = merge_exact(mg[k], gg[k]);
+                    have |= 1u << k;
                     if (fabs(v[k]) > theta) in |= 1u << k;
                 }
             }
@@ -150,17 +149,17 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
         const double S = s_tab[t];
         const double inv = i_tab ? i_tab[t] : __ddiv_rn(1.0, S);
         if (active) {
-            int c[4];
+            int c[CPT];
             const float invf = __double2float_rn(inv), capf = static_cast<float>(qa) + 1.0f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < CPT; ++k) {
                 c[k] = 0;
                 if ((in >> k) & 1u) {
-                    if (SRC == K1_SRC_MERGE && !((have >> k) & 1u)) v[k] = merge_exact(mg[k], gg[k]);
+                    if (!((have >> k) & 1u)) v[k] = merge_exact(mg[k], gg[k]);
                     const double os = scale_from_peak(fabs(v[k]), qo);  // scale_for over the 1-value row
                     p.ocode[row * E + ch + k] = static_cast<int8_t>(static_cast<int>(quant_code_div(v[k], os, qo)));
                     p.oscale[row * E + ch + k] = os;
-                } else if (SRC == K1_SRC_MERGE) {
+                } else {
                     // certified f32 quotient: |dq| <= (|q| + 1) (eps + 3 2^-24)
                     const float q = fminf(fmaxf(ap[k].v * invf, -capf), capf);
                     const float r = rintf(q);
@@ -171,24 +170,30 @@ __global__ void __launch_bounds__(256) k1_channel(const K1Params p) {
                         if (!((have >> k) & 1u)) v[k] = merge_exact(mg[k], gg[k]);
                         c[k] = quant_code_int(v[k], S, inv, qa, qai);
                     }
-                } else {
-                    c[k] = quant_code_int(v[k], S, inv, qa, qai);
                 }
             }
-            if (p.codes4)
-                *reinterpret_cast<uint16_t*>(p.codes4 + row * (E >> 1) + (ch >> 1)) = pack4(c[0], c[1], c[2], c[3]);
-            else
-                *reinterpret_cast<char4*>(p.codes + row * E + ch) =
-                    make_char4(static_cast<signed char>(c[0]), static_cast<signed char>(c[1]),
-                               static_cast<signed char>(c[2]), static_cast<signed char>(c[3]));
+            if constexpr (CPT == 4) {
+                if (p.codes4)
+                    *reinterpret_cast<uint16_t*>(p.codes4 + row * (E >> 1) + (ch >> 1)) = pack4(c[0], c[1], c[2], c[3]);
+                else
+                    *reinterpret_cast<char4*>(p.codes + row * E + ch) =
+                        make_char4(static_cast<signed char>(c[0]), static_cast<signed char>(c[1]),
+                                   static_cast<signed char>(c[2]), static_cast<signed char>(c[3]));
+            } else {
+                if (p.codes4)  // pack_int4: low nibble = even column
+                    p.codes4[row * (E >> 1) + (ch >> 1)] = static_cast<uint8_t>((c[0] & 0xF) | ((c[1] & 0xF) << 4));
+                else
+                    *reinterpret_cast<char2*>(p.codes + row * E + ch) =
+                        make_char2(static_cast<signed char>(c[0]), static_cast<signed char>(c[1]));
+            }
         }
-        // mask word of channels 32w..32w+31 from 8 lanes x 4 bits (all zero in the common case)
-        unsigned bits = active ? in << ((lane & 7) * 4) : 0u;
+        // mask word of channels 32w..32w+31 from 32/CPT lanes x CPT bits (all zero in the common case)
+        unsigned bits = active ? in << ((lane & (kLanesPerWord - 1)) * CPT) : 0u;
         if (__any_sync(0xffffffffu, bits != 0u)) {
 #pragma unroll
-            for (int o = 4; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+            for (int o = kLanesPerWord / 2; o >= 1; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
         }
-        if (active && (lane & 7) == 0) {
+        if (active && (lane & (kLanesPerWord - 1)) == 0) {
             p.omask[row * J + (ch >> 5)] = bits;
             if (bits) atomicAdd(p.ocnt + row, __popc(bits));
         }
@@ -838,9 +843,10 @@ static cudaError_t launch_channel(const K1Params& p, cudaStream_t st) {
         ++kernel_launch_counter();
         return cudaGetLastError();
     }
-    const int quads = p.E / 4, threads = quads >= 256 ? 256 : ((quads + 31) / 32) * 32;
-    dim3 grid((quads + threads - 1) / threads, p.S * nwin);
-    k1_channel<SRC><<<grid, threads, 0, st>>>(p);
+    constexpr int kCpt = K1_MERGE_CPT;
+    const int units = p.E / kCpt, threads = units >= 256 ? 256 : ((units + 31) / 32) * 32;
+    dim3 grid((units + threads - 1) / threads, p.S * nwin);
+    k1_channel<SRC, kCpt><<<grid, threads, 0, st>>>(p);
     ++kernel_launch_counter();
     return cudaGetLastError();
 }
