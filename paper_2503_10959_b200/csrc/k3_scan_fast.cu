@@ -1325,11 +1325,13 @@ static cudaError_t launch_kernel(const ScanDirs& P, int ndirs, const StepShared*
 // At batch 1 (BASELINE C1) a launch has a few warps on the whole GPU, so each step
 // costs its full instruction latency. Only the h update is sequential in t; the
 // a_bar / b_bar codes (their detector state runs per refresh window) and the output
-// sum are not. So: (A) codes for every (step, channel), one thread per (channel,
-// refresh window); (B) the f32 state update (k3_scan_c1<FS>) walking the steps with
-// the next step's codes in flight; (C) the outputs of every (step, channel) in
-// parallel. Same arithmetic as k3_scan_c1<FS>; the intermediates (73 B per
-// direction, sample, step and channel) stay in L2 at these sizes.
+// sum are not. So: (A) codes for every (step, channel) — detection per (step,
+// channel), the sticky state per channel, codes on sixteen lanes per channel
+// (k3s_codes16); (B) the f32 state update (k3_scan_c1<FS>) walking the steps on
+// sixteen lanes per channel, one state each (k3s_state16); (C) the outputs of every
+// (step, channel) in parallel (k3s_out). Same arithmetic as k3_scan_c1<FS>; the
+// intermediates (88 B per direction, sample, step and channel) stay in L2 at these
+// sizes.
 // phase A's record per (direction, sample, step, channel): a_bar codes (0..q) | b_bar codes |
 // the exact scales of the step (outlier channels: their own) | outlier flags after detection
 // plus the f32 scalars phase B's common path needs: f32 of the a scale, f32(S_b) f32(u)
