@@ -116,7 +116,9 @@ __global__ void __launch_bounds__(K2Cfg<EW, PK>::kThreads, 1)
     using L = K2Smem<BN, EW, ONEBOX>;
     constexpr int kStages = L::kStages, kEpiWarps = EW, kMaskWords = L::kMaskWords;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned for the 128B-swizzled tiles; indexed from the shared array (no integer
+    // round trip) so the compiler keeps the shared window: LDS / STS, not generic LD / ST
+    uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* empty = full + kStages;
     uint64_t* acc_full = empty + kStages;
