@@ -232,7 +232,7 @@ def op_model(name: str, *, rows: int, E: int, N: int, abits: int):
     return None, 0
 
 
-def kernel_rooflines(launches, *, B, L, E, N, blocks, abits, peaks, i8_tops, fp64_tflops, sms):
+def kernel_rooflines(launches, *, B, L, E, N, blocks, abits, peaks, i8_tops, fp64_tflops, sms, patch_k=None):
     """Per-op and per-family achieved rates from the per-op CUDA-event list of
     one single-stream forward (forward_profile_launches)."""
     names = op_names(blocks)
@@ -248,6 +248,16 @@ def kernel_rooflines(launches, *, B, L, E, N, blocks, abits, peaks, i8_tops, fp6
         f["n"] += 1
     out = {}
     for nm, f in fam.items():
+        if nm == "f64.patch_embed" and patch_k and fp64_tflops and f["n"]:
+            # detail::mm's separately rounded products and sums: 2 FP64 lane-ops per MAC against
+            # the measured FP64 peak (FMA = 2 flops, so fp64_tflops / 2 lane-ops per second)
+            t = f["ms"] / f["n"] * 1e-3
+            lane_ops = 2.0 * rows * patch_k * E
+            out[nm] = {"us_per_launch": round(t * 1e6, 2), "launches_per_fwd": f["n"], "bound": "fp64",
+                       "unit": "T lane-op/s", "achieved": lane_ops / t / 1e12, "peak": fp64_tflops / 2.0,
+                       "frac": lane_ops / t / 1e12 / (fp64_tflops / 2.0),
+                       "model": "M x K x R DMUL + DADD (no FMA: the reference's rounding), M = B*L, K = patch^2 x channels"}
+            continue
         if nm.startswith(("aux.patch", "aux.mean", "f64.")) or f["n"] == 0:
             continue
         t = f["ms"] / f["n"] * 1e-3  # mean seconds per launch
@@ -480,7 +490,8 @@ def run_ours(args):
         L, E, N = dims.tokens, dims.embed, dims.state
         peaks = measured_peaks()
         kern = kernel_rooflines(launches, B=B, L=L, E=E, N=N, blocks=dims.blocks, abits=args.abits, peaks=peaks,
-                                i8_tops=i8_peak, fp64_tflops=fp64_peak, sms=ctx.num_sms)
+                                i8_tops=i8_peak, fp64_tflops=fp64_peak, sms=ctx.num_sms,
+                                patch_k=dims.patch * dims.patch * dims.channels)
         cfg = dict(CONFIG, global_batch=B * world, parallelism=f"dp{world}", image=dims.image, seq_len=L,
                    embed=E, blocks=dims.blocks)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
