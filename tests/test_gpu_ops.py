@@ -287,3 +287,49 @@ def test_dgemm_tiles_sequential_k(gpu_ctx, M, R, K):
         got = gpu_ctx.dgemm(_dev(a), _dev(w), post=post, out=out, bias=_dev(bias) if post == ob.POST_BIAS else None)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), want), post
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("S,E", [(8, 768), (2, 128)])
+def test_detect_quantize_adversarial_values(oracle_checker, gpu_ctx, mode, S, E):
+    """K1's branch-free code test against quantize_code's round-half-away on
+    values placed on and next to half-integer quotients (S a power of two, so
+    (k + 1/2) S is exact), signed zeros, subnormals and quotients far beyond
+    the code range, for the staged kernel (S x E above one warp per SM), the
+    register window kernel and the literal kernel: every code, mask and
+    outlier value equals the oracle's split_quantize."""
+    import torch
+    T = 12
+    rng = np.random.default_rng(S * E + mode)
+    s_pow = 0.25
+    s_in = np.full(T, s_pow)
+    s_full = np.full(T, s_pow)
+    theta = 7.5 * s_pow * 1.2  # inlier quotients up to +-8.99: ties at every half-integer in range
+    k = rng.integers(-9, 9, size=(S, T, E)).astype(np.float64)
+    x = (k + 0.5) * s_pow
+    sel = rng.random((S, T, E))
+    x = np.where(sel < 0.2, np.nextafter(x, np.inf), x)
+    x = np.where((sel >= 0.2) & (sel < 0.4), np.nextafter(x, -np.inf), x)
+    x = np.where((sel >= 0.4) & (sel < 0.45), -0.0, x)
+    x = np.where((sel >= 0.45) & (sel < 0.5), 0.0, x)
+    x = np.where((sel >= 0.5) & (sel < 0.53), 3e-310 * np.sign(k + 0.5), x)
+    x = np.where((sel >= 0.53) & (sel < 0.55), 1e300 * np.sign(k + 0.5), x)
+    x = np.where((sel >= 0.55) & (sel < 0.57), 3e9 * np.sign(k + 0.5), x)  # |q| >= 2^31 (static: saturate)
+    xd = _dev(x)
+    _, masks, _ = oracle_checker.quant_stream(x.reshape(S, T, E, 1), theta, s_in, s_full, 4, 4, 8, mode)
+    for lit in (0, 2, 1):
+        res = gpu_ctx.detect_quantize(xd, S=S, T=T, E=E, theta=theta, s_in=_dev(s_in), s_full=_dev(s_full),
+                                      n_refresh=4, act_bits=4, outlier_bits=8, mode=mode, literal=lit)
+        torch.cuda.synchronize()
+        codes = res["codes"].cpu().numpy().reshape(S, T, E)
+        omask = _unpack(res["omask"].cpu().numpy(), E).reshape(S, T, E)
+        ocode = res["ocode"].cpu().numpy().reshape(S, T, E)
+        osc = res["oscale"].cpu().numpy().reshape(S, T, E)
+        assert np.array_equal(omask, masks), lit
+        for s in range(S):
+            for t in range(T):
+                chans = np.nonzero(masks[s, t])[0]
+                inl, oc, os_ = oracle_checker.split_quantize(x[s, t].reshape(E, 1), chans, s_pow, 4, 8)
+                assert np.array_equal(codes[s, t], inl[:, 0]), (lit, s, t)
+                assert np.array_equal(ocode[s, t, chans], oc[:, 0]), (lit, s, t)
+                assert np.array_equal(osc[s, t, chans], os_), (lit, s, t)
