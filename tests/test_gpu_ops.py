@@ -333,3 +333,48 @@ def test_detect_quantize_adversarial_values(oracle_checker, gpu_ctx, mode, S, E)
                 assert np.array_equal(codes[s, t], inl[:, 0]), (lit, s, t)
                 assert np.array_equal(ocode[s, t, chans], oc[:, 0]), (lit, s, t)
                 assert np.array_equal(osc[s, t, chans], os_), (lit, s, t)
+
+
+@pytest.mark.parametrize("post", [0, 1])
+def test_quant_linear_full_wave_shapes_match_small_m(gpu_ctx, post):
+    """The full-wave K2 shape (16 epilogue warps, one reused staging box, 4
+    operand stages: M = 4096, R = 1536, K = 768 -> 384 tiles) against the M <=
+    256 dp4a kernel (oracle-checked elsewhere) on the same rows, for the plain
+    store and the in_proj split into u0 / gate (POST_INPROJ), outlier terms and
+    the integer planes included."""
+    import torch
+    M, R, K = 4096, 1536, 768
+    rng = np.random.default_rng(post + 7)
+    w = rng.integers(-7, 8, size=(R, K), dtype=np.int8)
+    ws = rng.uniform(0.005, 0.02, size=R)
+    x = rng.integers(-7, 8, size=(M, K), dtype=np.int8)
+    mask = (rng.random((M, K)) < 0.01).astype(np.uint8)
+    x[mask.astype(bool)] = 0
+    ocode = np.where(mask.astype(bool), rng.integers(-127, 128, size=(M, K)), 0).astype(np.int8)
+    oscale = np.where(mask.astype(bool), rng.uniform(0.005, 0.02, size=(M, K)), 0.0)
+    act = dict(codes=_dev(x), s_row=_dev(rng.uniform(0.005, 0.02, size=M)), ocnt=_dev(mask.sum(axis=1).astype(np.int32)),
+               omask=_dev(_mask_words(mask)), ocode=_dev(ocode), oscale=_dev(oscale))
+    wd, wtd, wsd = _dev(w), _dev(w.T.copy()), _dev(ws)
+
+    def run(a, m):
+        if post == 1:
+            out = torch.zeros(m, R // 2, dtype=torch.float64, device="cuda")
+            out2 = torch.zeros(m, R // 2, dtype=torch.float64, device="cuda")
+            gpu_ctx.quant_linear(a, wd, wtd, wsd, post=1, out=out, out2=out2, split=R // 2)
+            y = torch.cat([out, out2], dim=1)
+        else:
+            y = torch.zeros(m, R, dtype=torch.float64, device="cuda")
+            gpu_ctx.quant_linear(a, wd, wtd, wsd, post=0, out=y)
+        ai = torch.zeros(m, R, dtype=torch.int32, device="cuda")
+        ao = torch.zeros(m, R, dtype=torch.int32, device="cuda")
+        gpu_ctx.quant_linear(a, wd, wtd, wsd, out=torch.zeros(m, R, dtype=torch.float64, device="cuda"),
+                             acc_in=ai, acc_out=ao)
+        torch.cuda.synchronize()
+        return y.cpu().numpy(), ai.cpu().numpy(), ao.cpu().numpy()
+
+    big = run(act, M)
+    for m0 in (0, 1920, 3840):
+        sub = {k: v[m0:m0 + 256].contiguous() for k, v in act.items()}
+        small = run(sub, 256)
+        for b, s_ in zip(big, small):
+            assert np.array_equal(b[m0:m0 + 256], s_), m0
