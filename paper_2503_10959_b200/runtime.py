@@ -227,7 +227,7 @@ class Context:
         return dict(codes=codes, s_row=s_row, ocnt=ocnt, omask=omask, ocode=ocode, oscale=oscale)
 
     def quant_linear(self, act: dict, w, wt, ws, *, post=L.POST_STORE, out=None, out2=None, split=0, acc_in=None,
-                     acc_out=None):
+                     acc_out=None, bias=None):
         """K2: hybrid quant-linear over K1's operand dict (int8 `codes` or nibble-packed
         `codes4`); returns `out`."""
         import torch
@@ -240,7 +240,7 @@ class Context:
         fn = self.lib.ouro_b200_quant_linear_packed if packed else self.lib.ouro_b200_quant_linear
         L.check(fn(self.h, M, R, K, _ptr(act["codes4"] if packed else act["codes"]), _ptr(act["s_row"]),
                    _ptr(act["ocnt"]), _ptr(act["omask"]), _ptr(act["ocode"]), _ptr(act["oscale"]), _ptr(w), _ptr(wt),
-                   _ptr(ws), post, _ptr(out), ld, _ptr(out2), split, None, _ptr(acc_in), _ptr(acc_out)))
+                   _ptr(ws), post, _ptr(out), ld, _ptr(out2), split, _ptr(bias), _ptr(acc_in), _ptr(acc_out)))
         return out
 
     def quant_scan(self, *, S, T, E, order, grid, u, proj, a, b_delta, o, mode, n_refresh=10, act_bits=8,

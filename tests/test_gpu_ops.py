@@ -335,12 +335,13 @@ def test_detect_quantize_adversarial_values(oracle_checker, gpu_ctx, mode, S, E)
                 assert np.array_equal(osc[s, t, chans], os_), (lit, s, t)
 
 
-@pytest.mark.parametrize("post", [0, 1])
+@pytest.mark.parametrize("post", [0, 1, 4])
 def test_quant_linear_full_wave_shapes_match_small_m(gpu_ctx, post):
     """The full-wave K2 shape (16 epilogue warps, one reused staging box, 4
     operand stages: M = 4096, R = 1536, K = 768 -> 384 tiles) against the M <=
     256 dp4a kernel (oracle-checked elsewhere) on the same rows, for the plain
-    store and the in_proj split into u0 / gate (POST_INPROJ), outlier terms and
+    store, the in_proj split into u0 / gate (POST_INPROJ) and x_proj's
+    softplus(y + b_delta) on the first columns (POST_XPROJ), outlier terms and
     the integer planes included."""
     import torch
     M, R, K = 4096, 1536, 768
@@ -355,6 +356,7 @@ def test_quant_linear_full_wave_shapes_match_small_m(gpu_ctx, post):
     act = dict(codes=_dev(x), s_row=_dev(rng.uniform(0.005, 0.02, size=M)), ocnt=_dev(mask.sum(axis=1).astype(np.int32)),
                omask=_dev(_mask_words(mask)), ocode=_dev(ocode), oscale=_dev(oscale))
     wd, wtd, wsd = _dev(w), _dev(w.T.copy()), _dev(ws)
+    bias = _dev(rng.normal(size=R))
 
     def run(a, m):
         if post == 1:
@@ -362,6 +364,9 @@ def test_quant_linear_full_wave_shapes_match_small_m(gpu_ctx, post):
             out2 = torch.zeros(m, R // 2, dtype=torch.float64, device="cuda")
             gpu_ctx.quant_linear(a, wd, wtd, wsd, post=1, out=out, out2=out2, split=R // 2)
             y = torch.cat([out, out2], dim=1)
+        elif post == 4:
+            y = torch.zeros(m, R, dtype=torch.float64, device="cuda")
+            gpu_ctx.quant_linear(a, wd, wtd, wsd, post=4, out=y, split=R // 2, bias=bias)
         else:
             y = torch.zeros(m, R, dtype=torch.float64, device="cuda")
             gpu_ctx.quant_linear(a, wd, wtd, wsd, post=0, out=y)
