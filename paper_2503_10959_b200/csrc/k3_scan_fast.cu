@@ -117,9 +117,8 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
 // delta and max_m |B_m|. One warp per (direction, step, group of kTabSamples
 // samples): the step's calibration fields (global loads of the scale tables, a
 // log2) are computed once and kept in the warp's shared record, then each sample
-// overwrites its B / C fields (lane j holds column E + j of the x_proj row; the
-// next sample's row is loaded before this one is written) and the record leaves as
-// 16-byte coalesced chunks.
+// overwrites its B / C fields (lane j holds column E + j of the x_proj row; all the
+// group's rows are loaded at once) and the record leaves as 16-byte coalesced chunks.
 constexpr int kTabSamples = 8;
 __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndirs, StepShared* __restrict__ out) {
     __shared__ StepShared rec[8];
@@ -162,9 +161,15 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
     const int s1 = min(S, s0 + kTabSamples);
     const size_t P2 = static_cast<size_t>(p.E) + 32;
     const double* col = p.proj + static_cast<size_t>(t) * P2 + p.E + lane;  // + s*T*P2 per sample
-    double v = col[static_cast<size_t>(s0) * T * P2];
-    for (int s = s0; s < s1; ++s) {
-        const double vn = s + 1 < s1 ? col[static_cast<size_t>(s + 1) * T * P2] : 0.0;
+    double vs[kTabSamples];  // every sample's B / C row of this step, loaded at once
+#pragma unroll
+    for (int j = 0; j < kTabSamples; ++j)
+        vs[j] = s0 + j < s1 ? col[static_cast<size_t>(s0 + j) * T * P2] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kTabSamples; ++j) {
+        const int s = s0 + j;
+        if (s >= s1) break;
+        const double v = vs[j];
         double bm = fabs(v);
 #pragma unroll
         for (int o = 8; o >= 1; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
@@ -188,7 +193,6 @@ __global__ void __launch_bounds__(256) k3_step_tables(const ScanDirs P, int ndir
         __syncwarp();
         uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<size_t>(dd) * S + s) * T + t);
         for (int k = lane; k < kChunks16; k += 32) dst[k] = src[k];
-        v = vn;
     }
 }
 
