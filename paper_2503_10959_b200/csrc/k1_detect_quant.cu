@@ -902,7 +902,13 @@ static K1Dirs k1_dirs(const K1Params* ps, int n) {
     d.p[0] = ps[0];
     d.p[1] = n > 1 ? ps[1] : ps[0];
     d.mirror = n > 1 && ps[0].order <= 0 && ps[1].order == 1;
-    const int rows = kK1StageBytes / (ps[0].E * 8);
+    // stage rows: 24 KB stages, but no more shared memory per CTA than the CTAs the
+    // registers allow can share (narrow E: more, smaller CTAs per SM; E = 384: 4 rows
+    // instead of 8, 8 CTAs per SM instead of 4)
+    const int threads = ((ps[0].E / 4 + 31) / 32) * 32;
+    const int ctas = std::max(1, 65536 / (80 * threads));
+    const int rows_smem = (220 * 1024 / ctas) / (kK1Stages * ps[0].E * 8);
+    const int rows = std::min(kK1StageBytes / (ps[0].E * 8), rows_smem);
     d.rc = std::max(1, std::min({rows, kK1MaxRc, ps[0].window}));
     return d;
 }
