@@ -227,9 +227,10 @@ ouro_status ouro_b200_model_use_graphs(ouro_b200_model* m, int on);
  * nibble-packed from K1 to K2, 0 (default) one int8 byte per code; "merge_fuse" = 1:
  * the out_proj input K1 runs as the f32-state scan's tail, 0 (default) its own
  * launch; "split_parts" in [1, 4] (default 2) runs a batch of
- * >= 32 * parts samples as that many independent sub-batches on their own
- * streams (results identical), 1 one stream; "feed_chunks" (default 8) = H2D
- * chunks of forward_host for batches >= 64. */
+ * >= 32 * parts samples and >= parts * "split_min_rows" (default 16384) token
+ * rows as that many independent sub-batches on their own streams (results
+ * identical), 1 one stream; "feed_chunks" (default 8) = H2D chunks of
+ * forward_host for batches >= 64. */
 ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long value);
 
 /* One forward with CUDA events around every launch: per kernel family

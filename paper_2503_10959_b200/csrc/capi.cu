@@ -680,6 +680,9 @@ ouro_status ouro_b200_model_set_option(ouro_b200_model* m, const char* key, long
         } else if (k == "feed_chunks") {
             require(value >= 1 && value <= 64, "model_set_option: feed_chunks must be in [1, 64]");
             m->m->feed_chunks = static_cast<int>(value);
+        } else if (k == "split_min_rows") {
+            require(value >= 0, "model_set_option: split_min_rows must be >= 0");
+            m->m->split_min_rows = static_cast<int>(value);
         } else if (k == "split_parts") {
             require(value >= 1 && value <= 4, "model_set_option: split_parts must be in [1, 4]");
             m->m->split_parts = static_cast<int>(value);

@@ -416,7 +416,8 @@ void Model::forward(const Calibration* cal, int mode, bool d1, bool d2, const do
     }
     upload_fp();
     const int np = std::min(split_parts, kMaxSplit);
-    const bool split = np > 1 && trace == nullptr && calib_peaks == nullptr && !timing.on && S >= np * kSplitMin;
+    const bool split = np > 1 && trace == nullptr && calib_peaks == nullptr && !timing.on && S >= np * kSplitMin &&
+                       static_cast<long>(S) * d.tokens() >= static_cast<long>(np) * split_min_rows;
     if (!split) {
         forward_impl(cal, mode, d1, d2, images, S, logits, trace, calib_peaks, feed, ctx->stream, w);
         return;

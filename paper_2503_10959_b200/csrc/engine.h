@@ -212,13 +212,17 @@ class Model {
         std::vector<cudaEvent_t> feed_events;  // host-feed chunk events, created on first use
     } w;
     void ensure_work(Work& wk, int S, bool trace);
-    // Split forward: a batch of >= parts * kSplitMin samples runs as `split_parts`
-    // independent sub-batches on their own streams (samples never interact), so
-    // each part's kernels fill the others' last-wave tails. Off for traces,
-    // calibration recording and per-family timing.
+    // Split forward: a batch of >= parts * kSplitMin samples and >= parts * split_min_rows
+    // token rows runs as `split_parts` independent sub-batches on their own streams
+    // (samples never interact), so each part's kernels fill the others' last-wave tails.
+    // Off for traces, calibration recording and per-family timing. Measured (ms per
+    // forward, parts 1 / 2): Vim-B 224² batch 256 69.4 / 68.6, Vim-B 448² batch 64 73.9 /
+    // 72.0 (50K rows each), Vim-S batch 64 12.12 / 12.76 (12.5K rows: smaller parts
+    // lose more to their own tails than the overlap wins), hence 16K rows per part.
     static constexpr int kSplitMin = 32;
     static constexpr int kMaxSplit = 4;
     int split_parts = 2;
+    int split_min_rows = 16384;
     int feed_chunks = 8;  // host-feed H2D chunks per forward (batches >= 64); e2e measured 2/4/8/16/32:
                           // 2599 / 2776 / 2795 / 2701 / 2682 images/s
     struct SplitPart {

@@ -346,6 +346,7 @@ def test_split_forward_identical(oracle_checker, gpu_ctx, graphs):
     ocal = om.calibrate(cimgs, spec)
     gcal = _import_calib(gm, ocal.export(), spec)
     gm.use_graphs(graphs)
+    gm.set_option("split_min_rows", 0)  # the toy batch is far below the default part size
     dev = torch.from_numpy(imgs).cuda()
     res = {}
     for parts in (1, 2, 4):
@@ -363,6 +364,7 @@ def test_split_forward_identical(oracle_checker, gpu_ctx, graphs):
                 assert np.array_equal(got, base), (parts, mode)
     assert rel_err(res[(2, 1)][0], om.forward(imgs, ocal, 1)) <= RTOL_F64
     gm.set_option("split_parts", 2)
+    gm.set_option("split_min_rows", 16384)
 
 
 def test_split_forward_with_spikes_identical(oracle_checker, gpu_ctx):
@@ -380,6 +382,7 @@ def test_split_forward_with_spikes_identical(oracle_checker, gpu_ctx):
     spec = _spec(4, n_refresh=5, rho=0.02)
     gcal = _import_calib(gm, om.calibrate(cimgs, spec).export(), spec)
     gm.set_spikes(ob.SpikeSettings(rate=0.3, gain=20.0, channels=2, salt=5))
+    gm.set_option("split_min_rows", 0)  # the toy batch is far below the default part size
     res = {}
     for parts in (1, 2, 4):
         gm.set_option("split_parts", parts)
